@@ -1,0 +1,439 @@
+/*
+ * eps_capi.h -- the drop-in C ABI of the B200 PipeTransformer hot path.
+ *
+ * The reference (arxiv 2102.03161 artifact, /root/reference/proj) exposes a
+ * header-only C++ API in namespace `eps` (proj/include/eps/*.hpp).  This file
+ * is the flat, FFI-friendly boundary over the same operators plus the sm_100a
+ * data plane: plain pointers and sizes, caller-owned buffers, `int` status
+ * codes and a thread-local error string.  Each entry cites the reference
+ * interface it replaces.  INTEGRATION.md shows the ctypes / C++ bindings.
+ *
+ * The same header is compiled twice:
+ *   - into paper_2102_03161_b200/libeps_b200.so (prefix `eps_`), the product;
+ *   - into oracle/_ref/libeps_ref.so (prefix `epsref_`, control plane only)
+ *     against the *reference's own* sources, which is how the parity tests
+ *     compare the two implementations call for call.
+ *
+ * Status codes: 0 ok, 1 invalid argument (std::invalid_argument), 2 domain
+ * (std::domain_error), 3 logic (std::logic_error), 4 config (ConfigError),
+ * 5 io (IoError), 6 cuda, 7 nccl, 8 capacity (output buffer too small),
+ * 9 other.
+ */
+#ifndef EPS_CAPI_H_
+#define EPS_CAPI_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#ifndef EPS_CAPI_PREFIX
+#define EPS_FN(name) eps_##name
+#else
+#define EPS_CAPI_CAT2(a, b) a##b
+#define EPS_CAPI_CAT(a, b) EPS_CAPI_CAT2(a, b)
+#define EPS_FN(name) EPS_CAPI_CAT(EPS_CAPI_PREFIX, name)
+#endif
+
+enum {
+  EPS_OK = 0,
+  EPS_EINVAL = 1,
+  EPS_EDOMAIN = 2,
+  EPS_ELOGIC = 3,
+  EPS_ECONFIG = 4,
+  EPS_EIO = 5,
+  EPS_ECUDA = 6,
+  EPS_ENCCL = 7,
+  EPS_ECAPACITY = 8,
+  EPS_EOTHER = 9
+};
+
+#define EPS_MAX_STAGES 64
+
+/* ---- value types (mirror the eps:: structs) --------------------------- */
+
+/* ModelSpec (model.hpp:15-30); arrays are caller-owned. */
+typedef struct {
+  int layers;
+  const int64_t* attention_params; /* [layers] */
+  const int64_t* mlp_params;       /* [layers] */
+  const int64_t* activation_bytes; /* [2*layers+1] */
+  int bytes_per_param;
+} eps_model_t;
+
+/* ClusterSpec (model.hpp:32-41). */
+typedef struct {
+  int node_count;
+  int gpus_per_node;
+  double gpu_memory_bytes;
+  double intra_node_bandwidth;
+  double inter_node_bandwidth;
+} eps_cluster_t;
+
+/* CostModel (cost_model.hpp:11-25), without the transition table. */
+typedef struct {
+  double c_fwd;
+  double backward_ratio;
+  double c_update;
+  double per_microbatch_overhead;
+  double allreduce_bucket_bytes;
+  double comm_latency;
+} eps_cost_model_t;
+
+/* CacheTierParams (autocache.hpp:11-22). */
+typedef struct {
+  double host_bandwidth;
+  double disk_bandwidth;
+  double host_capacity_bytes;
+  int window_batches;
+  int block_batches;
+  double read_latency;
+} eps_cache_tiers_t;
+
+/* Active sublayer sequence (SublayerSeq, model.hpp:66-74).  global_index
+ * may be NULL: then sublayer i has global index 2*frozen_layers + i. */
+typedef struct {
+  int n;
+  const int64_t* params;
+  const int* global_index;
+  int64_t frozen_params;
+  int frozen_layers;
+} eps_seq_t;
+
+/* PartitionPlan (autopipe.hpp:22-34). */
+typedef struct {
+  int pipeline_length;
+  int begin[EPS_MAX_STAGES];
+  int end[EPS_MAX_STAGES];
+  int64_t param_sums[EPS_MAX_STAGES];
+  double effective_sizes[EPS_MAX_STAGES];
+  int64_t frozen_params;
+  int frozen_layers;
+  double lambda_frozen;
+} eps_plan_t;
+
+/* StageLoad (schedule.hpp:27-32). */
+typedef struct {
+  double fwd_params;
+  double bwd_params;
+  double prefix_seconds_per_sample;
+  double in_bytes_per_sample;
+} eps_stage_load_t;
+
+/* TimedBlock (schedule.hpp:14-21); kind: 0 F, 1 B, 2 U, 3 XFER, 4 AR. */
+typedef struct {
+  int device;
+  int kind;
+  double start;
+  double end;
+  int micro_batch;
+  int bucket;
+} eps_block_t;
+
+/* IterationSchedule scalars (schedule.hpp:47-58). */
+typedef struct {
+  double makespan;
+  double compute_makespan;
+  double makespan_without_ar;
+  double total_bubble;
+  double allreduce_seconds;
+  double transfer_seconds;
+  double compute_seconds;
+  double exposed_comm;
+  int n_blocks;
+} eps_schedule_summary_t;
+
+/* TransitionMessage (autodp.hpp:47-56). */
+typedef struct {
+  int sender;
+  int receiver;
+  int epoch;
+  double lr_schedule_position;
+  int frozen_layers;
+  int new_pipeline_length;
+  int span_first;
+  int span_length;
+  char weights_version[32];
+} eps_msg_t;
+
+/* EpochRow (runner.hpp:15-31). */
+typedef struct {
+  int epoch;
+  int l_frozen;
+  int pipeline_length;
+  int replica_width;
+  int micro_batches;
+  double iteration_time;
+  double epoch_time;
+  double throughput;
+  double bubble_time;
+  double comm_time;
+  double exposed_comm_time;
+  int cache_enabled;
+  double transition_overhead;
+  double cache_transition_time;
+  double stall_time;
+} eps_epoch_row_t;
+
+typedef struct {
+  double total_seconds;
+  double baseline_total_seconds;
+  double speedup;
+  double comm_ratio;
+  double frozen_forward_per_sample;
+  double final_prefix_forward_per_sample;
+  int n_epochs;
+  int n_transitions;
+  int n_cache_events;
+} eps_run_summary_t;
+
+typedef struct eps_freeze eps_freeze_t;     /* FreezeState */
+typedef struct eps_scenario eps_scenario_t; /* ScenarioConfig */
+
+/* ---- errors ----------------------------------------------------------- */
+const char* EPS_FN(last_error)(void);
+
+/* ---- model.hpp -------------------------------------------------------- */
+/* vit_b16() / bert_large() presets (model.cpp:125-179). */
+int EPS_FN(model_preset)(const char* name, int64_t* attention_params, int64_t* mlp_params,
+                         int64_t* activation_bytes, int cap_layers, int* layers);
+int EPS_FN(model_validate)(const eps_model_t* model);
+int EPS_FN(model_prefix_params)(const eps_model_t* model, int layer, int64_t* out);
+/* m_partition (model.cpp:79-92). */
+int EPS_FN(m_partition)(const eps_model_t* model, int l_frozen, int64_t* params,
+                        int* global_index, int cap, int* n, int64_t* frozen_params);
+
+/* ---- freeze.hpp ------------------------------------------------------- */
+int EPS_FN(freeze_create)(double alpha, eps_freeze_t** out);
+void EPS_FN(freeze_destroy)(eps_freeze_t* state);
+int EPS_FN(freeze_frozen_count)(const eps_freeze_t* state, int* out);
+/* next_frozen_count (freeze.cpp:22-50). */
+int EPS_FN(next_frozen_count)(eps_freeze_t* state, const double* norms, int n_norms,
+                              int layer_count, int* out, double* raw_bound);
+/* frozen_bound_closed_form (freeze.cpp:52-60). */
+int EPS_FN(frozen_bound_closed_form)(int timestep, int layer_count, double alpha, double* out);
+/* SyntheticNormSource::at_epoch (freeze.cpp:121-152); profile 0 monotone, 1 early-random. */
+int EPS_FN(synthetic_norms)(int profile, uint64_t seed, int layers, int switchover_epoch,
+                            int epoch, double* out);
+/* TraceNormSource (freeze.cpp:62-113). */
+int EPS_FN(trace_norms)(const char* csv_path, int epoch, double* out, int cap, int* layers);
+
+/* ---- autopipe.hpp ----------------------------------------------------- */
+/* load_balance (autopipe.cpp:55-122); criterion 0 normalized-stddev, 1 paper-variance. */
+int EPS_FN(load_balance)(const eps_seq_t* seq, int partitions, double lambda_frozen,
+                         int criterion, eps_plan_t* out);
+/* try_compress (autopipe.cpp:124-158). */
+int EPS_FN(try_compress)(const eps_seq_t* seq, int current_k, double lambda_frozen,
+                         double m_gpu_initial, int criterion, eps_plan_t* out,
+                         int* attempt_k, double* attempt_max_eff, int attempt_cap,
+                         int* n_attempts);
+
+/* ---- schedule.hpp / chunks.hpp ---------------------------------------- */
+/* build_schedule (schedule.cpp:19-199). */
+int EPS_FN(build_schedule)(const eps_stage_load_t* stages, int n_stages, int micro_batches,
+                           double per_pipeline_batch, int integer_microbatches,
+                           int replica_width, int group_spans_nodes, double intra_bandwidth,
+                           double inter_bandwidth, int bytes_per_param,
+                           const eps_cost_model_t* cm, eps_schedule_summary_t* summary,
+                           double* bubble_per_device, eps_block_t* blocks, int block_cap);
+/* schedule_iteration (schedule.cpp:233-253). */
+int EPS_FN(schedule_iteration)(const eps_plan_t* plan, const eps_model_t* model,
+                               const eps_seq_t* seq, int micro_batches,
+                               double per_pipeline_batch, int replica_width,
+                               const eps_cluster_t* cluster, const eps_cost_model_t* cm,
+                               int cache_enabled, double cache_read_seconds_per_sample,
+                               eps_schedule_summary_t* summary);
+/* optimal_chunks (chunks.cpp:5-24); times_out gets 5K+1 makespans. */
+int EPS_FN(optimal_chunks)(const eps_plan_t* plan, const eps_model_t* model,
+                           const eps_seq_t* seq, double per_pipeline_batch, int replica_width,
+                           const eps_cluster_t* cluster, const eps_cost_model_t* cm,
+                           int cache_enabled, double cache_read_seconds_per_sample,
+                           int* chosen, double* times_out, int times_cap);
+
+/* ---- autodp.hpp ------------------------------------------------------- */
+/* Topology (autodp.cpp:11-79). */
+int EPS_FN(topology)(const eps_cluster_t* cluster, int pipeline_length, int* active_ranks,
+                     int cap, int* n_active, int* replica_width);
+/* transition (autodp.cpp:81-111). */
+int EPS_FN(transition)(const eps_cluster_t* cluster, int old_k, int new_k, int epoch,
+                       double lr_schedule_position, int frozen_layers,
+                       const char* weights_version, eps_msg_t* msgs, int cap, int* n);
+/* redistribute (autodp.cpp:113-151): ids holds all shards back to back,
+ * offsets[R+1] delimits them, ranks[R] are the owning active ranks. */
+int EPS_FN(redistribute)(int64_t dataset_size, const eps_cluster_t* cluster,
+                         int pipeline_length, int epoch, uint64_t seed, int* ranks,
+                         int64_t* offsets, int64_t* ids);
+/* ddp_skip_set (autodp.cpp:153-161). */
+int EPS_FN(ddp_skip_set)(const eps_plan_t* plan, const eps_seq_t* seq, int* global_index,
+                         int cap, int* n, int64_t* param_count);
+
+/* ---- autocache.hpp ---------------------------------------------------- */
+int EPS_FN(cache_read_seconds_per_sample)(const eps_model_t* model, int boundary_layer,
+                                          const eps_cache_tiers_t* tiers, double* out);
+/* should_cache (autocache.cpp:31-43). */
+int EPS_FN(should_cache)(int l_frozen, const eps_model_t* model, const eps_cost_model_t* cm,
+                         const eps_cache_tiers_t* tiers, double microbatch_samples,
+                         int* enable, double* read_seconds, double* forward_seconds);
+/* cache_transition (autocache.cpp:45-67). */
+int EPS_FN(cache_transition)(int enabled, int boundary_layer, const eps_cache_tiers_t* tiers,
+                             int old_boundary, int new_boundary, const eps_model_t* model,
+                             const eps_cost_model_t* cm, double* read_s, double* compute_s,
+                             double* write_s);
+
+/* ---- scenario.hpp / runner.hpp ---------------------------------------- */
+int EPS_FN(scenario_load)(const char* path, eps_scenario_t** out);
+int EPS_FN(scenario_parse)(const char* json_text, eps_scenario_t** out);
+void EPS_FN(scenario_destroy)(eps_scenario_t* cfg);
+int EPS_FN(scenario_to_json)(const eps_scenario_t* cfg, char* buf, size_t cap, size_t* len);
+/* simulate_run (runner.cpp:94-305). */
+int EPS_FN(simulate_run)(const eps_scenario_t* cfg, eps_epoch_row_t* rows, int cap,
+                         eps_run_summary_t* summary);
+/* Report writers (runner.cpp:340-418): kind 0 csv, 1 timeline json,
+ * 2 summary json, 3 transitions jsonl. */
+int EPS_FN(simulate_report)(const eps_scenario_t* cfg, int kind, char* buf, size_t cap,
+                            size_t* len);
+/* speedup_breakdown (runner.cpp:307-338): 6 rungs. */
+int EPS_FN(speedup_breakdown)(const eps_scenario_t* cfg, double* total_seconds,
+                              double* avg_throughput, double* speedup);
+int EPS_FN(parse_flags)(const char* list, int* freeze, int* autopipe, int* autodp,
+                        int* autocache);
+
+#ifndef EPS_REFERENCE_BUILD
+/* ---- B200 additions: executor-facing control plane -------------------- */
+
+/* EpochPlanner: runner.cpp's decision order for the real training loop. */
+typedef struct eps_planner eps_planner_t;
+typedef struct {
+  int epoch;
+  int l_frozen;
+  int pipeline_length;
+  int replica_width;
+  int micro_batches;
+  int plan_changed;
+  int cache_enabled;
+  int cache_boundary;
+  int cache_old_boundary;
+  int cache_moved;
+  int n_messages;
+  eps_plan_t plan;
+} eps_epoch_decision_t;
+
+int eps_planner_create(const eps_scenario_t* cfg, eps_planner_t** out);
+void eps_planner_destroy(eps_planner_t* p);
+/* norms_prev: the per-layer norms observed in epoch-1 (length = layers), or
+ * NULL to draw them from the scenario's own grad_norms source. */
+int eps_planner_begin_epoch(eps_planner_t* p, int epoch, const double* norms_prev,
+                            int n_norms, eps_epoch_decision_t* out);
+int eps_scenario_model(const eps_scenario_t* cfg, int64_t* attention_params,
+                       int64_t* mlp_params, int64_t* activation_bytes, int cap_layers,
+                       int* layers, int* bytes_per_param);
+
+/* profile_from_dims for ViT-style frontends (model.hpp additions). */
+int eps_vit_profile(int layers, int64_t hidden, int64_t mlp_dim, int image, int patch,
+                    int channels, int64_t classes, int64_t* attention_params,
+                    int64_t* mlp_params, int64_t* activation_bytes);
+int eps_bert_profile(int layers, int64_t hidden, int64_t mlp_dim, int64_t seq_len,
+                     int64_t position_table, int64_t vocab, int64_t head_params,
+                     int64_t* attention_params, int64_t* mlp_params,
+                     int64_t* activation_bytes);
+/* Integer micro-batch split (schedule.cpp:28-33). */
+int eps_microbatch_sizes(int per_pipeline_batch, int micro_batches, int* sizes);
+/* Real DDP bucket plan (schedule.cpp:137-162 order): per bucket, a list of
+ * (stage, offset, count) slices.  slice_bucket[i] = bucket of slice i. */
+int eps_plan_buckets(const int64_t* stage_params, int n_stages, int bytes_per_param,
+                     double bucket_bytes, int* slice_bucket, int* slice_stage,
+                     int64_t* slice_offset, int64_t* slice_count, int cap, int* n_slices,
+                     int* n_buckets);
+/* Grid coordinate of a global rank under K (replica, stage). */
+int eps_grid_coord(const eps_cluster_t* cluster, int pipeline_length, int global_rank,
+                   int* replica, int* stage);
+
+/* ---- data plane (sm_100a; stream-ordered; device pointers) ------------ */
+/* All kernels: bf16 = uint16 storage of bfloat16.  `stream` is a
+ * cudaStream_t.  No allocation; no host synchronisation.  Returns EPS_ECUDA
+ * on launch failure.  There is no CPU fallback. */
+
+/* GEMM C[M,N] = sum_k A(m,k) B(n,k), bf16 in, fp32 accumulate (tcgen05 +
+ * TMEM + TMA).  a_mn_major: A stored [K][M] (M contiguous) instead of
+ * [M][K]; b_mn_major: B stored [K][N] instead of [N][K].  lda/ldb/ldc in
+ * elements.  epilogue: see EPS_EPI_*.  aux/aux2 per epilogue. */
+enum {
+  EPS_EPI_STORE_BF16 = 0,     /* C = acc                                     */
+  EPS_EPI_BIAS_BF16 = 1,      /* C = acc + bias[n]                           */
+  EPS_EPI_BIAS_GELU_BF16 = 2, /* aux = acc + bias (pre-act), C = gelu(aux)   */
+  EPS_EPI_BIAS_RESID_BF16 = 3,/* C = acc + bias[n] + aux[m,n] (C may == aux) */
+  EPS_EPI_DGELU_BF16 = 4,     /* C = acc * gelu'(aux[m,n]); colsum -> bias   */
+  EPS_EPI_STORE_F32 = 5,      /* Cf32 = acc (beta 0)                         */
+  EPS_EPI_ACCUM_F32 = 6       /* Cf32 += acc (split-K / micro-batch accum)   */
+};
+int eps_gemm_bf16(int a_mn_major, int b_mn_major, int epilogue, const void* A, const void* B,
+                  void* C, const float* bias, void* aux, float* colsum, int64_t M, int64_t N,
+                  int64_t K, int64_t lda, int64_t ldb, int64_t ldc, int split_k, void* stream);
+
+/* LayerNorm over rows of width d (fp32 statistics). */
+int eps_layernorm_fwd(const void* x, const float* gamma, const float* beta, void* y,
+                      float* mean, float* rstd, int64_t rows, int64_t d, float eps,
+                      void* stream);
+/* dx (+)= LN'(dy); dgamma/dbeta accumulate (fp32).  If dres != NULL the
+ * result is dres + LN'(dy) (residual branch fused).  colsum_dx (optional)
+ * accumulates column sums of the produced dx (bias grad of the producer). */
+int eps_layernorm_bwd(const void* dy, const void* x, const float* gamma, const float* mean,
+                      const float* rstd, const void* dres, void* dx, float* dgamma,
+                      float* dbeta, float* colsum_dx, int64_t rows, int64_t d,
+                      float* workspace, void* stream);
+
+/* Multi-head attention on a packed qkv [B*T, 3*H*dh] (q | k | v, head-major
+ * inside each).  out [B*T, H*dh]; lse [B, H, T] fp32. */
+int eps_attn_fwd(const void* qkv, void* out, float* lse, int batch, int tokens, int heads,
+                 int head_dim, float scale, void* stream);
+int eps_attn_bwd(const void* qkv, const void* out, const void* dout, const float* lse,
+                 void* dqkv, float* dbias_qkv, int batch, int tokens, int heads, int head_dim,
+                 float scale, void* stream);
+
+/* Per-layer sum of squares of fp32 gradient tensors (freeze test).  Tensor i
+ * (length n[i]) belongs to segment seg[i]; out[s] = sum over its tensors
+ * (fp64 accumulation, fixed order => deterministic). */
+int eps_grad_sqnorm_segmented(const float* const* tensors, const int64_t* n, const int* seg,
+                              int n_tensors, double* out, int n_segments, void* workspace,
+                              size_t workspace_bytes, void* stream);
+
+/* AutoCache store: rows of row_bytes, keyed by sample id. */
+int eps_cache_gather(const void* store, const int64_t* ids, int n, int64_t row_bytes,
+                     void* dst, void* stream);
+int eps_cache_scatter(void* store, const int64_t* ids, int n, int64_t row_bytes,
+                      const void* src, void* stream);
+
+/* Fused SGD-momentum over an fp32 master copy + bf16 working copy:
+ * v = mu*v + g (+wd*p); p -= lr*v; p_bf16 = bf16(p); g = 0. */
+int eps_sgd_momentum(float* param, uint16_t* param_bf16, float* grad, float* momentum,
+                     int64_t n, float lr, float mu, float weight_decay, void* stream);
+/* Fused AdamW over the same layout (step is 1-based). */
+int eps_adamw(float* param, uint16_t* param_bf16, float* grad, float* m, float* v, int64_t n,
+              float lr, float beta1, float beta2, float eps, float weight_decay, int step,
+              void* stream);
+
+/* ViT frontend / head helpers. */
+int eps_patchify(const float* images, void* patches, int batch, int channels, int image,
+                 int patch, void* stream);
+int eps_vit_assemble(const void* patch_tokens, const float* cls, const float* pos, void* x,
+                     int batch, int tokens, int64_t d, void* stream);
+int eps_vit_assemble_bwd(const void* dx, float* dcls, float* dpos, void* dpatch_tokens,
+                         int batch, int tokens, int64_t d, void* stream);
+/* Softmax cross-entropy over logits [B, C] (bf16): loss_sum += sum_b
+ * -log p(label); dlogits = (p - onehot)/B in bf16. */
+int eps_softmax_xent(const void* logits, const int64_t* labels, void* dlogits, float* loss_sum,
+                     int batch, int classes, void* stream);
+int eps_gather_rows(const void* src, int64_t src_stride_rows, void* dst, int rows, int64_t d,
+                    int64_t offset_rows, void* stream);
+int eps_scatter_rows(const void* src, void* dst, int64_t dst_stride_rows, int rows, int64_t d,
+                     int64_t offset_rows, void* stream);
+int eps_colsum_bf16(const void* x, float* out, int64_t rows, int64_t cols, void* stream);
+#endif /* EPS_REFERENCE_BUILD */
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* EPS_CAPI_H_ */

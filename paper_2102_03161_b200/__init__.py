@@ -1,0 +1,9 @@
+"""B200-native PipeTransformer hot path (arXiv 2102.03161).
+
+The package holds the C-ABI library (libeps_b200.so: eps:: control plane +
+sm_100a kernels), its ctypes binding and the host-side training loop.
+"""
+import os
+
+PKG_DIR = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG_DIR, "libeps_b200.so")
