@@ -34,7 +34,7 @@ $(OBJDIR)/%.o: %.cu $(wildcard $(PKG)/csrc/kernels/*.cuh) include/eps_capi.h
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $@.ptxas.log || (cat $@.ptxas.log; false)
 
 $(LIB): $(CONTROL_OBJ) $(KERNEL_OBJ)
-	$(NVCC) $(ARCH) -shared -Xcompiler -fPIC -o $@ $^ -cudart static -lcuda
+	$(NVCC) $(ARCH) -shared -Xcompiler -fPIC -o $@ $^ -cudart static
 
 # ---- oracle: the reference compiled from its own sources -------------------
 REF       ?= /root/reference/proj

@@ -2,7 +2,7 @@
  * eps_capi.h -- the drop-in C ABI of the B200 PipeTransformer hot path.
  *
  * The reference (arxiv 2102.03161 artifact, /root/reference/proj) exposes a
- * header-only C++ API in namespace `eps` (proj/include/eps/*.hpp).  This file
+ * header-only C++ API in namespace `eps` (proj/include/eps/<module>.hpp).  This file
  * is the flat, FFI-friendly boundary over the same operators plus the sm_100a
  * data plane: plain pointers and sizes, caller-owned buffers, `int` status
  * codes and a thread-local error string.  Each entry cites the reference
@@ -388,10 +388,18 @@ int eps_layernorm_bwd(const void* dy, const void* x, const float* gamma, const f
  * inside each).  out [B*T, H*dh]; lse [B, H, T] fp32. */
 int eps_attn_fwd(const void* qkv, void* out, float* lse, int batch, int tokens, int heads,
                  int head_dim, float scale, void* stream);
-int eps_attn_bwd(const void* qkv, const void* out, const void* dout, const float* lse,
-                 void* dqkv, float* dbias_qkv, int batch, int tokens, int heads, int head_dim,
-                 float scale, void* stream);
+/* dqkv (bf16, same layout as qkv) is fully overwritten; dbias_qkv (fp32
+ * [3*H*dh], optional) accumulates its column sums; dsum_workspace: fp32
+ * [batch*heads*tokens] scratch. */
+int eps_attn_bwd_ws(const void* qkv, const void* out, const void* dout, const float* lse,
+                    void* dqkv, float* dbias_qkv, float* dsum_workspace, int batch, int tokens,
+                    int heads, int head_dim, float scale, void* stream);
 
+/* Flat-arena form: segment s = flat[seg_offsets[s], seg_offsets[s+1]) (host
+ * offsets, <= 64 segments); out: device double[n_segments]; workspace >=
+ * 8 * ceil(total / 65536) bytes. */
+int eps_grad_sqnorm_flat(const float* flat, const int64_t* seg_offsets, int n_segments,
+                         double* out, void* workspace, size_t workspace_bytes, void* stream);
 /* Per-layer sum of squares of fp32 gradient tensors (freeze test).  Tensor i
  * (length n[i]) belongs to segment seg[i]; out[s] = sum over its tensors
  * (fp64 accumulation, fixed order => deterministic). */
@@ -414,7 +422,9 @@ int eps_adamw(float* param, uint16_t* param_bf16, float* grad, float* m, float* 
               float lr, float beta1, float beta2, float eps, float weight_decay, int step,
               void* stream);
 
-/* ViT frontend / head helpers. */
+/* ViT frontend / head helpers.  eps_patchify: `image` = model side, or
+ * (stored side << 16) | model side to nearest-upsample a smaller stored
+ * image (CIFAR-shaped 32x32 -> 224) inside the same pass. */
 int eps_patchify(const float* images, void* patches, int batch, int channels, int image,
                  int patch, void* stream);
 int eps_vit_assemble(const void* patch_tokens, const float* cls, const float* pos, void* x,
@@ -425,11 +435,35 @@ int eps_vit_assemble_bwd(const void* dx, float* dcls, float* dpos, void* dpatch_
  * -log p(label); dlogits = (p - onehot)/B in bf16. */
 int eps_softmax_xent(const void* logits, const int64_t* labels, void* dlogits, float* loss_sum,
                      int batch, int classes, void* stream);
+/* Same with an explicit gradient scale (1/global batch under micro-batching)
+ * plus column sums of dlogits into dbias (fp32 [classes]). */
+int eps_softmax_xent_bias(const void* logits, const int64_t* labels, void* dlogits,
+                          float* loss_sum, float* dbias, int batch, int classes, int ld,
+                          float grad_scale, void* stream);
 int eps_gather_rows(const void* src, int64_t src_stride_rows, void* dst, int rows, int64_t d,
                     int64_t offset_rows, void* stream);
 int eps_scatter_rows(const void* src, void* dst, int64_t dst_stride_rows, int rows, int64_t d,
                      int64_t offset_rows, void* stream);
 int eps_colsum_bf16(const void* x, float* out, int64_t rows, int64_t cols, void* stream);
+
+/* ---- ViT stage executor (csrc/runtime/vit.cu) --------------------------- */
+/* geom = {layers, d, mlp_dim, heads, tokens, classes, image, stored_image,
+ *         patch, channels, max_batch}. */
+typedef struct eps_vit eps_vit_t;
+int eps_vit_layout(const int* geom, int64_t* param_total, int64_t* workspace_bytes,
+                   int64_t* segments, int64_t* tensors);
+int eps_vit_create(const int* geom, float* params, uint16_t* params_bf16, float* grads,
+                   float* momentum, void* workspace, eps_vit_t** out);
+void eps_vit_destroy(eps_vit_t* h);
+int eps_vit_train_step(eps_vit_t* h, const float* images, const int64_t* labels, int batch,
+                       int micro_batches, int l_frozen, int cache_mode, int cache_old,
+                       void* store, const int64_t* ids, float* loss_sum, void* stream);
+int eps_vit_sgd(eps_vit_t* h, int l_frozen, float lr, float momentum, float weight_decay,
+                void* stream);
+int eps_vit_layer_sqnorms(eps_vit_t* h, int l_frozen, double* out, void* stream);
+int eps_vit_forward_logits(eps_vit_t* h, const float* images, int batch, void* logits,
+                           void* stream);
+void* eps_vit_activation(eps_vit_t* h, int which, int layer);
 #endif /* EPS_REFERENCE_BUILD */
 
 #ifdef __cplusplus

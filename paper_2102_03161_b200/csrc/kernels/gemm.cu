@@ -1,0 +1,523 @@
+// Persistent, warp-specialised tcgen05 GEMM for the transformer block
+// contractions (QKV, out-proj, FC1, FC2 and their dgrad / wgrad).
+//
+//   C[M,N] = sum_k A(m,k) * B(n,k)      bf16 operands, fp32 accumulation
+//
+// Operands may be K-major ([rows][K], K contiguous) or MN-major ([K][rows])
+// so one kernel covers forward (A=X, B=W, both K-major), dgrad (B=W read
+// MN-major) and wgrad (A=dY^T, B=X^T, both MN-major, contraction over the
+// token rows) without any transpose copies.
+//
+// Roles (192 threads, one CTA per SM, persistent over output tiles):
+//   warp 0      TMA producer: 128B-swizzled A/B k-blocks into a STAGES ring
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
+//   warps 2..5  epilogue: tcgen05.ld -> fused bias / GELU / dGELU / residual
+//               / column-sum -> swizzled smem -> TMA store (or TMA reduce-add),
+//               double-buffered TMEM accumulators so the epilogue of tile i
+//               overlaps the MMAs of tile i+1.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <mutex>
+
+#include "eps_capi.h"
+#include "ptx.cuh"
+
+namespace eps_k {
+
+constexpr int kBM = 128;
+constexpr int kBK = 64;  // one 128B swizzle atom of bf16 along K
+constexpr int kThreads = 192;
+constexpr int kMnChunk = 64;  // MN extent of one swizzle atom (MN-major operands)
+
+struct GemmArgs {
+  int M, N, K;
+  int tiles_m, tiles_n, splits;
+  int k_blocks_per_split;
+  int epi;
+  void* C;
+  int64_t ldc;
+  const float* bias;
+  void* aux;
+  float* colsum;
+};
+
+template <int BN, int STAGES, bool A_MN, bool B_MN>
+struct GemmCfg {
+  static constexpr int kABytes = kBM * kBK * 2;
+  static constexpr int kBBytes = BN * kBK * 2;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kTmemCols = 2 * BN;  // double-buffered accumulator
+  static constexpr size_t kSmem = size_t(STAGES) * kStageBytes + 4 * 8192 /*epilogue*/ +
+                                  1024 /*align*/ + 256 /*barriers*/;
+  static constexpr uint32_t kIdesc = umma_idesc_bf16(kBM, BN, A_MN, B_MN);
+};
+
+// Byte offset of the UMMA_K=16 slice kk inside one k-block tile.
+template <bool MN>
+__device__ __forceinline__ uint32_t k_slice_offset(int kk) {
+  return MN ? uint32_t(kk) * 16u * 128u  // 16 K-rows of 128 B
+            : uint32_t(kk) * 32u;        // 16 bf16 along the swizzled row
+}
+
+template <bool MN>
+__device__ __forceinline__ uint64_t operand_desc(uint32_t base, int kk) {
+  // K-major: 8-row atoms 1024 B apart (SBO); LBO unused for swizzled K-major.
+  // MN-major: 64-wide MN chunks kBK*128 B apart (LBO), 8-K-row groups 1024 B apart (SBO).
+  return MN ? umma_sdesc(base + k_slice_offset<true>(kk), kBK * 128, 1024)
+            : umma_sdesc(base + k_slice_offset<false>(kk), 16, 1024);
+}
+
+template <int BN, bool MN>
+__device__ __forceinline__ void load_operand(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                             int row0, int k0) {
+  if constexpr (MN) {
+#pragma unroll
+    for (int j = 0; j < BN / kMnChunk; ++j)
+      tma_load_2d(static_cast<char*>(dst) + j * (kBK * 128), map, bar, row0 + j * kMnChunk, k0);
+  } else {
+    tma_load_2d(dst, map, bar, k0, row0);
+  }
+}
+
+// ---- epilogue ----------------------------------------------------------------
+// Each epilogue warp owns one TMEM lane quarter (32 output rows) and walks
+// its tiles in 32-column chunks.  Outputs are staged in a per-warp swizzled
+// smem ring and written with TMA stores (TMA reduce-add for fp32
+// accumulation): fully coalesced, asynchronous global traffic.  Element-wise
+// inputs (residual / GELU pre-activation) stream through a 3-deep TMA ring
+// that runs ahead across tile boundaries, so their latency hides behind the
+// MMAs of the next tile.
+constexpr int kEpiWarps = 4;
+constexpr int kEpiWarpBytes = 8192;
+constexpr int kChunkBf16 = 2048;  // 32x32 bf16
+constexpr int kAuxDepth = 3;
+
+__device__ __forceinline__ bool epi_reads_aux(int epi) {
+  return epi == EPS_EPI_BIAS_RESID_BF16 || epi == EPS_EPI_DGELU_BF16;
+}
+
+__device__ __forceinline__ void stage_bf16(uint32_t base, int lane, const float (&v)[32]) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    st_shared_v4(base + swz64(lane, q), pack_bf16(v[8 * q + 0], v[8 * q + 1]),
+                 pack_bf16(v[8 * q + 2], v[8 * q + 3]), pack_bf16(v[8 * q + 4], v[8 * q + 5]),
+                 pack_bf16(v[8 * q + 6], v[8 * q + 7]));
+}
+
+__device__ __forceinline__ void stage_f32(uint32_t base, int lane, const float (&v)[32]) {
+#pragma unroll
+  for (int q = 0; q < 8; ++q)
+    st_shared_v4(base + swz128(lane, q), __float_as_uint(v[4 * q]), __float_as_uint(v[4 * q + 1]),
+                 __float_as_uint(v[4 * q + 2]), __float_as_uint(v[4 * q + 3]));
+}
+
+__device__ __forceinline__ void read_aux(uint32_t base, int lane, float (&a)[32]) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint4 w = ld_shared_v4(base + swz64(lane, q));
+    a[8 * q + 0] = bf16_lo(w.x);
+    a[8 * q + 1] = bf16_hi(w.x);
+    a[8 * q + 2] = bf16_lo(w.y);
+    a[8 * q + 3] = bf16_hi(w.y);
+    a[8 * q + 4] = bf16_lo(w.z);
+    a[8 * q + 5] = bf16_hi(w.z);
+    a[8 * q + 6] = bf16_lo(w.w);
+    a[8 * q + 7] = bf16_hi(w.w);
+  }
+}
+
+template <int BN, int STAGES, bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
+                   const __grid_constant__ CUtensorMap map_b,
+                   const __grid_constant__ CUtensorMap map_c,
+                   const __grid_constant__ CUtensorMap map_x, const GemmArgs args) {
+  using Cfg = GemmCfg<BN, STAGES, A_MN, B_MN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* ring = smem;
+  uint8_t* epi_area = smem + STAGES * Cfg::kStageBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(epi_area + kEpiWarps * kEpiWarpBytes);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tmem_full = empty + STAGES;
+  uint64_t* tmem_empty = tmem_full + 2;
+  uint64_t* aux_full = tmem_empty + 2;  // [kEpiWarps][kAuxDepth]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aux_full + kAuxDepth * kEpiWarps);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&map_a);
+    tma_prefetch(&map_b);
+    tma_prefetch(&map_c);
+    tma_prefetch(&map_x);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tmem_full[s], 1);
+      mbar_init(&tmem_empty[s], kEpiWarps);
+    }
+    for (int s = 0; s < kAuxDepth * kEpiWarps; ++s) mbar_init(&aux_full[s], 1);
+    mbar_fence_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, Cfg::kTmemCols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int tiles = args.tiles_m * args.tiles_n;
+  const int units = tiles * args.splits;
+  const int kblocks_total = (args.K + kBK - 1) / kBK;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int split = u / tiles;
+        const int t = u - split * tiles;
+        const int m0 = (t / args.tiles_n) * kBM;
+        const int n0 = (t % args.tiles_n) * BN;
+        const int kb0 = split * args.k_blocks_per_split;
+        const int kb1 = min(kb0 + args.k_blocks_per_split, kblocks_total);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = ring + stage * Cfg::kStageBytes;
+          uint8_t* sb = sa + Cfg::kABytes;
+          mbar_expect_tx(&full[stage], Cfg::kStageBytes);
+          load_operand<kBM, A_MN>(sa, &map_a, &full[stage], m0, kb * kBK);
+          load_operand<BN, B_MN>(sb, &map_b, &full[stage], n0, kb * kBK);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        const int split = u / tiles;
+        const int kb0 = split * args.k_blocks_per_split;
+        const int kb1 = min(kb0 + args.k_blocks_per_split, kblocks_total);
+        mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + uint32_t(acc * BN);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_addr(ring + stage * Cfg::kStageBytes);
+          const uint32_t sb = sa + Cfg::kABytes;
+#pragma unroll
+          for (int kk = 0; kk < kBK / 16; ++kk)
+            tc_mma_bf16(d_tmem, operand_desc<A_MN>(sa, kk), operand_desc<B_MN>(sb, kk),
+                        Cfg::kIdesc, (kb > kb0 || kk > 0) ? 1u : 0u);
+          tc_commit(&empty[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        tc_commit(&tmem_full[acc]);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else {
+    const int ew = warp - 2;
+    const int quarter = warp & 3;  // TMEM lane quarter this warp may access
+    uint8_t* my_area = epi_area + ew * kEpiWarpBytes;
+    const uint32_t area_s = smem_addr(my_area);
+    uint64_t* my_aux_bar = aux_full + kAuxDepth * ew;
+    const int epi = args.epi;
+    const bool aux_in = epi_reads_aux(epi);
+    const bool f32_out = epi == EPS_EPI_STORE_F32 || epi == EPS_EPI_ACCUM_F32;
+    // Per-warp 8 KB: [out ring][aux ring].  aux epilogues: 1 x 2 KB out + 3 x 2 KB aux;
+    // GELU (2 outputs) and fp32: 2 x 4 KB out; plain bf16: 4 x 2 KB out.
+    const int out_bytes = (epi == EPS_EPI_BIAS_GELU_BF16 || f32_out) ? 4096 : 2048;
+    const int n_out = aux_in ? 1 : kEpiWarpBytes / out_bytes;
+    const uint32_t aux_s = area_s + kChunkBf16;
+
+    // Prefetch cursor over this warp's flattened (unit, chunk) stream.
+    int pf_u = blockIdx.x, pf_c = 0;
+    uint32_t pf_n = 0, use_n = 0;
+    auto chunks_of = [&](int u) {
+      const int t = u % tiles;
+      const int n0 = (t % args.tiles_n) * BN;
+      return min(BN / 32, (args.N - n0 + 31) / 32);
+    };
+    auto prefetch_until = [&](uint32_t limit) {
+      while (pf_u < units && pf_n < limit) {
+        const int t = pf_u % tiles;
+        const int row = (t / args.tiles_n) * kBM + quarter * 32;
+        const int col = (t % args.tiles_n) * BN + pf_c * 32;
+        const uint32_t slot = pf_n % kAuxDepth;
+        fence_proxy_async_smem();
+        mbar_expect_tx(&my_aux_bar[slot], kChunkBf16);
+        tma_load_2d(my_area + kChunkBf16 * (1 + slot), &map_x, &my_aux_bar[slot], col, row);
+        ++pf_n;
+        if (++pf_c == chunks_of(pf_u)) {
+          pf_c = 0;
+          pf_u += gridDim.x;
+        }
+      }
+    };
+    if (aux_in && lane == 0) prefetch_until(kAuxDepth);
+
+    uint32_t out_n = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      const int split = u / tiles;
+      const int t = u - split * tiles;
+      const int m0 = (t / args.tiles_n) * kBM;
+      const int n0 = (t % args.tiles_n) * BN;
+      const int row0 = m0 + quarter * 32;
+      const int chunks = min(BN / 32, (args.N - n0 + 31) / 32);
+      mbar_wait(&tmem_full[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t taddr = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(acc * BN);
+#pragma unroll 1
+      for (int c = 0; c < chunks; ++c) {
+        const int col0 = n0 + c * 32;
+        const int valid = min(32, args.N - col0);
+        uint32_t raw[32];
+        tmem_ld_32x32(taddr + uint32_t(c * 32), raw);
+        tmem_ld_wait();
+        float v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(raw[j]);
+        float x[32];
+        if (aux_in) {
+          const uint32_t slot = use_n % kAuxDepth;
+          mbar_wait(&my_aux_bar[slot], (use_n / kAuxDepth) & 1);
+          read_aux(aux_s + slot * kChunkBf16, lane, x);
+          ++use_n;
+          __syncwarp();  // every lane has read the slot before it is refilled
+          if (lane == 0) prefetch_until(use_n + kAuxDepth);
+        }
+        if (args.bias != nullptr) {
+          const float4* b4 = reinterpret_cast<const float4*>(args.bias + col0);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const float4 b = (q * 4 < valid) ? __ldg(b4 + q) : make_float4(0.f, 0.f, 0.f, 0.f);
+            v[4 * q] += b.x;
+            v[4 * q + 1] += b.y;
+            v[4 * q + 2] += b.z;
+            v[4 * q + 3] += b.w;
+          }
+        }
+        // reuse an out slot only after its previous TMA store has read it
+        if (lane == 0) {
+          if (n_out == 1) bulk_wait_read<0>();
+          else if (n_out == 2) bulk_wait_read<1>();
+          else bulk_wait_read<3>();
+        }
+        __syncwarp();
+        const uint32_t out_off = (out_n % uint32_t(n_out)) * uint32_t(out_bytes);
+        const uint32_t out_s = area_s + out_off;
+        switch (epi) {
+          case EPS_EPI_BIAS_GELU_BF16:
+            stage_bf16(out_s + kChunkBf16, lane, v);  // pre-activation -> map_x
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = gelu_f(v[j]);
+            stage_bf16(out_s, lane, v);
+            break;
+          case EPS_EPI_BIAS_RESID_BF16:
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] += x[j];
+            stage_bf16(out_s, lane, v);
+            break;
+          case EPS_EPI_DGELU_BF16:
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              v[j] = __bfloat162float(__float2bfloat16_rn(v[j] * gelu_grad_f(x[j])));
+            stage_bf16(out_s, lane, v);
+            break;
+          default:
+            if (f32_out) stage_f32(out_s, lane, v);
+            else stage_bf16(out_s, lane, v);
+            break;
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          if (epi == EPS_EPI_ACCUM_F32) {
+            tma_reduce_add_2d(&map_c, my_area + out_off, col0, row0);
+          } else {
+            tma_store_2d(&map_c, my_area + out_off, col0, row0);
+            if (epi == EPS_EPI_BIAS_GELU_BF16)
+              tma_store_2d(&map_x, my_area + out_off + kChunkBf16, col0, row0);
+          }
+          bulk_commit();
+        }
+        ++out_n;
+        if (epi == EPS_EPI_DGELU_BF16 && args.colsum != nullptr) {
+          // rows past M were zero-filled by TMA, so they contribute 0
+          const float s = warp_transpose_sum32(v);
+          if (lane < valid) atomicAdd(args.colsum + col0 + lane, s);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tmem_empty[acc]);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+    if (lane == 0) bulk_wait<0>();
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, Cfg::kTmemCols);
+  }
+}
+
+// ---- host side -------------------------------------------------------------
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault,
+                                         &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+// 2D tensor map: inner dim `inner` (contiguous), outer dim `outer` with a
+// row pitch of `ld` elements; zero fill for out-of-bounds boxes.
+bool make_map(CUtensorMap* map, const void* base, bool f32, int64_t inner, int64_t outer,
+              int64_t ld, int box_inner, int box_outer, CUtensorMapSwizzle swz) {
+  EncodeTiledFn fn = encode_fn();
+  if (fn == nullptr) return false;
+  const int esize = f32 ? 4 : 2;
+  const cuuint64_t dims[2] = {cuuint64_t(inner), cuuint64_t(outer)};
+  const cuuint64_t strides[1] = {cuuint64_t(ld) * esize};
+  const cuuint32_t box[2] = {cuuint32_t(box_inner), cuuint32_t(box_outer)};
+  const cuuint32_t estr[2] = {1u, 1u};
+  return fn(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+            const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int sm_count() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <int BN, int STAGES, bool A_MN, bool B_MN>
+int launch(const void* A, const void* B, int64_t lda, int64_t ldb, GemmArgs args,
+           cudaStream_t stream) {
+  using Cfg = GemmCfg<BN, STAGES, A_MN, B_MN>;
+  auto kern = gemm_tc_kernel<BN, STAGES, A_MN, B_MN>;
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(Cfg::kSmem)) != cudaSuccess)
+      return EPS_ECUDA;
+    configured = true;
+  }
+  CUtensorMap ma, mb, mc, mx;
+  const auto SW128 = CU_TENSOR_MAP_SWIZZLE_128B;
+  const auto SW64 = CU_TENSOR_MAP_SWIZZLE_64B;
+  // A(m,k): K-major -> [M][K]; MN-major -> [K][M].  Likewise B(n,k).
+  const bool ok_a = A_MN ? make_map(&ma, A, false, args.M, args.K, lda, 64, kBK, SW128)
+                         : make_map(&ma, A, false, args.K, args.M, lda, 64, kBM, SW128);
+  const bool ok_b = B_MN ? make_map(&mb, B, false, args.N, args.K, ldb, 64, kBK, SW128)
+                         : make_map(&mb, B, false, args.K, args.N, ldb, 64, BN, SW128);
+  const bool f32 = args.epi == EPS_EPI_STORE_F32 || args.epi == EPS_EPI_ACCUM_F32;
+  const bool ok_c = make_map(&mc, args.C, f32, args.N, args.M, args.ldc, 32, 32, f32 ? SW128 : SW64);
+  // aux: GELU pre-activation output, or residual / pre-activation input.
+  const void* xptr = args.aux != nullptr ? args.aux : args.C;
+  const bool ok_x = make_map(&mx, xptr, false, args.N, args.M, args.ldc, 32, 32, SW64);
+  if (!ok_a || !ok_b || !ok_c || !ok_x) return EPS_ECUDA;
+  const int units = args.tiles_m * args.tiles_n * args.splits;
+  const int grid = units < sm_count() ? units : sm_count();
+  kern<<<grid, kThreads, Cfg::kSmem, stream>>>(ma, mb, mc, mx, args);
+  return cudaGetLastError() == cudaSuccess ? EPS_OK : EPS_ECUDA;
+}
+
+}  // namespace eps_k
+
+extern "C" int eps_gemm_bf16(int a_mn_major, int b_mn_major, int epilogue, const void* A,
+                             const void* B, void* C, const float* bias, void* aux,
+                             float* colsum, int64_t M, int64_t N, int64_t K, int64_t lda,
+                             int64_t ldb, int64_t ldc, int split_k, void* stream) {
+  using namespace eps_k;
+  if (M <= 0 || N <= 0 || K <= 0 || N % 8 != 0 || lda % 8 != 0 || ldb % 8 != 0 ||
+      ldc % 8 != 0 || M > (int64_t(1) << 31) || epilogue < 0 || epilogue > EPS_EPI_ACCUM_F32)
+    return EPS_EINVAL;
+  if (split_k < 1) split_k = 1;
+  const bool needs_aux = epilogue == EPS_EPI_BIAS_GELU_BF16 || epilogue == EPS_EPI_BIAS_RESID_BF16 ||
+                         epilogue == EPS_EPI_DGELU_BF16;
+  if (needs_aux && aux == nullptr) return EPS_EINVAL;
+  if ((epilogue == EPS_EPI_BIAS_BF16 || epilogue == EPS_EPI_BIAS_GELU_BF16 ||
+       epilogue == EPS_EPI_BIAS_RESID_BF16) && bias == nullptr)
+    return EPS_EINVAL;
+  if (split_k > 1 && epilogue != EPS_EPI_ACCUM_F32) return EPS_EINVAL;
+  GemmArgs args{};
+  args.M = int(M);
+  args.N = int(N);
+  args.K = int(K);
+  args.epi = epilogue;
+  args.C = C;
+  args.ldc = ldc;
+  args.bias = (epilogue == EPS_EPI_BIAS_BF16 || epilogue == EPS_EPI_BIAS_GELU_BF16 ||
+               epilogue == EPS_EPI_BIAS_RESID_BF16) ? bias : nullptr;
+  args.aux = aux;
+  args.colsum = colsum;
+  const int kblocks = int((K + kBK - 1) / kBK);
+  if (split_k > kblocks) split_k = kblocks;
+  args.k_blocks_per_split = (kblocks + split_k - 1) / split_k;
+  args.splits = (kblocks + args.k_blocks_per_split - 1) / args.k_blocks_per_split;
+  args.tiles_m = int((M + kBM - 1) / kBM);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // BN = 256 when N fills it; 128 otherwise (fewer wasted MMA columns).
+  const bool wide = N % 256 == 0 || N >= 1024;
+  const int bn = wide ? 256 : 128;
+  args.tiles_n = int((N + bn - 1) / bn);
+  const int key = (a_mn_major ? 2 : 0) | (b_mn_major ? 1 : 0);
+  if (wide) {
+    switch (key) {
+      case 0: return launch<256, 4, false, false>(A, B, lda, ldb, args, st);
+      case 1: return launch<256, 4, false, true>(A, B, lda, ldb, args, st);
+      case 2: return launch<256, 4, true, false>(A, B, lda, ldb, args, st);
+      default: return launch<256, 4, true, true>(A, B, lda, ldb, args, st);
+    }
+  }
+  switch (key) {
+    case 0: return launch<128, 6, false, false>(A, B, lda, ldb, args, st);
+    case 1: return launch<128, 6, false, true>(A, B, lda, ldb, args, st);
+    case 2: return launch<128, 6, true, false>(A, B, lda, ldb, args, st);
+    default: return launch<128, 6, true, true>(A, B, lda, ldb, args, st);
+  }
+}

@@ -1,0 +1,519 @@
+// ViT training executor: the B200 realisation of the reference's modeled
+// F / B / U blocks (schedule.cpp:40-52, 184-193) for a stage that runs the
+// whole stack (K = 1) or a span of ATT/MLP sublayers (pipeline stages).
+//
+// Host C++ that launches the sm_100a kernels in this library; all memory is
+// caller-owned (a parameter arena and an activation workspace sized by
+// eps_vit_layout / eps_vit_workspace_bytes).  Freeze semantics follow the
+// reference's partition of the stack (model.cpp:79-92):
+//   * layers [0, L_frozen) are frozen: forward only, no stash needed, no
+//     backward, no optimizer update;
+//   * with AutoCache the frozen prefix is not run at all: the boundary
+//     activation X[L_frozen] is gathered from the HBM store by sample id;
+//     on a boundary move the delta [old, new) is forwarded once and the new
+//     boundary scattered back (autocache.cpp:45-67);
+//   * the lowest trainable layer skips its input-gradient write.
+// Parameter arena order = the reference's ModelSpec order, so each layer's
+// tensors are one contiguous segment (embed folded into layer 0, final LN +
+// head into layer L-1, model.cpp:137-142) -- the freeze test reduces those
+// segments and the optimizer walks one contiguous tail [layer L_f, end).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <new>
+#include <stdexcept>
+#include <vector>
+
+#include "eps_capi.h"
+
+namespace {
+
+struct Slot {
+  int64_t off = 0;
+  int64_t n = 0;
+};
+
+struct LayerSlots {
+  Slot ln1g, ln1b, wqkv, bqkv, wp, bp;  // ATT sublayer
+  Slot ln2g, ln2b, w1, b1, w2, b2;      // MLP sublayer
+};
+
+struct Geometry {
+  int layers, d, f, heads, tokens, classes, image, in_image, patch, channels, max_batch;
+  int classes_pad;  // head rows padded to a multiple of 8 (16 B TMA row pitch)
+  int patches() const { return (image / patch) * (image / patch); }
+  int patch_len() const { return channels * patch * patch; }
+  int head_dim() const { return d / heads; }
+};
+
+constexpr int64_t kAlign = 64;  // elements: 256 B for fp32, 128 B for bf16
+
+struct Layout {
+  Slot wpe, bpe, cls, pos;
+  std::vector<LayerSlots> layer;
+  Slot lnfg, lnfb, wh, bh;
+  std::vector<int64_t> seg;  // L+1 segment boundaries (freeze test / optimizer)
+  int64_t total = 0;
+
+  explicit Layout(const Geometry& g) {
+    int64_t at = 0;
+    auto take = [&](int64_t n) {
+      Slot s{at, n};
+      at += (n + kAlign - 1) / kAlign * kAlign;
+      return s;
+    };
+    const int64_t d = g.d, f = g.f;
+    seg.push_back(0);
+    wpe = take(d * g.patch_len());
+    bpe = take(d);
+    cls = take(d);
+    pos = take(int64_t(g.tokens) * d);
+    layer.resize(g.layers);
+    for (int l = 0; l < g.layers; ++l) {
+      if (l > 0) seg.push_back(at);
+      LayerSlots& s = layer[l];
+      s.ln1g = take(d);
+      s.ln1b = take(d);
+      s.wqkv = take(3 * d * d);
+      s.bqkv = take(3 * d);
+      s.wp = take(d * d);
+      s.bp = take(d);
+      s.ln2g = take(d);
+      s.ln2b = take(d);
+      s.w1 = take(f * d);
+      s.b1 = take(f);
+      s.w2 = take(d * f);
+      s.b2 = take(d);
+    }
+    lnfg = take(d);
+    lnfb = take(d);
+    wh = take(int64_t(g.classes_pad) * d);
+    bh = take(g.classes_pad);
+    total = at;
+    seg.push_back(total);
+  }
+};
+
+// Activation workspace carve (all [rows, width] bf16 unless noted).
+struct Acts {
+  std::vector<uint16_t*> X, H1, QKV, A, X1, H2, U, G;
+  std::vector<float*> mean1, rstd1, mean2, rstd2, lse;
+  uint16_t *patches = nullptr, *ptok = nullptr, *cls_rows = nullptr, *hf = nullptr,
+           *logits = nullptr, *dlogits = nullptr, *dhf = nullptr, *dcls = nullptr;
+  float *meanf = nullptr, *rstdf = nullptr;
+  uint16_t *dX = nullptr, *dH = nullptr, *dA = nullptr, *dQKV = nullptr, *dptok = nullptr;
+  float* dsum = nullptr;
+  double* sq_ws = nullptr;
+  size_t sq_ws_bytes = 0;
+  size_t bytes = 0;
+
+  Acts(const Geometry& g, int64_t param_total, uint8_t* base) {
+    const int64_t R = int64_t(g.max_batch) * g.tokens, d = g.d, f = g.f, L = g.layers;
+    const int64_t B = g.max_batch, BP = B * g.patches();
+    size_t at = 0;
+    auto take = [&](size_t bytes) {
+      uint8_t* p = base ? base + at : nullptr;
+      at += (bytes + 255) / 256 * 256;
+      return p;
+    };
+    auto bf = [&](int64_t n) { return reinterpret_cast<uint16_t*>(take(size_t(n) * 2)); };
+    auto fp = [&](int64_t n) { return reinterpret_cast<float*>(take(size_t(n) * 4)); };
+    for (int64_t l = 0; l <= L; ++l) X.push_back(bf(R * d));
+    for (int64_t l = 0; l < L; ++l) {
+      H1.push_back(bf(R * d));
+      QKV.push_back(bf(R * 3 * d));
+      A.push_back(bf(R * d));
+      X1.push_back(bf(R * d));
+      H2.push_back(bf(R * d));
+      U.push_back(bf(R * f));
+      G.push_back(bf(R * f));
+      mean1.push_back(fp(R));
+      rstd1.push_back(fp(R));
+      mean2.push_back(fp(R));
+      rstd2.push_back(fp(R));
+      lse.push_back(fp(B * g.heads * g.tokens));
+    }
+    patches = bf(BP * g.patch_len());
+    ptok = bf(BP * d);
+    cls_rows = bf(B * d);
+    hf = bf(B * d);
+    logits = bf(B * g.classes_pad);
+    dlogits = bf(B * g.classes_pad);
+    dhf = bf(B * d);
+    dcls = bf(B * d);
+    meanf = fp(B);
+    rstdf = fp(B);
+    dX = bf(R * d);
+    dH = bf(R * d);
+    dA = bf(R * d);
+    dQKV = bf(R * 3 * d);
+    dptok = bf(BP * d);
+    dsum = fp(B * g.heads * g.tokens);
+    sq_ws_bytes = size_t((param_total + 65535) / 65536 + 64) * 8;
+    sq_ws = reinterpret_cast<double*>(take(sq_ws_bytes));
+    bytes = at;
+  }
+};
+
+int check(int rc) {
+  if (rc != EPS_OK) throw rc;
+  return rc;
+}
+
+}  // namespace
+
+struct eps_vit {
+  Geometry g;
+  Layout lay;
+  Acts act;
+  float* p32;
+  uint16_t* p16;
+  float* g32;
+  float* mom;
+  float* loss_sum;  // device scalar owned by caller
+  eps_vit(const Geometry& geom, float* p, uint16_t* pb, float* gr, float* m, uint8_t* ws)
+      : g(geom), lay(geom), act(geom, lay.total, ws), p32(p), p16(pb), g32(gr), mom(m),
+        loss_sum(nullptr) {}
+
+  const uint16_t* W(const Slot& s) const { return p16 + s.off; }
+  const float* P(const Slot& s) const { return p32 + s.off; }
+  float* Gr(const Slot& s) const { return g32 + s.off; }
+
+  int split_for(int64_t rows) const {
+    // wgrad contracts over the token rows; split so the grid covers the SMs
+    return rows >= 16384 ? 8 : rows >= 4096 ? 4 : 1;
+  }
+
+  // ---- forward sublayers on rows [r0, r0+R) / samples [b0, b0+b) -----------
+  void embed_fwd(const float* images, int b0, int b, cudaStream_t st) {
+    const int64_t d = g.d, np = g.patches(), pl = g.patch_len();
+    uint16_t* patches = act.patches + int64_t(b0) * np * pl;
+    uint16_t* ptok = act.ptok + int64_t(b0) * np * d;
+    const int img_arg = (g.in_image != g.image) ? ((g.in_image << 16) | g.image) : g.image;
+    check(eps_patchify(images + int64_t(b0) * g.channels * g.in_image * g.in_image, patches, b,
+                       g.channels, img_arg, g.patch, st));
+    check(eps_gemm_bf16(0, 0, EPS_EPI_BIAS_BF16, patches, W(lay.wpe), ptok, P(lay.bpe), nullptr,
+                        nullptr, b * np, d, pl, pl, pl, d, 1, st));
+    check(eps_vit_assemble(ptok, P(lay.cls), P(lay.pos), act.X[0] + int64_t(b0) * g.tokens * d,
+                           b, g.tokens, d, st));
+  }
+
+  void att_fwd(int l, int b0, int b, cudaStream_t st) {
+    const LayerSlots& s = lay.layer[l];
+    const int64_t d = g.d, r0 = int64_t(b0) * g.tokens, R = int64_t(b) * g.tokens;
+    check(eps_layernorm_fwd(act.X[l] + r0 * d, P(s.ln1g), P(s.ln1b), act.H1[l] + r0 * d,
+                            act.mean1[l] + r0, act.rstd1[l] + r0, R, d, 1e-6f, st));
+    check(eps_gemm_bf16(0, 0, EPS_EPI_BIAS_BF16, act.H1[l] + r0 * d, W(s.wqkv),
+                        act.QKV[l] + r0 * 3 * d, P(s.bqkv), nullptr, nullptr, R, 3 * d, d, d, d,
+                        3 * d, 1, st));
+    check(eps_attn_fwd(act.QKV[l] + r0 * 3 * d, act.A[l] + r0 * d,
+                       act.lse[l] + int64_t(b0) * g.heads * g.tokens, b, g.tokens, g.heads,
+                       g.head_dim(), 1.0f / std::sqrt(float(g.head_dim())), st));
+    check(eps_gemm_bf16(0, 0, EPS_EPI_BIAS_RESID_BF16, act.A[l] + r0 * d, W(s.wp),
+                        act.X1[l] + r0 * d, P(s.bp), act.X[l] + r0 * d, nullptr, R, d, d, d, d,
+                        d, 1, st));
+  }
+
+  void mlp_fwd(int l, int b0, int b, cudaStream_t st) {
+    const LayerSlots& s = lay.layer[l];
+    const int64_t d = g.d, f = g.f, r0 = int64_t(b0) * g.tokens, R = int64_t(b) * g.tokens;
+    check(eps_layernorm_fwd(act.X1[l] + r0 * d, P(s.ln2g), P(s.ln2b), act.H2[l] + r0 * d,
+                            act.mean2[l] + r0, act.rstd2[l] + r0, R, d, 1e-6f, st));
+    check(eps_gemm_bf16(0, 0, EPS_EPI_BIAS_GELU_BF16, act.H2[l] + r0 * d, W(s.w1),
+                        act.G[l] + r0 * f, P(s.b1), act.U[l] + r0 * f, nullptr, R, f, d, d, d, f,
+                        1, st));
+    check(eps_gemm_bf16(0, 0, EPS_EPI_BIAS_RESID_BF16, act.G[l] + r0 * f, W(s.w2),
+                        act.X[l + 1] + r0 * d, P(s.b2), act.X1[l] + r0 * d, nullptr, R, d, f, f,
+                        f, d, 1, st));
+  }
+
+  // Head forward + loss + head backward; leaves dL/dX[L] in act.dX rows.
+  void head_fwd_bwd(const int64_t* labels, int b0, int b, int global_batch, cudaStream_t st) {
+    const int64_t d = g.d, C = g.classes_pad, T = g.tokens;
+    const LayerSlots& top = lay.layer[g.layers - 1];
+    uint16_t* cls = act.cls_rows + int64_t(b0) * d;
+    uint16_t* hf = act.hf + int64_t(b0) * d;
+    uint16_t* logits = act.logits + int64_t(b0) * C;
+    uint16_t* dlogits = act.dlogits + int64_t(b0) * C;
+    uint16_t* dhf = act.dhf + int64_t(b0) * d;
+    uint16_t* dcls = act.dcls + int64_t(b0) * d;
+    check(eps_gather_rows(act.X[g.layers] + int64_t(b0) * T * d, T * d, cls, b, d, 0, st));
+    check(eps_layernorm_fwd(cls, P(lay.lnfg), P(lay.lnfb), hf, act.meanf + b0, act.rstdf + b0, b,
+                            d, 1e-6f, st));
+    check(eps_gemm_bf16(0, 0, EPS_EPI_BIAS_BF16, hf, W(lay.wh), logits, P(lay.bh), nullptr,
+                        nullptr, b, C, d, d, d, C, 1, st));
+    check(eps_softmax_xent_bias(logits, labels + b0, dlogits, loss_sum, Gr(lay.bh), b, g.classes,
+                                int(C), 1.0f / float(global_batch), st));
+    check(eps_gemm_bf16(1, 1, EPS_EPI_ACCUM_F32, dlogits, hf, Gr(lay.wh), nullptr, nullptr,
+                        nullptr, C, d, b, C, d, d, 1, st));
+    check(eps_gemm_bf16(0, 1, EPS_EPI_STORE_BF16, dlogits, W(lay.wh), dhf, nullptr, nullptr,
+                        nullptr, b, d, C, C, d, d, 1, st));
+    // LN_f backward on the CLS rows; its dx column sum is top-layer FC2's bias grad
+    check(eps_layernorm_bwd(dhf, cls, P(lay.lnfg), act.meanf + b0, act.rstdf + b0, nullptr, dcls,
+                            Gr(lay.lnfg), Gr(lay.lnfb), Gr(top.b2), b, d, nullptr, st));
+    uint16_t* dX = act.dX + int64_t(b0) * T * d;
+    if (cudaMemsetAsync(dX, 0, size_t(b) * T * d * 2, st) != cudaSuccess) throw int(EPS_ECUDA);
+    check(eps_scatter_rows(dcls, dX, T * d, b, d, 0, st));
+  }
+
+  // ---- backward sublayers (dX holds dL/d(output) rows; updated in place) ----
+  void mlp_bwd(int l, int b0, int b, cudaStream_t st) {
+    const LayerSlots& s = lay.layer[l];
+    const int64_t d = g.d, f = g.f, r0 = int64_t(b0) * g.tokens, R = int64_t(b) * g.tokens;
+    uint16_t* dX = act.dX + r0 * d;
+    uint16_t* Gm = act.G[l] + r0 * f;
+    const int split = split_for(R);
+    check(eps_gemm_bf16(1, 1, EPS_EPI_ACCUM_F32, dX, Gm, Gr(s.w2), nullptr, nullptr, nullptr, d,
+                        f, R, d, f, f, split, st));
+    // du overwrites G (its last reader was the dW2 GEMM above)
+    check(eps_gemm_bf16(0, 1, EPS_EPI_DGELU_BF16, dX, W(s.w2), Gm, nullptr, act.U[l] + r0 * f,
+                        Gr(s.b1), R, f, d, d, f, f, 1, st));
+    check(eps_gemm_bf16(1, 1, EPS_EPI_ACCUM_F32, Gm, act.H2[l] + r0 * d, Gr(s.w1), nullptr,
+                        nullptr, nullptr, f, d, R, f, d, d, split, st));
+    check(eps_gemm_bf16(0, 1, EPS_EPI_STORE_BF16, Gm, W(s.w1), act.dH + r0 * d, nullptr, nullptr,
+                        nullptr, R, d, f, f, d, d, 1, st));
+    check(eps_layernorm_bwd(act.dH + r0 * d, act.X1[l] + r0 * d, P(s.ln2g), act.mean2[l] + r0,
+                            act.rstd2[l] + r0, dX, dX, Gr(s.ln2g), Gr(s.ln2b), Gr(s.bp), R, d,
+                            nullptr, st));
+  }
+
+  // need_dx: write dL/dX[l] (false for the lowest trainable layer when the
+  // layers below are frozen).  colsum_prev: bias grad of the sublayer that
+  // produced X[l] (FC2 of layer l-1), or null.
+  void att_bwd(int l, int b0, int b, bool need_dx, float* colsum_prev, cudaStream_t st) {
+    const LayerSlots& s = lay.layer[l];
+    const int64_t d = g.d, r0 = int64_t(b0) * g.tokens, R = int64_t(b) * g.tokens;
+    uint16_t* dX = act.dX + r0 * d;
+    const int split = split_for(R);
+    check(eps_gemm_bf16(1, 1, EPS_EPI_ACCUM_F32, dX, act.A[l] + r0 * d, Gr(s.wp), nullptr,
+                        nullptr, nullptr, d, d, R, d, d, d, split, st));
+    check(eps_gemm_bf16(0, 1, EPS_EPI_STORE_BF16, dX, W(s.wp), act.dA + r0 * d, nullptr, nullptr,
+                        nullptr, R, d, d, d, d, d, 1, st));
+    check(eps_attn_bwd_ws(act.QKV[l] + r0 * 3 * d, act.A[l] + r0 * d, act.dA + r0 * d,
+                          act.lse[l] + int64_t(b0) * g.heads * g.tokens, act.dQKV + r0 * 3 * d,
+                          Gr(s.bqkv), act.dsum + int64_t(b0) * g.heads * g.tokens, b, g.tokens,
+                          g.heads, g.head_dim(), 1.0f / std::sqrt(float(g.head_dim())), st));
+    check(eps_gemm_bf16(1, 1, EPS_EPI_ACCUM_F32, act.dQKV + r0 * 3 * d, act.H1[l] + r0 * d,
+                        Gr(s.wqkv), nullptr, nullptr, nullptr, 3 * d, d, R, 3 * d, d, d, split, st));
+    check(eps_gemm_bf16(0, 1, EPS_EPI_STORE_BF16, act.dQKV + r0 * 3 * d, W(s.wqkv),
+                        act.dH + r0 * d, nullptr, nullptr, nullptr, R, d, 3 * d, 3 * d, d, d, 1,
+                        st));
+    check(eps_layernorm_bwd(act.dH + r0 * d, act.X[l] + r0 * d, P(s.ln1g), act.mean1[l] + r0,
+                            act.rstd1[l] + r0, dX, need_dx ? dX : nullptr, Gr(s.ln1g), Gr(s.ln1b),
+                            need_dx ? colsum_prev : nullptr, R, d, nullptr, st));
+  }
+
+  void embed_bwd(int b0, int b, cudaStream_t st) {
+    const int64_t d = g.d, np = g.patches(), pl = g.patch_len();
+    uint16_t* dptok = act.dptok + int64_t(b0) * np * d;
+    check(eps_vit_assemble_bwd(act.dX + int64_t(b0) * g.tokens * d, Gr(lay.cls), Gr(lay.pos),
+                               dptok, b, g.tokens, d, st));
+    check(eps_colsum_bf16(dptok, Gr(lay.bpe), int64_t(b) * np, d, st));
+    check(eps_gemm_bf16(1, 1, EPS_EPI_ACCUM_F32, dptok, act.patches + int64_t(b0) * np * pl,
+                        Gr(lay.wpe), nullptr, nullptr, nullptr, d, pl, int64_t(b) * np, d, pl, pl,
+                        split_for(int64_t(b) * np), st));
+  }
+};
+
+namespace {
+
+Geometry make_geom(const int* gi) {
+  Geometry g{};
+  g.layers = gi[0];
+  g.d = gi[1];
+  g.f = gi[2];
+  g.heads = gi[3];
+  g.tokens = gi[4];
+  g.classes = gi[5];
+  g.image = gi[6];
+  g.in_image = gi[7];
+  g.patch = gi[8];
+  g.channels = gi[9];
+  g.max_batch = gi[10];
+  g.classes_pad = (g.classes + 7) / 8 * 8;
+  if (g.layers < 1 || g.d % g.heads != 0 || g.tokens != g.patches() + 1 || g.max_batch < 1 ||
+      g.classes < 1 || (g.d % 256 != 0 && g.d != 128))
+    throw std::invalid_argument("vit geometry");
+  return g;
+}
+
+template <typename F>
+int guard(F&& f) {
+  try {
+    f();
+    return EPS_OK;
+  } catch (int rc) {
+    return rc;
+  } catch (const std::bad_alloc&) {
+    return EPS_ECAPACITY;
+  } catch (...) {
+    return EPS_EINVAL;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+// geom: {layers, d, mlp_dim, heads, tokens, classes, image, stored_image,
+//        patch, channels, max_batch}.
+// Outputs: param_total (elements of each fp32 / bf16 arena), workspace
+// bytes, the L+1 layer segment offsets, and (optional) per-tensor offsets in
+// the order: wpe bpe cls pos, per layer ln1g ln1b wqkv bqkv wp bp ln2g ln2b
+// w1 b1 w2 b2, then lnfg lnfb wh bh  -> 4 + 12 L + 4 (offset, numel) pairs.
+int eps_vit_layout(const int* geom, int64_t* param_total, int64_t* workspace_bytes,
+                   int64_t* segments, int64_t* tensors) {
+  return guard([&] {
+    const Geometry g = make_geom(geom);
+    const Layout lay(g);
+    const Acts act(g, lay.total, nullptr);
+    *param_total = lay.total;
+    *workspace_bytes = int64_t(act.bytes);
+    if (segments)
+      for (size_t i = 0; i < lay.seg.size(); ++i) segments[i] = lay.seg[i];
+    if (tensors) {
+      int k = 0;
+      auto put = [&](const Slot& s) {
+        tensors[k++] = s.off;
+        tensors[k++] = s.n;
+      };
+      put(lay.wpe), put(lay.bpe), put(lay.cls), put(lay.pos);
+      for (const LayerSlots& s : lay.layer) {
+        put(s.ln1g), put(s.ln1b), put(s.wqkv), put(s.bqkv), put(s.wp), put(s.bp);
+        put(s.ln2g), put(s.ln2b), put(s.w1), put(s.b1), put(s.w2), put(s.b2);
+      }
+      put(lay.lnfg), put(lay.lnfb), put(lay.wh), put(lay.bh);
+    }
+  });
+}
+
+int eps_vit_create(const int* geom, float* params, uint16_t* params_bf16, float* grads,
+                   float* momentum, void* workspace, eps_vit** out) {
+  return guard([&] {
+    *out = new eps_vit(make_geom(geom), params, params_bf16, grads, momentum,
+                       static_cast<uint8_t*>(workspace));
+  });
+}
+
+void eps_vit_destroy(eps_vit* h) { delete h; }
+
+// One training iteration on a single stage holding the whole stack (K = 1):
+// GPipe over `micro_batches` slices of the batch (forward of every slice,
+// then backward of every slice in reverse, grads accumulating in fp32).
+//   cache_mode 0: no cache -- frozen prefix [0, L_f) recomputed forward-only;
+//   cache_mode 1: X[L_f] gathered from `store` rows `ids` (prefix skipped);
+//   cache_mode 2: boundary move old -> L_f: X[old] gathered (old > 0) or
+//                 computed from the images, [old, L_f) forwarded once, X[L_f]
+//                 scattered into the store.
+// loss_sum (device fp32) accumulates the summed per-sample loss.
+int eps_vit_train_step(eps_vit* h, const float* images, const int64_t* labels, int batch,
+                       int micro_batches, int l_frozen, int cache_mode, int cache_old,
+                       void* store, const int64_t* ids, float* loss_sum, void* stream) {
+  return guard([&] {
+    if (h == nullptr || batch < 1 || batch > h->g.max_batch || micro_batches < 1 ||
+        micro_batches > batch || l_frozen < 0 || l_frozen >= h->g.layers)
+      throw int(EPS_EINVAL);
+    if (cache_mode != 0 && (store == nullptr || ids == nullptr || l_frozen == 0))
+      throw int(EPS_EINVAL);
+    auto st = static_cast<cudaStream_t>(stream);
+    h->loss_sum = loss_sum;
+    const int L = h->g.layers;
+    const int64_t row_bytes = int64_t(h->g.tokens) * h->g.d * 2;
+    std::vector<int> b0s, bs;
+    for (int m = 0, at = 0; m < micro_batches; ++m) {
+      const int n = batch / micro_batches + (m < batch % micro_batches ? 1 : 0);
+      b0s.push_back(at);
+      bs.push_back(n);
+      at += n;
+    }
+    for (int m = 0; m < micro_batches; ++m) {
+      const int b0 = b0s[m], b = bs[m];
+      const int64_t xoff = int64_t(b0) * h->g.tokens * h->g.d;
+      int start = 0;  // first layer to run forward
+      if (cache_mode == 1) {
+        check(eps_cache_gather(store, ids + b0, b, row_bytes, h->act.X[l_frozen] + xoff, st));
+        start = l_frozen;
+      } else if (cache_mode == 2 && cache_old > 0) {
+        check(eps_cache_gather(store, ids + b0, b, row_bytes, h->act.X[cache_old] + xoff, st));
+        start = cache_old;
+      }
+      if (start == 0) h->embed_fwd(images, b0, b, st);
+      for (int l = start; l < L; ++l) {
+        if (cache_mode == 2 && l == l_frozen)
+          check(eps_cache_scatter(store, ids + b0, b, row_bytes, h->act.X[l] + xoff, st));
+        h->att_fwd(l, b0, b, st);
+        h->mlp_fwd(l, b0, b, st);
+      }
+      h->head_fwd_bwd(labels, b0, b, batch, st);
+    }
+    for (int m = micro_batches - 1; m >= 0; --m) {
+      const int b0 = b0s[m], b = bs[m];
+      // head_fwd_bwd left dL/dX[L] for slice m in dX; later slices' backward
+      // must not clobber it, so slices are processed as forward-all /
+      // backward-all only when their dX rows are disjoint (they are: rows
+      // are indexed by sample).
+      for (int l = L - 1; l >= l_frozen; --l) {
+        h->mlp_bwd(l, b0, b, st);
+        const bool need_dx = l > l_frozen || l == 0;
+        h->att_bwd(l, b0, b, need_dx, l > 0 ? h->Gr(h->lay.layer[l - 1].b2) : nullptr, st);
+      }
+      if (l_frozen == 0) h->embed_bwd(b0, b, st);
+    }
+  });
+}
+
+// Fused SGD-momentum over the trainable tail [segment L_f, end).
+int eps_vit_sgd(eps_vit* h, int l_frozen, float lr, float momentum, float weight_decay,
+                void* stream) {
+  return guard([&] {
+    const int64_t begin = h->lay.seg[l_frozen];
+    check(eps_sgd_momentum(h->p32 + begin, h->p16 + begin, h->g32 + begin, h->mom + begin,
+                           h->lay.total - begin, lr, momentum, weight_decay, stream));
+  });
+}
+
+// Per-layer gradient sum of squares (freeze test input) for layers
+// [l_frozen, L) into out[l] (device double[L]); frozen layers are zeroed.
+int eps_vit_layer_sqnorms(eps_vit* h, int l_frozen, double* out, void* stream) {
+  return guard([&] {
+    const int L = h->g.layers;
+    auto st = static_cast<cudaStream_t>(stream);
+    if (l_frozen > 0 && cudaMemsetAsync(out, 0, sizeof(double) * l_frozen, st) != cudaSuccess)
+      throw int(EPS_ECUDA);
+    std::vector<int64_t> offs(h->lay.seg.begin() + l_frozen, h->lay.seg.end());
+    check(eps_grad_sqnorm_flat(h->g32, offs.data(), L - l_frozen, out + l_frozen, h->act.sq_ws,
+                               h->act.sq_ws_bytes, st));
+  });
+}
+
+// Forward-only inference of the logits (used by tests): batch rows of
+// images through all layers; logits bf16 [batch, classes_pad] into `logits`.
+int eps_vit_forward_logits(eps_vit* h, const float* images, int batch, void* logits,
+                           void* stream) {
+  return guard([&] {
+    auto st = static_cast<cudaStream_t>(stream);
+    const int64_t d = h->g.d, T = h->g.tokens;
+    h->embed_fwd(images, 0, batch, st);
+    for (int l = 0; l < h->g.layers; ++l) {
+      h->att_fwd(l, 0, batch, st);
+      h->mlp_fwd(l, 0, batch, st);
+    }
+    check(eps_gather_rows(h->act.X[h->g.layers], T * d, h->act.cls_rows, batch, d, 0, st));
+    check(eps_layernorm_fwd(h->act.cls_rows, h->P(h->lay.lnfg), h->P(h->lay.lnfb), h->act.hf,
+                            h->act.meanf, h->act.rstdf, batch, d, 1e-6f, st));
+    check(eps_gemm_bf16(0, 0, EPS_EPI_BIAS_BF16, h->act.hf, h->W(h->lay.wh), logits,
+                        h->P(h->lay.bh), nullptr, nullptr, batch, h->g.classes_pad, d, d, d,
+                        h->g.classes_pad, 1, st));
+  });
+}
+
+// Device pointer to an internal activation buffer (tests / cache warm-up):
+// which 0 = X[layer] (residual stream entering `layer`), 1 = dX scratch.
+void* eps_vit_activation(eps_vit* h, int which, int layer) {
+  if (which == 0 && layer >= 0 && layer <= h->g.layers) return h->act.X[layer];
+  if (which == 1) return h->act.dX;
+  return nullptr;
+}
+
+}  // extern "C"

@@ -1,0 +1,62 @@
+"""Time the tcgen05 GEMM on the ViT-B/16 block shapes (CUDA events)."""
+import json
+import sys
+
+import torch
+
+sys.path.insert(0, ".")
+from paper_2102_03161_b200 import ops  # noqa: E402
+
+R = 400 * 197
+SHAPES = {  # name: (M, N, K, a_mn, b_mn, epi, split)
+    "fwd_qkv": (R, 2304, 768, False, False, ops.EPI_BIAS_BF16, 1),
+    "fwd_proj": (R, 768, 768, False, False, ops.EPI_BIAS_RESID_BF16, 1),
+    "fwd_fc1": (R, 3072, 768, False, False, ops.EPI_BIAS_GELU_BF16, 1),
+    "fwd_fc2": (R, 768, 3072, False, False, ops.EPI_BIAS_RESID_BF16, 1),
+    "dgrad_fc2": (R, 3072, 768, False, True, ops.EPI_DGELU_BF16, 1),
+    "dgrad_qkv": (R, 768, 2304, False, True, ops.EPI_STORE_BF16, 1),
+    "wgrad_qkv": (2304, 768, R, True, True, ops.EPI_ACCUM_F32, 8),
+    "wgrad_fc2": (768, 3072, R, True, True, ops.EPI_ACCUM_F32, 8),
+    "square8k": (8192, 8192, 8192, False, False, ops.EPI_STORE_BF16, 1),
+}
+
+
+def run(name, M, N, K, a_mn, b_mn, epi, split, iters=20):
+    dev = torch.device("cuda")
+    a = torch.randn((K, M) if a_mn else (M, K), device=dev).bfloat16()
+    b = torch.randn((K, N) if b_mn else (N, K), device=dev).bfloat16()
+    f32 = epi in (ops.EPI_STORE_F32, ops.EPI_ACCUM_F32)
+    out = torch.zeros(M, N, device=dev, dtype=torch.float32 if f32 else torch.bfloat16)
+    bias = torch.randn(N, device=dev)
+    aux = torch.randn(M, N, device=dev).bfloat16() if epi in (2, 3, 4) else None
+    colsum = torch.zeros(N, device=dev) if epi == 4 else None
+    kw = dict(a_mn=a_mn, b_mn=b_mn, epilogue=epi, bias=bias, aux=aux, colsum=colsum,
+              split_k=split)
+    for _ in range(3):
+        ops.gemm(a, b, out, **kw)
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(iters):
+        ops.gemm(a, b, out, **kw)
+    e.record()
+    torch.cuda.synchronize()
+    ms = s.elapsed_time(e) / iters
+    tf = 2 * M * N * K / ms / 1e9
+    # torch reference speed for context
+    A = a.t() if a_mn else a
+    B = b.t() if b_mn else b
+    s.record()
+    for _ in range(iters):
+        torch.matmul(A, B.t())
+    e.record()
+    torch.cuda.synchronize()
+    tms = s.elapsed_time(e) / iters
+    return dict(name=name, ms=round(ms, 4), tflops=round(tf, 1), torch_ms=round(tms, 4),
+                torch_tflops=round(2 * M * N * K / tms / 1e9, 1))
+
+
+if __name__ == "__main__":
+    names = sys.argv[1:] or list(SHAPES)
+    for n in names:
+        print(json.dumps(run(n, *SHAPES[n])), flush=True)
