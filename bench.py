@@ -1,0 +1,421 @@
+"""Benchmark: ViT-B/16 freeze-training samples/sec on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = one training iteration of the per-pipeline batch (400 synthetic
+224x224 ImageNet-shaped images, BASELINE.json configs[1]): forward, backward
+and the fused SGD-momentum update of every trainable layer, executed by the
+sm_100a kernels of libeps_b200.so through the C ABI.  The epoch-0 decision
+of the reference's planner (runner.cpp:94-229, replayed by eps_planner) fixes
+L_frozen = 0, K, R and M; `value` is that no-freeze step's whole-job
+throughput with inputs resident in HBM.  `e2e` is the same step through the
+public executor API with the images copied from pinned host memory every
+step and the loss read back.  `freeze_schedule` replays the planner's
+per-epoch decisions (L_frozen, AutoCache gather / boundary move) on the
+device and reports the measured end-to-end speedup vs no-freeze
+(runner.cpp:298 semantics: baseline total time / freeze total time).
+
+N > 1 (torchrun, one rank per GPU, NCCL): every rank is an AutoDP replica
+holding the whole stack (K = 1) and the active-layer gradients are averaged
+with one NCCL all-reduce per step -- the AutoPipe P2P executor for K > 1 is
+not built yet, so `config.parallelism` says dp{N} and `config.planner` shows
+what the reference planner would pick.
+
+`--impl reference` times the reference path's CPU implementation -- the fp32
+restatement in oracle/vit_fp32.py (the reference itself has no tensor code,
+SURVEY.md section 0) -- on the host cores, on a bounded sample of the same
+workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+CFG = "vit-b16"
+METRIC = "ViT-B/16 train samples/sec"
+UNIT = "samples/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default=CFG)
+    ap.add_argument("--no-schedule", action="store_true", help="skip the freeze-schedule replay")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ---- clocks sampling (B200_PROFILING.md clocks line) -------------------------
+class ClockSampler:
+    QUERY = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.QUERY}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.thread:
+            self.thread.join(timeout=2)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        sm.sort()
+        med = sm[len(sm) // 2] if sm else None
+        return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p, "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, \
+            "fallback"
+
+
+def layer_flops(g) -> float:
+    """F = 2T(4d^2 + 2df) + 4T^2 d per sample per layer (forward)."""
+    T, d, f = g.tokens, g.hidden, g.mlp_dim
+    return 2.0 * T * (4 * d * d + 2 * d * f) + 4.0 * T * T * d
+
+
+def sample_flops(g, l_frozen: int = 0, cached: bool = False) -> float:
+    """Algorithmic training FLOPs per sample; embedding / head
+    counted as their GEMMs (3x trainable, 1x frozen)."""
+    F = layer_flops(g)
+    L = g.layers
+    n_patch = (g.image // g.patch) ** 2
+    embed = 2.0 * n_patch * g.hidden * g.channels * g.patch * g.patch
+    head = 2.0 * g.hidden * g.classes
+    total = 3.0 * head
+    for l in range(L):
+        if l >= l_frozen:
+            total += (2.0 if (l == l_frozen and l_frozen > 0) else 3.0) * F
+        elif not cached:
+            total += F
+    if l_frozen == 0:
+        total += 3.0 * embed
+    elif not cached:
+        total += embed
+    return total
+
+
+# ---- reference arm -------------------------------------------------------------
+def cpu_baseline(g, seconds: float, batch: int = 4):
+    """fp32 CPU restatement of the train step (oracle/vit_fp32.py) on the host
+    cores: samples/sec over a bounded sample of `batch`-image steps."""
+    from oracle import vit_fp32
+    from paper_2102_03161_b200.vit import init_params
+    cores = os.cpu_count() or 1
+    torch.set_num_threads(cores)
+    params = init_params(g, seed=17)
+    gen = torch.Generator().manual_seed(5)
+    images = torch.randn(batch, g.channels, g.input_image, g.input_image, generator=gen)
+    labels = torch.randint(0, g.classes, (batch,), generator=gen)
+    vit_fp32.train_step(params, images, labels, g, 0)  # warm-up
+    n, t0 = 0, time.perf_counter()
+    while True:
+        _, grads, _ = vit_fp32.train_step(params, images, labels, g, 0)
+        with torch.no_grad():
+            for k in params:
+                params[k] -= 1e-3 * grads[k]
+        n += 1
+        el = time.perf_counter() - t0
+        if el >= seconds:
+            break
+    return {"value": n * batch / el, "unit": UNIT, "cores": torch.get_num_threads(),
+            "kind": "port",
+            "sample": f"{n} steps x {batch} images of the {g.image}px ViT-B/16 train step "
+                      f"(fp32, forward+backward+SGD) in {el:.1f}s"}
+
+
+def run_reference(args, world, rank):
+    from paper_2102_03161_b200.configs import GEOMETRIES, BATCH
+    if rank != 0:
+        return
+    g = GEOMETRIES[args.config]
+    # warm-up + K steps of the bounded sample, timed as one window
+    cb = cpu_baseline(g, args.cpu_seconds)
+    v = cb["value"]
+    out = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * BATCH[args.config] / v,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+           "data": "synthetic",
+           "config": {"workload": f"{args.config} 224px batch {BATCH[args.config]} train step "
+                                  "(bounded CPU sample)", "global_batch": BATCH[args.config] *
+                      max(1, args.gpus), "seq_len": g.tokens, "parallelism": "cpu"},
+           "cpu_baseline": cb,
+           "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+# ---- our arm -------------------------------------------------------------------
+def main_ours(args, world, rank, local):
+    from paper_2102_03161_b200 import LIB_PATH, configs, ops
+    from paper_2102_03161_b200.capi import EpsApi
+    from paper_2102_03161_b200.planner import Planner
+    from paper_2102_03161_b200.vit import VitExecutor
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    g = configs.GEOMETRIES[args.config]
+    batch = configs.BATCH[args.config]
+    scen = configs.scenario(args.config, world)
+    api = EpsApi(LIB_PATH, "eps_")
+    planner = Planner(api, scen)
+    decisions = [planner.begin_epoch(e) for e in range(configs.EPOCHS[args.config])]
+    d0 = decisions[0]
+    micro = d0.micro_batches if d0.pipeline_length == 1 else 1
+
+    ex = VitExecutor(g, max_batch=batch, seed=17, device=dev)
+    gen = torch.Generator(device=dev).manual_seed(1234 + rank)
+    images = torch.randn(batch, g.channels, g.input_image, g.input_image, device=dev,
+                         generator=gen)
+    labels = torch.randint(0, g.classes, (batch,), device=dev, generator=gen)
+    stream = torch.cuda.current_stream()
+
+    def allreduce(l_frozen):
+        if world > 1:
+            begin = ex.segments[l_frozen]
+            dist.all_reduce(ex.g32[begin:], op=dist.ReduceOp.AVG)
+
+    def step(imgs, lf=0, cache_mode=0, cache_old=0, store=None, ids=None):
+        loss = ex.train_step(imgs, labels, micro_batches=micro, l_frozen=lf,
+                             cache_mode=cache_mode, cache_old=cache_old, store=store, ids=ids)
+        allreduce(lf)
+        ex.sgd(lf, lr=1e-3, momentum=0.9)
+        return loss
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def timed(fn, steps):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        s.record(stream)
+        for _ in range(steps):
+            fn()
+        e.record(stream)
+        barrier()
+        return max_over_ranks(s.elapsed_time(e)) / steps
+
+    # ---- value: no-freeze step, inputs resident in HBM -------------------------
+    for _ in range(args.warmup):
+        step(images)
+    clocks = ClockSampler(local)
+    clocks.start()
+    n_launch0 = ops.launch_count()
+    ms = timed(lambda: step(images), args.steps)
+    launches = ops.launch_count() - n_launch0
+    clock_rec = clocks.stop()
+    value = world * batch / (ms / 1000.0)
+
+    # ---- roofline: one instrumented step, per-class CUDA-event times -----------
+    ex.timing(True)
+    step(images)
+    torch.cuda.synchronize()
+    cls = ex.timing_read()
+    ex.timing(False)
+    peaks, peak_kind = measured_peaks()
+    gemm = cls["gemm"]
+    gemm_tflops = gemm["flops"] / (gemm["ms"] / 1000.0) / 1e12
+    peak_tc = peaks["bf16_tflops_sustained"]
+    roofline = {"bound": "tensor", "kernel": "eps_k::gemm_tc_kernel (all block GEMMs of a step)",
+                "achieved": round(gemm_tflops, 1), "peak": peak_tc, "unit": "TFLOP/s",
+                "frac": round(gemm_tflops / peak_tc, 4), "traffic": None,
+                "peak_kind": f"{peak_kind} bf16_tflops_sustained",
+                "launches_per_step": gemm["launches"],
+                "share_of_step": round(gemm["ms"] / sum(c["ms"] for c in cls.values()), 4)}
+    kernels = {}
+    for name, c in cls.items():
+        if c["launches"] == 0:
+            continue
+        k = {"ms_per_step": round(c["ms"], 3), "launches": c["launches"]}
+        if c["flops"]:
+            k["tflops"] = round(c["flops"] / (c["ms"] / 1000.0) / 1e12, 1)
+        if c["bytes"]:
+            k["gbs"] = round(c["bytes"] / (c["ms"] / 1000.0) / 1e9, 1)
+            k["hbm_frac"] = round(k["gbs"] / peaks["hbm_gbs"], 4)
+        kernels[name] = k
+    mfu = sample_flops(g) * value / world / 1e12 / peak_tc
+
+    # ---- e2e: host-pinned inputs copied every step, loss read back -------------
+    h_images = images.cpu().pin_memory()
+    h_labels = labels.cpu().pin_memory()
+    d_images = torch.empty_like(images)
+    h2d = h_images.numel() * h_images.element_size() + h_labels.numel() * 8
+
+    def e2e_step():
+        d_images.copy_(h_images, non_blocking=True)
+        labels.copy_(h_labels, non_blocking=True)
+        loss = step(d_images)
+        return float(loss.item())
+
+    for _ in range(2):
+        e2e_step()
+    e2e_ms = timed(e2e_step, args.steps)
+    e2e_value = world * batch / (e2e_ms / 1000.0)
+
+    # ---- freeze schedule: the planner's per-epoch decisions on the device ------
+    sched = None
+    if not args.no_schedule and world == 1:
+        sched = freeze_schedule(ex, g, batch, micro, decisions, images, labels, step, timed,
+                                ms, dev)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cpu = cpu_baseline(g, args.cpu_seconds)
+
+    if rank == 0:
+        out = {"metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
+               "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+               "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+               "dtype": "bf16", "data": "synthetic (seeded N(0,1) images, U[0,1000) labels; "
+                                         "random trunc-normal weights)",
+               "config": {"workload": f"{args.config}: ViT-B/16 224px, batch {batch} per "
+                                      "pipeline, no-freeze train step (fwd+bwd+SGD)",
+                          "model": "ViT-B/16", "global_batch": batch * world,
+                          "seq_len": g.tokens, "parallelism": f"dp{world}",
+                          "micro_batches": micro,
+                          "planner": {"K": d0.pipeline_length, "R": d0.replica_width,
+                                      "M": d0.micro_batches},
+                          "l2": "working set (>20 GB of activations) far exceeds the 126 MB L2"},
+               "e2e": {"value": round(e2e_value, 2), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                       "d2h_bytes_per_step": 4, "ms_per_step": round(e2e_ms, 3)},
+               "gpu_launches": launches,
+               "roofline": roofline,
+               "kernels": kernels,
+               "mfu": round(mfu, 4),
+               "clocks": clock_rec,
+               "freeze_schedule": sched,
+               "cpu_baseline": cpu}
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def freeze_schedule(ex, g, batch, micro, decisions, images, labels, step, timed, ms0, dev):
+    """Per-epoch steady-state step time under the planner's decisions.
+
+    Epoch e runs L_frozen(e) with the frozen prefix either recomputed
+    (cache off), gathered from the HBM store (cache on, boundary unchanged)
+    or -- on a boundary-move epoch -- gathered from the old boundary,
+    forwarded over [old, new) and scattered at the new one (autocache.cpp:45-67).
+    Speedup = sum_e t_nofreeze / sum_e t_e (runner.cpp:298; iterations per
+    epoch are equal so they cancel)."""
+    row_elems = g.tokens * g.hidden
+    store = torch.zeros(batch, row_elems, dtype=torch.bfloat16, device=dev)
+    ids = torch.randperm(batch, generator=torch.Generator().manual_seed(3)).to(dev)
+    memo = {}
+    rows = []
+    for d in decisions:
+        lf = d.l_frozen
+        if not d.cache_enabled:
+            key = (lf, 0, 0)
+        elif d.cache_moved:
+            key = (lf, 2, d.cache_old_boundary)
+        else:
+            key = (lf, 1, 0)
+        if key not in memo:
+            lf_, mode, old = key
+            if mode == 1:  # fill the store at this boundary first
+                step(images, lf_, 2, 0, store, ids)
+            fn = (lambda lf_=lf_, mode=mode, old=old:
+                  step(images, lf_, mode, old, store if mode else None, ids if mode else None))
+            fn()
+            memo[key] = timed(fn, 3)
+        t = memo[key]
+        rows.append({"epoch": d.epoch, "l_frozen": lf, "K": d.pipeline_length,
+                     "R": d.replica_width, "M": d.micro_batches,
+                     "cache": ["off", "gather", "move"][key[1]], "ms_per_step": round(t, 3),
+                     "samples_per_s": round(batch / (t / 1000.0), 1)})
+    base = ms0 * len(rows)
+    tot = sum(r["ms_per_step"] for r in rows)
+    return {"epochs": rows, "no_freeze_ms_per_step": round(ms0, 3),
+            "speedup_vs_no_freeze": round(base / tot, 4),
+            "note": "measured on 1 GPU (K=1); per-epoch decisions from the reference planner"}
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+    main_ours(args, world, rank, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -446,6 +446,9 @@ int eps_scatter_rows(const void* src, void* dst, int64_t dst_stride_rows, int ro
                      int64_t offset_rows, void* stream);
 int eps_colsum_bf16(const void* x, float* out, int64_t rows, int64_t cols, void* stream);
 
+/* Kernels launched by this library in this process (launch accounting). */
+unsigned long long eps_launch_count(void);
+
 /* ---- ViT stage executor (csrc/runtime/vit.cu) --------------------------- */
 /* geom = {layers, d, mlp_dim, heads, tokens, classes, image, stored_image,
  *         patch, channels, max_batch}. */
@@ -464,6 +467,24 @@ int eps_vit_layer_sqnorms(eps_vit_t* h, int l_frozen, double* out, void* stream)
 int eps_vit_forward_logits(eps_vit_t* h, const float* images, int batch, void* logits,
                            void* stream);
 void* eps_vit_activation(eps_vit_t* h, int which, int layer);
+/* Per-kernel-class CUDA-event timing of the executor's launches (bench /
+ * roofline).  While enabled every launch is bracketed by events on its
+ * stream.  eps_vit_timing_read synchronises the recorded events and returns,
+ * per class c (EPS_TC_*), ms[c] total device time, flops[c] algorithmic
+ * FLOPs (2MNK per GEMM; 4T^2 d per attention forward, 2x backward), bytes[c]
+ * algorithmic HBM bytes, count[c] launches; then clears the record. */
+enum {
+  EPS_TC_GEMM = 0,
+  EPS_TC_ATTN = 1,
+  EPS_TC_NORM = 2,
+  EPS_TC_ELTWISE = 3,
+  EPS_TC_CACHE = 4,
+  EPS_TC_OPTIM = 5,
+  EPS_TC_SQNORM = 6,
+  EPS_TC_COUNT = 7
+};
+int eps_vit_timing_enable(eps_vit_t* h, int on);
+int eps_vit_timing_read(eps_vit_t* h, double* ms, double* flops, double* bytes, int64_t* count);
 #endif /* EPS_REFERENCE_BUILD */
 
 #ifdef __cplusplus

@@ -167,6 +167,8 @@ def next_frozen_count(st: FreezeState, norms: Sequence[float], L: int) -> int:
 
 
 def frozen_bound_closed_form(T: int, L: int, alpha: float) -> float:  # freeze.cpp:52-60
+    if not (0.0 < alpha < 1.0):
+        raise ValueError("frozen_bound_closed_form: alpha must be in (0,1)")
     al = alpha * L
     s = al / (1.0 - alpha)
     for t in range(2, T + 1):

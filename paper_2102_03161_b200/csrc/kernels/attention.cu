@@ -542,7 +542,7 @@ int attn_fwd_launch(const void* qkv, void* out, float* lse, int B, int T, int H,
   if (smem > 227 * 1024) return EPS_EINVAL;
   cudaFuncSetAttribute(attn_fwd_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   dim3 grid(B * H, (T + kBlk - 1) / kBlk);
-  attn_fwd_kernel<DH><<<grid, kAttWarps * 32, smem, st>>>(
+  count_launch(); attn_fwd_kernel<DH><<<grid, kAttWarps * 32, smem, st>>>(
       static_cast<const uint16_t*>(qkv), static_cast<uint16_t*>(out), lse, T, H,
       scale * 1.4426950408889634f);
   return cudaGetLastError() == cudaSuccess ? EPS_OK : EPS_ECUDA;
@@ -555,17 +555,17 @@ int attn_bwd_launch(const void* qkv, const void* out, const void* dout, const fl
   const size_t smem = bwd_smem<DH>(T);
   if (smem > 227 * 1024) return EPS_EINVAL;
   const int64_t warps = int64_t(B) * T * H;
-  attn_bwd_dot_kernel<DH><<<unsigned((warps * 32 + 255) / 256), 256, 0, st>>>(
+  count_launch(); attn_bwd_dot_kernel<DH><<<unsigned((warps * 32 + 255) / 256), 256, 0, st>>>(
       static_cast<const uint16_t*>(out), static_cast<const uint16_t*>(dout), dsum, B, T, H);
   cudaFuncSetAttribute(attn_bwd_dkdv_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        int(smem));
   cudaFuncSetAttribute(attn_bwd_dq_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        int(smem));
   dim3 grid(B * H, (T + kBlk - 1) / kBlk);
-  attn_bwd_dkdv_kernel<DH><<<grid, kAttWarps * 32, smem, st>>>(
+  count_launch(); attn_bwd_dkdv_kernel<DH><<<grid, kAttWarps * 32, smem, st>>>(
       static_cast<const uint16_t*>(qkv), static_cast<const uint16_t*>(dout), lse, dsum,
       static_cast<uint16_t*>(dqkv), dbias, T, H, scale);
-  attn_bwd_dq_kernel<DH><<<grid, kAttWarps * 32, smem, st>>>(
+  count_launch(); attn_bwd_dq_kernel<DH><<<grid, kAttWarps * 32, smem, st>>>(
       static_cast<const uint16_t*>(qkv), static_cast<const uint16_t*>(dout), lse, dsum,
       static_cast<uint16_t*>(dqkv), dbias, T, H, scale);
   return cudaGetLastError() == cudaSuccess ? EPS_OK : EPS_ECUDA;

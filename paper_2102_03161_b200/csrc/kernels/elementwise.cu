@@ -282,7 +282,7 @@ extern "C" int eps_patchify(const float* images, void* patches, int batch, int c
   const int out_side = image & 0xFFFF;
   const int in_side = (image >> 16) ? (image >> 16) : out_side;
   if (patch % 4 != 0 || out_side % patch != 0) return EPS_EINVAL;
-  patchify_kernel<<<num_sms() * 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+  count_launch(); patchify_kernel<<<num_sms() * 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(
       images, static_cast<uint16_t*>(patches), batch, channels, in_side, out_side, patch);
   return ok_or_cuda();
 }
@@ -290,7 +290,7 @@ extern "C" int eps_patchify(const float* images, void* patches, int batch, int c
 extern "C" int eps_vit_assemble(const void* patch_tokens, const float* cls, const float* pos,
                                 void* x, int batch, int tokens, int64_t d, void* stream) {
   if (d % 8 != 0) return EPS_EINVAL;
-  assemble_kernel<<<num_sms() * 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+  count_launch(); assemble_kernel<<<num_sms() * 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const uint16_t*>(patch_tokens), cls, pos, static_cast<uint16_t*>(x), batch,
       tokens, int(d));
   return ok_or_cuda();
@@ -299,7 +299,7 @@ extern "C" int eps_vit_assemble(const void* patch_tokens, const float* cls, cons
 extern "C" int eps_vit_assemble_bwd(const void* dx, float* dcls, float* dpos, void* dpatch_tokens,
                                     int batch, int tokens, int64_t d, void* stream) {
   dim3 grid(tokens, unsigned((d + 255) / 256));
-  assemble_bwd_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+  count_launch(); assemble_bwd_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const uint16_t*>(dx), dcls, dpos, static_cast<uint16_t*>(dpatch_tokens), batch,
       tokens, int(d));
   return ok_or_cuda();
@@ -307,7 +307,7 @@ extern "C" int eps_vit_assemble_bwd(const void* dx, float* dcls, float* dpos, vo
 
 extern "C" int eps_softmax_xent(const void* logits, const int64_t* labels, void* dlogits,
                                 float* loss_sum, int batch, int classes, void* stream) {
-  xent_kernel<<<(batch + 7) / 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+  count_launch(); xent_kernel<<<(batch + 7) / 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const uint16_t*>(logits), labels, static_cast<uint16_t*>(dlogits), loss_sum,
       nullptr, batch, classes, classes, 1.0f / batch);
   return ok_or_cuda();
@@ -316,7 +316,7 @@ extern "C" int eps_softmax_xent(const void* logits, const int64_t* labels, void*
 extern "C" int eps_softmax_xent_bias(const void* logits, const int64_t* labels, void* dlogits,
                                      float* loss_sum, float* dbias, int batch, int classes,
                                      int ld, float grad_scale, void* stream) {
-  xent_kernel<<<(batch + 7) / 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+  count_launch(); xent_kernel<<<(batch + 7) / 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const uint16_t*>(logits), labels, static_cast<uint16_t*>(dlogits), loss_sum,
       dbias, batch, classes, ld, grad_scale);
   return ok_or_cuda();
@@ -329,7 +329,7 @@ extern "C" int eps_sgd_momentum(float* param, uint16_t* param_bf16, float* grad,
        reinterpret_cast<uintptr_t>(momentum)) % 16 ||
       reinterpret_cast<uintptr_t>(param_bf16) % 8)
     return EPS_EINVAL;
-  sgd_kernel<<<num_sms() * 4, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+  count_launch(); sgd_kernel<<<num_sms() * 4, 256, 0, static_cast<cudaStream_t>(stream)>>>(
       param, param_bf16, grad, momentum, n, lr, mu, weight_decay);
   return ok_or_cuda();
 }
@@ -339,7 +339,7 @@ extern "C" int eps_adamw(float* param, uint16_t* param_bf16, float* grad, float*
                          float weight_decay, int step, void* stream) {
   if (n <= 0) return EPS_OK;
   const float c1 = 1.f - powf(beta1, float(step)), c2 = 1.f - powf(beta2, float(step));
-  adamw_kernel<<<num_sms() * 4, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+  count_launch(); adamw_kernel<<<num_sms() * 4, 256, 0, static_cast<cudaStream_t>(stream)>>>(
       param, param_bf16, grad, m, v, n, lr, beta1, beta2, eps, weight_decay, c1, c2);
   return ok_or_cuda();
 }
@@ -366,8 +366,8 @@ extern "C" int eps_grad_sqnorm_flat(const float* flat, const int64_t* seg_offset
   if (workspace_bytes < size_t(blocks) * sizeof(double)) return EPS_ECAPACITY;
   auto st = static_cast<cudaStream_t>(stream);
   double* partial = static_cast<double*>(workspace);
-  if (blocks > 0) sqnorm_partial_kernel<<<blocks, 512, 0, st>>>(flat, t, partial);
-  sqnorm_final_kernel<<<1, 64, 0, st>>>(partial, t, out);
+  if (blocks > 0) { count_launch(); sqnorm_partial_kernel<<<blocks, 512, 0, st>>>(flat, t, partial); }
+  count_launch(); sqnorm_final_kernel<<<1, 64, 0, st>>>(partial, t, out);
   return ok_or_cuda();
 }
 
@@ -401,7 +401,7 @@ extern "C" int eps_cache_gather(const void* store, const int64_t* ids, int n, in
   if (n <= 0) return EPS_OK;
   if (row_bytes % 16) return EPS_EINVAL;
   dim3 grid(unsigned(std::min<int64_t>((row_bytes / 16 + 255) / 256, 64)), unsigned(n));
-  cache_copy_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+  count_launch(); cache_copy_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const uint8_t*>(store), static_cast<uint8_t*>(dst), ids, row_bytes, true);
   return ok_or_cuda();
 }
@@ -411,7 +411,7 @@ extern "C" int eps_cache_scatter(void* store, const int64_t* ids, int n, int64_t
   if (n <= 0) return EPS_OK;
   if (row_bytes % 16) return EPS_EINVAL;
   dim3 grid(unsigned(std::min<int64_t>((row_bytes / 16 + 255) / 256, 64)), unsigned(n));
-  cache_copy_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+  count_launch(); cache_copy_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const uint8_t*>(src), static_cast<uint8_t*>(store), ids, row_bytes, false);
   return ok_or_cuda();
 }
@@ -420,7 +420,7 @@ extern "C" int eps_gather_rows(const void* src, int64_t src_stride_rows, void* d
                                int64_t d, int64_t offset_rows, void* stream) {
   if (rows <= 0) return EPS_OK;
   dim3 grid(unsigned((d / 8 + 255) / 256), unsigned(rows));
-  rows_copy_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+  count_launch(); rows_copy_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const uint16_t*>(src) + offset_rows * src_stride_rows, src_stride_rows,
       static_cast<uint16_t*>(dst), d, rows, d);
   return ok_or_cuda();
@@ -430,7 +430,7 @@ extern "C" int eps_scatter_rows(const void* src, void* dst, int64_t dst_stride_r
                                 int64_t d, int64_t offset_rows, void* stream) {
   if (rows <= 0) return EPS_OK;
   dim3 grid(unsigned((d / 8 + 255) / 256), unsigned(rows));
-  rows_copy_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+  count_launch(); rows_copy_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const uint16_t*>(src), d,
       static_cast<uint16_t*>(dst) + offset_rows * dst_stride_rows, dst_stride_rows, rows, d);
   return ok_or_cuda();
@@ -441,7 +441,10 @@ extern "C" int eps_colsum_bf16(const void* x, float* out, int64_t rows, int64_t 
   if (rows <= 0) return EPS_OK;
   const int64_t rpb = 256;
   dim3 grid(unsigned((cols + 255) / 256), unsigned((rows + rpb - 1) / rpb));
-  colsum_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+  count_launch(); colsum_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const uint16_t*>(x), out, rows, cols, rpb);
   return ok_or_cuda();
 }
+
+// Number of kernels this library has launched in the process so far.
+extern "C" unsigned long long eps_launch_count(void) { return eps_k::launch_counter().load(); }

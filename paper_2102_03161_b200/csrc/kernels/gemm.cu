@@ -462,7 +462,7 @@ int launch(const void* A, const void* B, int64_t lda, int64_t ldb, GemmArgs args
   if (!ok_a || !ok_b || !ok_c || !ok_x) return EPS_ECUDA;
   const int units = args.tiles_m * args.tiles_n * args.splits;
   const int grid = units < sm_count() ? units : sm_count();
-  kern<<<grid, kThreads, Cfg::kSmem, stream>>>(ma, mb, mc, mx, args);
+  count_launch(); kern<<<grid, kThreads, Cfg::kSmem, stream>>>(ma, mb, mc, mx, args);
   return cudaGetLastError() == cudaSuccess ? EPS_OK : EPS_ECUDA;
 }
 

@@ -192,7 +192,7 @@ template <int EPL>
 int ln_launch(const void* x, const float* gamma, const float* beta, void* y, float* mean,
               float* rstd, int64_t rows, float eps, cudaStream_t st) {
   const int64_t blocks = (rows + kLnWarps - 1) / kLnWarps;
-  ln_fwd_kernel<EPL><<<unsigned(blocks), kLnWarps * 32, 0, st>>>(
+  count_launch(); ln_fwd_kernel<EPL><<<unsigned(blocks), kLnWarps * 32, 0, st>>>(
       static_cast<const uint16_t*>(x), gamma, beta, static_cast<uint16_t*>(y), mean, rstd, rows,
       eps);
   return cudaGetLastError() == cudaSuccess ? EPS_OK : EPS_ECUDA;
@@ -210,7 +210,7 @@ int ln_bwd_launch(const void* dy, const void* x, const float* gamma, const float
                          int(smem));
     configured = true;
   }
-  ln_bwd_kernel<EPL><<<ln_grid_bwd(rows), kLnWarps * 32, smem, st>>>(
+  count_launch(); ln_bwd_kernel<EPL><<<ln_grid_bwd(rows), kLnWarps * 32, smem, st>>>(
       static_cast<const uint16_t*>(dy), static_cast<const uint16_t*>(x), gamma, mean, rstd,
       static_cast<const uint16_t*>(dres), static_cast<uint16_t*>(dx), dgamma, dbeta, colsum,
       rows);

@@ -236,3 +236,16 @@ __device__ __forceinline__ uint32_t swz128(int r, int c) {
   return uint32_t(r * 128 + ((c ^ (r & 7)) << 4));
 }
 }  // namespace eps_k
+
+// ---- launch accounting (host) ------------------------------------------------
+// Every kernel launch in libeps_b200.so bumps this process-wide counter, so
+// bench.py can report how many of *our* kernels ran inside its timed region
+// (eps_launch_count in eps_capi.h).
+#include <atomic>
+namespace eps_k {
+inline std::atomic<unsigned long long>& launch_counter() {
+  static std::atomic<unsigned long long> n{0};
+  return n;
+}
+inline void count_launch() { launch_counter().fetch_add(1, std::memory_order_relaxed); }
+}  // namespace eps_k

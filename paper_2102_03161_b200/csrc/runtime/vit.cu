@@ -175,6 +175,50 @@ struct eps_vit {
   eps_vit(const Geometry& geom, float* p, uint16_t* pb, float* gr, float* m, uint8_t* ws)
       : g(geom), lay(geom), act(geom, lay.total, ws), p32(p), p16(pb), g32(gr), mom(m),
         loss_sum(nullptr) {}
+  ~eps_vit() {
+    for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
+  }
+
+  // ---- per-class launch timing (eps_vit_timing_*) ----------------------------
+  struct Rec {
+    int cls;
+    double flops, bytes;
+    cudaEvent_t a, b;
+  };
+  bool timing = false;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
+  std::vector<Rec> recs;
+  cudaEvent_t next_event() {
+    if (ev_used == ev_pool.size()) {
+      cudaEvent_t e;
+      if (cudaEventCreate(&e) != cudaSuccess) throw int(EPS_ECUDA);
+      ev_pool.push_back(e);
+    }
+    return ev_pool[ev_used++];
+  }
+  // Run one C-ABI launch; when timing, bracket it with events on `st`.
+  template <typename F>
+  void run(int cls, double flops, double bytes, cudaStream_t st, F&& launch) {
+    if (!timing) {
+      check(launch());
+      return;
+    }
+    Rec r{cls, flops, bytes, next_event(), next_event()};
+    cudaEventRecord(r.a, st);
+    check(launch());
+    cudaEventRecord(r.b, st);
+    recs.push_back(r);
+  }
+  // GEMM with algorithmic FLOPs 2MNK.
+  void mm(int a_mn, int b_mn, int epi, const void* A, const void* B, void* C, const float* bias,
+          void* aux, float* colsum, int64_t M, int64_t N, int64_t K, int64_t lda, int64_t ldb,
+          int64_t ldc, int split, cudaStream_t st) {
+    run(EPS_TC_GEMM, 2.0 * double(M) * double(N) * double(K), 0.0, st, [&] {
+      return eps_gemm_bf16(a_mn, b_mn, epi, A, B, C, bias, aux, colsum, M, N, K, lda, ldb, ldc,
+                           split, st);
+    });
+  }
 
   const uint16_t* W(const Slot& s) const { return p16 + s.off; }
   const float* P(const Slot& s) const { return p32 + s.off; }
@@ -191,41 +235,41 @@ struct eps_vit {
     uint16_t* patches = act.patches + int64_t(b0) * np * pl;
     uint16_t* ptok = act.ptok + int64_t(b0) * np * d;
     const int img_arg = (g.in_image != g.image) ? ((g.in_image << 16) | g.image) : g.image;
-    check(eps_patchify(images + int64_t(b0) * g.channels * g.in_image * g.in_image, patches, b,
-                       g.channels, img_arg, g.patch, st));
-    check(eps_gemm_bf16(0, 0, EPS_EPI_BIAS_BF16, patches, W(lay.wpe), ptok, P(lay.bpe), nullptr,
-                        nullptr, b * np, d, pl, pl, pl, d, 1, st));
-    check(eps_vit_assemble(ptok, P(lay.cls), P(lay.pos), act.X[0] + int64_t(b0) * g.tokens * d,
-                           b, g.tokens, d, st));
+    run(EPS_TC_ELTWISE, 0.0, 0.0, static_cast<cudaStream_t>(st), [&] { return eps_patchify(images + int64_t(b0) * g.channels * g.in_image * g.in_image, patches, b,
+                       g.channels, img_arg, g.patch, st); });
+    mm(0, 0, EPS_EPI_BIAS_BF16, patches, W(lay.wpe), ptok, P(lay.bpe), nullptr,
+                        nullptr, b * np, d, pl, pl, pl, d, 1, st);
+    run(EPS_TC_ELTWISE, 0.0, 0.0, static_cast<cudaStream_t>(st), [&] { return eps_vit_assemble(ptok, P(lay.cls), P(lay.pos), act.X[0] + int64_t(b0) * g.tokens * d,
+                           b, g.tokens, d, st); });
   }
 
   void att_fwd(int l, int b0, int b, cudaStream_t st) {
     const LayerSlots& s = lay.layer[l];
     const int64_t d = g.d, r0 = int64_t(b0) * g.tokens, R = int64_t(b) * g.tokens;
-    check(eps_layernorm_fwd(act.X[l] + r0 * d, P(s.ln1g), P(s.ln1b), act.H1[l] + r0 * d,
-                            act.mean1[l] + r0, act.rstd1[l] + r0, R, d, 1e-6f, st));
-    check(eps_gemm_bf16(0, 0, EPS_EPI_BIAS_BF16, act.H1[l] + r0 * d, W(s.wqkv),
+    run(EPS_TC_NORM, 0.0, 4.0 * double(R) * double(d), static_cast<cudaStream_t>(st), [&] { return eps_layernorm_fwd(act.X[l] + r0 * d, P(s.ln1g), P(s.ln1b), act.H1[l] + r0 * d,
+                            act.mean1[l] + r0, act.rstd1[l] + r0, R, d, 1e-6f, st); });
+    mm(0, 0, EPS_EPI_BIAS_BF16, act.H1[l] + r0 * d, W(s.wqkv),
                         act.QKV[l] + r0 * 3 * d, P(s.bqkv), nullptr, nullptr, R, 3 * d, d, d, d,
-                        3 * d, 1, st));
-    check(eps_attn_fwd(act.QKV[l] + r0 * 3 * d, act.A[l] + r0 * d,
+                        3 * d, 1, st);
+    run(EPS_TC_ATTN, 4.0 * b * double(g.tokens) * g.tokens * g.heads * g.head_dim(), 8.0 * b * double(g.tokens) * g.heads * g.head_dim(), static_cast<cudaStream_t>(st), [&] { return eps_attn_fwd(act.QKV[l] + r0 * 3 * d, act.A[l] + r0 * d,
                        act.lse[l] + int64_t(b0) * g.heads * g.tokens, b, g.tokens, g.heads,
-                       g.head_dim(), 1.0f / std::sqrt(float(g.head_dim())), st));
-    check(eps_gemm_bf16(0, 0, EPS_EPI_BIAS_RESID_BF16, act.A[l] + r0 * d, W(s.wp),
+                       g.head_dim(), 1.0f / std::sqrt(float(g.head_dim())), st); });
+    mm(0, 0, EPS_EPI_BIAS_RESID_BF16, act.A[l] + r0 * d, W(s.wp),
                         act.X1[l] + r0 * d, P(s.bp), act.X[l] + r0 * d, nullptr, R, d, d, d, d,
-                        d, 1, st));
+                        d, 1, st);
   }
 
   void mlp_fwd(int l, int b0, int b, cudaStream_t st) {
     const LayerSlots& s = lay.layer[l];
     const int64_t d = g.d, f = g.f, r0 = int64_t(b0) * g.tokens, R = int64_t(b) * g.tokens;
-    check(eps_layernorm_fwd(act.X1[l] + r0 * d, P(s.ln2g), P(s.ln2b), act.H2[l] + r0 * d,
-                            act.mean2[l] + r0, act.rstd2[l] + r0, R, d, 1e-6f, st));
-    check(eps_gemm_bf16(0, 0, EPS_EPI_BIAS_GELU_BF16, act.H2[l] + r0 * d, W(s.w1),
+    run(EPS_TC_NORM, 0.0, 4.0 * double(R) * double(d), static_cast<cudaStream_t>(st), [&] { return eps_layernorm_fwd(act.X1[l] + r0 * d, P(s.ln2g), P(s.ln2b), act.H2[l] + r0 * d,
+                            act.mean2[l] + r0, act.rstd2[l] + r0, R, d, 1e-6f, st); });
+    mm(0, 0, EPS_EPI_BIAS_GELU_BF16, act.H2[l] + r0 * d, W(s.w1),
                         act.G[l] + r0 * f, P(s.b1), act.U[l] + r0 * f, nullptr, R, f, d, d, d, f,
-                        1, st));
-    check(eps_gemm_bf16(0, 0, EPS_EPI_BIAS_RESID_BF16, act.G[l] + r0 * f, W(s.w2),
+                        1, st);
+    mm(0, 0, EPS_EPI_BIAS_RESID_BF16, act.G[l] + r0 * f, W(s.w2),
                         act.X[l + 1] + r0 * d, P(s.b2), act.X1[l] + r0 * d, nullptr, R, d, f, f,
-                        f, d, 1, st));
+                        f, d, 1, st);
   }
 
   // Head forward + loss + head backward; leaves dL/dX[L] in act.dX rows.
@@ -238,23 +282,23 @@ struct eps_vit {
     uint16_t* dlogits = act.dlogits + int64_t(b0) * C;
     uint16_t* dhf = act.dhf + int64_t(b0) * d;
     uint16_t* dcls = act.dcls + int64_t(b0) * d;
-    check(eps_gather_rows(act.X[g.layers] + int64_t(b0) * T * d, T * d, cls, b, d, 0, st));
-    check(eps_layernorm_fwd(cls, P(lay.lnfg), P(lay.lnfb), hf, act.meanf + b0, act.rstdf + b0, b,
-                            d, 1e-6f, st));
-    check(eps_gemm_bf16(0, 0, EPS_EPI_BIAS_BF16, hf, W(lay.wh), logits, P(lay.bh), nullptr,
-                        nullptr, b, C, d, d, d, C, 1, st));
-    check(eps_softmax_xent_bias(logits, labels + b0, dlogits, loss_sum, Gr(lay.bh), b, g.classes,
-                                int(C), 1.0f / float(global_batch), st));
-    check(eps_gemm_bf16(1, 1, EPS_EPI_ACCUM_F32, dlogits, hf, Gr(lay.wh), nullptr, nullptr,
-                        nullptr, C, d, b, C, d, d, 1, st));
-    check(eps_gemm_bf16(0, 1, EPS_EPI_STORE_BF16, dlogits, W(lay.wh), dhf, nullptr, nullptr,
-                        nullptr, b, d, C, C, d, d, 1, st));
+    run(EPS_TC_ELTWISE, 0.0, 0.0, static_cast<cudaStream_t>(st), [&] { return eps_gather_rows(act.X[g.layers] + int64_t(b0) * T * d, T * d, cls, b, d, 0, st); });
+    run(EPS_TC_NORM, 0.0, 4.0 * double(b) * double(d), static_cast<cudaStream_t>(st), [&] { return eps_layernorm_fwd(cls, P(lay.lnfg), P(lay.lnfb), hf, act.meanf + b0, act.rstdf + b0, b,
+                            d, 1e-6f, st); });
+    mm(0, 0, EPS_EPI_BIAS_BF16, hf, W(lay.wh), logits, P(lay.bh), nullptr,
+                        nullptr, b, C, d, d, d, C, 1, st);
+    run(EPS_TC_ELTWISE, 0.0, 0.0, static_cast<cudaStream_t>(st), [&] { return eps_softmax_xent_bias(logits, labels + b0, dlogits, loss_sum, Gr(lay.bh), b, g.classes,
+                                int(C), 1.0f / float(global_batch), st); });
+    mm(1, 1, EPS_EPI_ACCUM_F32, dlogits, hf, Gr(lay.wh), nullptr, nullptr,
+                        nullptr, C, d, b, C, d, d, 1, st);
+    mm(0, 1, EPS_EPI_STORE_BF16, dlogits, W(lay.wh), dhf, nullptr, nullptr,
+                        nullptr, b, d, C, C, d, d, 1, st);
     // LN_f backward on the CLS rows; its dx column sum is top-layer FC2's bias grad
-    check(eps_layernorm_bwd(dhf, cls, P(lay.lnfg), act.meanf + b0, act.rstdf + b0, nullptr, dcls,
-                            Gr(lay.lnfg), Gr(lay.lnfb), Gr(top.b2), b, d, nullptr, st));
+    run(EPS_TC_NORM, 0.0, 8.0 * double(b) * double(d), static_cast<cudaStream_t>(st), [&] { return eps_layernorm_bwd(dhf, cls, P(lay.lnfg), act.meanf + b0, act.rstdf + b0, nullptr, dcls,
+                            Gr(lay.lnfg), Gr(lay.lnfb), Gr(top.b2), b, d, nullptr, st); });
     uint16_t* dX = act.dX + int64_t(b0) * T * d;
     if (cudaMemsetAsync(dX, 0, size_t(b) * T * d * 2, st) != cudaSuccess) throw int(EPS_ECUDA);
-    check(eps_scatter_rows(dcls, dX, T * d, b, d, 0, st));
+    run(EPS_TC_ELTWISE, 0.0, 0.0, static_cast<cudaStream_t>(st), [&] { return eps_scatter_rows(dcls, dX, T * d, b, d, 0, st); });
   }
 
   // ---- backward sublayers (dX holds dL/d(output) rows; updated in place) ----
@@ -264,18 +308,18 @@ struct eps_vit {
     uint16_t* dX = act.dX + r0 * d;
     uint16_t* Gm = act.G[l] + r0 * f;
     const int split = split_for(R);
-    check(eps_gemm_bf16(1, 1, EPS_EPI_ACCUM_F32, dX, Gm, Gr(s.w2), nullptr, nullptr, nullptr, d,
-                        f, R, d, f, f, split, st));
+    mm(1, 1, EPS_EPI_ACCUM_F32, dX, Gm, Gr(s.w2), nullptr, nullptr, nullptr, d,
+                        f, R, d, f, f, split, st);
     // du overwrites G (its last reader was the dW2 GEMM above)
-    check(eps_gemm_bf16(0, 1, EPS_EPI_DGELU_BF16, dX, W(s.w2), Gm, nullptr, act.U[l] + r0 * f,
-                        Gr(s.b1), R, f, d, d, f, f, 1, st));
-    check(eps_gemm_bf16(1, 1, EPS_EPI_ACCUM_F32, Gm, act.H2[l] + r0 * d, Gr(s.w1), nullptr,
-                        nullptr, nullptr, f, d, R, f, d, d, split, st));
-    check(eps_gemm_bf16(0, 1, EPS_EPI_STORE_BF16, Gm, W(s.w1), act.dH + r0 * d, nullptr, nullptr,
-                        nullptr, R, d, f, f, d, d, 1, st));
-    check(eps_layernorm_bwd(act.dH + r0 * d, act.X1[l] + r0 * d, P(s.ln2g), act.mean2[l] + r0,
+    mm(0, 1, EPS_EPI_DGELU_BF16, dX, W(s.w2), Gm, nullptr, act.U[l] + r0 * f,
+                        Gr(s.b1), R, f, d, d, f, f, 1, st);
+    mm(1, 1, EPS_EPI_ACCUM_F32, Gm, act.H2[l] + r0 * d, Gr(s.w1), nullptr,
+                        nullptr, nullptr, f, d, R, f, d, d, split, st);
+    mm(0, 1, EPS_EPI_STORE_BF16, Gm, W(s.w1), act.dH + r0 * d, nullptr, nullptr,
+                        nullptr, R, d, f, f, d, d, 1, st);
+    run(EPS_TC_NORM, 0.0, 8.0 * double(R) * double(d), static_cast<cudaStream_t>(st), [&] { return eps_layernorm_bwd(act.dH + r0 * d, act.X1[l] + r0 * d, P(s.ln2g), act.mean2[l] + r0,
                             act.rstd2[l] + r0, dX, dX, Gr(s.ln2g), Gr(s.ln2b), Gr(s.bp), R, d,
-                            nullptr, st));
+                            nullptr, st); });
   }
 
   // need_dx: write dL/dX[l] (false for the lowest trainable layer when the
@@ -286,33 +330,33 @@ struct eps_vit {
     const int64_t d = g.d, r0 = int64_t(b0) * g.tokens, R = int64_t(b) * g.tokens;
     uint16_t* dX = act.dX + r0 * d;
     const int split = split_for(R);
-    check(eps_gemm_bf16(1, 1, EPS_EPI_ACCUM_F32, dX, act.A[l] + r0 * d, Gr(s.wp), nullptr,
-                        nullptr, nullptr, d, d, R, d, d, d, split, st));
-    check(eps_gemm_bf16(0, 1, EPS_EPI_STORE_BF16, dX, W(s.wp), act.dA + r0 * d, nullptr, nullptr,
-                        nullptr, R, d, d, d, d, d, 1, st));
-    check(eps_attn_bwd_ws(act.QKV[l] + r0 * 3 * d, act.A[l] + r0 * d, act.dA + r0 * d,
+    mm(1, 1, EPS_EPI_ACCUM_F32, dX, act.A[l] + r0 * d, Gr(s.wp), nullptr,
+                        nullptr, nullptr, d, d, R, d, d, d, split, st);
+    mm(0, 1, EPS_EPI_STORE_BF16, dX, W(s.wp), act.dA + r0 * d, nullptr, nullptr,
+                        nullptr, R, d, d, d, d, d, 1, st);
+    run(EPS_TC_ATTN, 8.0 * b * double(g.tokens) * g.tokens * g.heads * g.head_dim(), 18.0 * b * double(g.tokens) * g.heads * g.head_dim(), static_cast<cudaStream_t>(st), [&] { return eps_attn_bwd_ws(act.QKV[l] + r0 * 3 * d, act.A[l] + r0 * d, act.dA + r0 * d,
                           act.lse[l] + int64_t(b0) * g.heads * g.tokens, act.dQKV + r0 * 3 * d,
                           Gr(s.bqkv), act.dsum + int64_t(b0) * g.heads * g.tokens, b, g.tokens,
-                          g.heads, g.head_dim(), 1.0f / std::sqrt(float(g.head_dim())), st));
-    check(eps_gemm_bf16(1, 1, EPS_EPI_ACCUM_F32, act.dQKV + r0 * 3 * d, act.H1[l] + r0 * d,
-                        Gr(s.wqkv), nullptr, nullptr, nullptr, 3 * d, d, R, 3 * d, d, d, split, st));
-    check(eps_gemm_bf16(0, 1, EPS_EPI_STORE_BF16, act.dQKV + r0 * 3 * d, W(s.wqkv),
+                          g.heads, g.head_dim(), 1.0f / std::sqrt(float(g.head_dim())), st); });
+    mm(1, 1, EPS_EPI_ACCUM_F32, act.dQKV + r0 * 3 * d, act.H1[l] + r0 * d,
+                        Gr(s.wqkv), nullptr, nullptr, nullptr, 3 * d, d, R, 3 * d, d, d, split, st);
+    mm(0, 1, EPS_EPI_STORE_BF16, act.dQKV + r0 * 3 * d, W(s.wqkv),
                         act.dH + r0 * d, nullptr, nullptr, nullptr, R, d, 3 * d, 3 * d, d, d, 1,
-                        st));
-    check(eps_layernorm_bwd(act.dH + r0 * d, act.X[l] + r0 * d, P(s.ln1g), act.mean1[l] + r0,
+                        st);
+    run(EPS_TC_NORM, 0.0, 8.0 * double(R) * double(d), static_cast<cudaStream_t>(st), [&] { return eps_layernorm_bwd(act.dH + r0 * d, act.X[l] + r0 * d, P(s.ln1g), act.mean1[l] + r0,
                             act.rstd1[l] + r0, dX, need_dx ? dX : nullptr, Gr(s.ln1g), Gr(s.ln1b),
-                            need_dx ? colsum_prev : nullptr, R, d, nullptr, st));
+                            need_dx ? colsum_prev : nullptr, R, d, nullptr, st); });
   }
 
   void embed_bwd(int b0, int b, cudaStream_t st) {
     const int64_t d = g.d, np = g.patches(), pl = g.patch_len();
     uint16_t* dptok = act.dptok + int64_t(b0) * np * d;
-    check(eps_vit_assemble_bwd(act.dX + int64_t(b0) * g.tokens * d, Gr(lay.cls), Gr(lay.pos),
-                               dptok, b, g.tokens, d, st));
-    check(eps_colsum_bf16(dptok, Gr(lay.bpe), int64_t(b) * np, d, st));
-    check(eps_gemm_bf16(1, 1, EPS_EPI_ACCUM_F32, dptok, act.patches + int64_t(b0) * np * pl,
+    run(EPS_TC_ELTWISE, 0.0, 0.0, static_cast<cudaStream_t>(st), [&] { return eps_vit_assemble_bwd(act.dX + int64_t(b0) * g.tokens * d, Gr(lay.cls), Gr(lay.pos),
+                               dptok, b, g.tokens, d, st); });
+    run(EPS_TC_ELTWISE, 0.0, 0.0, static_cast<cudaStream_t>(st), [&] { return eps_colsum_bf16(dptok, Gr(lay.bpe), int64_t(b) * np, d, st); });
+    mm(1, 1, EPS_EPI_ACCUM_F32, dptok, act.patches + int64_t(b0) * np * pl,
                         Gr(lay.wpe), nullptr, nullptr, nullptr, d, pl, int64_t(b) * np, d, pl, pl,
-                        split_for(int64_t(b) * np), st));
+                        split_for(int64_t(b) * np), st);
   }
 };
 
@@ -432,16 +476,16 @@ int eps_vit_train_step(eps_vit* h, const float* images, const int64_t* labels, i
       const int64_t xoff = int64_t(b0) * h->g.tokens * h->g.d;
       int start = 0;  // first layer to run forward
       if (cache_mode == 1) {
-        check(eps_cache_gather(store, ids + b0, b, row_bytes, h->act.X[l_frozen] + xoff, st));
+        h->run(EPS_TC_CACHE, 0.0, 2.0 * b * double(row_bytes), static_cast<cudaStream_t>(st), [&] { return eps_cache_gather(store, ids + b0, b, row_bytes, h->act.X[l_frozen] + xoff, st); });
         start = l_frozen;
       } else if (cache_mode == 2 && cache_old > 0) {
-        check(eps_cache_gather(store, ids + b0, b, row_bytes, h->act.X[cache_old] + xoff, st));
+        h->run(EPS_TC_CACHE, 0.0, 2.0 * b * double(row_bytes), static_cast<cudaStream_t>(st), [&] { return eps_cache_gather(store, ids + b0, b, row_bytes, h->act.X[cache_old] + xoff, st); });
         start = cache_old;
       }
       if (start == 0) h->embed_fwd(images, b0, b, st);
       for (int l = start; l < L; ++l) {
         if (cache_mode == 2 && l == l_frozen)
-          check(eps_cache_scatter(store, ids + b0, b, row_bytes, h->act.X[l] + xoff, st));
+          h->run(EPS_TC_CACHE, 0.0, 2.0 * b * double(row_bytes), static_cast<cudaStream_t>(st), [&] { return eps_cache_scatter(store, ids + b0, b, row_bytes, h->act.X[l] + xoff, st); });
         h->att_fwd(l, b0, b, st);
         h->mlp_fwd(l, b0, b, st);
       }
@@ -468,8 +512,8 @@ int eps_vit_sgd(eps_vit* h, int l_frozen, float lr, float momentum, float weight
                 void* stream) {
   return guard([&] {
     const int64_t begin = h->lay.seg[l_frozen];
-    check(eps_sgd_momentum(h->p32 + begin, h->p16 + begin, h->g32 + begin, h->mom + begin,
-                           h->lay.total - begin, lr, momentum, weight_decay, stream));
+    h->run(EPS_TC_OPTIM, 0.0, 26.0 * double(h->lay.total - begin), static_cast<cudaStream_t>(stream), [&] { return eps_sgd_momentum(h->p32 + begin, h->p16 + begin, h->g32 + begin, h->mom + begin,
+                           h->lay.total - begin, lr, momentum, weight_decay, stream); });
   });
 }
 
@@ -482,8 +526,8 @@ int eps_vit_layer_sqnorms(eps_vit* h, int l_frozen, double* out, void* stream) {
     if (l_frozen > 0 && cudaMemsetAsync(out, 0, sizeof(double) * l_frozen, st) != cudaSuccess)
       throw int(EPS_ECUDA);
     std::vector<int64_t> offs(h->lay.seg.begin() + l_frozen, h->lay.seg.end());
-    check(eps_grad_sqnorm_flat(h->g32, offs.data(), L - l_frozen, out + l_frozen, h->act.sq_ws,
-                               h->act.sq_ws_bytes, st));
+    h->run(EPS_TC_SQNORM, 0.0, 4.0 * double(h->lay.total - h->lay.seg[l_frozen]), static_cast<cudaStream_t>(st), [&] { return eps_grad_sqnorm_flat(h->g32, offs.data(), L - l_frozen, out + l_frozen, h->act.sq_ws,
+                               h->act.sq_ws_bytes, st); });
   });
 }
 
@@ -499,12 +543,12 @@ int eps_vit_forward_logits(eps_vit* h, const float* images, int batch, void* log
       h->att_fwd(l, 0, batch, st);
       h->mlp_fwd(l, 0, batch, st);
     }
-    check(eps_gather_rows(h->act.X[h->g.layers], T * d, h->act.cls_rows, batch, d, 0, st));
-    check(eps_layernorm_fwd(h->act.cls_rows, h->P(h->lay.lnfg), h->P(h->lay.lnfb), h->act.hf,
-                            h->act.meanf, h->act.rstdf, batch, d, 1e-6f, st));
-    check(eps_gemm_bf16(0, 0, EPS_EPI_BIAS_BF16, h->act.hf, h->W(h->lay.wh), logits,
+    h->run(EPS_TC_ELTWISE, 0.0, 0.0, static_cast<cudaStream_t>(st), [&] { return eps_gather_rows(h->act.X[h->g.layers], T * d, h->act.cls_rows, batch, d, 0, st); });
+    h->run(EPS_TC_NORM, 0.0, 4.0 * double(batch) * double(d), static_cast<cudaStream_t>(st), [&] { return eps_layernorm_fwd(h->act.cls_rows, h->P(h->lay.lnfg), h->P(h->lay.lnfb), h->act.hf,
+                            h->act.meanf, h->act.rstdf, batch, d, 1e-6f, st); });
+    h->mm(0, 0, EPS_EPI_BIAS_BF16, h->act.hf, h->W(h->lay.wh), logits,
                         h->P(h->lay.bh), nullptr, nullptr, batch, h->g.classes_pad, d, d, d,
-                        h->g.classes_pad, 1, st));
+                        h->g.classes_pad, 1, st);
   });
 }
 
@@ -514,6 +558,38 @@ void* eps_vit_activation(eps_vit* h, int which, int layer) {
   if (which == 0 && layer >= 0 && layer <= h->g.layers) return h->act.X[layer];
   if (which == 1) return h->act.dX;
   return nullptr;
+}
+
+int eps_vit_timing_enable(eps_vit* h, int on) {
+  return guard([&] {
+    if (h == nullptr) throw int(EPS_EINVAL);
+    h->timing = on != 0;
+    h->recs.clear();
+    h->ev_used = 0;
+  });
+}
+
+int eps_vit_timing_read(eps_vit* h, double* ms, double* flops, double* bytes, int64_t* count) {
+  return guard([&] {
+    if (h == nullptr) throw int(EPS_EINVAL);
+    for (int c = 0; c < EPS_TC_COUNT; ++c) {
+      if (ms) ms[c] = 0;
+      if (flops) flops[c] = 0;
+      if (bytes) bytes[c] = 0;
+      if (count) count[c] = 0;
+    }
+    for (const auto& r : h->recs) {
+      if (cudaEventSynchronize(r.b) != cudaSuccess) throw int(EPS_ECUDA);
+      float t = 0.f;
+      if (cudaEventElapsedTime(&t, r.a, r.b) != cudaSuccess) throw int(EPS_ECUDA);
+      if (ms) ms[r.cls] += t;
+      if (flops) flops[r.cls] += r.flops;
+      if (bytes) bytes[r.cls] += r.bytes;
+      if (count) count[r.cls] += 1;
+    }
+    h->recs.clear();
+    h->ev_used = 0;
+  });
 }
 
 }  // extern "C"

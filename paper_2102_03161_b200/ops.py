@@ -110,6 +110,14 @@ def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor, *, a_mn: bool = Fa
     return out
 
 
+def launch_count() -> int:
+    """Kernels libeps_b200.so has launched in this process (eps_launch_count)."""
+    f = api().lib.eps_launch_count
+    f.restype = C.c_ulonglong
+    f.argtypes = []
+    return int(f())
+
+
 def call(name: str, *args):
     """Raw C-ABI call with status check (tensors converted to pointers)."""
     lib = api().lib

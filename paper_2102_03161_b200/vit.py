@@ -156,6 +156,7 @@ class VitExecutor:
         f = getattr(ops.api().lib, name)
         f.restype = C.c_int
         conv = [C.c_void_p(a.data_ptr()) if isinstance(a, torch.Tensor) else a for a in args]
+        # ctypes arrays pass through unchanged
         rc = f(self.h, *conv)
         if rc != 0:
             raise RuntimeError(f"{name} failed with status {rc}")
@@ -201,6 +202,23 @@ class VitExecutor:
         s = torch.cuda.current_stream()
         self._call("eps_vit_forward_logits", images, b, out, C.c_void_p(s.cuda_stream))
         return out[:, :self.g.classes]
+
+    # -- instrumentation ---------------------------------------------------
+    TIMING_CLASSES = ("gemm", "attention", "layernorm", "eltwise", "cache", "optimizer",
+                      "sqnorm")
+
+    def timing(self, on: bool):
+        """Bracket every executor launch with CUDA events on its stream."""
+        self._call("eps_vit_timing_enable", int(on))
+
+    def timing_read(self) -> Dict[str, dict]:
+        """Per kernel class: device ms, algorithmic FLOPs / bytes, launches."""
+        n = len(self.TIMING_CLASSES)
+        ms, fl, by = (C.c_double * n)(), (C.c_double * n)(), (C.c_double * n)()
+        cnt = (C.c_int64 * n)()
+        self._call("eps_vit_timing_read", ms, fl, by, cnt)
+        return {c: {"ms": ms[i], "flops": fl[i], "bytes": by[i], "launches": cnt[i]}
+                for i, c in enumerate(self.TIMING_CLASSES)}
 
     def boundary_activation(self, layer: int, batch: int) -> torch.Tensor:
         """View of X[layer] rows for the first `batch` samples (bf16)."""
