@@ -571,12 +571,23 @@ int attn_bwd_launch(const void* qkv, const void* out, const void* dout, const fl
   return cudaGetLastError() == cudaSuccess ? EPS_OK : EPS_ECUDA;
 }
 
+bool attn_tc_supported(int T, int head_dim);
+int attn_fwd_tc(const void* qkv, void* out, float* lse, int B, int T, int H, float scale,
+                cudaStream_t st);
+int attn_bwd_tc(const void* qkv, const void* out, const void* dout, const float* lse, void* dqkv,
+                float* dbias, float* dsum, int B, int T, int H, float scale, cudaStream_t st);
+
 }  // namespace eps_k
 
+// head_dim 64, T <= 384: tcgen05/TMEM kernels (attention_tc.cu); head_dim 32
+// (the tiny ViT): the mma.sync kernels above.
 extern "C" int eps_attn_fwd(const void* qkv, void* out, float* lse, int batch, int tokens,
                             int heads, int head_dim, float scale, void* stream) {
   using namespace eps_k;
   auto st = static_cast<cudaStream_t>(stream);
+  if (batch < 1 || tokens < 1 || heads < 1) return EPS_EINVAL;
+  if (attn_tc_supported(tokens, head_dim))
+    return attn_fwd_tc(qkv, out, lse, batch, tokens, heads, scale, st);
   switch (head_dim) {
     case 32: return attn_fwd_launch<32>(qkv, out, lse, batch, tokens, heads, scale, st);
     case 64: return attn_fwd_launch<64>(qkv, out, lse, batch, tokens, heads, scale, st);
@@ -591,6 +602,10 @@ extern "C" int eps_attn_bwd_ws(const void* qkv, const void* out, const void* dou
                                int head_dim, float scale, void* stream) {
   using namespace eps_k;
   auto st = static_cast<cudaStream_t>(stream);
+  if (batch < 1 || tokens < 1 || heads < 1) return EPS_EINVAL;
+  if (attn_tc_supported(tokens, head_dim))
+    return attn_bwd_tc(qkv, out, dout, lse, dqkv, dbias_qkv, dsum_workspace, batch, tokens, heads,
+                       scale, st);
   switch (head_dim) {
     case 32:
       return attn_bwd_launch<32>(qkv, out, dout, lse, dqkv, dbias_qkv, dsum_workspace, batch,

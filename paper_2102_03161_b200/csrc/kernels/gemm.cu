@@ -19,10 +19,10 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
-#include <mutex>
 
 #include "eps_capi.h"
 #include "ptx.cuh"
+#include "tma_host.cuh"
 
 namespace eps_k {
 
@@ -387,52 +387,6 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // ---- host side -------------------------------------------------------------
-
-using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
-                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
-                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
-                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-EncodeTiledFn encode_fn() {
-  static EncodeTiledFn fn = nullptr;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault,
-                                         &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<EncodeTiledFn>(p);
-  });
-  return fn;
-}
-
-// 2D tensor map: inner dim `inner` (contiguous), outer dim `outer` with a
-// row pitch of `ld` elements; zero fill for out-of-bounds boxes.
-bool make_map(CUtensorMap* map, const void* base, bool f32, int64_t inner, int64_t outer,
-              int64_t ld, int box_inner, int box_outer, CUtensorMapSwizzle swz) {
-  EncodeTiledFn fn = encode_fn();
-  if (fn == nullptr) return false;
-  const int esize = f32 ? 4 : 2;
-  const cuuint64_t dims[2] = {cuuint64_t(inner), cuuint64_t(outer)};
-  const cuuint64_t strides[1] = {cuuint64_t(ld) * esize};
-  const cuuint32_t box[2] = {cuuint32_t(box_inner), cuuint32_t(box_outer)};
-  const cuuint32_t estr[2] = {1u, 1u};
-  return fn(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
-            const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
-            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
-int sm_count() {
-  static int n = 0;
-  if (n == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
-}
 
 template <int BN, int STAGES, bool A_MN, bool B_MN>
 int launch(const void* A, const void* B, int64_t lda, int64_t ldb, GemmArgs args,
