@@ -8,13 +8,14 @@
 // MN-major) and wgrad (A=dY^T, B=X^T, both MN-major, contraction over the
 // token rows) without any transpose copies.
 //
-// Roles (192 threads, one CTA per SM, persistent over output tiles):
+// Roles (320 threads, one CTA per SM, persistent over output tiles):
 //   warp 0      TMA producer: 128B-swizzled A/B k-blocks into a STAGES ring
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
-//   warps 2..5  epilogue: tcgen05.ld -> fused bias / GELU / dGELU / residual
-//               / column-sum -> swizzled smem -> TMA store (or TMA reduce-add),
-//               double-buffered TMEM accumulators so the epilogue of tile i
-//               overlaps the MMAs of tile i+1.
+//   warps 2..9  epilogue, two warps per TMEM lane quarter taking alternate
+//               32-column chunks: tcgen05.ld -> fused bias / GELU / dGELU /
+//               residual / column-sum -> swizzled smem -> TMA store (or TMA
+//               reduce-add); double-buffered TMEM accumulators so the epilogue
+//               of tile i overlaps the MMAs of tile i+1.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -28,7 +29,8 @@ namespace eps_k {
 
 constexpr int kBM = 128;
 constexpr int kBK = 64;  // one 128B swizzle atom of bf16 along K
-constexpr int kThreads = 192;
+constexpr int kEpiWarps = 8;
+constexpr int kThreads = 64 + 32 * kEpiWarps;
 constexpr int kMnChunk = 64;  // MN extent of one swizzle atom (MN-major operands)
 
 struct GemmArgs {
@@ -49,7 +51,7 @@ struct GemmCfg {
   static constexpr int kBBytes = BN * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kTmemCols = 2 * BN;  // double-buffered accumulator
-  static constexpr size_t kSmem = size_t(STAGES) * kStageBytes + 4 * 8192 /*epilogue*/ +
+  static constexpr size_t kSmem = size_t(STAGES) * kStageBytes + 8 * 4096 /*epilogue*/ +
                                   1024 /*align*/ + 256 /*barriers*/;
   static constexpr uint32_t kIdesc = umma_idesc_bf16(kBM, BN, A_MN, B_MN);
 };
@@ -82,17 +84,14 @@ __device__ __forceinline__ void load_operand(void* dst, const CUtensorMap* map, 
 }
 
 // ---- epilogue ----------------------------------------------------------------
-// Each epilogue warp owns one TMEM lane quarter (32 output rows) and walks
-// its tiles in 32-column chunks.  Outputs are staged in a per-warp swizzled
-// smem ring and written with TMA stores (TMA reduce-add for fp32
-// accumulation): fully coalesced, asynchronous global traffic.  Element-wise
-// inputs (residual / GELU pre-activation) stream through a 3-deep TMA ring
-// that runs ahead across tile boundaries, so their latency hides behind the
-// MMAs of the next tile.
-constexpr int kEpiWarps = 4;
-constexpr int kEpiWarpBytes = 8192;
+// Two warps per TMEM lane quarter (32 output rows) walk alternate 32-column
+// chunks of each tile.  Outputs are staged in a per-warp swizzled 4 KB smem
+// ring and written with TMA stores (TMA reduce-add for fp32 accumulation):
+// coalesced, asynchronous global traffic.  Element-wise inputs (residual /
+// GELU pre-activation) are loaded straight into registers one chunk ahead of
+// use, so their latency hides behind the current chunk's math.
+constexpr int kEpiWarpBytes = 4096;
 constexpr int kChunkBf16 = 2048;  // 32x32 bf16
-constexpr int kAuxDepth = 3;
 
 __device__ __forceinline__ bool epi_reads_aux(int epi) {
   return epi == EPS_EPI_BIAS_RESID_BF16 || epi == EPS_EPI_DGELU_BF16;
@@ -113,18 +112,30 @@ __device__ __forceinline__ void stage_f32(uint32_t base, int lane, const float (
                  __float_as_uint(v[4 * q + 2]), __float_as_uint(v[4 * q + 3]));
 }
 
-__device__ __forceinline__ void read_aux(uint32_t base, int lane, float (&a)[32]) {
+// One row's 32 bf16 aux values (64 B) of chunk `col0`; zero past M / N.
+__device__ __forceinline__ void load_aux_row(const uint16_t* aux, int64_t ld, int row, int M,
+                                             int col0, int N, uint4 (&dst)[4]) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) dst[q] = make_uint4(0u, 0u, 0u, 0u);
+  if (row < M) {
+    const uint4* src = reinterpret_cast<const uint4*>(aux + int64_t(row) * ld + col0);
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (col0 + 8 * q < N) dst[q] = src[q];
+  }
+}
+
+__device__ __forceinline__ void unpack_aux(const uint4 (&w)[4], float (&a)[32]) {
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    const uint4 w = ld_shared_v4(base + swz64(lane, q));
-    a[8 * q + 0] = bf16_lo(w.x);
-    a[8 * q + 1] = bf16_hi(w.x);
-    a[8 * q + 2] = bf16_lo(w.y);
-    a[8 * q + 3] = bf16_hi(w.y);
-    a[8 * q + 4] = bf16_lo(w.z);
-    a[8 * q + 5] = bf16_hi(w.z);
-    a[8 * q + 6] = bf16_lo(w.w);
-    a[8 * q + 7] = bf16_hi(w.w);
+    a[8 * q + 0] = bf16_lo(w[q].x);
+    a[8 * q + 1] = bf16_hi(w[q].x);
+    a[8 * q + 2] = bf16_lo(w[q].y);
+    a[8 * q + 3] = bf16_hi(w[q].y);
+    a[8 * q + 4] = bf16_lo(w[q].z);
+    a[8 * q + 5] = bf16_hi(w[q].z);
+    a[8 * q + 6] = bf16_lo(w[q].w);
+    a[8 * q + 7] = bf16_hi(w[q].w);
   }
 }
 
@@ -144,8 +155,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* tmem_full = empty + STAGES;
   uint64_t* tmem_empty = tmem_full + 2;
-  uint64_t* aux_full = tmem_empty + 2;  // [kEpiWarps][kAuxDepth]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aux_full + kAuxDepth * kEpiWarps);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -163,7 +173,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tmem_full[s], 1);
       mbar_init(&tmem_empty[s], kEpiWarps);
     }
-    for (int s = 0; s < kAuxDepth * kEpiWarps; ++s) mbar_init(&aux_full[s], 1);
     mbar_fence_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, Cfg::kTmemCols);
@@ -235,45 +244,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else {
-    const int ew = warp - 2;
-    const int quarter = warp & 3;  // TMEM lane quarter this warp may access
+    const int ew = warp - 2;         // 0..7
+    const int quarter = warp & 3;    // TMEM lane quarter this warp may access
+    const int part = ew >> 2;        // this warp takes chunks part, part+2, ...
     uint8_t* my_area = epi_area + ew * kEpiWarpBytes;
     const uint32_t area_s = smem_addr(my_area);
-    uint64_t* my_aux_bar = aux_full + kAuxDepth * ew;
     const int epi = args.epi;
     const bool aux_in = epi_reads_aux(epi);
     const bool f32_out = epi == EPS_EPI_STORE_F32 || epi == EPS_EPI_ACCUM_F32;
-    // Per-warp 8 KB: [out ring][aux ring].  aux epilogues: 1 x 2 KB out + 3 x 2 KB aux;
-    // GELU (2 outputs) and fp32: 2 x 4 KB out; plain bf16: 4 x 2 KB out.
+    // Per-warp 4 KB out ring: GELU (2 outputs) and fp32 chunks take 4 KB, bf16 2 KB.
     const int out_bytes = (epi == EPS_EPI_BIAS_GELU_BF16 || f32_out) ? 4096 : 2048;
-    const int n_out = aux_in ? 1 : kEpiWarpBytes / out_bytes;
-    const uint32_t aux_s = area_s + kChunkBf16;
-
-    // Prefetch cursor over this warp's flattened (unit, chunk) stream.
-    int pf_u = blockIdx.x, pf_c = 0;
-    uint32_t pf_n = 0, use_n = 0;
-    auto chunks_of = [&](int u) {
-      const int t = u % tiles;
-      const int n0 = (t % args.tiles_n) * BN;
-      return min(BN / 32, (args.N - n0 + 31) / 32);
-    };
-    auto prefetch_until = [&](uint32_t limit) {
-      while (pf_u < units && pf_n < limit) {
-        const int t = pf_u % tiles;
-        const int row = (t / args.tiles_n) * kBM + quarter * 32;
-        const int col = (t % args.tiles_n) * BN + pf_c * 32;
-        const uint32_t slot = pf_n % kAuxDepth;
-        fence_proxy_async_smem();
-        mbar_expect_tx(&my_aux_bar[slot], kChunkBf16);
-        tma_load_2d(my_area + kChunkBf16 * (1 + slot), &map_x, &my_aux_bar[slot], col, row);
-        ++pf_n;
-        if (++pf_c == chunks_of(pf_u)) {
-          pf_c = 0;
-          pf_u += gridDim.x;
-        }
-      }
-    };
-    if (aux_in && lane == 0) prefetch_until(kAuxDepth);
+    const int n_out = kEpiWarpBytes / out_bytes;
+    const uint16_t* auxp = static_cast<const uint16_t*>(args.aux);
 
     uint32_t out_n = 0;
     int acc = 0;
@@ -284,29 +266,29 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int m0 = (t / args.tiles_n) * kBM;
       const int n0 = (t % args.tiles_n) * BN;
       const int row0 = m0 + quarter * 32;
+      const int my_row = row0 + lane;
       const int chunks = min(BN / 32, (args.N - n0 + 31) / 32);
+      uint4 xa[4];
+      if (aux_in && part < chunks)
+        load_aux_row(auxp, args.ldc, my_row, args.M, n0 + part * 32, args.N, xa);
       mbar_wait(&tmem_full[acc], acc_phase);
       tc_fence_after();
       const uint32_t taddr = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(acc * BN);
 #pragma unroll 1
-      for (int c = 0; c < chunks; ++c) {
+      for (int c = part; c < chunks; c += 2) {
         const int col0 = n0 + c * 32;
         const int valid = min(32, args.N - col0);
         uint32_t raw[32];
         tmem_ld_32x32(taddr + uint32_t(c * 32), raw);
+        uint4 xn[4];
+        if (aux_in && c + 2 < chunks)
+          load_aux_row(auxp, args.ldc, my_row, args.M, col0 + 64, args.N, xn);
         tmem_ld_wait();
         float v[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(raw[j]);
         float x[32];
-        if (aux_in) {
-          const uint32_t slot = use_n % kAuxDepth;
-          mbar_wait(&my_aux_bar[slot], (use_n / kAuxDepth) & 1);
-          read_aux(aux_s + slot * kChunkBf16, lane, x);
-          ++use_n;
-          __syncwarp();  // every lane has read the slot before it is refilled
-          if (lane == 0) prefetch_until(use_n + kAuxDepth);
-        }
+        if (aux_in) unpack_aux(xa, x);
         if (args.bias != nullptr) {
           const float4* b4 = reinterpret_cast<const float4*>(args.bias + col0);
 #pragma unroll
@@ -321,8 +303,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // reuse an out slot only after its previous TMA store has read it
         if (lane == 0) {
           if (n_out == 1) bulk_wait_read<0>();
-          else if (n_out == 2) bulk_wait_read<1>();
-          else bulk_wait_read<3>();
+          else bulk_wait_read<1>();
         }
         __syncwarp();
         const uint32_t out_off = (out_n % uint32_t(n_out)) * uint32_t(out_bytes);
@@ -364,9 +345,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         ++out_n;
         if (epi == EPS_EPI_DGELU_BF16 && args.colsum != nullptr) {
-          // rows past M were zero-filled by TMA, so they contribute 0
+          // rows past M were zero-filled by TMA (and aux zeroed), so they contribute 0
           const float s = warp_transpose_sum32(v);
           if (lane < valid) atomicAdd(args.colsum + col0 + lane, s);
+        }
+        if (aux_in) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) xa[q] = xn[q];
         }
       }
       tc_fence_before();
@@ -410,7 +395,8 @@ int launch(const void* A, const void* B, int64_t lda, int64_t ldb, GemmArgs args
                          : make_map(&mb, B, false, args.K, args.N, ldb, 64, BN, SW128);
   const bool f32 = args.epi == EPS_EPI_STORE_F32 || args.epi == EPS_EPI_ACCUM_F32;
   const bool ok_c = make_map(&mc, args.C, f32, args.N, args.M, args.ldc, 32, 32, f32 ? SW128 : SW64);
-  // aux: GELU pre-activation output, or residual / pre-activation input.
+  // aux: GELU pre-activation output (TMA store); residual / pre-activation
+  // inputs are read with plain loads.
   const void* xptr = args.aux != nullptr ? args.aux : args.C;
   const bool ok_x = make_map(&mx, xptr, false, args.N, args.M, args.ldc, 32, 32, SW64);
   if (!ok_a || !ok_b || !ok_c || !ok_x) return EPS_ECUDA;
