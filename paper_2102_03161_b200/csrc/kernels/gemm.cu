@@ -257,6 +257,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int n_out = kEpiWarpBytes / out_bytes;
     const uint16_t* auxp = static_cast<const uint16_t*>(args.aux);
 
+    // Pull a tile's aux rows (this lane's row, this warp's chunks) into L2
+    // one tile ahead, so the register loads below hit L2 instead of HBM.
+    auto prefetch_aux = [&](int uu) {
+      if (!aux_in || uu >= units) return;
+      const int tt = uu % tiles;
+      const int pn0 = (tt % args.tiles_n) * BN;
+      const int prow = (tt / args.tiles_n) * kBM + quarter * 32 + lane;
+      if (prow >= args.M) return;
+      const int pch = min(BN / 32, (args.N - pn0 + 31) / 32);
+      for (int c = part; c < pch; c += 2) prefetch_l2(auxp + int64_t(prow) * args.ldc + pn0 + c * 32);
+    };
+    prefetch_aux(blockIdx.x);
+
     uint32_t out_n = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -268,6 +281,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int row0 = m0 + quarter * 32;
       const int my_row = row0 + lane;
       const int chunks = min(BN / 32, (args.N - n0 + 31) / 32);
+      prefetch_aux(u + gridDim.x);
       uint4 xa[4];
       if (aux_in && part < chunks)
         load_aux_row(auxp, args.ldc, my_row, args.M, n0 + part * 32, args.N, xa);
