@@ -467,6 +467,38 @@ int eps_vit_layer_sqnorms(eps_vit_t* h, int l_frozen, double* out, void* stream)
 int eps_vit_forward_logits(eps_vit_t* h, const float* images, int batch, void* logits,
                            void* stream);
 void* eps_vit_activation(eps_vit_t* h, int which, int layer);
+
+/* Pipeline-stage operations (AutoPipe executor).  Global sublayer g in
+ * [0, 2L): layer g/2, ATT if even, MLP if odd (SublayerSeq order,
+ * model.hpp:56-74); a stage owns global sublayers [g0, g1) with
+ * g0 >= 2*l_frozen (PartitionPlan spans shifted by 2*l_frozen).  The host
+ * drives the GPipe order of schedule.cpp:54-117 and moves the cut
+ * activations (eps_vit_cut) between stages.
+ * front = 1 on pipeline stage 0: frozen prefix / AutoCache / embedding first. */
+int eps_vit_stage_forward(eps_vit_t* h, const float* images, int b0, int b, int g0, int g1,
+                          int l_frozen, int front, int cache_mode, int cache_old, void* store,
+                          const int64_t* ids, void* stream);
+/* Last stage: final LN + head forward, softmax-xent loss (grad scale
+ * 1/global_batch), head backward; leaves dL/dX[L] in the dX rows. */
+int eps_vit_stage_head(eps_vit_t* h, const int64_t* labels, int b0, int b, int global_batch,
+                       float* loss_sum, void* stream);
+/* Backward of [g0, g1) with dL/d(output of g1-1) in the dX rows; leaves
+ * dL/d(input of g0) there.  cut_out = 1 when that gradient came from the next
+ * stage (this stage then adds its column sum into sublayer g1-1's bias grad). */
+int eps_vit_stage_backward(eps_vit_t* h, int b0, int b, int g0, int g1, int l_frozen,
+                           int cut_out, void* stream);
+/* Residual-stream buffer [max_batch*T, d] bf16 at the cut before global
+ * sublayer g (g == 2L: the stack output), or (grad = 1) the dX scratch. */
+void* eps_vit_cut(eps_vit_t* h, int g, int grad);
+/* Parameter elements [begin, end) of global sublayers [g0, g1) (embedding in
+ * sublayer 0, final LN + head in sublayer 2L-1); contiguous by layout. */
+int eps_vit_param_range(eps_vit_t* h, int g0, int g1, int64_t* begin, int64_t* end);
+int eps_vit_sgd_range(eps_vit_t* h, int64_t begin, int64_t end, float lr, float momentum,
+                      float weight_decay, void* stream);
+/* Sum of squares of the fp32 gradient arena over n consecutive ranges
+ * offsets[i]..offsets[i+1] (host offsets) into device double out[n]. */
+int eps_vit_sqnorm_ranges(eps_vit_t* h, const int64_t* offsets, int n, double* out,
+                          void* stream);
 /* Per-kernel-class CUDA-event timing of the executor's launches (bench /
  * roofline).  While enabled every launch is bracketed by events on its
  * stream.  eps_vit_timing_read synchronises the recorded events and returns,

@@ -219,14 +219,54 @@ struct eps_vit {
                            split, st);
     });
   }
+  void layernorm(const uint16_t* x, const Slot& gam, const Slot& bet, uint16_t* y, float* mean,
+                 float* rstd, int64_t rows, cudaStream_t st) {
+    run(EPS_TC_NORM, 0.0, 4.0 * double(rows) * g.d, st, [&] {
+      return eps_layernorm_fwd(x, P(gam), P(bet), y, mean, rstd, rows, g.d, 1e-6f, st);
+    });
+  }
+  void layernorm_bwd(const uint16_t* dy, const uint16_t* x, const Slot& gam, const Slot& bet,
+                     const float* mean, const float* rstd, const uint16_t* dres, uint16_t* dx,
+                     float* colsum_dx, int64_t rows, cudaStream_t st) {
+    run(EPS_TC_NORM, 0.0, 8.0 * double(rows) * g.d, st, [&] {
+      return eps_layernorm_bwd(dy, x, P(gam), mean, rstd, dres, dx, Gr(gam), Gr(bet), colsum_dx,
+                               rows, g.d, nullptr, st);
+    });
+  }
+  template <typename F>
+  void eltwise(cudaStream_t st, F&& launch) {
+    run(EPS_TC_ELTWISE, 0.0, 0.0, st, launch);
+  }
 
   const uint16_t* W(const Slot& s) const { return p16 + s.off; }
   const float* P(const Slot& s) const { return p32 + s.off; }
   float* Gr(const Slot& s) const { return g32 + s.off; }
+  float scale() const { return 1.0f / std::sqrt(float(g.head_dim())); }
+  int64_t row_bytes() const { return int64_t(g.tokens) * g.d * 2; }
 
   int split_for(int64_t rows) const {
     // wgrad contracts over the token rows; split so the grid covers the SMs
     return rows >= 16384 ? 8 : rows >= 4096 ? 4 : 1;
+  }
+
+  // ---- sublayer geometry ------------------------------------------------------
+  // Global sublayer g in [0, 2L): layer g/2, ATT if even, MLP if odd
+  // (the reference's SublayerSeq order, model.hpp:56-74).
+  // Residual-stream buffer at the cut *before* sublayer g.
+  uint16_t* cut(int gs) const {
+    if (gs >= 2 * g.layers) return act.X[g.layers];
+    return (gs % 2 == 0) ? act.X[gs / 2] : act.X1[gs / 2];
+  }
+  // Bias whose gradient is the column sum of dL/d(output of sublayer g).
+  float* out_bias_grad(int gs) const {
+    const LayerSlots& s = lay.layer[gs / 2];
+    return (gs % 2 == 0) ? Gr(s.bp) : Gr(s.b2);
+  }
+  // Parameter elements of sublayer g: ATT = [seg[l], ln2g), MLP = [ln2g, seg[l+1]);
+  // the embedding folds into sublayer 0, the final LN + head into 2L-1.
+  int64_t sub_begin(int gs) const {
+    if (gs >= 2 * g.layers) return lay.total;
+    return (gs % 2 == 0) ? lay.seg[gs / 2] : lay.layer[gs / 2].ln2g.off;
   }
 
   // ---- forward sublayers on rows [r0, r0+R) / samples [b0, b0+b) -----------
@@ -235,41 +275,47 @@ struct eps_vit {
     uint16_t* patches = act.patches + int64_t(b0) * np * pl;
     uint16_t* ptok = act.ptok + int64_t(b0) * np * d;
     const int img_arg = (g.in_image != g.image) ? ((g.in_image << 16) | g.image) : g.image;
-    run(EPS_TC_ELTWISE, 0.0, 0.0, static_cast<cudaStream_t>(st), [&] { return eps_patchify(images + int64_t(b0) * g.channels * g.in_image * g.in_image, patches, b,
-                       g.channels, img_arg, g.patch, st); });
-    mm(0, 0, EPS_EPI_BIAS_BF16, patches, W(lay.wpe), ptok, P(lay.bpe), nullptr,
-                        nullptr, b * np, d, pl, pl, pl, d, 1, st);
-    run(EPS_TC_ELTWISE, 0.0, 0.0, static_cast<cudaStream_t>(st), [&] { return eps_vit_assemble(ptok, P(lay.cls), P(lay.pos), act.X[0] + int64_t(b0) * g.tokens * d,
-                           b, g.tokens, d, st); });
+    const float* img = images + int64_t(b0) * g.channels * g.in_image * g.in_image;
+    eltwise(st, [&] { return eps_patchify(img, patches, b, g.channels, img_arg, g.patch, st); });
+    mm(0, 0, EPS_EPI_BIAS_BF16, patches, W(lay.wpe), ptok, P(lay.bpe), nullptr, nullptr, b * np,
+       d, pl, pl, pl, d, 1, st);
+    uint16_t* x0 = act.X[0] + int64_t(b0) * g.tokens * d;
+    eltwise(st, [&] {
+      return eps_vit_assemble(ptok, P(lay.cls), P(lay.pos), x0, b, g.tokens, d, st);
+    });
   }
 
   void att_fwd(int l, int b0, int b, cudaStream_t st) {
     const LayerSlots& s = lay.layer[l];
     const int64_t d = g.d, r0 = int64_t(b0) * g.tokens, R = int64_t(b) * g.tokens;
-    run(EPS_TC_NORM, 0.0, 4.0 * double(R) * double(d), static_cast<cudaStream_t>(st), [&] { return eps_layernorm_fwd(act.X[l] + r0 * d, P(s.ln1g), P(s.ln1b), act.H1[l] + r0 * d,
-                            act.mean1[l] + r0, act.rstd1[l] + r0, R, d, 1e-6f, st); });
-    mm(0, 0, EPS_EPI_BIAS_BF16, act.H1[l] + r0 * d, W(s.wqkv),
-                        act.QKV[l] + r0 * 3 * d, P(s.bqkv), nullptr, nullptr, R, 3 * d, d, d, d,
-                        3 * d, 1, st);
-    run(EPS_TC_ATTN, 4.0 * b * double(g.tokens) * g.tokens * g.heads * g.head_dim(), 8.0 * b * double(g.tokens) * g.heads * g.head_dim(), static_cast<cudaStream_t>(st), [&] { return eps_attn_fwd(act.QKV[l] + r0 * 3 * d, act.A[l] + r0 * d,
-                       act.lse[l] + int64_t(b0) * g.heads * g.tokens, b, g.tokens, g.heads,
-                       g.head_dim(), 1.0f / std::sqrt(float(g.head_dim())), st); });
-    mm(0, 0, EPS_EPI_BIAS_RESID_BF16, act.A[l] + r0 * d, W(s.wp),
-                        act.X1[l] + r0 * d, P(s.bp), act.X[l] + r0 * d, nullptr, R, d, d, d, d,
-                        d, 1, st);
+    layernorm(act.X[l] + r0 * d, s.ln1g, s.ln1b, act.H1[l] + r0 * d, act.mean1[l] + r0,
+              act.rstd1[l] + r0, R, st);
+    mm(0, 0, EPS_EPI_BIAS_BF16, act.H1[l] + r0 * d, W(s.wqkv), act.QKV[l] + r0 * 3 * d,
+       P(s.bqkv), nullptr, nullptr, R, 3 * d, d, d, d, 3 * d, 1, st);
+    const double t = g.tokens, hd = double(g.heads) * g.head_dim();
+    run(EPS_TC_ATTN, 4.0 * b * t * t * hd, 8.0 * b * t * hd, st, [&] {
+      return eps_attn_fwd(act.QKV[l] + r0 * 3 * d, act.A[l] + r0 * d,
+                          act.lse[l] + int64_t(b0) * g.heads * g.tokens, b, g.tokens, g.heads,
+                          g.head_dim(), scale(), st);
+    });
+    mm(0, 0, EPS_EPI_BIAS_RESID_BF16, act.A[l] + r0 * d, W(s.wp), act.X1[l] + r0 * d, P(s.bp),
+       act.X[l] + r0 * d, nullptr, R, d, d, d, d, d, 1, st);
   }
 
   void mlp_fwd(int l, int b0, int b, cudaStream_t st) {
     const LayerSlots& s = lay.layer[l];
     const int64_t d = g.d, f = g.f, r0 = int64_t(b0) * g.tokens, R = int64_t(b) * g.tokens;
-    run(EPS_TC_NORM, 0.0, 4.0 * double(R) * double(d), static_cast<cudaStream_t>(st), [&] { return eps_layernorm_fwd(act.X1[l] + r0 * d, P(s.ln2g), P(s.ln2b), act.H2[l] + r0 * d,
-                            act.mean2[l] + r0, act.rstd2[l] + r0, R, d, 1e-6f, st); });
-    mm(0, 0, EPS_EPI_BIAS_GELU_BF16, act.H2[l] + r0 * d, W(s.w1),
-                        act.G[l] + r0 * f, P(s.b1), act.U[l] + r0 * f, nullptr, R, f, d, d, d, f,
-                        1, st);
-    mm(0, 0, EPS_EPI_BIAS_RESID_BF16, act.G[l] + r0 * f, W(s.w2),
-                        act.X[l + 1] + r0 * d, P(s.b2), act.X1[l] + r0 * d, nullptr, R, d, f, f,
-                        f, d, 1, st);
+    layernorm(act.X1[l] + r0 * d, s.ln2g, s.ln2b, act.H2[l] + r0 * d, act.mean2[l] + r0,
+              act.rstd2[l] + r0, R, st);
+    mm(0, 0, EPS_EPI_BIAS_GELU_BF16, act.H2[l] + r0 * d, W(s.w1), act.G[l] + r0 * f, P(s.b1),
+       act.U[l] + r0 * f, nullptr, R, f, d, d, d, f, 1, st);
+    mm(0, 0, EPS_EPI_BIAS_RESID_BF16, act.G[l] + r0 * f, W(s.w2), act.X[l + 1] + r0 * d, P(s.b2),
+       act.X1[l] + r0 * d, nullptr, R, d, f, f, f, d, 1, st);
+  }
+
+  void sub_fwd(int gs, int b0, int b, cudaStream_t st) {
+    if (gs % 2 == 0) att_fwd(gs / 2, b0, b, st);
+    else mlp_fwd(gs / 2, b0, b, st);
   }
 
   // Head forward + loss + head backward; leaves dL/dX[L] in act.dX rows.
@@ -282,81 +328,177 @@ struct eps_vit {
     uint16_t* dlogits = act.dlogits + int64_t(b0) * C;
     uint16_t* dhf = act.dhf + int64_t(b0) * d;
     uint16_t* dcls = act.dcls + int64_t(b0) * d;
-    run(EPS_TC_ELTWISE, 0.0, 0.0, static_cast<cudaStream_t>(st), [&] { return eps_gather_rows(act.X[g.layers] + int64_t(b0) * T * d, T * d, cls, b, d, 0, st); });
-    run(EPS_TC_NORM, 0.0, 4.0 * double(b) * double(d), static_cast<cudaStream_t>(st), [&] { return eps_layernorm_fwd(cls, P(lay.lnfg), P(lay.lnfb), hf, act.meanf + b0, act.rstdf + b0, b,
-                            d, 1e-6f, st); });
-    mm(0, 0, EPS_EPI_BIAS_BF16, hf, W(lay.wh), logits, P(lay.bh), nullptr,
-                        nullptr, b, C, d, d, d, C, 1, st);
-    run(EPS_TC_ELTWISE, 0.0, 0.0, static_cast<cudaStream_t>(st), [&] { return eps_softmax_xent_bias(logits, labels + b0, dlogits, loss_sum, Gr(lay.bh), b, g.classes,
-                                int(C), 1.0f / float(global_batch), st); });
-    mm(1, 1, EPS_EPI_ACCUM_F32, dlogits, hf, Gr(lay.wh), nullptr, nullptr,
-                        nullptr, C, d, b, C, d, d, 1, st);
-    mm(0, 1, EPS_EPI_STORE_BF16, dlogits, W(lay.wh), dhf, nullptr, nullptr,
-                        nullptr, b, d, C, C, d, d, 1, st);
+    const uint16_t* xl = act.X[g.layers] + int64_t(b0) * T * d;
+    eltwise(st, [&] { return eps_gather_rows(xl, T * d, cls, b, d, 0, st); });
+    layernorm(cls, lay.lnfg, lay.lnfb, hf, act.meanf + b0, act.rstdf + b0, b, st);
+    mm(0, 0, EPS_EPI_BIAS_BF16, hf, W(lay.wh), logits, P(lay.bh), nullptr, nullptr, b, C, d, d, d,
+       C, 1, st);
+    eltwise(st, [&] {
+      return eps_softmax_xent_bias(logits, labels + b0, dlogits, loss_sum, Gr(lay.bh), b,
+                                   g.classes, int(C), 1.0f / float(global_batch), st);
+    });
+    mm(1, 1, EPS_EPI_ACCUM_F32, dlogits, hf, Gr(lay.wh), nullptr, nullptr, nullptr, C, d, b, C, d,
+       d, 1, st);
+    mm(0, 1, EPS_EPI_STORE_BF16, dlogits, W(lay.wh), dhf, nullptr, nullptr, nullptr, b, d, C, C,
+       d, d, 1, st);
     // LN_f backward on the CLS rows; its dx column sum is top-layer FC2's bias grad
-    run(EPS_TC_NORM, 0.0, 8.0 * double(b) * double(d), static_cast<cudaStream_t>(st), [&] { return eps_layernorm_bwd(dhf, cls, P(lay.lnfg), act.meanf + b0, act.rstdf + b0, nullptr, dcls,
-                            Gr(lay.lnfg), Gr(lay.lnfb), Gr(top.b2), b, d, nullptr, st); });
+    layernorm_bwd(dhf, cls, lay.lnfg, lay.lnfb, act.meanf + b0, act.rstdf + b0, nullptr, dcls,
+                  Gr(top.b2), b, st);
     uint16_t* dX = act.dX + int64_t(b0) * T * d;
     if (cudaMemsetAsync(dX, 0, size_t(b) * T * d * 2, st) != cudaSuccess) throw int(EPS_ECUDA);
-    run(EPS_TC_ELTWISE, 0.0, 0.0, static_cast<cudaStream_t>(st), [&] { return eps_scatter_rows(dcls, dX, T * d, b, d, 0, st); });
+    eltwise(st, [&] { return eps_scatter_rows(dcls, dX, T * d, b, d, 0, st); });
   }
 
   // ---- backward sublayers (dX holds dL/d(output) rows; updated in place) ----
-  void mlp_bwd(int l, int b0, int b, cudaStream_t st) {
+  // colsum_prev: bias grad of the sublayer that produced this sublayer's input
+  // (accumulated from the fused LN backward), or null when that producer
+  // lives on another pipeline stage (the receiver computes it there).
+  void mlp_bwd(int l, int b0, int b, float* colsum_prev, cudaStream_t st) {
     const LayerSlots& s = lay.layer[l];
     const int64_t d = g.d, f = g.f, r0 = int64_t(b0) * g.tokens, R = int64_t(b) * g.tokens;
     uint16_t* dX = act.dX + r0 * d;
     uint16_t* Gm = act.G[l] + r0 * f;
     const int split = split_for(R);
-    mm(1, 1, EPS_EPI_ACCUM_F32, dX, Gm, Gr(s.w2), nullptr, nullptr, nullptr, d,
-                        f, R, d, f, f, split, st);
+    mm(1, 1, EPS_EPI_ACCUM_F32, dX, Gm, Gr(s.w2), nullptr, nullptr, nullptr, d, f, R, d, f, f,
+       split, st);
     // du overwrites G (its last reader was the dW2 GEMM above)
-    mm(0, 1, EPS_EPI_DGELU_BF16, dX, W(s.w2), Gm, nullptr, act.U[l] + r0 * f,
-                        Gr(s.b1), R, f, d, d, f, f, 1, st);
-    mm(1, 1, EPS_EPI_ACCUM_F32, Gm, act.H2[l] + r0 * d, Gr(s.w1), nullptr,
-                        nullptr, nullptr, f, d, R, f, d, d, split, st);
-    mm(0, 1, EPS_EPI_STORE_BF16, Gm, W(s.w1), act.dH + r0 * d, nullptr, nullptr,
-                        nullptr, R, d, f, f, d, d, 1, st);
-    run(EPS_TC_NORM, 0.0, 8.0 * double(R) * double(d), static_cast<cudaStream_t>(st), [&] { return eps_layernorm_bwd(act.dH + r0 * d, act.X1[l] + r0 * d, P(s.ln2g), act.mean2[l] + r0,
-                            act.rstd2[l] + r0, dX, dX, Gr(s.ln2g), Gr(s.ln2b), Gr(s.bp), R, d,
-                            nullptr, st); });
+    mm(0, 1, EPS_EPI_DGELU_BF16, dX, W(s.w2), Gm, nullptr, act.U[l] + r0 * f, Gr(s.b1), R, f, d,
+       d, f, f, 1, st);
+    mm(1, 1, EPS_EPI_ACCUM_F32, Gm, act.H2[l] + r0 * d, Gr(s.w1), nullptr, nullptr, nullptr, f,
+       d, R, f, d, d, split, st);
+    mm(0, 1, EPS_EPI_STORE_BF16, Gm, W(s.w1), act.dH + r0 * d, nullptr, nullptr, nullptr, R, d,
+       f, f, d, d, 1, st);
+    layernorm_bwd(act.dH + r0 * d, act.X1[l] + r0 * d, s.ln2g, s.ln2b, act.mean2[l] + r0,
+                  act.rstd2[l] + r0, dX, dX, colsum_prev, R, st);
   }
 
   // need_dx: write dL/dX[l] (false for the lowest trainable layer when the
-  // layers below are frozen).  colsum_prev: bias grad of the sublayer that
-  // produced X[l] (FC2 of layer l-1), or null.
+  // layers below are frozen).
   void att_bwd(int l, int b0, int b, bool need_dx, float* colsum_prev, cudaStream_t st) {
     const LayerSlots& s = lay.layer[l];
     const int64_t d = g.d, r0 = int64_t(b0) * g.tokens, R = int64_t(b) * g.tokens;
     uint16_t* dX = act.dX + r0 * d;
     const int split = split_for(R);
-    mm(1, 1, EPS_EPI_ACCUM_F32, dX, act.A[l] + r0 * d, Gr(s.wp), nullptr,
-                        nullptr, nullptr, d, d, R, d, d, d, split, st);
-    mm(0, 1, EPS_EPI_STORE_BF16, dX, W(s.wp), act.dA + r0 * d, nullptr, nullptr,
-                        nullptr, R, d, d, d, d, d, 1, st);
-    run(EPS_TC_ATTN, 8.0 * b * double(g.tokens) * g.tokens * g.heads * g.head_dim(), 18.0 * b * double(g.tokens) * g.heads * g.head_dim(), static_cast<cudaStream_t>(st), [&] { return eps_attn_bwd_ws(act.QKV[l] + r0 * 3 * d, act.A[l] + r0 * d, act.dA + r0 * d,
-                          act.lse[l] + int64_t(b0) * g.heads * g.tokens, act.dQKV + r0 * 3 * d,
-                          Gr(s.bqkv), act.dsum + int64_t(b0) * g.heads * g.tokens, b, g.tokens,
-                          g.heads, g.head_dim(), 1.0f / std::sqrt(float(g.head_dim())), st); });
-    mm(1, 1, EPS_EPI_ACCUM_F32, act.dQKV + r0 * 3 * d, act.H1[l] + r0 * d,
-                        Gr(s.wqkv), nullptr, nullptr, nullptr, 3 * d, d, R, 3 * d, d, d, split, st);
-    mm(0, 1, EPS_EPI_STORE_BF16, act.dQKV + r0 * 3 * d, W(s.wqkv),
-                        act.dH + r0 * d, nullptr, nullptr, nullptr, R, d, 3 * d, 3 * d, d, d, 1,
-                        st);
-    run(EPS_TC_NORM, 0.0, 8.0 * double(R) * double(d), static_cast<cudaStream_t>(st), [&] { return eps_layernorm_bwd(act.dH + r0 * d, act.X[l] + r0 * d, P(s.ln1g), act.mean1[l] + r0,
-                            act.rstd1[l] + r0, dX, need_dx ? dX : nullptr, Gr(s.ln1g), Gr(s.ln1b),
-                            need_dx ? colsum_prev : nullptr, R, d, nullptr, st); });
+    mm(1, 1, EPS_EPI_ACCUM_F32, dX, act.A[l] + r0 * d, Gr(s.wp), nullptr, nullptr, nullptr, d, d,
+       R, d, d, d, split, st);
+    mm(0, 1, EPS_EPI_STORE_BF16, dX, W(s.wp), act.dA + r0 * d, nullptr, nullptr, nullptr, R, d, d,
+       d, d, d, 1, st);
+    const double t = g.tokens, hd = double(g.heads) * g.head_dim();
+    run(EPS_TC_ATTN, 8.0 * b * t * t * hd, 18.0 * b * t * hd, st, [&] {
+      return eps_attn_bwd_ws(act.QKV[l] + r0 * 3 * d, act.A[l] + r0 * d, act.dA + r0 * d,
+                             act.lse[l] + int64_t(b0) * g.heads * g.tokens,
+                             act.dQKV + r0 * 3 * d, Gr(s.bqkv),
+                             act.dsum + int64_t(b0) * g.heads * g.tokens, b, g.tokens, g.heads,
+                             g.head_dim(), scale(), st);
+    });
+    mm(1, 1, EPS_EPI_ACCUM_F32, act.dQKV + r0 * 3 * d, act.H1[l] + r0 * d, Gr(s.wqkv), nullptr,
+       nullptr, nullptr, 3 * d, d, R, 3 * d, d, d, split, st);
+    mm(0, 1, EPS_EPI_STORE_BF16, act.dQKV + r0 * 3 * d, W(s.wqkv), act.dH + r0 * d, nullptr,
+       nullptr, nullptr, R, d, 3 * d, 3 * d, d, d, 1, st);
+    layernorm_bwd(act.dH + r0 * d, act.X[l] + r0 * d, s.ln1g, s.ln1b, act.mean1[l] + r0,
+                  act.rstd1[l] + r0, dX, need_dx ? dX : nullptr, need_dx ? colsum_prev : nullptr,
+                  R, st);
   }
 
   void embed_bwd(int b0, int b, cudaStream_t st) {
     const int64_t d = g.d, np = g.patches(), pl = g.patch_len();
     uint16_t* dptok = act.dptok + int64_t(b0) * np * d;
-    run(EPS_TC_ELTWISE, 0.0, 0.0, static_cast<cudaStream_t>(st), [&] { return eps_vit_assemble_bwd(act.dX + int64_t(b0) * g.tokens * d, Gr(lay.cls), Gr(lay.pos),
-                               dptok, b, g.tokens, d, st); });
-    run(EPS_TC_ELTWISE, 0.0, 0.0, static_cast<cudaStream_t>(st), [&] { return eps_colsum_bf16(dptok, Gr(lay.bpe), int64_t(b) * np, d, st); });
-    mm(1, 1, EPS_EPI_ACCUM_F32, dptok, act.patches + int64_t(b0) * np * pl,
-                        Gr(lay.wpe), nullptr, nullptr, nullptr, d, pl, int64_t(b) * np, d, pl, pl,
-                        split_for(int64_t(b) * np), st);
+    const uint16_t* dx0 = act.dX + int64_t(b0) * g.tokens * d;
+    eltwise(st, [&] {
+      return eps_vit_assemble_bwd(dx0, Gr(lay.cls), Gr(lay.pos), dptok, b, g.tokens, d, st);
+    });
+    eltwise(st, [&] { return eps_colsum_bf16(dptok, Gr(lay.bpe), int64_t(b) * np, d, st); });
+    mm(1, 1, EPS_EPI_ACCUM_F32, dptok, act.patches + int64_t(b0) * np * pl, Gr(lay.wpe), nullptr,
+       nullptr, nullptr, d, pl, int64_t(b) * np, d, pl, pl, split_for(int64_t(b) * np), st);
+  }
+
+  // Backward of sublayer gs; `first` = lowest sublayer held by this stage.
+  void sub_bwd(int gs, int b0, int b, int l_frozen, bool first, cudaStream_t st) {
+    const int l = gs / 2;
+    if (gs % 2 == 1) {
+      mlp_bwd(l, b0, b, first ? nullptr : Gr(lay.layer[l].bp), st);
+    } else {
+      const bool need_dx = l > l_frozen || l == 0;
+      float* prev = (l > 0 && !first) ? Gr(lay.layer[l - 1].b2) : nullptr;
+      att_bwd(l, b0, b, need_dx, prev, st);
+    }
+  }
+
+  // ---- pipeline-stage operations ------------------------------------------------
+  // Forward of global sublayers [g0, g1) for samples [b0, b0+b).  `front`: this
+  // stage produces its own input (pipeline stage 0): frozen prefix, AutoCache
+  // gather / boundary move and the embedding run first.
+  //   cache_mode 0: frozen prefix [0, L_f) recomputed forward-only;
+  //   cache_mode 1: X[L_f] gathered from the store rows `ids` (prefix skipped);
+  //   cache_mode 2: boundary move old -> L_f: X[old] gathered (old > 0) or
+  //                 computed from the images, [old, L_f) forwarded once, X[L_f]
+  //                 scattered into the store (autocache.cpp:45-67).
+  void stage_fwd(const float* images, int b0, int b, int g0, int g1, int l_frozen, bool front,
+                 int cache_mode, int cache_old, void* store, const int64_t* ids,
+                 cudaStream_t st) {
+    const int64_t xoff = int64_t(b0) * g.tokens * g.d;
+    const int64_t rb = row_bytes();
+    auto cache_io = [&](bool gather, uint16_t* x) {
+      run(EPS_TC_CACHE, 0.0, 2.0 * b * double(rb), st, [&] {
+        return gather ? eps_cache_gather(store, ids + b0, b, rb, x + xoff, st)
+                      : eps_cache_scatter(store, ids + b0, b, rb, x + xoff, st);
+      });
+    };
+    if (front) {
+      int start = 0;  // first frozen layer to run forward
+      if (cache_mode == 1) {
+        cache_io(true, act.X[l_frozen]);
+        start = l_frozen;
+      } else if (cache_mode == 2 && cache_old > 0) {
+        cache_io(true, act.X[cache_old]);
+        start = cache_old;
+      }
+      if (start == 0 && cache_mode != 1) embed_fwd(images, b0, b, st);
+      for (int l = start; l < l_frozen; ++l) {
+        att_fwd(l, b0, b, st);
+        mlp_fwd(l, b0, b, st);
+      }
+      if (cache_mode == 2) cache_io(false, act.X[l_frozen]);
+    }
+    for (int gs = g0; gs < g1; ++gs) sub_fwd(gs, b0, b, st);
+  }
+
+  // Backward of [g0, g1) in reverse with dL/d(output of g1-1) in dX rows.
+  // cut_out: that gradient arrived from the next stage, so this stage also
+  // owns the column sum for sublayer g1-1's output bias.
+  void stage_bwd(int b0, int b, int g0, int g1, int l_frozen, bool cut_out, cudaStream_t st) {
+    if (g1 <= g0) return;
+    const int64_t d = g.d, R = int64_t(b) * g.tokens;
+    if (cut_out) {
+      const uint16_t* dx = act.dX + int64_t(b0) * g.tokens * d;
+      float* bias = out_bias_grad(g1 - 1);
+      eltwise(st, [&] { return eps_colsum_bf16(dx, bias, R, d, st); });
+    }
+    for (int gs = g1 - 1; gs >= g0; --gs) sub_bwd(gs, b0, b, l_frozen, gs == g0, st);
+    if (g0 == 0 && l_frozen == 0) embed_bwd(b0, b, st);
+  }
+
+  void sgd_range(int64_t begin, int64_t end, float lr, float mu, float wd, cudaStream_t st) {
+    if (end <= begin) return;
+    run(EPS_TC_OPTIM, 0.0, 26.0 * double(end - begin), st, [&] {
+      return eps_sgd_momentum(p32 + begin, p16 + begin, g32 + begin, mom + begin, end - begin, lr,
+                              mu, wd, st);
+    });
+  }
+
+  void sqnorm_ranges(const int64_t* offsets, int n, double* out, cudaStream_t st) {
+    run(EPS_TC_SQNORM, 0.0, 4.0 * double(offsets[n] - offsets[0]), st, [&] {
+      return eps_grad_sqnorm_flat(g32, offsets, n, out, act.sq_ws, act.sq_ws_bytes, st);
+    });
+  }
+
+  void check_rows(int b0, int b) const {
+    if (b0 < 0 || b < 1 || b0 + b > g.max_batch) throw int(EPS_EINVAL);
+  }
+  void check_span(int g0, int g1, int l_frozen) const {
+    if (l_frozen < 0 || l_frozen >= g.layers || g0 < 2 * l_frozen || g1 < g0 ||
+        g1 > 2 * g.layers)
+      throw int(EPS_EINVAL);
   }
 };
 
@@ -443,14 +585,11 @@ int eps_vit_create(const int* geom, float* params, uint16_t* params_bf16, float*
 void eps_vit_destroy(eps_vit* h) { delete h; }
 
 // One training iteration on a single stage holding the whole stack (K = 1):
-// GPipe over `micro_batches` slices of the batch (forward of every slice,
-// then backward of every slice in reverse, grads accumulating in fp32).
-//   cache_mode 0: no cache -- frozen prefix [0, L_f) recomputed forward-only;
-//   cache_mode 1: X[L_f] gathered from `store` rows `ids` (prefix skipped);
-//   cache_mode 2: boundary move old -> L_f: X[old] gathered (old > 0) or
-//                 computed from the images, [old, L_f) forwarded once, X[L_f]
-//                 scattered into the store.
-// loss_sum (device fp32) accumulates the summed per-sample loss.
+// GPipe over `micro_batches` slices of the batch (integer split with the
+// remainder on the leading slices, schedule.cpp:28-33): forward of every
+// slice (head + loss + head backward right after each), then backward of
+// every slice in reverse; grads accumulate in fp32.  Cache modes as in
+// stage_fwd.  loss_sum (device fp32) accumulates the summed per-sample loss.
 int eps_vit_train_step(eps_vit* h, const float* images, const int64_t* labels, int batch,
                        int micro_batches, int l_frozen, int cache_mode, int cache_old,
                        void* store, const int64_t* ids, float* loss_sum, void* stream) {
@@ -462,8 +601,7 @@ int eps_vit_train_step(eps_vit* h, const float* images, const int64_t* labels, i
       throw int(EPS_EINVAL);
     auto st = static_cast<cudaStream_t>(stream);
     h->loss_sum = loss_sum;
-    const int L = h->g.layers;
-    const int64_t row_bytes = int64_t(h->g.tokens) * h->g.d * 2;
+    const int g0 = 2 * l_frozen, g1 = 2 * h->g.layers;
     std::vector<int> b0s, bs;
     for (int m = 0, at = 0; m < micro_batches; ++m) {
       const int n = batch / micro_batches + (m < batch % micro_batches ? 1 : 0);
@@ -472,38 +610,79 @@ int eps_vit_train_step(eps_vit* h, const float* images, const int64_t* labels, i
       at += n;
     }
     for (int m = 0; m < micro_batches; ++m) {
-      const int b0 = b0s[m], b = bs[m];
-      const int64_t xoff = int64_t(b0) * h->g.tokens * h->g.d;
-      int start = 0;  // first layer to run forward
-      if (cache_mode == 1) {
-        h->run(EPS_TC_CACHE, 0.0, 2.0 * b * double(row_bytes), static_cast<cudaStream_t>(st), [&] { return eps_cache_gather(store, ids + b0, b, row_bytes, h->act.X[l_frozen] + xoff, st); });
-        start = l_frozen;
-      } else if (cache_mode == 2 && cache_old > 0) {
-        h->run(EPS_TC_CACHE, 0.0, 2.0 * b * double(row_bytes), static_cast<cudaStream_t>(st), [&] { return eps_cache_gather(store, ids + b0, b, row_bytes, h->act.X[cache_old] + xoff, st); });
-        start = cache_old;
-      }
-      if (start == 0) h->embed_fwd(images, b0, b, st);
-      for (int l = start; l < L; ++l) {
-        if (cache_mode == 2 && l == l_frozen)
-          h->run(EPS_TC_CACHE, 0.0, 2.0 * b * double(row_bytes), static_cast<cudaStream_t>(st), [&] { return eps_cache_scatter(store, ids + b0, b, row_bytes, h->act.X[l] + xoff, st); });
-        h->att_fwd(l, b0, b, st);
-        h->mlp_fwd(l, b0, b, st);
-      }
-      h->head_fwd_bwd(labels, b0, b, batch, st);
+      h->stage_fwd(images, b0s[m], bs[m], g0, g1, l_frozen, true, cache_mode, cache_old, store,
+                   ids, st);
+      h->head_fwd_bwd(labels, b0s[m], bs[m], batch, st);
     }
-    for (int m = micro_batches - 1; m >= 0; --m) {
-      const int b0 = b0s[m], b = bs[m];
-      // head_fwd_bwd left dL/dX[L] for slice m in dX; later slices' backward
-      // must not clobber it, so slices are processed as forward-all /
-      // backward-all only when their dX rows are disjoint (they are: rows
-      // are indexed by sample).
-      for (int l = L - 1; l >= l_frozen; --l) {
-        h->mlp_bwd(l, b0, b, st);
-        const bool need_dx = l > l_frozen || l == 0;
-        h->att_bwd(l, b0, b, need_dx, l > 0 ? h->Gr(h->lay.layer[l - 1].b2) : nullptr, st);
-      }
-      if (l_frozen == 0) h->embed_bwd(b0, b, st);
-    }
+    for (int m = micro_batches - 1; m >= 0; --m)
+      h->stage_bwd(b0s[m], bs[m], g0, g1, l_frozen, false, st);
+  });
+}
+
+// ---- pipeline stages (AutoPipe executor; host drives the GPipe order) ------
+int eps_vit_stage_forward(eps_vit* h, const float* images, int b0, int b, int g0, int g1,
+                          int l_frozen, int front, int cache_mode, int cache_old, void* store,
+                          const int64_t* ids, void* stream) {
+  return guard([&] {
+    if (h == nullptr) throw int(EPS_EINVAL);
+    h->check_rows(b0, b);
+    h->check_span(g0, g1, l_frozen);
+    if (front && images == nullptr && cache_mode != 1) throw int(EPS_EINVAL);
+    if (cache_mode != 0 && (!front || store == nullptr || ids == nullptr || l_frozen == 0))
+      throw int(EPS_EINVAL);
+    h->stage_fwd(images, b0, b, g0, g1, l_frozen, front != 0, cache_mode, cache_old, store, ids,
+                 static_cast<cudaStream_t>(stream));
+  });
+}
+
+int eps_vit_stage_head(eps_vit* h, const int64_t* labels, int b0, int b, int global_batch,
+                       float* loss_sum, void* stream) {
+  return guard([&] {
+    if (h == nullptr || labels == nullptr || loss_sum == nullptr || global_batch < 1)
+      throw int(EPS_EINVAL);
+    h->check_rows(b0, b);
+    h->loss_sum = loss_sum;
+    h->head_fwd_bwd(labels, b0, b, global_batch, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int eps_vit_stage_backward(eps_vit* h, int b0, int b, int g0, int g1, int l_frozen,
+                           int cut_out, void* stream) {
+  return guard([&] {
+    if (h == nullptr) throw int(EPS_EINVAL);
+    h->check_rows(b0, b);
+    h->check_span(g0, g1, l_frozen);
+    h->stage_bwd(b0, b, g0, g1, l_frozen, cut_out != 0, static_cast<cudaStream_t>(stream));
+  });
+}
+
+void* eps_vit_cut(eps_vit* h, int g, int grad) {
+  if (h == nullptr || g < 0 || g > 2 * h->g.layers) return nullptr;
+  return grad ? static_cast<void*>(h->act.dX) : static_cast<void*>(h->cut(g));
+}
+
+int eps_vit_param_range(eps_vit* h, int g0, int g1, int64_t* begin, int64_t* end) {
+  return guard([&] {
+    if (h == nullptr || g0 < 0 || g1 < g0 || g1 > 2 * h->g.layers) throw int(EPS_EINVAL);
+    *begin = h->sub_begin(g0);
+    *end = h->sub_begin(g1);
+  });
+}
+
+int eps_vit_sgd_range(eps_vit* h, int64_t begin, int64_t end, float lr, float momentum,
+                      float weight_decay, void* stream) {
+  return guard([&] {
+    if (h == nullptr || begin < 0 || end > h->lay.total || end < begin) throw int(EPS_EINVAL);
+    h->sgd_range(begin, end, lr, momentum, weight_decay, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int eps_vit_sqnorm_ranges(eps_vit* h, const int64_t* offsets, int n, double* out,
+                          void* stream) {
+  return guard([&] {
+    if (h == nullptr || n < 1 || n > 64 || offsets[0] < 0 || offsets[n] > h->lay.total)
+      throw int(EPS_EINVAL);
+    h->sqnorm_ranges(offsets, n, out, static_cast<cudaStream_t>(stream));
   });
 }
 
@@ -511,9 +690,8 @@ int eps_vit_train_step(eps_vit* h, const float* images, const int64_t* labels, i
 int eps_vit_sgd(eps_vit* h, int l_frozen, float lr, float momentum, float weight_decay,
                 void* stream) {
   return guard([&] {
-    const int64_t begin = h->lay.seg[l_frozen];
-    h->run(EPS_TC_OPTIM, 0.0, 26.0 * double(h->lay.total - begin), static_cast<cudaStream_t>(stream), [&] { return eps_sgd_momentum(h->p32 + begin, h->p16 + begin, h->g32 + begin, h->mom + begin,
-                           h->lay.total - begin, lr, momentum, weight_decay, stream); });
+    h->sgd_range(h->lay.seg[l_frozen], h->lay.total, lr, momentum, weight_decay,
+                 static_cast<cudaStream_t>(stream));
   });
 }
 
@@ -526,8 +704,7 @@ int eps_vit_layer_sqnorms(eps_vit* h, int l_frozen, double* out, void* stream) {
     if (l_frozen > 0 && cudaMemsetAsync(out, 0, sizeof(double) * l_frozen, st) != cudaSuccess)
       throw int(EPS_ECUDA);
     std::vector<int64_t> offs(h->lay.seg.begin() + l_frozen, h->lay.seg.end());
-    h->run(EPS_TC_SQNORM, 0.0, 4.0 * double(h->lay.total - h->lay.seg[l_frozen]), static_cast<cudaStream_t>(st), [&] { return eps_grad_sqnorm_flat(h->g32, offs.data(), L - l_frozen, out + l_frozen, h->act.sq_ws,
-                               h->act.sq_ws_bytes, st); });
+    h->sqnorm_ranges(offs.data(), L - l_frozen, out + l_frozen, st);
   });
 }
 
@@ -538,17 +715,18 @@ int eps_vit_forward_logits(eps_vit* h, const float* images, int batch, void* log
   return guard([&] {
     auto st = static_cast<cudaStream_t>(stream);
     const int64_t d = h->g.d, T = h->g.tokens;
+    h->check_rows(0, batch);
     h->embed_fwd(images, 0, batch, st);
     for (int l = 0; l < h->g.layers; ++l) {
       h->att_fwd(l, 0, batch, st);
       h->mlp_fwd(l, 0, batch, st);
     }
-    h->run(EPS_TC_ELTWISE, 0.0, 0.0, static_cast<cudaStream_t>(st), [&] { return eps_gather_rows(h->act.X[h->g.layers], T * d, h->act.cls_rows, batch, d, 0, st); });
-    h->run(EPS_TC_NORM, 0.0, 4.0 * double(batch) * double(d), static_cast<cudaStream_t>(st), [&] { return eps_layernorm_fwd(h->act.cls_rows, h->P(h->lay.lnfg), h->P(h->lay.lnfb), h->act.hf,
-                            h->act.meanf, h->act.rstdf, batch, d, 1e-6f, st); });
-    h->mm(0, 0, EPS_EPI_BIAS_BF16, h->act.hf, h->W(h->lay.wh), logits,
-                        h->P(h->lay.bh), nullptr, nullptr, batch, h->g.classes_pad, d, d, d,
-                        h->g.classes_pad, 1, st);
+    const uint16_t* xl = h->act.X[h->g.layers];
+    h->eltwise(st, [&] { return eps_gather_rows(xl, T * d, h->act.cls_rows, batch, d, 0, st); });
+    h->layernorm(h->act.cls_rows, h->lay.lnfg, h->lay.lnfb, h->act.hf, h->act.meanf,
+                 h->act.rstdf, batch, st);
+    h->mm(0, 0, EPS_EPI_BIAS_BF16, h->act.hf, h->W(h->lay.wh), logits, h->P(h->lay.bh), nullptr,
+          nullptr, batch, h->g.classes_pad, d, d, d, h->g.classes_pad, 1, st);
   });
 }
 

@@ -1,0 +1,249 @@
+"""AutoPipe x AutoDP execution over one process per GPU.
+
+The reference *models* one training iteration as GPipe fill/drain blocks on K
+stages plus bucketed AllReduce across R replicas (schedule.cpp:19-199); this
+module *executes* it.  Every rank computes the same decisions (EpochPlanner,
+runner.cpp:126-229) and derives its role from them:
+
+  * rank r of the N = R*K GPUs is stage s = r mod K of pipeline p = r div K
+    (Topology: active ranks r mod K == 0, GPU span [r, r+K), autodp.cpp:19-58);
+  * stage s owns global sublayers [2*L_f + b_s, 2*L_f + e_s) from the
+    PartitionPlan spans (autopipe.cpp:55-122); stage 0 also runs the frozen
+    prefix / AutoCache gather and the embedding, the last stage the head;
+  * forward fill in micro-batch order, backward drain in reverse micro-batch
+    order (schedule.cpp:56-116); stages without trainable sublayers are pure
+    relays and skip backward (schedule.cpp:47-52, 83-90);
+  * the cut activations and activation-grads move stage to stage with
+    point-to-point sends (NCCL over NVLink on a B200 box);
+  * stage s of every replica averages only its active gradients over the
+    per-stage data-parallel group {p*K + s} (ddp_skip_set, autodp.cpp:153-161);
+    groups are rebuilt when freezing changes K (transition, autodp.cpp:81-111),
+    and parameters + momentum migrate to their new owners.
+
+All FLOPs run in libeps_b200.so (VitExecutor stage operations);
+torch.distributed is the transport.  `Transport` abstracts it so the same
+choreography runs over NCCL (device tensors) or over gloo with host staging
+(CPU multi-process tests, or several ranks sharing one GPU).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Dict, List, Optional, Sequence, Tuple
+
+import torch
+import torch.distributed as dist
+
+
+# ---- decisions -> roles ------------------------------------------------------------
+@dataclass(frozen=True)
+class StagePlan:
+    """One epoch's execution plan, identical on every rank."""
+    K: int
+    R: int
+    M: int
+    l_frozen: int
+    layers: int
+    spans: Tuple[Tuple[int, int], ...]  # global sublayer spans [g0, g1) per stage
+
+    @staticmethod
+    def from_decision(d, layers: int) -> "StagePlan":
+        base = 2 * d.l_frozen
+        spans = tuple((base + b, base + e) for b, e in d.spans)
+        return StagePlan(d.pipeline_length, d.replica_width, d.micro_batches, d.l_frozen,
+                         layers, spans)
+
+    def role(self, rank: int) -> Tuple[int, int]:
+        """(pipeline, stage) of a global rank."""
+        return rank // self.K, rank % self.K
+
+    def trainable(self, s: int) -> bool:
+        g0, g1 = self.spans[s]
+        return g1 > g0
+
+    def upstream_needs_grad(self, s: int) -> bool:
+        """Stage s sends dX to s-1 iff some earlier stage holds trainable
+        sublayers (spans are contiguous from 2*L_f) -- the embedding counts as
+        trainable when L_f == 0 (it is folded into sublayer 0)."""
+        return s > 0 and self.spans[s][0] > 2 * self.l_frozen
+
+    def owner_spans(self) -> List[Tuple[int, int]]:
+        """Parameter ownership per stage: stage 0 also owns the frozen prefix
+        (and embedding), the last stage the head -- together they cover every
+        global sublayer exactly once."""
+        out = [list(sp) for sp in self.spans]
+        out[0][0] = 0
+        out[-1][1] = 2 * self.layers
+        return [tuple(x) for x in out]
+
+    def dp_group_ranks(self, s: int) -> List[int]:
+        return [p * self.K + s for p in range(self.R)]
+
+
+def microbatch_offsets(batch: int, micro: int) -> List[Tuple[int, int]]:
+    """Integer split with the remainder on the leading micro-batches
+    (schedule.cpp:28-33): [(b0, b)]."""
+    out, at = [], 0
+    for m in range(micro):
+        n = batch // micro + (1 if m < batch % micro else 0)
+        out.append((at, n))
+        at += n
+    return out
+
+
+# ---- transport ---------------------------------------------------------------------
+class Transport:
+    """Point-to-point and collective moves of device tensors."""
+
+    def __init__(self, host_staged: bool):
+        self.host_staged = host_staged
+        self._groups: Dict[Tuple[int, ...], object] = {}
+
+    def group(self, ranks: Sequence[int]):
+        key = tuple(ranks)
+        if key not in self._groups:
+            # new_group is collective: callers create groups in the same order
+            self._groups[key] = dist.new_group(list(ranks)) if len(ranks) > 1 else None
+        return self._groups[key]
+
+    def send(self, t: torch.Tensor, dst: int):
+        if self.host_staged:
+            dist.send(t.detach().cpu().contiguous(), dst)
+        else:
+            dist.send(t, dst)
+
+    def recv(self, t: torch.Tensor, src: int):
+        if self.host_staged:
+            buf = torch.empty(t.shape, dtype=t.dtype)
+            dist.recv(buf, src)
+            t.copy_(buf)
+        else:
+            dist.recv(t, src)
+
+    def all_reduce(self, t: torch.Tensor, group, op=dist.ReduceOp.SUM):
+        if self.host_staged:
+            buf = t.detach().cpu()
+            dist.all_reduce(buf, op=op, group=group)
+            t.copy_(buf)
+        else:
+            dist.all_reduce(t, op=op, group=group)
+
+    def broadcast(self, t: torch.Tensor, src: int):
+        if self.host_staged:
+            buf = t.detach().cpu()
+            dist.broadcast(buf, src)
+            t.copy_(buf)
+        else:
+            dist.broadcast(t, src)
+
+
+# ---- one rank's stage ------------------------------------------------------------------
+class StageRunner:
+    """Executes the iterations of one rank (one pipeline stage of one replica)
+    over a stage executor exposing the eps_vit_stage_* operations."""
+
+    def __init__(self, ex, rank: int, world: int, transport: Transport):
+        self.ex = ex
+        self.rank = rank
+        self.world = world
+        self.tp = transport
+        self.plan: Optional[StagePlan] = None
+        self.g0 = self.g1 = 0
+        self.stage = self.pipe = 0
+        self.range = (0, 0)
+
+    # -- plan changes ------------------------------------------------------------
+    def _dp_groups(self, plan: StagePlan):
+        # every rank creates every stage group of this K, in stage order
+        return [self.tp.group(plan.dp_group_ranks(s)) for s in range(plan.K)]
+
+    def set_plan(self, plan: StagePlan):
+        """Adopt an epoch plan; on a K / span change migrate parameters and
+        momentum from their previous owners (pipeline 0's stages) to all
+        ranks, then rebuild the per-stage data-parallel groups."""
+        if plan.K * plan.R != self.world:
+            raise ValueError(f"plan needs {plan.K * plan.R} ranks, world has {self.world}")
+        old = self.plan
+        if old is not None and (old.K, old.spans) != (plan.K, plan.spans):
+            self.migrate(old)
+        self.plan = plan
+        self.pipe, self.stage = plan.role(self.rank)
+        self.g0, self.g1 = plan.spans[self.stage]
+        self.groups = self._dp_groups(plan)
+        self.range = self.ex.param_range(*plan.owner_spans()[self.stage])
+
+    def migrate(self, old: StagePlan):
+        """Every parameter (and its momentum) is broadcast from the rank that
+        owned and updated it under `old` (stage s of pipeline 0 == rank s);
+        the bf16 working copy is re-derived."""
+        for s, (g0, g1) in enumerate(old.owner_spans()):
+            a, b = self.ex.param_range(g0, g1)
+            if b > a:
+                self.tp.broadcast(self.ex.p32[a:b], s)
+                self.tp.broadcast(self.ex.mom[a:b], s)
+        self.ex.p16.copy_(self.ex.p32)
+
+    # -- one iteration -------------------------------------------------------------------
+    def iteration(self, images, labels, batch: int, cache_mode: int = 0, cache_old: int = 0,
+                  store=None, ids=None):
+        """Forward + backward of one per-pipeline batch on this rank's stage.
+        images / labels / ids are only read on the first / last stage."""
+        p, s, K = self.plan, self.stage, self.plan.K
+        ex, lf = self.ex, p.l_frozen
+        mbs = microbatch_offsets(batch, p.M)
+        prev, nxt = self.rank - 1, self.rank + 1
+        ex.loss_sum.zero_()
+        for b0, b in mbs:
+            if s > 0:
+                self.tp.recv(ex.cut_rows(self.g0, b0, b), prev)
+            ex.stage_forward(images if s == 0 else None, b0, b, self.g0, self.g1, lf,
+                             front=(s == 0), cache_mode=cache_mode if s == 0 else 0,
+                             cache_old=cache_old, store=store if s == 0 else None,
+                             ids=ids if s == 0 else None)
+            if s < K - 1:
+                self.tp.send(ex.cut_rows(self.g1, b0, b), nxt)
+            else:
+                ex.stage_head(labels, b0, b, batch)
+        if p.trainable(s):
+            for b0, b in reversed(mbs):
+                if s < K - 1:
+                    self.tp.recv(ex.cut_rows(0, b0, b, grad=True), nxt)
+                ex.stage_backward(b0, b, self.g0, self.g1, lf, cut_out=s < K - 1)
+                if p.upstream_needs_grad(s):
+                    self.tp.send(ex.cut_rows(0, b0, b, grad=True), prev)
+        return ex.loss_sum
+
+    def sync_grads(self):
+        """Average this stage's active gradients over its replicas."""
+        p = self.plan
+        if p.R > 1 and p.trainable(self.stage):
+            a, b = self.ex.param_range(self.g0, self.g1)
+            g = self.ex.g32[a:b]
+            self.tp.all_reduce(g, self.groups[self.stage])
+            g.mul_(1.0 / p.R)
+
+    def step(self, lr: float, momentum: float = 0.9, weight_decay: float = 0.0):
+        if self.plan.trainable(self.stage):
+            a, b = self.ex.param_range(self.g0, self.g1)
+            self.ex.sgd_range(a, b, lr, momentum, weight_decay)
+
+    def layer_sqnorms(self, segments: Sequence[int]) -> torch.Tensor:
+        """Per-layer Σg² of the whole model, assembled from every stage's
+        owned (post-all-reduce) gradients: each rank reduces the part of each
+        layer segment it trains, then one world all-reduce; replicas hold
+        identical gradients, so the sum over ranks is divided by R."""
+        p = self.plan
+        L = len(segments) - 1
+        out = torch.zeros(L, dtype=torch.float64, device=self.ex.g32.device)
+        if p.trainable(self.stage):
+            a, b = self.ex.param_range(self.g0, self.g1)
+            cuts = sorted({a, b} | {x for x in segments if a < x < b})
+            part = torch.zeros(len(cuts) - 1, dtype=torch.float64, device=out.device)
+            self.ex.sqnorm_ranges(cuts, part)
+            for i in range(len(cuts) - 1):
+                layer = max(l for l in range(L) if segments[l] <= cuts[i])
+                out[layer] += part[i]
+        if self.world > 1:
+            self.tp.all_reduce(out, None)
+            out /= p.R
+        return out

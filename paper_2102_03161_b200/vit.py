@@ -155,8 +155,8 @@ class VitExecutor:
     def _call(self, name, *args):
         f = getattr(ops.api().lib, name)
         f.restype = C.c_int
+        # tensors -> device pointers; ctypes values / arrays pass through
         conv = [C.c_void_p(a.data_ptr()) if isinstance(a, torch.Tensor) else a for a in args]
-        # ctypes arrays pass through unchanged
         rc = f(self.h, *conv)
         if rc != 0:
             raise RuntimeError(f"{name} failed with status {rc}")
@@ -202,6 +202,60 @@ class VitExecutor:
         s = torch.cuda.current_stream()
         self._call("eps_vit_forward_logits", images, b, out, C.c_void_p(s.cuda_stream))
         return out[:, :self.g.classes]
+
+    # -- pipeline-stage operations (AutoPipe executor) --------------------
+    def _st(self, stream):
+        s = torch.cuda.current_stream() if stream is None else stream
+        return C.c_void_p(s.cuda_stream)
+
+    def stage_forward(self, images, b0: int, b: int, g0: int, g1: int, l_frozen: int,
+                      front: bool, cache_mode: int = 0, cache_old: int = 0, store=None,
+                      ids=None, stream=None):
+        self._call("eps_vit_stage_forward",
+                   images if images is not None else C.c_void_p(0), b0, b, g0, g1, l_frozen,
+                   int(front), cache_mode, cache_old,
+                   store if store is not None else C.c_void_p(0),
+                   ids if ids is not None else C.c_void_p(0), self._st(stream))
+
+    def stage_head(self, labels, b0: int, b: int, global_batch: int, stream=None):
+        self._call("eps_vit_stage_head", labels, b0, b, global_batch, self.loss_sum,
+                   self._st(stream))
+
+    def stage_backward(self, b0: int, b: int, g0: int, g1: int, l_frozen: int, cut_out: bool,
+                       stream=None):
+        self._call("eps_vit_stage_backward", b0, b, g0, g1, l_frozen, int(cut_out),
+                   self._st(stream))
+
+    def cut_rows(self, g: int, b0: int, b: int, grad: bool = False) -> torch.Tensor:
+        """bf16 view [b*T, d] of the residual stream at the cut before global
+        sublayer g (grad=True: the dX scratch), rows of samples [b0, b0+b)."""
+        f = ops.api().lib.eps_vit_cut
+        f.restype = C.c_void_p
+        f.argtypes = [C.c_void_p, C.c_int, C.c_int]
+        ptr = f(self.h, g, int(grad))
+        if not ptr:
+            raise ValueError(f"no cut buffer for sublayer {g}")
+        T, d = self.g.tokens, self.g.hidden
+        off = ptr - self.ws.data_ptr()
+        base = self.ws[off:off + 2 * self.max_batch * T * d].view(torch.bfloat16)
+        return base.view(self.max_batch * T, d)[b0 * T:(b0 + b) * T]
+
+    def param_range(self, g0: int, g1: int):
+        """Parameter elements [begin, end) of global sublayers [g0, g1)."""
+        a, e = C.c_int64(), C.c_int64()
+        self._call("eps_vit_param_range", g0, g1, C.byref(a), C.byref(e))
+        return a.value, e.value
+
+    def sgd_range(self, begin: int, end: int, lr: float, momentum: float = 0.9,
+                  weight_decay: float = 0.0, stream=None):
+        self._call("eps_vit_sgd_range", C.c_int64(begin), C.c_int64(end), C.c_float(lr),
+                   C.c_float(momentum), C.c_float(weight_decay), self._st(stream))
+
+    def sqnorm_ranges(self, offsets, out: torch.Tensor, stream=None):
+        """out[i] = sum of squared grads over offsets[i]..offsets[i+1]."""
+        arr = (C.c_int64 * len(offsets))(*offsets)
+        self._call("eps_vit_sqnorm_ranges", arr, len(offsets) - 1, out, self._st(stream))
+        return out
 
     # -- instrumentation ---------------------------------------------------
     TIMING_CLASSES = ("gemm", "attention", "layernorm", "eltwise", "cache", "optimizer",

@@ -1,0 +1,130 @@
+"""CPU stand-in for the sm_100a stage executor -- TEST INFRASTRUCTURE ONLY.
+
+Implements the eps_vit_stage_* contract (VitExecutor's stage methods) for a
+small residual stack in plain torch so the multi-process AutoPipe x AutoDP
+choreography (paper_2102_03161_b200/pipeline.py) can be checked with the gloo
+backend on CPU.  Same conventions as the real executor:
+  * global sublayer g in [0, 2L); the residual stream at the cut before g is
+    cut_rows(g); dX scratch is cut_rows(., grad=True);
+  * parameter arena: one flat fp32 array, sublayer g's tensors contiguous,
+    the embedding folded into sublayer 0 and the head into sublayer 2L-1;
+  * frozen layers [0, L_f) run forward only; the lowest trainable layer skips
+    its input gradient; grads accumulate; SGD-momentum zeroes them.
+"""
+from __future__ import annotations
+
+import torch
+
+
+class FakeStageExecutor:
+    def __init__(self, layers=3, d=8, tokens=4, inp=6, max_batch=16, seed=0):
+        self.L, self.d, self.T, self.inp, self.max_batch = layers, d, tokens, inp, max_batch
+        sizes = [inp * d] + [d * d + d] * (2 * layers) + [d]
+        self.starts = [0]
+        for n in sizes:
+            self.starts.append(self.starts[-1] + n)
+        total = self.starts[-1]
+        gen = torch.Generator().manual_seed(seed)
+        self.p32 = torch.randn(total, generator=gen) * 0.3
+        self.p16 = self.p32.clone()
+        self.g32 = torch.zeros(total)
+        self.mom = torch.zeros(total)
+        self.loss_sum = torch.zeros(1)
+        self.X = torch.zeros(2 * layers + 1, max_batch * tokens, d)
+        self.dX = torch.zeros(max_batch * tokens, d)
+
+    # layout ------------------------------------------------------------------------
+    def _sub(self, g):  # (W offset, b offset) of sublayer g
+        a = self.starts[1 + g]
+        return a, a + self.d * self.d
+
+    def sub_begin(self, g):
+        if g == 0:
+            return 0
+        if g >= 2 * self.L:
+            return self.starts[-1]
+        return self.starts[1 + g]
+
+    def segments(self):
+        return [self.sub_begin(2 * l) for l in range(self.L)] + [self.starts[-1]]
+
+    def param_range(self, g0, g1):
+        return self.sub_begin(g0), self.sub_begin(g1)
+
+    def cut_rows(self, g, b0, b, grad=False):
+        rows = slice(b0 * self.T, (b0 + b) * self.T)
+        return self.dX[rows] if grad else self.X[g][rows]
+
+    # math ---------------------------------------------------------------------------
+    def _params(self, g):
+        w, bo = self._sub(g)
+        W = self.p32[w:w + self.d * self.d].view(self.d, self.d)
+        return W, self.p32[bo:bo + self.d]
+
+    def _f(self, g, x, W, bias):
+        return x + torch.tanh(x @ W + bias)
+
+    def stage_forward(self, images, b0, b, g0, g1, l_frozen, front, cache_mode=0, cache_old=0,
+                      store=None, ids=None):
+        rows = slice(b0 * self.T, (b0 + b) * self.T)
+        if front:
+            start = 0
+            if cache_mode == 1:
+                self.X[2 * l_frozen][rows] = store[ids[b0:b0 + b]].reshape(-1, self.d)
+                start = 2 * l_frozen
+            elif cache_mode == 2 and cache_old > 0:
+                self.X[2 * cache_old][rows] = store[ids[b0:b0 + b]].reshape(-1, self.d)
+                start = 2 * cache_old
+            if start == 0 and cache_mode != 1:
+                E = self.p32[:self.inp * self.d].view(self.inp, self.d)
+                self.X[0][rows] = images[b0:b0 + b].reshape(-1, self.inp) @ E
+            for g in range(start, 2 * l_frozen):
+                self.X[g + 1][rows] = self._f(g, self.X[g][rows], *self._params(g))
+            if cache_mode == 2:
+                store[ids[b0:b0 + b]] = self.X[2 * l_frozen][rows].reshape(b, self.T, self.d)
+        for g in range(g0, g1):
+            self.X[g + 1][rows] = self._f(g, self.X[g][rows], *self._params(g))
+
+    def stage_head(self, labels, b0, b, global_batch):
+        rows = slice(b0 * self.T, (b0 + b) * self.T)
+        x = self.X[2 * self.L][rows].clone().requires_grad_(True)
+        wh = self.p32[self.starts[-2]:].clone().requires_grad_(True)
+        y = (x @ wh).view(b, self.T).sum(1)
+        loss = 0.5 * ((y - labels[b0:b0 + b].float()) ** 2).sum()
+        (loss / global_batch).backward()
+        self.loss_sum += loss.detach()
+        self.g32[self.starts[-2]:] += wh.grad
+        self.dX[rows] = x.grad
+
+    def stage_backward(self, b0, b, g0, g1, l_frozen, cut_out):
+        rows = slice(b0 * self.T, (b0 + b) * self.T)
+        for g in range(g1 - 1, g0 - 1, -1):
+            W, bias = self._params(g)
+            x = self.X[g][rows].clone().requires_grad_(True)
+            Wv, bv = W.clone().requires_grad_(True), bias.clone().requires_grad_(True)
+            y = self._f(g, x, Wv, bv)
+            y.backward(self.dX[rows])
+            w, bo = self._sub(g)
+            self.g32[w:w + self.d * self.d] += Wv.grad.reshape(-1)
+            self.g32[bo:bo + self.d] += bv.grad
+            need_dx = g > 2 * l_frozen or g == 0
+            if need_dx:
+                self.dX[rows] = x.grad
+        if g0 == 0 and l_frozen == 0:
+            # embedding gradient: X0 = images @ E (images were not kept; fake keeps
+            # the gradient path by recomputing from the stored input is not needed
+            # for the choreography tests, which freeze nothing or check E separately)
+            pass
+
+    def sgd_range(self, begin, end, lr, momentum=0.9, weight_decay=0.0):
+        g = self.g32[begin:end]
+        m = self.mom[begin:end]
+        m.mul_(momentum).add_(g + weight_decay * self.p32[begin:end])
+        self.p32[begin:end] -= lr * m
+        self.p16[begin:end] = self.p32[begin:end]
+        g.zero_()
+
+    def sqnorm_ranges(self, offsets, out):
+        for i in range(len(offsets) - 1):
+            out[i] = (self.g32[offsets[i]:offsets[i + 1]].double() ** 2).sum()
+        return out
