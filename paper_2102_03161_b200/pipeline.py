@@ -176,6 +176,8 @@ class StageRunner:
         """Every parameter (and its momentum) is broadcast from the rank that
         owned and updated it under `old` (stage s of pipeline 0 == rank s);
         the bf16 working copy is re-derived."""
+        if self.world == 1:
+            return  # a single rank owns everything already
         for s, (g0, g1) in enumerate(old.owner_spans()):
             a, b = self.ex.param_range(g0, g1)
             if b > a:
