@@ -15,11 +15,12 @@ per-epoch decisions (L_frozen, AutoCache gather / boundary move) on the
 device and reports the measured end-to-end speedup vs no-freeze
 (runner.cpp:298 semantics: baseline total time / freeze total time).
 
-N > 1 (torchrun, one rank per GPU, NCCL): every rank is an AutoDP replica
-holding the whole stack (K = 1) and the active-layer gradients are averaged
-with one NCCL all-reduce per step -- the AutoPipe P2P executor for K > 1 is
-not built yet, so `config.parallelism` says dp{N} and `config.planner` shows
-what the reference planner would pick.
+N > 1 (torchrun, one rank per GPU, NCCL): the ranks execute the planner's
+plan -- K-stage GPipe pipelines (cut activations / gradients over NCCL
+point-to-point on NVLink) times R AutoDP replicas (per-stage NCCL all-reduce
+of the active gradients).  At epoch 0 the reference plans K = N, R = 1, so
+the per-step work is one 400-image batch at every N ("scaling": "strong");
+the freeze schedule forks replicas as layers freeze.
 
 `--impl reference` times the reference path's CPU implementation -- the fp32
 restatement in oracle/vit_fp32.py (the reference itself has no tensor code,
@@ -57,6 +58,8 @@ def parse():
     ap.add_argument("--no-schedule", action="store_true", help="skip the freeze-schedule replay")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--gloo-one-gpu", action="store_true",
+                    help="test mode: all ranks share cuda:0, gloo with host-staged transfers")
     return ap.parse_args()
 
 
@@ -214,39 +217,40 @@ def run_reference(args, world, rank):
 def main_ours(args, world, rank, local):
     from paper_2102_03161_b200 import LIB_PATH, configs, ops
     from paper_2102_03161_b200.capi import EpsApi
+    from paper_2102_03161_b200.pipeline import StagePlan, StageRunner, Transport
     from paper_2102_03161_b200.planner import Planner
     from paper_2102_03161_b200.vit import VitExecutor
 
-    dev = torch.device("cuda", local)
+    one_gpu = args.gloo_one_gpu
+    dev = torch.device("cuda", 0 if one_gpu else local)
     torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     g = configs.GEOMETRIES[args.config]
     batch = configs.BATCH[args.config]
     scen = configs.scenario(args.config, world)
-    api = EpsApi(LIB_PATH, "eps_")
-    planner = Planner(api, scen)
+    planner = Planner(EpsApi(LIB_PATH, "eps_"), scen)
     decisions = [planner.begin_epoch(e) for e in range(configs.EPOCHS[args.config])]
-    d0 = decisions[0]
-    micro = d0.micro_batches if d0.pipeline_length == 1 else 1
+    plan0 = StagePlan.from_decision(decisions[0], g.layers)
 
     ex = VitExecutor(g, max_batch=batch, seed=17, device=dev)
-    gen = torch.Generator(device=dev).manual_seed(1234 + rank)
+    runner = StageRunner(ex, rank, world, Transport(host_staged=one_gpu))
+    runner.set_plan(plan0)
+    pipe, stage = plan0.role(rank)
+    gen = torch.Generator(device=dev).manual_seed(1234 + pipe)
     images = torch.randn(batch, g.channels, g.input_image, g.input_image, device=dev,
                          generator=gen)
     labels = torch.randint(0, g.classes, (batch,), device=dev, generator=gen)
     stream = torch.cuda.current_stream()
 
-    def allreduce(l_frozen):
-        if world > 1:
-            begin = ex.segments[l_frozen]
-            dist.all_reduce(ex.g32[begin:], op=dist.ReduceOp.AVG)
-
-    def step(imgs, lf=0, cache_mode=0, cache_old=0, store=None, ids=None):
-        loss = ex.train_step(imgs, labels, micro_batches=micro, l_frozen=lf,
-                             cache_mode=cache_mode, cache_old=cache_old, store=store, ids=ids)
-        allreduce(lf)
-        ex.sgd(lf, lr=1e-3, momentum=0.9)
+    def step(imgs, cache_mode=0, cache_old=0, store=None, ids=None):
+        loss = runner.iteration(imgs, labels, batch, cache_mode=cache_mode, cache_old=cache_old,
+                                store=store, ids=ids)
+        runner.sync_grads()
+        runner.step(lr=1e-3, momentum=0.9)
         return loss
 
     def barrier():
@@ -254,11 +258,11 @@ def main_ours(args, world, rank, local):
             dist.barrier()
         torch.cuda.synchronize()
 
-    def max_over_ranks(x: float) -> float:
+    def reduce(x: float, op) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t = torch.tensor([x], device="cpu" if one_gpu else dev, dtype=torch.float64)
+        dist.all_reduce(t, op=op)
         return float(t.item())
 
     def timed(fn, steps):
@@ -269,18 +273,19 @@ def main_ours(args, world, rank, local):
             fn()
         e.record(stream)
         barrier()
-        return max_over_ranks(s.elapsed_time(e)) / steps
+        return reduce(s.elapsed_time(e), dist.ReduceOp.MAX if world > 1 else None) / steps
 
-    # ---- value: no-freeze step, inputs resident in HBM -------------------------
+    # ---- value: the epoch-0 (no-freeze) iteration, inputs resident in HBM ------
     for _ in range(args.warmup):
         step(images)
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(dev.index)
     clocks.start()
     n_launch0 = ops.launch_count()
     ms = timed(lambda: step(images), args.steps)
-    launches = ops.launch_count() - n_launch0
+    launches = int(reduce(float(ops.launch_count() - n_launch0),
+                          dist.ReduceOp.SUM if world > 1 else None))
     clock_rec = clocks.stop()
-    value = world * batch / (ms / 1000.0)
+    value = plan0.R * batch / (ms / 1000.0)
 
     # ---- roofline: one instrumented step, per-class CUDA-event times -----------
     ex.timing(True)
@@ -288,6 +293,9 @@ def main_ours(args, world, rank, local):
     torch.cuda.synchronize()
     cls = ex.timing_read()
     ex.timing(False)
+    for c in cls.values():  # whole-job sums (every rank's launches)
+        for k in ("ms", "flops", "bytes", "launches"):
+            c[k] = reduce(float(c[k]), dist.ReduceOp.SUM if world > 1 else None)
     peaks, peak_kind = measured_peaks()
     gemm = cls["gemm"]
     gemm_tflops = gemm["flops"] / (gemm["ms"] / 1000.0) / 1e12
@@ -296,13 +304,13 @@ def main_ours(args, world, rank, local):
                 "achieved": round(gemm_tflops, 1), "peak": peak_tc, "unit": "TFLOP/s",
                 "frac": round(gemm_tflops / peak_tc, 4), "traffic": None,
                 "peak_kind": f"{peak_kind} bf16_tflops_sustained",
-                "launches_per_step": gemm["launches"],
+                "launches_per_step": int(gemm["launches"]),
                 "share_of_step": round(gemm["ms"] / sum(c["ms"] for c in cls.values()), 4)}
     kernels = {}
     for name, c in cls.items():
         if c["launches"] == 0:
             continue
-        k = {"ms_per_step": round(c["ms"], 3), "launches": c["launches"]}
+        k = {"ms_per_step": round(c["ms"] / world, 3), "launches": int(c["launches"])}
         if c["flops"]:
             k["tflops"] = round(c["flops"] / (c["ms"] / 1000.0) / 1e12, 1)
         if c["bytes"]:
@@ -315,45 +323,49 @@ def main_ours(args, world, rank, local):
     h_images = images.cpu().pin_memory()
     h_labels = labels.cpu().pin_memory()
     d_images = torch.empty_like(images)
-    h2d = h_images.numel() * h_images.element_size() + h_labels.numel() * 8
+    first, last = stage == 0, stage == plan0.K - 1
+    h2d = (h_images.numel() * 4 + h_labels.numel() * 8) * plan0.R
 
     def e2e_step():
-        d_images.copy_(h_images, non_blocking=True)
-        labels.copy_(h_labels, non_blocking=True)
+        if first:
+            d_images.copy_(h_images, non_blocking=True)
+        if last:
+            labels.copy_(h_labels, non_blocking=True)
         loss = step(d_images)
-        return float(loss.item())
+        return float(loss.item()) if last else 0.0
 
     for _ in range(2):
         e2e_step()
     e2e_ms = timed(e2e_step, args.steps)
-    e2e_value = world * batch / (e2e_ms / 1000.0)
+    e2e_value = plan0.R * batch / (e2e_ms / 1000.0)
 
     # ---- freeze schedule: the planner's per-epoch decisions on the device ------
     sched = None
-    if not args.no_schedule and world == 1:
-        sched = freeze_schedule(ex, g, batch, micro, decisions, images, labels, step, timed,
-                                ms, dev)
+    if not args.no_schedule:
+        sched = freeze_schedule(runner, g, batch, decisions, images, step, timed, ms, dev)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline(g, args.cpu_seconds)
 
     if rank == 0:
+        par = f"pipe{plan0.K}" + (f"xdp{plan0.R}" if plan0.R > 1 else "")
         out = {"metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
                "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
-               "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+               "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+               "vs_baseline": None,
                "dtype": "bf16", "data": "synthetic (seeded N(0,1) images, U[0,1000) labels; "
                                          "random trunc-normal weights)",
                "config": {"workload": f"{args.config}: ViT-B/16 224px, batch {batch} per "
-                                      "pipeline, no-freeze train step (fwd+bwd+SGD)",
-                          "model": "ViT-B/16", "global_batch": batch * world,
-                          "seq_len": g.tokens, "parallelism": f"dp{world}",
-                          "micro_batches": micro,
-                          "planner": {"K": d0.pipeline_length, "R": d0.replica_width,
-                                      "M": d0.micro_batches},
+                                      "pipeline, no-freeze iteration (fwd+bwd+SGD) under the "
+                                      "reference planner's epoch-0 plan",
+                          "model": "ViT-B/16", "global_batch": batch * plan0.R,
+                          "seq_len": g.tokens, "parallelism": par,
+                          "planner": {"K": plan0.K, "R": plan0.R, "M": plan0.M,
+                                      "spans": [list(x) for x in plan0.spans]},
                           "l2": "working set (>20 GB of activations) far exceeds the 126 MB L2"},
                "e2e": {"value": round(e2e_value, 2), "unit": UNIT, "h2d_bytes_per_step": h2d,
-                       "d2h_bytes_per_step": 4, "ms_per_step": round(e2e_ms, 3)},
+                       "d2h_bytes_per_step": 4 * plan0.R, "ms_per_step": round(e2e_ms, 3)},
                "gpu_launches": launches,
                "roofline": roofline,
                "kernels": kernels,
@@ -366,46 +378,49 @@ def main_ours(args, world, rank, local):
         dist.destroy_process_group()
 
 
-def freeze_schedule(ex, g, batch, micro, decisions, images, labels, step, timed, ms0, dev):
-    """Per-epoch steady-state step time under the planner's decisions.
+def freeze_schedule(runner, g, batch, decisions, images, step, timed, ms0, dev):
+    """Per-epoch steady-state iteration time under the planner's decisions.
 
-    Epoch e runs L_frozen(e) with the frozen prefix either recomputed
-    (cache off), gathered from the HBM store (cache on, boundary unchanged)
-    or -- on a boundary-move epoch -- gathered from the old boundary,
-    forwarded over [old, new) and scattered at the new one (autocache.cpp:45-67).
-    Speedup = sum_e t_nofreeze / sum_e t_e (runner.cpp:298; iterations per
-    epoch are equal so they cancel)."""
-    row_elems = g.tokens * g.hidden
-    store = torch.zeros(batch, row_elems, dtype=torch.bfloat16, device=dev)
+    Epoch e runs L_frozen(e) on its K(e)-stage pipelines x R(e) replicas (the
+    runner migrates weights and regroups on every plan change) with the
+    frozen prefix either recomputed (cache off), gathered from the HBM store
+    (cache on) or -- on a boundary-move epoch -- gathered from the old
+    boundary, forwarded over [old, new) and scattered at the new one
+    (autocache.cpp:45-67).  An epoch holds the same samples at every width,
+    so its time is proportional to t_e / R_e; speedup vs no-freeze (K0, R0,
+    all layers trained: runner.cpp:67-90, 298) = sum_e t_0/R_0 / sum_e t_e/R_e."""
+    from paper_2102_03161_b200.pipeline import StagePlan
+    store = torch.zeros(batch, g.tokens * g.hidden, dtype=torch.bfloat16, device=dev)
     ids = torch.randperm(batch, generator=torch.Generator().manual_seed(3)).to(dev)
-    memo = {}
-    rows = []
+    memo, rows = {}, []
+    r0 = decisions[0].replica_width
     for d in decisions:
-        lf = d.l_frozen
+        plan = StagePlan.from_decision(d, g.layers)
         if not d.cache_enabled:
-            key = (lf, 0, 0)
+            mode, old = 0, 0
         elif d.cache_moved:
-            key = (lf, 2, d.cache_old_boundary)
+            mode, old = 2, d.cache_old_boundary
         else:
-            key = (lf, 1, 0)
+            mode, old = 1, 0
+        key = (plan, mode, old)
         if key not in memo:
-            lf_, mode, old = key
+            runner.set_plan(plan)
             if mode == 1:  # fill the store at this boundary first
-                step(images, lf_, 2, 0, store, ids)
-            fn = (lambda lf_=lf_, mode=mode, old=old:
-                  step(images, lf_, mode, old, store if mode else None, ids if mode else None))
+                step(images, 2, 0, store, ids)
+            fn = lambda: step(images, mode, old, store if mode else None, ids if mode else None)
             fn()
             memo[key] = timed(fn, 3)
         t = memo[key]
-        rows.append({"epoch": d.epoch, "l_frozen": lf, "K": d.pipeline_length,
-                     "R": d.replica_width, "M": d.micro_batches,
-                     "cache": ["off", "gather", "move"][key[1]], "ms_per_step": round(t, 3),
-                     "samples_per_s": round(batch / (t / 1000.0), 1)})
-    base = ms0 * len(rows)
-    tot = sum(r["ms_per_step"] for r in rows)
-    return {"epochs": rows, "no_freeze_ms_per_step": round(ms0, 3),
+        rows.append({"epoch": d.epoch, "l_frozen": d.l_frozen, "K": plan.K, "R": plan.R,
+                     "M": plan.M, "cache": ["off", "move", "gather"][[0, 2, 1].index(mode)],
+                     "ms_per_iteration": round(t, 3),
+                     "samples_per_s": round(plan.R * batch / (t / 1000.0), 1)})
+    base = sum(ms0 / r0 for _ in rows)
+    tot = sum(r["ms_per_iteration"] / r["R"] for r in rows)
+    return {"epochs": rows, "no_freeze_ms_per_iteration": round(ms0, 3),
             "speedup_vs_no_freeze": round(base / tot, 4),
-            "note": "measured on 1 GPU (K=1); per-epoch decisions from the reference planner"}
+            "note": "per-epoch decisions from the reference planner, each executed on the "
+                    "device (K-stage pipelines x R replicas)"}
 
 
 def main():
