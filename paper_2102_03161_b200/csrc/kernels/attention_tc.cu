@@ -524,6 +524,479 @@ __global__ void __launch_bounds__(kThreads, 2)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Fused, persistent backward for T <= 256.  One CTA per SM walks the (b, h)
+// heads; per head Q, dO, K, V (<= 256 rows each) sit in smem and the
+// (128-key tile j, 64-query chunk c) pairs are visited once, so every exp is
+// evaluated once:
+//   S^T = K_j Q_c^T, dP^T = V_j dO_c^T                 (SS MMAs -> TMEM)
+//   P^T = exp2(S^T*scale*log2e - lse2[q]), dS^T = P^T (dP^T - D[q])
+//        (8 warps: key row per lane, 32 queries per warp; P^T / dS^T back
+//         into TMEM as bf16, dS^T also into a smem staging tile)
+//   dV_j += P^T dO_c, dK_j += dS^T Q_c                 (TS MMAs, A in TMEM)
+//   dQ_t += dS_t K_j once both 64-query halves of 128-query tile t are staged
+//                                                     (SS MMA, A MN-major)
+// S^T / dP^T are double-buffered in TMEM and the MMA issue runs one chunk
+// ahead of the exp work; dS staging is double-buffered in smem.
+// TMEM (512 cols): [S^T 64 | dP^T 64] x 2 | dV 64 | dK 64 | dQ_0 64 | dQ_1 64.
+// The next head's tiles are prefetched into L2 while this one computes.
+constexpr int kDsChunk = kTile * kRowBytes;  // [128 keys][64 queries] bf16 = 16 KB
+constexpr int kBwdThreads = 64 + 8 * 32;
+
+__device__ __forceinline__ void tma_prefetch_3d(const void* tmap, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];" ::"l"(
+                   reinterpret_cast<uint64_t>(tmap)),
+               "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+
+__global__ void __launch_bounds__(kBwdThreads, 1)
+    attn_bwd_fused_tc_kernel(const __grid_constant__ CUtensorMap map_qkv,
+                             const __grid_constant__ CUtensorMap map_do, const Params p,
+                             int n_heads) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  const int nt = (p.T + kTile - 1) / kTile;  // 128-row tiles of keys / queries (1 or 2)
+  const int Tr = nt * kTile;                 // rows loaded (zero-filled past T)
+  const int nc = Tr / kChunk;                // 64-query chunks per key tile
+  const int n_it = nt * nc;                  // iterations per head (even)
+  uint8_t* sQ = smem;
+  uint8_t* sO = sQ + Tr * kRowBytes;
+  uint8_t* sK = sO + Tr * kRowBytes;
+  uint8_t* sV = sK + Tr * kRowBytes;
+  uint8_t* sS = sV + Tr * kRowBytes;  // dS staging: 2 buffers x 2 chunks x 16 KB
+  float* sL = reinterpret_cast<float*>(sS + 4 * kDsChunk);
+  float* sD = sL + Tr;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sD + Tr);
+  enum { FULL = 0, EMPTY, SF0, SF1, PF0, PF1, AC0, AC1, KVF, KVE, DQF, DQE, NBAR };
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + NBAR);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int HD = p.H * kD;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch(&map_qkv);
+    tma_prefetch(&map_do);
+    for (int i = 0; i < NBAR; ++i)
+      mbar_init(&bar[i], (i == PF0 || i == PF1 || i == KVE || i == DQE) ? 8 : 1);
+    mbar_fence_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tdV = tmem + 256, tdK = tmem + 320, tdQ = tmem + 384;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int hi = 0;
+      for (int bh = blockIdx.x; bh < n_heads; bh += gridDim.x, ++hi) {
+        const int b = bh / p.H, h = bh % p.H;
+        mbar_wait(&bar[EMPTY], (hi & 1) ^ 1);
+        mbar_expect_tx(&bar[FULL], uint32_t(4 * Tr) * kRowBytes);
+        load_rows(sQ, &map_qkv, &bar[FULL], h * kD, 0, Tr, b);
+        load_rows(sO, &map_do, &bar[FULL], h * kD, 0, Tr, b);
+        load_rows(sK, &map_qkv, &bar[FULL], HD + h * kD, 0, Tr, b);
+        load_rows(sV, &map_qkv, &bar[FULL], 2 * HD + h * kD, 0, Tr, b);
+        const int nb = bh + gridDim.x;  // warm L2 with the next head
+        if (nb < n_heads) {
+          const int b2 = nb / p.H, h2 = nb % p.H;
+          for (int r = 0; r < Tr; r += kChunk) {
+            tma_prefetch_3d(&map_qkv, h2 * kD, r, b2);
+            tma_prefetch_3d(&map_do, h2 * kD, r, b2);
+            tma_prefetch_3d(&map_qkv, HD + h2 * kD, r, b2);
+            tma_prefetch_3d(&map_qkv, 2 * HD + h2 * kD, r, b2);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const uint32_t q_s = smem_addr(sQ), o_s = smem_addr(sO), k_s = smem_addr(sK),
+                     v_s = smem_addr(sV), ds_s = smem_addr(sS);
+      const uint32_t idesc_kk = umma_idesc_bf16(128, kChunk, false, false);
+      const uint32_t idesc_km = umma_idesc_bf16(128, kD, false, true);
+      const uint32_t idesc_mm = umma_idesc_bf16(128, kD, true, true);
+      int it0 = 0, kt = 0, hi = 0;
+      // dV / dK / dQ work of iteration `it` (k-th of its head)
+      auto post = [&](int it, int k) {
+        const int bsel = it & 1, j = k / nc, c = k % nc;
+        mbar_wait(&bar[PF0 + bsel], (it >> 1) & 1);
+        tc_fence_after();
+        if (c == 0 && kt > 0) {  // dK / dV of the previous key tile read out
+          mbar_wait(&bar[KVE], (kt - 1) & 1);
+          tc_fence_after();
+        }
+        const uint32_t tS = tmem + uint32_t(bsel * 128), tdP = tS + 64;
+        const uint32_t qc = q_s + uint32_t(c * kChunk) * kRowBytes;
+        const uint32_t oc = o_s + uint32_t(c * kChunk) * kRowBytes;
+#pragma unroll
+        for (int kk = 0; kk < kChunk / 16; ++kk) {
+          const uint32_t acc = (c > 0 || kk > 0) ? 1u : 0u;
+          tc_mma_bf16_ts(tdV, tS + uint32_t(kk * 8), mndesc(oc + uint32_t(kk * 16) * kRowBytes),
+                         idesc_km, acc);
+          tc_mma_bf16_ts(tdK, tdP + uint32_t(kk * 8), mndesc(qc + uint32_t(kk * 16) * kRowBytes),
+                         idesc_km, acc);
+        }
+        if (c & 1) {  // both halves of 128-query tile c/2 staged: dQ_t += dS_t K_j
+          const int t = c >> 1;
+          if (j == 0 && t == 0 && hi > 0) {
+            mbar_wait(&bar[DQE], (hi - 1) & 1);
+            tc_fence_after();
+          }
+          const uint32_t stg = ds_s + uint32_t(((it >> 1) & 1) * 2) * uint32_t(kDsChunk);
+          const uint32_t kj = k_s + uint32_t(j * kTile) * kRowBytes;
+#pragma unroll
+          for (int kk = 0; kk < kTile / 16; ++kk)
+            tc_mma_bf16(tdQ + uint32_t(t * kD), umma_sdesc(stg + uint32_t(kk) * 2048u, kDsChunk, 1024),
+                        mndesc(kj + uint32_t(kk * 16) * kRowBytes), idesc_mm,
+                        (j > 0 || kk > 0) ? 1u : 0u);
+        }
+        tc_commit(&bar[AC0 + bsel]);
+        if (c == nc - 1) {
+          tc_commit(&bar[KVF]);
+          ++kt;
+        }
+      };
+      for (int bh = blockIdx.x; bh < n_heads; bh += gridDim.x, ++hi) {
+        mbar_wait(&bar[FULL], hi & 1);
+        tc_fence_after();
+        for (int k = 0; k < n_it; ++k) {
+          const int it = it0 + k, bsel = it & 1, j = k / nc, c = k % nc;
+          if (it >= 2) {  // post(it - 2) finished reading this S^T / dP^T buffer
+            mbar_wait(&bar[AC0 + bsel], ((it >> 1) - 1) & 1);
+            tc_fence_after();
+          }
+          const uint32_t tS = tmem + uint32_t(bsel * 128), tdP = tS + 64;
+          const uint32_t kj = k_s + uint32_t(j * kTile) * kRowBytes;
+          const uint32_t vj = v_s + uint32_t(j * kTile) * kRowBytes;
+          const uint32_t qc = q_s + uint32_t(c * kChunk) * kRowBytes;
+          const uint32_t oc = o_s + uint32_t(c * kChunk) * kRowBytes;
+#pragma unroll
+          for (int kk = 0; kk < kD / 16; ++kk)
+            tc_mma_bf16(tS, kdesc(kj, kk), kdesc(qc, kk), idesc_kk, kk > 0 ? 1u : 0u);
+#pragma unroll
+          for (int kk = 0; kk < kD / 16; ++kk)
+            tc_mma_bf16(tdP, kdesc(vj, kk), kdesc(oc, kk), idesc_kk, kk > 0 ? 1u : 0u);
+          tc_commit(&bar[SF0 + bsel]);
+          if (k > 0) post(it - 1, k - 1);
+        }
+        post(it0 + n_it - 1, n_it - 1);
+        tc_commit(&bar[DQF]);
+        tc_commit(&bar[EMPTY]);
+        it0 += n_it;
+      }
+    }
+  } else {
+    const int half = (warp - 2) >> 2;  // which 32 of the chunk's 64 queries
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    const uint32_t lane_off = uint32_t(quarter * 32) << 16;
+    const int tid = threadIdx.x - 64;  // 0..255
+    int it0 = 0, kt = 0, hi = 0;
+    for (int bh = blockIdx.x; bh < n_heads; bh += gridDim.x, ++hi) {
+      const int b = bh / p.H, h = bh % p.H;
+      mbar_wait(&bar[FULL], hi & 1);
+      // prologue: lse (log2 domain) and D = rowsum(dO * O) per query
+      for (int q = tid; q < Tr; q += 256) {
+        float Dq = 0.f, l2 = 0.f;
+        if (q < p.T) {
+          const uint4* o4 =
+              reinterpret_cast<const uint4*>(p.out + (int64_t(b) * p.T + q) * HD + h * kD);
+          const uint32_t rowa = smem_addr(sO) + uint32_t(q >> 3) * 1024u;
+#pragma unroll
+          for (int v = 0; v < 8; ++v) {
+            const uint4 a = __ldg(o4 + v);
+            const uint4 d = ld_shared_v4(rowa + uint32_t(swz128(q & 7, v)));
+            Dq += bf16_lo(a.x) * bf16_lo(d.x) + bf16_hi(a.x) * bf16_hi(d.x) +
+                  bf16_lo(a.y) * bf16_lo(d.y) + bf16_hi(a.y) * bf16_hi(d.y) +
+                  bf16_lo(a.z) * bf16_lo(d.z) + bf16_hi(a.z) * bf16_hi(d.z) +
+                  bf16_lo(a.w) * bf16_lo(d.w) + bf16_hi(a.w) * bf16_hi(d.w);
+          }
+          l2 = p.lse[int64_t(bh) * p.T + q] * kLog2e;
+        }
+        sL[q] = l2;
+        sD[q] = Dq;
+      }
+      asm volatile("bar.sync 5, 256;" ::: "memory");
+      for (int k = 0; k < n_it; ++k) {
+        const int it = it0 + k, bsel = it & 1, j = k / nc, c = k % nc;
+        const int key = j * kTile + row;
+        const bool valid_k = key < p.T;
+        const int q0 = c * kChunk + half * 32;
+        mbar_wait(&bar[SF0 + bsel], (it >> 1) & 1);
+        tc_fence_after();
+        const uint32_t tS = tmem + uint32_t(bsel * 128) + lane_off, tdP = tS + 64;
+        uint32_t sv[32], dp[32];
+        tmem_ld_32x32(tS + uint32_t(half * 32), sv);
+        tmem_ld_32x32(tdP + uint32_t(half * 32), dp);
+        float lq[32], dq[32];
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+          const float4 a = *reinterpret_cast<const float4*>(sL + q0 + 4 * v);
+          const float4 d = *reinterpret_cast<const float4*>(sD + q0 + 4 * v);
+          lq[4 * v] = a.x, lq[4 * v + 1] = a.y, lq[4 * v + 2] = a.z, lq[4 * v + 3] = a.w;
+          dq[4 * v] = d.x, dq[4 * v + 1] = d.y, dq[4 * v + 2] = d.z, dq[4 * v + 3] = d.w;
+        }
+        tmem_ld_wait();
+        // both warps of this lane quarter have read their S^T / dP^T columns
+        // before either overwrites the buffer's first 32 columns with bf16 pairs
+        asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
+        const float sl2 = p.scale_log2;
+        const int qlim = valid_k ? p.T - q0 : 0;  // valid query columns of this warp
+        uint32_t pp[16], pd[16];
+#pragma unroll
+        for (int jj = 0; jj < 16; ++jj) {
+          const float p0 = (2 * jj < qlim) ? fast_exp2(fmaf(__uint_as_float(sv[2 * jj]), sl2, -lq[2 * jj])) : 0.f;
+          const float p1 =
+              (2 * jj + 1 < qlim) ? fast_exp2(fmaf(__uint_as_float(sv[2 * jj + 1]), sl2, -lq[2 * jj + 1])) : 0.f;
+          pp[jj] = pack_bf16(p0, p1);
+          pd[jj] = pack_bf16(p0 * (__uint_as_float(dp[2 * jj]) - dq[2 * jj]),
+                             p1 * (__uint_as_float(dp[2 * jj + 1]) - dq[2 * jj + 1]));
+        }
+        tmem_st_32x32_x16(tS + uint32_t(half * 16), pp);
+        tmem_st_32x32_x16(tdP + uint32_t(half * 16), pd);
+        // dS^T row -> staging buffer (tile parity), chunk c&1, pieces half*4 .. +3
+        const uint32_t chunk = smem_addr(sS) +
+                               uint32_t(((it >> 1) & 1) * 2 + (c & 1)) * uint32_t(kDsChunk) +
+                               uint32_t(row >> 3) * 1024u;
+#pragma unroll
+        for (int v = 0; v < 4; ++v)
+          st_shared_v4(chunk + uint32_t(swz128(row & 7, half * 4 + v)), pd[4 * v], pd[4 * v + 1],
+                       pd[4 * v + 2], pd[4 * v + 3]);
+        fence_proxy_async_smem();
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bar[PF0 + bsel]);
+        if (c == nc - 1) {
+          // dV_j (half 0) / dK_j (half 1) complete: store + bias column sums
+          mbar_wait(&bar[KVF], kt & 1);
+          tc_fence_after();
+          float v[64];
+          load_tmem_row64((half ? tdK : tdV) + lane_off, v);
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&bar[KVE]);
+          const float sc = half ? p.scale : 1.f;
+#pragma unroll
+          for (int d = 0; d < 64; ++d)
+            v[d] = valid_k ? __bfloat162float(__float2bfloat16_rn(v[d] * sc)) : 0.f;
+          const int col = (half ? HD : 2 * HD) + h * kD;
+          if (valid_k) store_row64(p.dqkv + (int64_t(b) * p.T + key) * (3 * HD) + col, v);
+          if (p.dbias != nullptr) colsum64(v, p.dbias + col);
+          ++kt;
+        }
+      }
+      // dQ tiles: warp half t stores 128-query tile t
+      mbar_wait(&bar[DQF], hi & 1);
+      tc_fence_after();
+      float v[64];
+      if (half < nt) load_tmem_row64(tdQ + uint32_t(half * kD) + lane_off, v);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bar[DQE]);
+      if (half < nt) {
+        const int q = half * kTile + row;
+        const bool valid_q = q < p.T;
+#pragma unroll
+        for (int d = 0; d < 64; ++d)
+          v[d] = valid_q ? __bfloat162float(__float2bfloat16_rn(v[d] * p.scale)) : 0.f;
+        if (valid_q) store_row64(p.dqkv + (int64_t(b) * p.T + q) * (3 * HD) + h * kD, v);
+        if (p.dbias != nullptr) colsum64(v, p.dbias + h * kD);
+      }
+      // sL / sD are rewritten by the next head's prologue only after all
+      // 256 exp threads are done with them
+      asm volatile("bar.sync 5, 256;" ::: "memory");
+      it0 += n_it;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+size_t bwd_fused_smem(int T) {
+  const int Tr = (T + kTile - 1) / kTile * kTile;
+  return size_t(4 * Tr) * kRowBytes + 4 * size_t(kDsChunk) + size_t(2 * Tr) * 4 + 1024 + 256;
+}
+
+// ---------------------------------------------------------------------------
+// Persistent forward for T <= 256: one CTA per SM walks the (b, h) heads;
+// Q, K, V of a head (<= 256 rows each) are double-buffered in smem so the
+// TMA load of the next head overlaps this head's math.  Two softmax
+// warpgroups own the two 128-query tiles (S_c in TMEM columns [256c, +Tp),
+// P_c written back in place, O_c at 256c + 128), so both tiles' exp work and
+// the MMAs of the other tile proceed concurrently.
+constexpr int kFwdThreads = 64 + 8 * 32;
+
+__global__ void __launch_bounds__(kFwdThreads, 1)
+    attn_fwd_persistent_tc_kernel(const __grid_constant__ CUtensorMap map_qkv, const Params p,
+                                  int n_heads) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  const int nt = (p.T + kTile - 1) / kTile;
+  const int Tr = nt * kTile;
+  const int Tp = p.Tp;  // S columns (pad64(T) <= 256)
+  const size_t buf_bytes = size_t(3 * Tr) * kRowBytes;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 2 * buf_bytes);
+  // 0-1 full[buf], 2-3 empty[buf], 4-5 s[c], 6-7 p[c], 8-9 o[c], 10-11 tfree[c]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 12);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int HD = p.H * kD;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch(&map_qkv);
+    for (int i = 0; i < 12; ++i) mbar_init(&bar[i], (i >= 6 && i < 8) || i >= 10 ? 4 : 1);
+    mbar_fence_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int i = 0;
+      for (int bh = blockIdx.x; bh < n_heads; bh += gridDim.x, ++i) {
+        const int buf = i & 1, b = bh / p.H, h = bh % p.H;
+        mbar_wait(&bar[2 + buf], ((i >> 1) & 1) ^ 1);
+        uint8_t* base = smem + buf * buf_bytes;
+        mbar_expect_tx(&bar[buf], uint32_t(3 * Tr) * kRowBytes);
+        load_rows(base, &map_qkv, &bar[buf], h * kD, 0, Tr, b);
+        load_rows(base + Tr * kRowBytes, &map_qkv, &bar[buf], HD + h * kD, 0, Tr, b);
+        load_rows(base + 2 * Tr * kRowBytes, &map_qkv, &bar[buf], 2 * HD + h * kD, 0, Tr, b);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      const int nsplit = Tp > 256 ? 2 : 1;  // (Tp <= 256 here)
+      const int nc = Tp / nsplit;
+      const uint32_t idesc_s = umma_idesc_bf16(128, nc, false, false);
+      const uint32_t idesc_o = umma_idesc_bf16(128, kD, false, true);
+      int i = 0;
+      for (int bh = blockIdx.x; bh < n_heads; bh += gridDim.x, ++i) {
+        const int buf = i & 1;
+        mbar_wait(&bar[buf], (i >> 1) & 1);
+        tc_fence_after();
+        const uint32_t q_s = smem_addr(smem + buf * buf_bytes);
+        const uint32_t k_s = q_s + uint32_t(Tr * kRowBytes), v_s = k_s + uint32_t(Tr * kRowBytes);
+        for (int c = 0; c < nt; ++c) {
+          mbar_wait(&bar[10 + c], (i & 1) ^ 1);  // WG c done with last head's S/O
+          tc_fence_after();
+          const uint32_t tS = tmem + uint32_t(256 * c);
+          const uint32_t qc = q_s + uint32_t(c * kTile) * kRowBytes;
+          for (int sp = 0; sp < nsplit; ++sp)
+#pragma unroll
+            for (int kk = 0; kk < kD / 16; ++kk)
+              tc_mma_bf16(tS + uint32_t(sp * nc), kdesc(qc, kk),
+                          kdesc(k_s + uint32_t(sp * nc) * kRowBytes, kk), idesc_s,
+                          kk > 0 ? 1u : 0u);
+          tc_commit(&bar[4 + c]);
+        }
+        for (int c = 0; c < nt; ++c) {
+          mbar_wait(&bar[6 + c], i & 1);
+          tc_fence_after();
+          const uint32_t tS = tmem + uint32_t(256 * c);
+          for (int kk = 0; kk < Tp / 16; ++kk)
+            tc_mma_bf16_ts(tS + 128, tS + uint32_t(kk * 8),
+                           mndesc(v_s + uint32_t(kk * 16) * kRowBytes), idesc_o, kk > 0 ? 1u : 0u);
+          tc_commit(&bar[8 + c]);
+        }
+        tc_commit(&bar[2 + buf]);  // smem buffer free once every MMA above is done
+      }
+    }
+  } else {
+    const int wg = (warp - 2) >> 2;  // query tile of this warpgroup
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    const uint32_t lane_off = uint32_t(quarter * 32) << 16;
+    const uint32_t tS = tmem + uint32_t(256 * wg) + lane_off;
+    if (wg < nt) {
+      int i = 0;
+      const int nch = (p.T + 31) / 32;  // S chunks holding valid keys
+      for (int bh = blockIdx.x; bh < n_heads; bh += gridDim.x, ++i) {
+        const int b = bh / p.H, h = bh % p.H;
+        const int q = wg * kTile + row;
+        mbar_wait(&bar[4 + wg], i & 1);
+        tc_fence_after();
+        float m = -FLT_MAX;
+        for (int c = 0; c < nch; ++c) {
+          uint32_t r[32];
+          tmem_ld_32x32(tS + uint32_t(c * 32), r);
+          tmem_ld_wait();
+          if (c * 32 + 32 <= p.T) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) m = fmaxf(m, __uint_as_float(r[j]));
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (c * 32 + j < p.T) m = fmaxf(m, __uint_as_float(r[j]));
+          }
+        }
+        const float ms = m * p.scale_log2;
+        float sum = 0.f;
+        for (int c = 0; c < Tp / 32; ++c) {
+          uint32_t pk[16];
+          if (c < nch) {
+            uint32_t r[32];
+            tmem_ld_32x32(tS + uint32_t(c * 32), r);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const int k = c * 32 + 2 * j;
+              const float e0 =
+                  k < p.T ? fast_exp2(fmaf(__uint_as_float(r[2 * j]), p.scale_log2, -ms)) : 0.f;
+              const float e1 =
+                  k + 1 < p.T ? fast_exp2(fmaf(__uint_as_float(r[2 * j + 1]), p.scale_log2, -ms))
+                              : 0.f;
+              sum += e0 + e1;
+              pk[j] = pack_bf16(e0, e1);
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) pk[j] = 0u;  // keys past T: P = 0
+          }
+          tmem_st_32x32_x16(tS + uint32_t(c * 16), pk);
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bar[6 + wg]);
+        if (q < p.T) p.lse[int64_t(bh) * p.T + q] = (ms + __log2f(sum)) * kLn2;
+        mbar_wait(&bar[8 + wg], i & 1);
+        tc_fence_after();
+        float o[64];
+        load_tmem_row64(tS + 128, o);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bar[10 + wg]);
+        if (q < p.T) {
+          const float inv = 1.f / sum;
+#pragma unroll
+          for (int j = 0; j < 64; ++j) o[j] *= inv;
+          store_row64(p.out_w + (int64_t(b) * p.T + q) * HD + h * kD, o);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+size_t fwd_persistent_smem(int T) {
+  const int Tr = (T + kTile - 1) / kTile * kTile;
+  return 2 * size_t(3 * Tr) * kRowBytes + 1024 + 128;
+}
+
 size_t fwd_smem(int Tp) { return size_t(kTile + 2 * Tp) * kRowBytes + 1024 + 64; }
 size_t bwd_dq_smem(int Tp) { return size_t(2 * kTile + 2 * Tp) * kRowBytes + 1024 + 64; }
 size_t bwd_dkdv_smem(int Tp) {
@@ -558,6 +1031,15 @@ int attn_fwd_tc(const void* qkv, void* out, float* lse, int B, int T, int H, flo
   p.scale_log2 = scale * kLog2e;
   p.out_w = static_cast<uint16_t*>(out);
   p.lse = lse;
+  if (T <= 2 * kTile) {
+    const size_t sp = fwd_persistent_smem(T);
+    if (!ensure_smem(attn_fwd_persistent_tc_kernel, sp)) return EPS_ECUDA;
+    const int heads = B * H;
+    const int grid = heads < sm_count() ? heads : sm_count();
+    count_launch();
+    attn_fwd_persistent_tc_kernel<<<grid, kFwdThreads, sp, st>>>(m, p, heads);
+    return cudaGetLastError() == cudaSuccess ? EPS_OK : EPS_ECUDA;
+  }
   const size_t smem = fwd_smem(Tp);
   if (!ensure_smem(attn_fwd_tc_kernel, smem)) return EPS_ECUDA;
   dim3 grid((T + kTile - 1) / kTile, B * H);
@@ -587,6 +1069,15 @@ int attn_bwd_tc(const void* qkv, const void* out, const void* dout, const float*
   p.dsum = dsum;
   p.dqkv = static_cast<uint16_t*>(dqkv);
   p.dbias = dbias;
+  if (T <= 2 * kTile) {
+    const size_t sf = bwd_fused_smem(T);
+    if (!ensure_smem(attn_bwd_fused_tc_kernel, sf)) return EPS_ECUDA;
+    const int heads = B * H;
+    count_launch();
+    attn_bwd_fused_tc_kernel<<<heads < sm_count() ? heads : sm_count(), kBwdThreads, sf, st>>>(
+        mq, mo, p, heads);
+    return cudaGetLastError() == cudaSuccess ? EPS_OK : EPS_ECUDA;
+  }
   const size_t s1 = bwd_dq_smem(Tp), s2 = bwd_dkdv_smem(Tp);
   if (!ensure_smem(attn_bwd_dq_tc_kernel, s1) || !ensure_smem(attn_bwd_dkdv_tc_kernel, s2))
     return EPS_ECUDA;

@@ -78,12 +78,21 @@ __global__ void __launch_bounds__(kLnWarps * 32)
   const float rs = rsqrtf(warp_sum(q) * (1.0f / D) + eps);
   float o[EPL];
 #pragma unroll
-  for (int i = 0; i < S::NV; ++i)
+  for (int i = 0; i < S::NV; ++i) {
+    // gamma / beta as 16B vectors (VEC consecutive columns per lane)
+    const float4* g4 = reinterpret_cast<const float4*>(gamma + (i * 32 + lane) * S::VEC);
+    const float4* b4 = reinterpret_cast<const float4*>(beta + (i * 32 + lane) * S::VEC);
 #pragma unroll
-    for (int j = 0; j < S::VEC; ++j) {
-      const int col = (i * 32 + lane) * S::VEC + j;
-      o[i * S::VEC + j] = (v[i * S::VEC + j] - mu) * rs * __ldg(gamma + col) + __ldg(beta + col);
+    for (int j4 = 0; j4 < S::VEC / 4; ++j4) {
+      const float4 gg = __ldg(g4 + j4), bb = __ldg(b4 + j4);
+      float* vo = o + i * S::VEC + 4 * j4;
+      const float* vi = v + i * S::VEC + 4 * j4;
+      vo[0] = (vi[0] - mu) * rs * gg.x + bb.x;
+      vo[1] = (vi[1] - mu) * rs * gg.y + bb.y;
+      vo[2] = (vi[2] - mu) * rs * gg.z + bb.z;
+      vo[3] = (vi[3] - mu) * rs * gg.w + bb.w;
     }
+  }
   uint16_t* yr = y + row * D;
 #pragma unroll
   for (int i = 0; i < S::NV; ++i) store_vec<S::VEC>(yr + (i * 32 + lane) * S::VEC, o + i * S::VEC);
@@ -117,11 +126,20 @@ __global__ void __launch_bounds__(kLnWarps * 32)
     }
   for (int64_t row = int64_t(blockIdx.x) * kLnWarps + warp; row < rows;
        row += int64_t(gridDim.x) * kLnWarps) {
-    float g[EPL], xv[EPL];
+    float g[EPL], xv[EPL], r[EPL];
 #pragma unroll
     for (int i = 0; i < S::NV; ++i) {
       load_vec<S::VEC>(dy + row * D + (i * 32 + lane) * S::VEC, g + i * S::VEC);
       load_vec<S::VEC>(x + row * D + (i * 32 + lane) * S::VEC, xv + i * S::VEC);
+    }
+    // all of the row's loads in flight at once (one HBM round trip per row)
+    if (dres != nullptr) {
+#pragma unroll
+      for (int i = 0; i < S::NV; ++i)
+        load_vec<S::VEC>(dres + row * D + (i * 32 + lane) * S::VEC, r + i * S::VEC);
+    } else {
+#pragma unroll
+      for (int i = 0; i < EPL; ++i) r[i] = 0.f;
     }
     const float mu = __ldg(mean + row), rs = __ldg(rstd + row);
     float s1 = 0.f, s2 = 0.f;
@@ -138,15 +156,6 @@ __global__ void __launch_bounds__(kLnWarps * 32)
     }
     s1 = warp_sum(s1) * (1.0f / D);
     s2 = warp_sum(s2) * (1.0f / D);
-    float r[EPL];
-    if (dres != nullptr) {
-#pragma unroll
-      for (int i = 0; i < S::NV; ++i)
-        load_vec<S::VEC>(dres + row * D + (i * 32 + lane) * S::VEC, r + i * S::VEC);
-    } else {
-#pragma unroll
-      for (int i = 0; i < EPL; ++i) r[i] = 0.f;
-    }
 #pragma unroll
     for (int i = 0; i < EPL; ++i) {
       r[i] += rs * (g[i] - s1 - xv[i] * s2);
