@@ -366,7 +366,8 @@ enum {
   EPS_EPI_BIAS_RESID_BF16 = 3,/* C = acc + bias[n] + aux[m,n] (C may == aux) */
   EPS_EPI_DGELU_BF16 = 4,     /* C = acc * gelu'(aux[m,n]); colsum -> bias   */
   EPS_EPI_STORE_F32 = 5,      /* Cf32 = acc (beta 0)                         */
-  EPS_EPI_ACCUM_F32 = 6       /* Cf32 += acc (split-K / micro-batch accum)   */
+  EPS_EPI_ACCUM_F32 = 6,      /* Cf32 += acc (split-K / micro-batch accum)   */
+  EPS_EPI_RESID_BF16 = 7      /* C = acc + aux[m,n] (residual-gradient add)  */
 };
 int eps_gemm_bf16(int a_mn_major, int b_mn_major, int epilogue, const void* A, const void* B,
                   void* C, const float* bias, void* aux, float* colsum, int64_t M, int64_t N,
@@ -517,6 +518,55 @@ enum {
 };
 int eps_vit_timing_enable(eps_vit_t* h, int on);
 int eps_vit_timing_read(eps_vit_t* h, double* ms, double* flops, double* bytes, int64_t* count);
+/* ---- BERT front end / heads (csrc/kernels/bert_ops.cu) ------------------ */
+/* E[b*T+t] = word[tok] + pos[t] + type[seg] (fp32 tables -> bf16 rows). */
+int eps_bert_embed_fwd(const int64_t* tokens, const int64_t* segments, const float* word,
+                       const float* pos, const float* type, void* out, int batch,
+                       int tokens_per_sample, int64_t d, void* stream);
+/* Scatter-add of dE rows into the fp32 word / position / type gradients. */
+int eps_bert_embed_bwd(const void* d_embed, const int64_t* tokens, const int64_t* segments,
+                       float* dword, float* dpos, float* dtype, int batch,
+                       int tokens_per_sample, int64_t d, void* stream);
+/* SQuAD span loss over logits [batch*T, ld] (columns 0 start, 1 end):
+ * loss_sum += sum_b (CE_start + CE_end)/2; dlogits scaled by grad_scale;
+ * dbias[0..1] += column sums of dlogits. */
+int eps_span_xent(const void* logits, const int64_t* start, const int64_t* end, void* dlogits,
+                  float* loss_sum, float* dbias, int batch, int tokens_per_sample, int ld,
+                  float grad_scale, void* stream);
+int eps_tanh_fwd(const void* x, void* y, int64_t n, void* stream);
+int eps_tanh_bwd(const void* dy, const void* y, void* dx, int64_t n, void* stream);
+
+/* ---- BERT stage executor (csrc/runtime/bert.cu) -------------------------- */
+/* Same contract as eps_vit_*; geom = {layers, d, mlp_dim, heads, tokens,
+ * classes, vocab, positions, head_kind (0 pooled CLS, 1 SQuAD span), pooler,
+ * max_batch}.  `state` holds the optimizer state: momentum (SGD) or m | v
+ * (AdamW, 2 x param_total).  Front-stage inputs: int64 tokens [batch_rows*T]
+ * followed by segment ids [batch_rows*T]; labels: class [gb] (head 0) or
+ * start [gb] followed by end [gb] (head 1). */
+typedef struct eps_bert eps_bert_t;
+int eps_bert_layout(const int* geom, int64_t* param_total, int64_t* workspace_bytes,
+                    int64_t* segments, int64_t* tensors);
+int eps_bert_create(const int* geom, float* params, uint16_t* params_bf16, float* grads,
+                    float* state, void* workspace, eps_bert_t** out);
+void eps_bert_destroy(eps_bert_t* h);
+int eps_bert_stage_forward(eps_bert_t* h, const int64_t* inputs, int batch_rows, int b0, int b,
+                           int g0, int g1, int l_frozen, int front, int cache_mode, int cache_old,
+                           void* store, const int64_t* ids, void* stream);
+int eps_bert_stage_head(eps_bert_t* h, const int64_t* labels, int b0, int b, int global_batch,
+                        float* loss_sum, void* stream);
+int eps_bert_stage_backward(eps_bert_t* h, int b0, int b, int g0, int g1, int l_frozen,
+                            int cut_out, void* stream);
+void* eps_bert_cut(eps_bert_t* h, int g, int grad);
+int eps_bert_param_range(eps_bert_t* h, int g0, int g1, int64_t* begin, int64_t* end);
+int eps_bert_sgd_range(eps_bert_t* h, int64_t begin, int64_t end, float lr, float momentum,
+                       float weight_decay, void* stream);
+int eps_bert_adamw_range(eps_bert_t* h, int64_t begin, int64_t end, float lr, float beta1,
+                         float beta2, float eps, float weight_decay, int step, void* stream);
+int eps_bert_sqnorm_ranges(eps_bert_t* h, const int64_t* offsets, int n, double* out,
+                           void* stream);
+int eps_bert_timing_enable(eps_bert_t* h, int on);
+int eps_bert_timing_read(eps_bert_t* h, double* ms, double* flops, double* bytes,
+                         int64_t* count);
 #endif /* EPS_REFERENCE_BUILD */
 
 #ifdef __cplusplus

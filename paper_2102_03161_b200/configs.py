@@ -35,6 +35,7 @@ class Geometry:
     vocab: int = 30522
     positions: int = 512
     pooler: bool = True
+    head: str = "cls"      # BERT head: "cls" (pooled CLS classifier) | "qa" (SQuAD span)
 
     @property
     def head_dim(self) -> int:
@@ -75,10 +76,17 @@ GEOMETRIES: Dict[str, Geometry] = {
     # 3. ViT-B/16 on CIFAR-100-shaped 32x32 data, upsampled on device to 224
     "vit-b16-cifar100": Geometry("vit", 12, 768, 3072, 12, 197, 100, input_image=32),
     # 4. BERT-base, seq 384, SQuAD span head (pooler + 2 outputs)
-    "bert-base-384": Geometry("bert", 12, 768, 3072, 12, 384, 2),
+    "bert-base-384": Geometry("bert", 12, 768, 3072, 12, 384, 2, head="qa"),
     # 5. BERT-large, seq 128, 2-class GLUE head (pooler + 2 outputs)
     "bert-large-128": Geometry("bert", 24, 1024, 4096, 16, 128, 2),
+    # test-size BERTs (parity tests only; not BASELINE configs)
+    "tiny-bert-qa": Geometry("bert", 2, 128, 512, 2, 64, 2, vocab=1000, positions=128,
+                             head="qa"),
+    "tiny-bert-cls": Geometry("bert", 2, 256, 1024, 4, 48, 3, vocab=500, positions=64),
 }
+
+# the five BASELINE.json configs (parity + golden decision fixtures)
+BASELINE_CONFIGS = ["tiny-vit", "vit-b16", "vit-b16-cifar100", "bert-base-384", "bert-large-128"]
 
 BATCH = {"tiny-vit": 64, "vit-b16": 400, "vit-b16-cifar100": 320, "bert-base-384": 64,
          "bert-large-128": 64}

@@ -94,7 +94,8 @@ constexpr int kEpiWarpBytes = 4096;
 constexpr int kChunkBf16 = 2048;  // 32x32 bf16
 
 __device__ __forceinline__ bool epi_reads_aux(int epi) {
-  return epi == EPS_EPI_BIAS_RESID_BF16 || epi == EPS_EPI_DGELU_BF16;
+  return epi == EPS_EPI_BIAS_RESID_BF16 || epi == EPS_EPI_DGELU_BF16 ||
+         epi == EPS_EPI_RESID_BF16;
 }
 
 __device__ __forceinline__ void stage_bf16(uint32_t base, int lane, const float (&v)[32]) {
@@ -330,6 +331,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             stage_bf16(out_s, lane, v);
             break;
           case EPS_EPI_BIAS_RESID_BF16:
+          case EPS_EPI_RESID_BF16:
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] += x[j];
             stage_bf16(out_s, lane, v);
@@ -428,11 +430,11 @@ extern "C" int eps_gemm_bf16(int a_mn_major, int b_mn_major, int epilogue, const
                              int64_t ldb, int64_t ldc, int split_k, void* stream) {
   using namespace eps_k;
   if (M <= 0 || N <= 0 || K <= 0 || N % 8 != 0 || lda % 8 != 0 || ldb % 8 != 0 ||
-      ldc % 8 != 0 || M > (int64_t(1) << 31) || epilogue < 0 || epilogue > EPS_EPI_ACCUM_F32)
+      ldc % 8 != 0 || M > (int64_t(1) << 31) || epilogue < 0 || epilogue > EPS_EPI_RESID_BF16)
     return EPS_EINVAL;
   if (split_k < 1) split_k = 1;
   const bool needs_aux = epilogue == EPS_EPI_BIAS_GELU_BF16 || epilogue == EPS_EPI_BIAS_RESID_BF16 ||
-                         epilogue == EPS_EPI_DGELU_BF16;
+                         epilogue == EPS_EPI_DGELU_BF16 || epilogue == EPS_EPI_RESID_BF16;
   if (needs_aux && aux == nullptr) return EPS_EINVAL;
   if ((epilogue == EPS_EPI_BIAS_BF16 || epilogue == EPS_EPI_BIAS_GELU_BF16 ||
        epilogue == EPS_EPI_BIAS_RESID_BF16) && bias == nullptr)

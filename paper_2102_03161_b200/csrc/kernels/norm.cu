@@ -159,8 +159,9 @@ __global__ void __launch_bounds__(kLnWarps * 32)
 #pragma unroll
     for (int i = 0; i < EPL; ++i) {
       r[i] += rs * (g[i] - s1 - xv[i] * s2);
-      // accumulate the stored (bf16-rounded) value so bias grads match the tensor
-      acc_c[i] += __bfloat162float(__float2bfloat16_rn(r[i]));
+      // column sums from the fp32 value (bias grads are sums over many rows
+      // that cancel; summing bf16-rounded rows would add ~2^-9 sqrt(rows) noise)
+      acc_c[i] += r[i];
     }
     if (dx != nullptr) {
 #pragma unroll

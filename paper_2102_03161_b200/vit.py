@@ -83,7 +83,10 @@ def init_params(g: Geometry, seed: int) -> Dict[str, torch.Tensor]:
 
 
 class VitExecutor:
-    """One stage holding the whole ViT stack (K = 1) on the current GPU."""
+    """The ViT stage executor on the current GPU (the whole stack at K = 1, or
+    the sublayer span of one pipeline stage)."""
+
+    PREFIX = "eps_vit_"
 
     def __init__(self, g: Geometry, max_batch: int, seed: int = 17, device=None,
                  params: Optional[Dict[str, torch.Tensor]] = None):
@@ -115,9 +118,9 @@ class VitExecutor:
 
     def __del__(self):
         if getattr(self, "h", None):
-            lib = ops.api().lib
-            lib.eps_vit_destroy.restype = None
-            lib.eps_vit_destroy(self.h)
+            f = getattr(ops.api().lib, self.PREFIX + "destroy")
+            f.restype = None
+            f(self.h)
             self.h = None
 
     # -- parameters --------------------------------------------------------
@@ -187,8 +190,9 @@ class VitExecutor:
                    C.c_float(weight_decay), C.c_void_p(s.cuda_stream))
 
     def layer_sqnorms(self, l_frozen: int, stream=None) -> torch.Tensor:
-        s = torch.cuda.current_stream() if stream is None else stream
-        self._call("eps_vit_layer_sqnorms", l_frozen, self.sq, C.c_void_p(s.cuda_stream))
+        """Per-layer gradient sum of squares (device fp64 [L]; frozen layers 0)."""
+        self.sq.zero_()
+        self.sqnorm_ranges(self.segments[l_frozen:], self.sq[l_frozen:], stream)
         return self.sq
 
     def layer_norms(self, l_frozen: int):
@@ -211,25 +215,25 @@ class VitExecutor:
     def stage_forward(self, images, b0: int, b: int, g0: int, g1: int, l_frozen: int,
                       front: bool, cache_mode: int = 0, cache_old: int = 0, store=None,
                       ids=None, stream=None):
-        self._call("eps_vit_stage_forward",
+        self._call(self.PREFIX + "stage_forward",
                    images if images is not None else C.c_void_p(0), b0, b, g0, g1, l_frozen,
                    int(front), cache_mode, cache_old,
                    store if store is not None else C.c_void_p(0),
                    ids if ids is not None else C.c_void_p(0), self._st(stream))
 
     def stage_head(self, labels, b0: int, b: int, global_batch: int, stream=None):
-        self._call("eps_vit_stage_head", labels, b0, b, global_batch, self.loss_sum,
+        self._call(self.PREFIX + "stage_head", labels, b0, b, global_batch, self.loss_sum,
                    self._st(stream))
 
     def stage_backward(self, b0: int, b: int, g0: int, g1: int, l_frozen: int, cut_out: bool,
                        stream=None):
-        self._call("eps_vit_stage_backward", b0, b, g0, g1, l_frozen, int(cut_out),
+        self._call(self.PREFIX + "stage_backward", b0, b, g0, g1, l_frozen, int(cut_out),
                    self._st(stream))
 
     def cut_rows(self, g: int, b0: int, b: int, grad: bool = False) -> torch.Tensor:
         """bf16 view [b*T, d] of the residual stream at the cut before global
         sublayer g (grad=True: the dX scratch), rows of samples [b0, b0+b)."""
-        f = ops.api().lib.eps_vit_cut
+        f = getattr(ops.api().lib, self.PREFIX + "cut")
         f.restype = C.c_void_p
         f.argtypes = [C.c_void_p, C.c_int, C.c_int]
         ptr = f(self.h, g, int(grad))
@@ -243,18 +247,18 @@ class VitExecutor:
     def param_range(self, g0: int, g1: int):
         """Parameter elements [begin, end) of global sublayers [g0, g1)."""
         a, e = C.c_int64(), C.c_int64()
-        self._call("eps_vit_param_range", g0, g1, C.byref(a), C.byref(e))
+        self._call(self.PREFIX + "param_range", g0, g1, C.byref(a), C.byref(e))
         return a.value, e.value
 
     def sgd_range(self, begin: int, end: int, lr: float, momentum: float = 0.9,
                   weight_decay: float = 0.0, stream=None):
-        self._call("eps_vit_sgd_range", C.c_int64(begin), C.c_int64(end), C.c_float(lr),
+        self._call(self.PREFIX + "sgd_range", C.c_int64(begin), C.c_int64(end), C.c_float(lr),
                    C.c_float(momentum), C.c_float(weight_decay), self._st(stream))
 
     def sqnorm_ranges(self, offsets, out: torch.Tensor, stream=None):
         """out[i] = sum of squared grads over offsets[i]..offsets[i+1]."""
         arr = (C.c_int64 * len(offsets))(*offsets)
-        self._call("eps_vit_sqnorm_ranges", arr, len(offsets) - 1, out, self._st(stream))
+        self._call(self.PREFIX + "sqnorm_ranges", arr, len(offsets) - 1, out, self._st(stream))
         return out
 
     # -- instrumentation ---------------------------------------------------
@@ -263,14 +267,14 @@ class VitExecutor:
 
     def timing(self, on: bool):
         """Bracket every executor launch with CUDA events on its stream."""
-        self._call("eps_vit_timing_enable", int(on))
+        self._call(self.PREFIX + "timing_enable", int(on))
 
     def timing_read(self) -> Dict[str, dict]:
         """Per kernel class: device ms, algorithmic FLOPs / bytes, launches."""
         n = len(self.TIMING_CLASSES)
         ms, fl, by = (C.c_double * n)(), (C.c_double * n)(), (C.c_double * n)()
         cnt = (C.c_int64 * n)()
-        self._call("eps_vit_timing_read", ms, fl, by, cnt)
+        self._call(self.PREFIX + "timing_read", ms, fl, by, cnt)
         return {c: {"ms": ms[i], "flops": fl[i], "bytes": by[i], "launches": cnt[i]}
                 for i, c in enumerate(self.TIMING_CLASSES)}
 

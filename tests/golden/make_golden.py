@@ -26,7 +26,7 @@ def main():
     for name in ("vit_reference", "bert_reference", "ideal_multiplicative"):
         # re-serialised through the reference's own scenario_to_json
         cases.append((name, ref.scenario(os.path.join(REF_CONFIGS, name + ".json")).to_json()))
-    for cid in configs.GEOMETRIES:
+    for cid in configs.BASELINE_CONFIGS:
         for g in ((1,) if cid == "tiny-vit" else (1, 2, 4, 8)):
             cases.append((f"{cid}-g{g}", configs.scenario(cid, g)))
             cases.append((f"{cid}-g{g}-nofreeze", configs.no_freeze(configs.scenario(cid, g))))
