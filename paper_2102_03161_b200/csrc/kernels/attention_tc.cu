@@ -742,14 +742,20 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         // both warps of this lane quarter have read their S^T / dP^T columns
         // before either overwrites the buffer's first 32 columns with bf16 pairs
         asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
+        // No masking: rows / columns past T hold zero-filled K, V (resp. Q, dO)
+        // and lse2 = D = 0, so their P^T is finite and every product that
+        // reaches a stored value is zero (dQ += dS K_j with K_j row = 0,
+        // dV / dK rows past T are not stored, dS = p (0 - 0) for q >= T).
+        // (Rows of keys past T get p = 0 outright, so an extreme lse can never
+        // turn them into inf * 0 inside the dQ MMA.)
         const float sl2 = p.scale_log2;
-        const int qlim = valid_k ? p.T - q0 : 0;  // valid query columns of this warp
+        const float koff = valid_k ? 0.f : 1e30f;
         uint32_t pp[16], pd[16];
 #pragma unroll
         for (int jj = 0; jj < 16; ++jj) {
-          const float p0 = (2 * jj < qlim) ? fast_exp2(fmaf(__uint_as_float(sv[2 * jj]), sl2, -lq[2 * jj])) : 0.f;
+          const float p0 = fast_exp2(fmaf(__uint_as_float(sv[2 * jj]), sl2, -(lq[2 * jj] + koff)));
           const float p1 =
-              (2 * jj + 1 < qlim) ? fast_exp2(fmaf(__uint_as_float(sv[2 * jj + 1]), sl2, -lq[2 * jj + 1])) : 0.f;
+              fast_exp2(fmaf(__uint_as_float(sv[2 * jj + 1]), sl2, -(lq[2 * jj + 1] + koff)));
           pp[jj] = pack_bf16(p0, p1);
           pd[jj] = pack_bf16(p0 * (__uint_as_float(dp[2 * jj]) - dq[2 * jj]),
                              p1 * (__uint_as_float(dp[2 * jj + 1]) - dq[2 * jj + 1]));
@@ -938,22 +944,32 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
               if (c * 32 + j < p.T) m = fmaxf(m, __uint_as_float(r[j]));
           }
         }
-        const float ms = m * p.scale_log2;
+        const float sl2 = p.scale_log2;
+        const float ms = m * sl2;
         float sum = 0.f;
         for (int c = 0; c < Tp / 32; ++c) {
           uint32_t pk[16];
-          if (c < nch) {
+          if (c * 32 + 32 <= p.T) {  // full chunk: no key mask
+            uint32_t r[32];
+            tmem_ld_32x32(tS + uint32_t(c * 32), r);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const float e0 = fast_exp2(fmaf(__uint_as_float(r[2 * j]), sl2, -ms));
+              const float e1 = fast_exp2(fmaf(__uint_as_float(r[2 * j + 1]), sl2, -ms));
+              sum += e0 + e1;
+              pk[j] = pack_bf16(e0, e1);
+            }
+          } else if (c < nch) {
             uint32_t r[32];
             tmem_ld_32x32(tS + uint32_t(c * 32), r);
             tmem_ld_wait();
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
               const int k = c * 32 + 2 * j;
-              const float e0 =
-                  k < p.T ? fast_exp2(fmaf(__uint_as_float(r[2 * j]), p.scale_log2, -ms)) : 0.f;
+              const float e0 = k < p.T ? fast_exp2(fmaf(__uint_as_float(r[2 * j]), sl2, -ms)) : 0.f;
               const float e1 =
-                  k + 1 < p.T ? fast_exp2(fmaf(__uint_as_float(r[2 * j + 1]), p.scale_log2, -ms))
-                              : 0.f;
+                  k + 1 < p.T ? fast_exp2(fmaf(__uint_as_float(r[2 * j + 1]), sl2, -ms)) : 0.f;
               sum += e0 + e1;
               pk[j] = pack_bf16(e0, e1);
             }
