@@ -306,6 +306,16 @@ def main_ours(args, world, rank, local):
                 "peak_kind": f"{peak_kind} bf16_tflops_sustained",
                 "launches_per_step": int(gemm["launches"]),
                 "share_of_step": round(gemm["ms"] / sum(c["ms"] for c in cls.values()), 4)}
+    # DRAM traffic per GEMM launch from the committed ncu --set full capture
+    # (tools/gemm_traffic.py; layer-1 forward QKV / proj / FC1 / FC2 launches)
+    try:
+        with open(os.path.join(ROOT, "profiles", "gemm_traffic.json")) as f:
+            tr = json.load(f)
+        roofline["traffic"] = round(tr["mean_dram_bytes_per_launch"])
+        roofline["traffic_note"] = ("dram bytes per launch, mean of the profiled launches in "
+                                    "profiles/gemm_traffic.json")
+    except (OSError, KeyError, ValueError):
+        pass
     kernels = {}
     for name, c in cls.items():
         if c["launches"] == 0:
