@@ -488,6 +488,11 @@ int eps_vit_stage_head(eps_vit_t* h, const int64_t* labels, int b0, int b, int g
  * stage (this stage then adds its column sum into sublayer g1-1's bias grad). */
 int eps_vit_stage_backward(eps_vit_t* h, int b0, int b, int g0, int g1, int l_frozen,
                            int cut_out, void* stream);
+/* Same over a piece [g0, g1) of a stage whose lowest sublayer is stage_g0
+ * (pieces walked top-down; cut_out only on the topmost piece) -- lets the
+ * host launch a gradient bucket's all-reduce as soon as its sublayers are done. */
+int eps_vit_stage_backward_part(eps_vit_t* h, int b0, int b, int g0, int g1, int stage_g0,
+                                int l_frozen, int cut_out, void* stream);
 /* Residual-stream buffer [max_batch*T, d] bf16 at the cut before global
  * sublayer g (g == 2L: the stack output), or (grad = 1) the dX scratch. */
 void* eps_vit_cut(eps_vit_t* h, int g, int grad);
@@ -556,6 +561,8 @@ int eps_bert_stage_head(eps_bert_t* h, const int64_t* labels, int b0, int b, int
                         float* loss_sum, void* stream);
 int eps_bert_stage_backward(eps_bert_t* h, int b0, int b, int g0, int g1, int l_frozen,
                             int cut_out, void* stream);
+int eps_bert_stage_backward_part(eps_bert_t* h, int b0, int b, int g0, int g1, int stage_g0,
+                                 int l_frozen, int cut_out, void* stream);
 void* eps_bert_cut(eps_bert_t* h, int g, int grad);
 int eps_bert_param_range(eps_bert_t* h, int g0, int g1, int64_t* begin, int64_t* end);
 int eps_bert_sgd_range(eps_bert_t* h, int64_t begin, int64_t end, float lr, float momentum,

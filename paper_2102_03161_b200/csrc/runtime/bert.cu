@@ -610,6 +610,18 @@ int eps_bert_stage_head(eps_bert* h, const int64_t* labels, int b0, int b, int g
   });
 }
 
+int eps_bert_stage_backward_part(eps_bert* h, int b0, int b, int g0, int g1, int stage_g0,
+                                 int l_frozen, int cut_out, void* stream) {
+  (void)cut_out;
+  (void)stage_g0;  // post-norm: every bias gradient stays inside its sublayer
+  return guard([&] {
+    if (h == nullptr || stage_g0 > g0) throw int(EPS_EINVAL);
+    h->check_rows(b0, b);
+    h->check_span(g0, g1, l_frozen);
+    h->stage_bwd(b0, b, g0, g1, l_frozen, static_cast<cudaStream_t>(stream));
+  });
+}
+
 int eps_bert_stage_backward(eps_bert* h, int b0, int b, int g0, int g1, int l_frozen,
                             int cut_out, void* stream) {
   (void)cut_out;  // post-norm: bias grads never straddle a cut

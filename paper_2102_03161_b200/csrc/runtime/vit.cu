@@ -466,7 +466,10 @@ struct eps_vit {
   // Backward of [g0, g1) in reverse with dL/d(output of g1-1) in dX rows.
   // cut_out: that gradient arrived from the next stage, so this stage also
   // owns the column sum for sublayer g1-1's output bias.
-  void stage_bwd(int b0, int b, int g0, int g1, int l_frozen, bool cut_out, cudaStream_t st) {
+  // Sublayers [g0, g1) of a stage whose lowest sublayer is stage_g0 (the host
+  // may walk a stage's span in pieces, e.g. to launch gradient buckets early).
+  void stage_bwd(int b0, int b, int g0, int g1, int stage_g0, int l_frozen, bool cut_out,
+                 cudaStream_t st) {
     if (g1 <= g0) return;
     const int64_t d = g.d, R = int64_t(b) * g.tokens;
     if (cut_out) {
@@ -474,7 +477,7 @@ struct eps_vit {
       float* bias = out_bias_grad(g1 - 1);
       eltwise(st, [&] { return eps_colsum_bf16(dx, bias, R, d, st); });
     }
-    for (int gs = g1 - 1; gs >= g0; --gs) sub_bwd(gs, b0, b, l_frozen, gs == g0, st);
+    for (int gs = g1 - 1; gs >= g0; --gs) sub_bwd(gs, b0, b, l_frozen, gs == stage_g0, st);
     if (g0 == 0 && l_frozen == 0) embed_bwd(b0, b, st);
   }
 
@@ -615,7 +618,7 @@ int eps_vit_train_step(eps_vit* h, const float* images, const int64_t* labels, i
       h->head_fwd_bwd(labels, b0s[m], bs[m], batch, st);
     }
     for (int m = micro_batches - 1; m >= 0; --m)
-      h->stage_bwd(b0s[m], bs[m], g0, g1, l_frozen, false, st);
+      h->stage_bwd(b0s[m], bs[m], g0, g1, g0, l_frozen, false, st);
   });
 }
 
@@ -652,7 +655,18 @@ int eps_vit_stage_backward(eps_vit* h, int b0, int b, int g0, int g1, int l_froz
     if (h == nullptr) throw int(EPS_EINVAL);
     h->check_rows(b0, b);
     h->check_span(g0, g1, l_frozen);
-    h->stage_bwd(b0, b, g0, g1, l_frozen, cut_out != 0, static_cast<cudaStream_t>(stream));
+    h->stage_bwd(b0, b, g0, g1, g0, l_frozen, cut_out != 0, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int eps_vit_stage_backward_part(eps_vit* h, int b0, int b, int g0, int g1, int stage_g0,
+                                int l_frozen, int cut_out, void* stream) {
+  return guard([&] {
+    if (h == nullptr || stage_g0 > g0) throw int(EPS_EINVAL);
+    h->check_rows(b0, b);
+    h->check_span(stage_g0, g1, l_frozen);
+    h->stage_bwd(b0, b, g0, g1, stage_g0, l_frozen, cut_out != 0,
+                 static_cast<cudaStream_t>(stream));
   });
 }
 

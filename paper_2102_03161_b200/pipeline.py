@@ -120,13 +120,16 @@ class Transport:
         else:
             dist.recv(t, src)
 
-    def all_reduce(self, t: torch.Tensor, group, op=dist.ReduceOp.SUM):
+    def all_reduce(self, t: torch.Tensor, group, op=dist.ReduceOp.SUM, async_op: bool = False):
+        """Returns a work handle for an asynchronous NCCL all-reduce (the
+        collective runs on NCCL's stream, ordered after the kernels already
+        queued on the current stream), else None."""
         if self.host_staged:
             buf = t.detach().cpu()
             dist.all_reduce(buf, op=op, group=group)
             t.copy_(buf)
-        else:
-            dist.all_reduce(t, op=op, group=group)
+            return None
+        return dist.all_reduce(t, op=op, group=group, async_op=async_op)
 
     def broadcast(self, t: torch.Tensor, src: int):
         if self.host_staged:
@@ -138,19 +141,32 @@ class Transport:
 
 
 # ---- one rank's stage ------------------------------------------------------------------
+BUCKET_BYTES = 25.0e6  # CostModel::allreduce_bucket_bytes (cost_model.hpp:16)
+
+
 class StageRunner:
     """Executes the iterations of one rank (one pipeline stage of one replica)
-    over a stage executor exposing the eps_vit_stage_* operations."""
+    over a stage executor exposing the eps_vit_stage_* operations.
 
-    def __init__(self, ex, rank: int, world: int, transport: Transport):
+    Gradient synchronisation follows the reference's DDP model
+    (schedule.cpp:133-178): the stage's active parameters form ~25 MB buckets
+    in reverse sublayer order, and each bucket's all-reduce is launched as soon
+    as the last micro-batch's backward has finished its sublayers, overlapping
+    the rest of the drain."""
+
+    def __init__(self, ex, rank: int, world: int, transport: Transport,
+                 bucket_bytes: float = BUCKET_BYTES):
         self.ex = ex
         self.rank = rank
         self.world = world
         self.tp = transport
+        self.bucket_bytes = bucket_bytes
         self.plan: Optional[StagePlan] = None
         self.g0 = self.g1 = 0
         self.stage = self.pipe = 0
         self.range = (0, 0)
+        self.buckets: List[Tuple[int, int]] = []
+        self.pending: List[Tuple[object, int, int]] = []
 
     # -- plan changes ------------------------------------------------------------
     def _dp_groups(self, plan: StagePlan):
@@ -171,6 +187,19 @@ class StageRunner:
         self.g0, self.g1 = plan.spans[self.stage]
         self.groups = self._dp_groups(plan)
         self.range = self.ex.param_range(*plan.owner_spans()[self.stage])
+        self.buckets = self._plan_buckets() if plan.R > 1 else []
+
+    def _plan_buckets(self) -> List[Tuple[int, int]]:
+        """Sublayer pieces [g_lo, g_hi) of this stage, top first, each closed
+        once its fp32 gradients reach the bucket size."""
+        out, hi, acc = [], self.g1, 0
+        for g in range(self.g1 - 1, self.g0 - 1, -1):
+            a, b = self.ex.param_range(g, g + 1)
+            acc += 4 * (b - a)
+            if acc >= self.bucket_bytes or g == self.g0:
+                out.append((g, hi))
+                hi, acc = g, 0
+        return out
 
     def migrate(self, old: StagePlan):
         """Every parameter (and its momentum) is broadcast from the rank that
@@ -207,22 +236,34 @@ class StageRunner:
             else:
                 ex.stage_head(labels, b0, b, batch)
         if p.trainable(s):
-            for b0, b in reversed(mbs):
+            for i, (b0, b) in enumerate(reversed(mbs)):
                 if s < K - 1:
                     self.tp.recv(ex.cut_rows(0, b0, b, grad=True), nxt)
-                ex.stage_backward(b0, b, self.g0, self.g1, lf, cut_out=s < K - 1)
+                if self.buckets and i == len(mbs) - 1:
+                    # last micro-batch of the drain: walk the stage bucket by bucket
+                    # and start each bucket's all-reduce once its grads are final
+                    for j, (lo, hi) in enumerate(self.buckets):
+                        ex.stage_backward_part(b0, b, lo, hi, self.g0, lf,
+                                               cut_out=(s < K - 1 and j == 0))
+                        a, e = ex.param_range(lo, hi)
+                        work = self.tp.all_reduce(ex.g32[a:e], self.groups[s], async_op=True)
+                        self.pending.append((work, a, e))
+                else:
+                    ex.stage_backward(b0, b, self.g0, self.g1, lf, cut_out=s < K - 1)
                 if p.upstream_needs_grad(s):
                     self.tp.send(ex.cut_rows(0, b0, b, grad=True), prev)
         return ex.loss_sum
 
     def sync_grads(self):
-        """Average this stage's active gradients over its replicas."""
+        """Finish the bucket all-reduces of this iteration and average this
+        stage's active gradients over its replicas."""
         p = self.plan
         if p.R > 1 and p.trainable(self.stage):
-            a, b = self.ex.param_range(self.g0, self.g1)
-            g = self.ex.g32[a:b]
-            self.tp.all_reduce(g, self.groups[self.stage])
-            g.mul_(1.0 / p.R)
+            for work, a, e in self.pending:
+                if work is not None:
+                    work.wait()
+                self.ex.g32[a:e].mul_(1.0 / p.R)
+            self.pending = []
 
     def step(self, lr: float, momentum: float = 0.9, weight_decay: float = 0.0):
         if self.plan.trainable(self.stage):

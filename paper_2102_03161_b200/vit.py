@@ -230,6 +230,11 @@ class VitExecutor:
         self._call(self.PREFIX + "stage_backward", b0, b, g0, g1, l_frozen, int(cut_out),
                    self._st(stream))
 
+    def stage_backward_part(self, b0: int, b: int, g0: int, g1: int, stage_g0: int,
+                            l_frozen: int, cut_out: bool, stream=None):
+        self._call(self.PREFIX + "stage_backward_part", b0, b, g0, g1, stage_g0, l_frozen,
+                   int(cut_out), self._st(stream))
+
     def cut_rows(self, g: int, b0: int, b: int, grad: bool = False) -> torch.Tensor:
         """bf16 view [b*T, d] of the residual stream at the cut before global
         sublayer g (grad=True: the dX scratch), rows of samples [b0, b0+b)."""

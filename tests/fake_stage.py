@@ -116,6 +116,9 @@ class FakeStageExecutor:
             # for the choreography tests, which freeze nothing or check E separately)
             pass
 
+    def stage_backward_part(self, b0, b, g0, g1, stage_g0, l_frozen, cut_out):
+        self.stage_backward(b0, b, g0, g1, l_frozen, cut_out)
+
     def sgd_range(self, begin, end, lr, momentum=0.9, weight_decay=0.0):
         g = self.g32[begin:end]
         m = self.mom[begin:end]

@@ -67,7 +67,8 @@ def _worker(rank, world, port, name, out_dir):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         ex = FakeStageExecutor(layers=L, seed=0)
-        run = StageRunner(ex, rank, world, Transport(host_staged=True))
+        # a small bucket cap so the DP scenarios exercise several buckets
+        run = StageRunner(ex, rank, world, Transport(host_staged=True), bucket_bytes=600)
         losses = []
         for p, seeds in SCENARIOS[name]():
             run.set_plan(p)

@@ -78,7 +78,9 @@ def _worker(rank, world, port, name, out):
         g = GEOMETRIES[CFG]
         plan, seeds = PLANS[name]
         ex = VitExecutor(g, max_batch=BATCH, params=init_params(g, seed=3), device="cuda:0")
-        run = StageRunner(ex, rank, world, Transport(host_staged=True))
+        # small buckets: the replicated plans walk the last micro-batch's drain in
+        # several pieces, each all-reduced as soon as it is final
+        run = StageRunner(ex, rank, world, Transport(host_staged=True), bucket_bytes=200_000)
         run.set_plan(plan)
         pipe, stage = plan.role(rank)
         x, y = _data(seeds[pipe], g)
