@@ -75,7 +75,7 @@ class Trainer:
     def __init__(self, scenario: dict, geometry: Geometry, *, iterations_per_epoch: int,
                  seed: int = 17, lr: float = 1e-3, momentum: float = 0.9,
                  rank: int = 0, world: int = 1, device=None, host_staged: bool = False,
-                 device_norms: bool = True):
+                 device_norms: bool = True, cache_tier: str = "hbm"):
         self.g = geometry
         self.api = EpsApi(LIB_PATH, "eps_")
         self.planner = Planner(self.api, scenario)
@@ -104,6 +104,14 @@ class Trainer:
                                   device=self.device, generator=gen)
         self.labels = torch.randint(0, g.classes, (self.dataset,), device=self.device,
                                     generator=gen)
+        # AutoCache tier: "hbm" (device store) or "host" (pinned host memory,
+        # read / written by the same kernels over the host link -- the real
+        # counterpart of the reference's host tier, autocache.cpp:69-150)
+        if cache_tier not in ("hbm", "host"):
+            raise ValueError("cache_tier must be 'hbm' or 'host'")
+        if cache_tier == "host" and world > 1 and not host_staged:
+            raise NotImplementedError("host-tier store exchange over NCCL (needs device staging)")
+        self.cache_tier = cache_tier
         self.store: Optional[torch.Tensor] = None
         self.norms_prev: Optional[List[float]] = None
 
@@ -121,8 +129,8 @@ class Trainer:
         stage-0 GPU holds all rows (zero the rest, sum over stage-0 ranks)."""
         if plan.R == 1:
             return
-        keep = torch.zeros(self.dataset, dtype=torch.bool, device=self.device)
-        keep[written] = True
+        keep = torch.zeros(self.dataset, dtype=torch.bool, device=self.store.device)
+        keep[written.to(self.store.device)] = True
         if self.runner.stage == 0:
             self.store[~keep] = 0
         group = self.tp.group([p * plan.K for p in range(plan.R)])
@@ -142,8 +150,11 @@ class Trainer:
         if d.cache_enabled and d.cache_boundary != d.l_frozen:
             raise NotImplementedError("cache boundary below L_frozen (policy flip) not executed")
         if d.cache_enabled and self.store is None:
-            self.store = torch.zeros(self.dataset, self.g.tokens, self.g.hidden,
-                                     dtype=torch.bfloat16, device=self.device)
+            shape = (self.dataset, self.g.tokens, self.g.hidden)
+            if self.cache_tier == "host":
+                self.store = torch.zeros(shape, dtype=torch.bfloat16).pin_memory()
+            else:
+                self.store = torch.zeros(shape, dtype=torch.bfloat16, device=self.device)
         if self.store is not None and d.plan_changed and self.world > 1:
             # a fork makes new stage-0 GPUs: they receive the complete store
             # from rank 0 (stage 0 of pipeline 0 always holds every row)

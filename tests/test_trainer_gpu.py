@@ -85,14 +85,15 @@ def _port():
     return p
 
 
-def _worker(rank, world, port, out):
+def _worker(rank, world, port, out, tier="hbm"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         torch.cuda.set_device(0)
         scen = _elastic_scenario()
         tr = Trainer(scen, configs.GEOMETRIES["tiny-vit"], iterations_per_epoch=2, rank=rank,
-                     world=world, device="cuda:0", host_staged=True, device_norms=False)
+                     world=world, device="cuda:0", host_staged=True, device_norms=False,
+                     cache_tier=tier)
         rows = tr.run()
         torch.save([(r.l_frozen, r.k, r.r, r.m, r.cache_enabled, r.mean_loss) for r in rows],
                    os.path.join(out, f"tr_{rank}.pt"))
@@ -100,8 +101,9 @@ def _worker(rank, world, port, out):
         dist.destroy_process_group()
 
 
-def test_two_rank_elastic_run(cuda, tmp_path):
-    mp.spawn(_worker, args=(2, _port(), str(tmp_path)), nprocs=2, join=True)
+@pytest.mark.parametrize("tier", ["hbm", "host"])
+def test_two_rank_elastic_run(cuda, tmp_path, tier):
+    mp.spawn(_worker, args=(2, _port(), str(tmp_path), tier), nprocs=2, join=True)
     a, b = (torch.load(tmp_path / f"tr_{r}.pt") for r in range(2))
     assert [x[:5] for x in a] == [x[:5] for x in b]
     ks = [x[1] for x in a]

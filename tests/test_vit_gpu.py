@@ -115,3 +115,30 @@ def test_sgd_step_and_loss_decreases(cuda):
     torch.cuda.synchronize()
     assert losses[-1] < losses[0] - 0.1, losses
     assert ex.g32.abs().max().item() == 0.0  # optimizer consumed the grads
+
+
+def test_cache_host_tier(cuda):
+    """AutoCache host tier: the store in pinned host
+    memory, read and written by the same gather / scatter kernels over the
+    host link (UVA), gives the same step as the HBM store."""
+    g = GEOMETRIES["tiny-vit"]
+    batch, lf = 8, 2
+    params = init_params(g, seed=3)
+    images, labels = _data(g, batch, seed=9)
+    images, labels = images.cuda(), labels.cuda()
+    ids = torch.tensor([5, 1, 30, 7, 8, 2, 0, 19], device=cuda)
+    dev_store = torch.zeros(32, g.tokens, g.hidden, dtype=torch.bfloat16, device=cuda)
+    host_store = torch.zeros(32, g.tokens, g.hidden, dtype=torch.bfloat16).pin_memory()
+    ex = VitExecutor(g, max_batch=batch, params=params)
+    ex.train_step(images, labels, l_frozen=lf, cache_mode=2, store=dev_store, ids=ids)
+    ex.train_step(images, labels, l_frozen=lf, cache_mode=2, store=host_store, ids=ids)
+    torch.cuda.synchronize()
+    assert torch.equal(host_store, dev_store.cpu())
+    ex.g32.zero_()
+    a = ex.train_step(images, labels, l_frozen=lf, cache_mode=1, store=dev_store, ids=ids).item()
+    ga = ex.g32.clone()
+    ex.g32.zero_()
+    b = ex.train_step(images, labels, l_frozen=lf, cache_mode=1, store=host_store, ids=ids).item()
+    torch.cuda.synchronize()
+    assert a == b
+    assert torch.allclose(ga, ex.g32, rtol=1e-5, atol=1e-7)
