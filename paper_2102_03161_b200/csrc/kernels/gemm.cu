@@ -45,14 +45,19 @@ struct GemmArgs {
   float* colsum;
 };
 
-template <int BN, int STAGES, bool A_MN, bool B_MN>
+// EPIB: per-epilogue-warp smem bytes.  4 KB: output staging only (aux inputs
+// come through registers); 8 KB: 2 KB output + a 3-deep 2 KB TMA ring for the
+// aux input (residual / GELU pre-activation), used with BN = 192 so the
+// mainloop ring still keeps 4 stages.
+template <int BN, int STAGES, bool A_MN, bool B_MN, int EPIB>
 struct GemmCfg {
   static constexpr int kABytes = kBM * kBK * 2;
   static constexpr int kBBytes = BN * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
-  static constexpr int kTmemCols = 2 * BN;  // double-buffered accumulator
-  static constexpr size_t kSmem = size_t(STAGES) * kStageBytes + 8 * 4096 /*epilogue*/ +
-                                  1024 /*align*/ + 256 /*barriers*/;
+  // double-buffered accumulator (2 x BN columns), allocation rounded to a power of two
+  static constexpr int kTmemCols = 2 * BN <= 256 ? 256 : 512;
+  static constexpr size_t kSmem = size_t(STAGES) * kStageBytes + 8 * size_t(EPIB) /*epilogue*/ +
+                                  1024 /*align*/ + 512 /*barriers*/;
   static constexpr uint32_t kIdesc = umma_idesc_bf16(kBM, BN, A_MN, B_MN);
 };
 
@@ -126,6 +131,21 @@ __device__ __forceinline__ void load_aux_row(const uint16_t* aux, int64_t ld, in
   }
 }
 
+__device__ __forceinline__ void read_aux_smem(uint32_t base, int lane, float (&a)[32]) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint4 w = ld_shared_v4(base + swz64(lane, q));
+    a[8 * q + 0] = bf16_lo(w.x);
+    a[8 * q + 1] = bf16_hi(w.x);
+    a[8 * q + 2] = bf16_lo(w.y);
+    a[8 * q + 3] = bf16_hi(w.y);
+    a[8 * q + 4] = bf16_lo(w.z);
+    a[8 * q + 5] = bf16_hi(w.z);
+    a[8 * q + 6] = bf16_lo(w.w);
+    a[8 * q + 7] = bf16_hi(w.w);
+  }
+}
+
 __device__ __forceinline__ void unpack_aux(const uint4 (&w)[4], float (&a)[32]) {
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
@@ -140,23 +160,26 @@ __device__ __forceinline__ void unpack_aux(const uint4 (&w)[4], float (&a)[32]) 
   }
 }
 
-template <int BN, int STAGES, bool A_MN, bool B_MN>
+constexpr int kAuxDepth = 3;
+
+template <int BN, int STAGES, bool A_MN, bool B_MN, int EPIB>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
                    const __grid_constant__ CUtensorMap map_b,
                    const __grid_constant__ CUtensorMap map_c,
                    const __grid_constant__ CUtensorMap map_x, const GemmArgs args) {
-  using Cfg = GemmCfg<BN, STAGES, A_MN, B_MN>;
+  using Cfg = GemmCfg<BN, STAGES, A_MN, B_MN, EPIB>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* ring = smem;
   uint8_t* epi_area = smem + STAGES * Cfg::kStageBytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(epi_area + kEpiWarps * kEpiWarpBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(epi_area + kEpiWarps * EPIB);
   uint64_t* empty = full + STAGES;
   uint64_t* tmem_full = empty + STAGES;
   uint64_t* tmem_empty = tmem_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+  uint64_t* aux_full = tmem_empty + 2;  // [kEpiWarps][kAuxDepth]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aux_full + kAuxDepth * kEpiWarps);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -174,6 +197,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tmem_full[s], 1);
       mbar_init(&tmem_empty[s], kEpiWarps);
     }
+    for (int s = 0; s < kAuxDepth * kEpiWarps; ++s) mbar_init(&aux_full[s], 1);
     mbar_fence_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, Cfg::kTmemCols);
@@ -248,20 +272,50 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int ew = warp - 2;         // 0..7
     const int quarter = warp & 3;    // TMEM lane quarter this warp may access
     const int part = ew >> 2;        // this warp takes chunks part, part+2, ...
-    uint8_t* my_area = epi_area + ew * kEpiWarpBytes;
+    uint8_t* my_area = epi_area + ew * EPIB;
     const uint32_t area_s = smem_addr(my_area);
     const int epi = args.epi;
     const bool aux_in = epi_reads_aux(epi);
+    const bool aux_tma = aux_in && EPIB >= 8192;  // aux through the TMA ring
     const bool f32_out = epi == EPS_EPI_STORE_F32 || epi == EPS_EPI_ACCUM_F32;
-    // Per-warp 4 KB out ring: GELU (2 outputs) and fp32 chunks take 4 KB, bf16 2 KB.
+    // Per-warp out ring: GELU (2 outputs) and fp32 chunks take 4 KB, bf16 2 KB;
+    // with the aux TMA ring: one 2 KB out slot + kAuxDepth 2 KB aux slots.
     const int out_bytes = (epi == EPS_EPI_BIAS_GELU_BF16 || f32_out) ? 4096 : 2048;
-    const int n_out = kEpiWarpBytes / out_bytes;
+    const int n_out = aux_tma ? 1 : kEpiWarpBytes / out_bytes;
     const uint16_t* auxp = static_cast<const uint16_t*>(args.aux);
+    uint64_t* my_aux_bar = aux_full + kAuxDepth * ew;
+    const uint32_t aux_s = area_s + kChunkBf16;
+    // TMA prefetch cursor over this warp's (tile, chunk) stream: c = part, part+2, ...
+    int pf_u = blockIdx.x, pf_c = part;
+    uint32_t pf_n = 0, use_n = 0;
+    auto chunks_of = [&](int uu) {
+      const int tt = uu % tiles;
+      return min(BN / 32, (args.N - (tt % args.tiles_n) * BN + 31) / 32);
+    };
+    auto tma_prefetch_until = [&](uint32_t limit) {
+      while (pf_n < limit) {
+        while (pf_u < units && pf_c >= chunks_of(pf_u)) {
+          pf_u += gridDim.x;
+          pf_c = part;
+        }
+        if (pf_u >= units) return;
+        const int tt = pf_u % tiles;
+        const int row = (tt / args.tiles_n) * kBM + quarter * 32;
+        const int col = (tt % args.tiles_n) * BN + pf_c * 32;
+        const uint32_t slot = pf_n % kAuxDepth;
+        fence_proxy_async_smem();
+        mbar_expect_tx(&my_aux_bar[slot], kChunkBf16);
+        tma_load_2d(my_area + kChunkBf16 * (1 + slot), &map_x, &my_aux_bar[slot], col, row);
+        ++pf_n;
+        pf_c += 2;
+      }
+    };
+    if (aux_tma && lane == 0) tma_prefetch_until(kAuxDepth);
 
     // Pull a tile's aux rows (this lane's row, this warp's chunks) into L2
     // one tile ahead, so the register loads below hit L2 instead of HBM.
     auto prefetch_aux = [&](int uu) {
-      if (!aux_in || uu >= units) return;
+      if (!aux_in || aux_tma || uu >= units) return;
       const int tt = uu % tiles;
       const int pn0 = (tt % args.tiles_n) * BN;
       const int prow = (tt / args.tiles_n) * kBM + quarter * 32 + lane;
@@ -284,7 +338,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int chunks = min(BN / 32, (args.N - n0 + 31) / 32);
       prefetch_aux(u + gridDim.x);
       uint4 xa[4];
-      if (aux_in && part < chunks)
+      if (aux_in && !aux_tma && part < chunks)
         load_aux_row(auxp, args.ldc, my_row, args.M, n0 + part * 32, args.N, xa);
       mbar_wait(&tmem_full[acc], acc_phase);
       tc_fence_after();
@@ -296,14 +350,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t raw[32];
         tmem_ld_32x32(taddr + uint32_t(c * 32), raw);
         uint4 xn[4];
-        if (aux_in && c + 2 < chunks)
+        if (aux_in && !aux_tma && c + 2 < chunks)
           load_aux_row(auxp, args.ldc, my_row, args.M, col0 + 64, args.N, xn);
         tmem_ld_wait();
         float v[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(raw[j]);
         float x[32];
-        if (aux_in) unpack_aux(xa, x);
+        if (aux_tma) {
+          const uint32_t slot = use_n % kAuxDepth;
+          mbar_wait(&my_aux_bar[slot], (use_n / kAuxDepth) & 1);
+          read_aux_smem(aux_s + slot * kChunkBf16, lane, x);
+          ++use_n;
+          __syncwarp();  // every lane has read the slot before it is refilled
+          if (lane == 0) tma_prefetch_until(use_n + kAuxDepth);
+        } else if (aux_in) {
+          unpack_aux(xa, x);
+        }
         if (args.bias != nullptr) {
           const float4* b4 = reinterpret_cast<const float4*>(args.bias + col0);
 #pragma unroll
@@ -365,7 +428,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const float s = warp_transpose_sum32(v);
           if (lane < valid) atomicAdd(args.colsum + col0 + lane, s);
         }
-        if (aux_in) {
+        if (aux_in && !aux_tma) {
 #pragma unroll
           for (int q = 0; q < 4; ++q) xa[q] = xn[q];
         }
@@ -389,11 +452,11 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 // ---- host side -------------------------------------------------------------
 
-template <int BN, int STAGES, bool A_MN, bool B_MN>
+template <int BN, int STAGES, bool A_MN, bool B_MN, int EPIB = 4096>
 int launch(const void* A, const void* B, int64_t lda, int64_t ldb, GemmArgs args,
            cudaStream_t stream) {
-  using Cfg = GemmCfg<BN, STAGES, A_MN, B_MN>;
-  auto kern = gemm_tc_kernel<BN, STAGES, A_MN, B_MN>;
+  using Cfg = GemmCfg<BN, STAGES, A_MN, B_MN, EPIB>;
+  auto kern = gemm_tc_kernel<BN, STAGES, A_MN, B_MN, EPIB>;
   static bool configured = false;
   if (!configured) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -457,11 +520,24 @@ extern "C" int eps_gemm_bf16(int a_mn_major, int b_mn_major, int epilogue, const
   args.splits = (kblocks + args.k_blocks_per_split - 1) / args.k_blocks_per_split;
   args.tiles_m = int((M + kBM - 1) / kBM);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int key = (a_mn_major ? 2 : 0) | (b_mn_major ? 1 : 0);
+  // Epilogues that read an aux input (residual, GELU pre-activation) are
+  // latency-bound on it: BN = 192 tiles free smem for a 3-deep TMA aux ring.
+  const bool aux_epi = epilogue == EPS_EPI_BIAS_RESID_BF16 || epilogue == EPS_EPI_DGELU_BF16 ||
+                       epilogue == EPS_EPI_RESID_BF16;
+  if (aux_epi && N >= 192) {
+    args.tiles_n = int((N + 191) / 192);
+    switch (key) {
+      case 0: return launch<192, 4, false, false, 8192>(A, B, lda, ldb, args, st);
+      case 1: return launch<192, 4, false, true, 8192>(A, B, lda, ldb, args, st);
+      case 2: return launch<192, 4, true, false, 8192>(A, B, lda, ldb, args, st);
+      default: return launch<192, 4, true, true, 8192>(A, B, lda, ldb, args, st);
+    }
+  }
   // BN = 256 when N fills it; 128 otherwise (fewer wasted MMA columns).
   const bool wide = N % 256 == 0 || N >= 1024;
   const int bn = wide ? 256 : 128;
   args.tiles_n = int((N + bn - 1) / bn);
-  const int key = (a_mn_major ? 2 : 0) | (b_mn_major ? 1 : 0);
   if (wide) {
     switch (key) {
       case 0: return launch<256, 4, false, false>(A, B, lda, ldb, args, st);
