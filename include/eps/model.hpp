@@ -19,11 +19,11 @@ namespace eps {
 // the per-sample bytes of the tensor entering global sublayer g (2L+1
 // entries; entry 2L is the model output).  Mirrors model.hpp:15-30.
 struct ModelSpec {
-  std::string name;
-  std::vector<std::int64_t> attention_params;
-  std::vector<std::int64_t> mlp_params;
-  std::vector<std::int64_t> activation_bytes;
-  int bytes_per_param = 4;
+  std::string name;                            // preset or scenario label
+  std::vector<std::int64_t> attention_params;  // ATT block of layer l (QKV + out-proj + LN)
+  std::vector<std::int64_t> mlp_params;        // MLP block of layer l (fc1 + fc2 + LN)
+  std::vector<std::int64_t> activation_bytes;  // per sample, tensor entering sublayer g
+  int bytes_per_param = 4;                     // gradient element size for bucket sizing
 
   int layer_count() const { return static_cast<int>(attention_params.size()); }
   std::int64_t total_params() const;
@@ -33,23 +33,23 @@ struct ModelSpec {
 };
 
 struct ClusterSpec {
-  int node_count = 1;
-  int gpus_per_node = 1;
-  double gpu_memory_bytes = 16e9;
-  double intra_node_bandwidth = 15.754e9;  // bytes/s
-  double inter_node_bandwidth = 5e9;       // bytes/s
+  int node_count = 1;                      // N
+  int gpus_per_node = 1;                   // I (power of two)
+  double gpu_memory_bytes = 16e9;          // per device
+  double intra_node_bandwidth = 15.754e9;  // bytes/s between GPUs of one node
+  double inter_node_bandwidth = 5e9;       // bytes/s across nodes
 
   int total_gpus() const { return node_count * gpus_per_node; }
   void validate() const;
 };
 
 struct TrainingConfig {
-  double per_pipeline_batch = 400.0;
-  int epochs = 10;
-  int iterations_per_epoch = 100;
-  double alpha = 1.0 / 3.0;
-  double lambda_frozen = 1.0 / 6.0;
-  int freeze_check_interval = 1;
+  double per_pipeline_batch = 400.0;  // samples per pipeline per iteration
+  int epochs = 10;                    // epochs of the run
+  int iterations_per_epoch = 100;     // at the initial replica count
+  double alpha = 1.0 / 3.0;           // freeze aggressiveness
+  double lambda_frozen = 1.0 / 6.0;   // memory weight of frozen parameters
+  int freeze_check_interval = 1;      // epochs between freeze decisions
 
   void validate() const;
 };
@@ -57,9 +57,9 @@ struct TrainingConfig {
 enum class SublayerKind { kAttention, kMlp };
 
 struct Sublayer {
-  SublayerKind kind = SublayerKind::kAttention;
-  int layer_index = 0;
-  std::int64_t params = 0;
+  SublayerKind kind = SublayerKind::kAttention;  // ATT or MLP half of a layer
+  int layer_index = 0;                           // transformer layer
+  std::int64_t params = 0;                       // trainable parameters
 
   // ATT of layer i is 2i, MLP is 2i+1 (model.hpp:61-63).
   int global_index() const {
@@ -68,20 +68,22 @@ struct Sublayer {
 };
 
 struct SublayerSeq {
-  std::vector<Sublayer> active;
-  std::int64_t frozen_params = 0;
-  int frozen_layers = 0;
+  std::vector<Sublayer> active;    // trainable sublayers in order
+  std::int64_t frozen_params = 0;  // S_frozen = params of layers [0, L_frozen)
+  int frozen_layers = 0;           // L_frozen
 
   std::int64_t active_params() const;
 };
 
+// Frozen block [0, l_frozen) + the active ATT, MLP sequence (model.cpp:79-92).
 SublayerSeq m_partition(const ModelSpec& model, int l_frozen);
 
-ModelSpec uniform_model(int layers, std::int64_t attention_params,
-                        std::int64_t mlp_params, std::int64_t activation_bytes);
+// L identical layers (model.cpp:94-105).
+ModelSpec uniform_model(int layers, std::int64_t attention_params, std::int64_t mlp_params,
+                        std::int64_t activation_bytes);
 
-ModelSpec vit_b16();
-ModelSpec bert_large();
+ModelSpec vit_b16();     // 86,566,120 parameters (model.cpp:125-150)
+ModelSpec bert_large();  // 335,143,938 parameters (model.cpp:152-179)
 
 // ---- B200 additions (no reference counterpart) ---------------------------
 
