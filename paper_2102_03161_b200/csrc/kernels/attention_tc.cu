@@ -91,7 +91,12 @@ __device__ __forceinline__ void load_tmem_row64(uint32_t taddr, float (&v)[64]) 
   }
 }
 
+// Phase timestamps (clock64) of the fused backward, CTA 0, first 16
+// iterations -- a profiling aid (eps_attn_trace_*), off unless enabled.
+__device__ long long g_trace[16 * 8];
+
 struct Params {
+  int trace;
   int T, H, Tp, n_split;
   float scale, scale_log2;
   const uint16_t* out;  // forward output (bwd: for D = rowsum(dO * O))
@@ -621,8 +626,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       // dV / dK / dQ work of iteration `it` (k-th of its head)
       auto post = [&](int it, int k) {
         const int bsel = it & 1, j = k / nc, c = k % nc;
+        const bool tr = p.trace && blockIdx.x == 0 && it < 16;
+        if (tr) g_trace[it * 8 + 2] = clock64();
         mbar_wait(&bar[PF0 + bsel], (it >> 1) & 1);
         tc_fence_after();
+        if (tr) g_trace[it * 8 + 3] = clock64();
         if (c == 0 && kt > 0) {  // dK / dV of the previous key tile read out
           mbar_wait(&bar[KVE], (kt - 1) & 1);
           tc_fence_after();
@@ -663,6 +671,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         tc_fence_after();
         for (int k = 0; k < n_it; ++k) {
           const int it = it0 + k, bsel = it & 1, j = k / nc, c = k % nc;
+          const bool tr = p.trace && blockIdx.x == 0 && it < 16;
+          if (tr) g_trace[it * 8 + 0] = clock64();
           if (it >= 2) {  // post(it - 2) finished reading this S^T / dP^T buffer
             mbar_wait(&bar[AC0 + bsel], ((it >> 1) - 1) & 1);
             tc_fence_after();
@@ -679,6 +689,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           for (int kk = 0; kk < kD / 16; ++kk)
             tc_mma_bf16(tdP, kdesc(vj, kk), kdesc(oc, kk), idesc_kk, kk > 0 ? 1u : 0u);
           tc_commit(&bar[SF0 + bsel]);
+          if (tr) g_trace[it * 8 + 1] = clock64();
           if (k > 0) post(it - 1, k - 1);
         }
         post(it0 + n_it - 1, n_it - 1);
@@ -724,8 +735,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const int key = j * kTile + row;
         const bool valid_k = key < p.T;
         const int q0 = c * kChunk + half * 32;
+        const bool tr = p.trace && blockIdx.x == 0 && it < 16 && warp == 2 && lane == 0;
         mbar_wait(&bar[SF0 + bsel], (it >> 1) & 1);
         tc_fence_after();
+        if (tr) g_trace[it * 8 + 4] = clock64();
         const uint32_t tS = tmem + uint32_t(bsel * 128) + lane_off, tdP = tS + 64;
         uint32_t sv[32], dp[32];
         tmem_ld_32x32(tS + uint32_t(half * 32), sv);
@@ -739,9 +752,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           dq[4 * v] = d.x, dq[4 * v + 1] = d.y, dq[4 * v + 2] = d.z, dq[4 * v + 3] = d.w;
         }
         tmem_ld_wait();
+        if (tr) g_trace[it * 8 + 5] = clock64();
         // both warps of this lane quarter have read their S^T / dP^T columns
         // before either overwrites the buffer's first 32 columns with bf16 pairs
         asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
+        if (tr) g_trace[it * 8 + 6] = clock64();
         // No masking: rows / columns past T hold zero-filled K, V (resp. Q, dO)
         // and lse2 = D = 0, so their P^T is finite and every product that
         // reaches a stored value is zero (dQ += dS K_j with K_j row = 0,
@@ -775,6 +790,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&bar[PF0 + bsel]);
+        if (tr) g_trace[it * 8 + 7] = clock64();
         if (c == nc - 1) {
           // dV_j (half 0) / dK_j (half 1) complete: store + bias column sums
           mbar_wait(&bar[KVF], kt & 1);
@@ -1064,6 +1080,8 @@ int attn_fwd_tc(const void* qkv, void* out, float* lse, int B, int T, int H, flo
   return cudaGetLastError() == cudaSuccess ? EPS_OK : EPS_ECUDA;
 }
 
+int g_trace_on = 0;
+
 int attn_bwd_tc(const void* qkv, const void* out, const void* dout, const float* lse, void* dqkv,
                 float* dbias, float* dsum, int B, int T, int H, float scale, cudaStream_t st) {
   using namespace attn_tc;
@@ -1085,6 +1103,7 @@ int attn_bwd_tc(const void* qkv, const void* out, const void* dout, const float*
   p.dsum = dsum;
   p.dqkv = static_cast<uint16_t*>(dqkv);
   p.dbias = dbias;
+  p.trace = g_trace_on;
   if (T <= 2 * kTile) {
     const size_t sf = bwd_fused_smem(T);
     if (!ensure_smem(attn_bwd_fused_tc_kernel, sf)) return EPS_ECUDA;
@@ -1106,3 +1125,15 @@ int attn_bwd_tc(const void* qkv, const void* out, const void* dout, const float*
 }
 
 }  // namespace eps_k
+
+// Profiling aid: phase timestamps of the fused attention backward (CTA 0).
+extern "C" int eps_attn_trace_enable(int on) {
+  eps_k::g_trace_on = on;
+  return EPS_OK;
+}
+extern "C" int eps_attn_trace_read(long long* out, int n) {
+  if (n > 16 * 8) n = 16 * 8;
+  return cudaMemcpyFromSymbol(out, eps_k::attn_tc::g_trace, sizeof(long long) * n) == cudaSuccess
+             ? EPS_OK
+             : EPS_ECUDA;
+}

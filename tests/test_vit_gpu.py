@@ -140,5 +140,5 @@ def test_cache_host_tier(cuda):
     ex.g32.zero_()
     b = ex.train_step(images, labels, l_frozen=lf, cache_mode=1, store=host_store, ids=ids).item()
     torch.cuda.synchronize()
-    assert a == b
+    assert abs(a - b) <= 1e-6 * abs(a)  # loss sum uses fp32 atomics
     assert torch.allclose(ga, ex.g32, rtol=1e-5, atol=1e-7)
