@@ -396,11 +396,6 @@ int eps_attn_bwd_ws(const void* qkv, const void* out, const void* dout, const fl
                     void* dqkv, float* dbias_qkv, float* dsum_workspace, int batch, int tokens,
                     int heads, int head_dim, float scale, void* stream);
 
-/* Profiling aid: clock64 phase stamps of the fused attention backward
- * (CTA 0, first 16 iterations, 8 stamps each). */
-int eps_attn_trace_enable(int on);
-int eps_attn_trace_read(long long* out, int n);
-
 /* Flat-arena form: segment s = flat[seg_offsets[s], seg_offsets[s+1]) (host
  * offsets, <= 64 segments); out: device double[n_segments]; workspace >=
  * 8 * ceil(total / 65536) bytes. */

@@ -91,12 +91,7 @@ __device__ __forceinline__ void load_tmem_row64(uint32_t taddr, float (&v)[64]) 
   }
 }
 
-// Phase timestamps (clock64) of the fused backward, CTA 0, first 16
-// iterations -- a profiling aid (eps_attn_trace_*), off unless enabled.
-__device__ long long g_trace[16 * 8];
-
 struct Params {
-  int trace;
   int T, H, Tp, n_split;
   float scale, scale_log2;
   const uint16_t* out;  // forward output (bwd: for D = rowsum(dO * O))
@@ -626,11 +621,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       // dV / dK / dQ work of iteration `it` (k-th of its head)
       auto post = [&](int it, int k) {
         const int bsel = it & 1, j = k / nc, c = k % nc;
-        const bool tr = p.trace && blockIdx.x == 0 && it < 16;
-        if (tr) g_trace[it * 8 + 2] = clock64();
         mbar_wait(&bar[PF0 + bsel], (it >> 1) & 1);
         tc_fence_after();
-        if (tr) g_trace[it * 8 + 3] = clock64();
         if (c == 0 && kt > 0) {  // dK / dV of the previous key tile read out
           mbar_wait(&bar[KVE], (kt - 1) & 1);
           tc_fence_after();
@@ -641,10 +633,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 #pragma unroll
         for (int kk = 0; kk < kChunk / 16; ++kk) {
           const uint32_t acc = (c > 0 || kk > 0) ? 1u : 0u;
-          tc_mma_bf16_ts(tdV, tS + uint32_t(kk * 8), mndesc(oc + uint32_t(kk * 16) * kRowBytes),
-                         idesc_km, acc);
-          tc_mma_bf16_ts(tdK, tdP + uint32_t(kk * 8), mndesc(qc + uint32_t(kk * 16) * kRowBytes),
-                         idesc_km, acc);
+          // 16-query slice kk sits at column 32*(kk/2) + 8*(kk%2) (see the exp loop)
+          const uint32_t pcol = uint32_t(32 * (kk >> 1) + 8 * (kk & 1));
+          tc_mma_bf16_ts(tdV, tS + pcol, mndesc(oc + uint32_t(kk * 16) * kRowBytes), idesc_km, acc);
+          tc_mma_bf16_ts(tdK, tdP + pcol, mndesc(qc + uint32_t(kk * 16) * kRowBytes), idesc_km, acc);
         }
         if (c & 1) {  // both halves of 128-query tile c/2 staged: dQ_t += dS_t K_j
           const int t = c >> 1;
@@ -671,8 +663,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         tc_fence_after();
         for (int k = 0; k < n_it; ++k) {
           const int it = it0 + k, bsel = it & 1, j = k / nc, c = k % nc;
-          const bool tr = p.trace && blockIdx.x == 0 && it < 16;
-          if (tr) g_trace[it * 8 + 0] = clock64();
           if (it >= 2) {  // post(it - 2) finished reading this S^T / dP^T buffer
             mbar_wait(&bar[AC0 + bsel], ((it >> 1) - 1) & 1);
             tc_fence_after();
@@ -689,7 +679,6 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           for (int kk = 0; kk < kD / 16; ++kk)
             tc_mma_bf16(tdP, kdesc(vj, kk), kdesc(oc, kk), idesc_kk, kk > 0 ? 1u : 0u);
           tc_commit(&bar[SF0 + bsel]);
-          if (tr) g_trace[it * 8 + 1] = clock64();
           if (k > 0) post(it - 1, k - 1);
         }
         post(it0 + n_it - 1, n_it - 1);
@@ -735,62 +724,63 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         const int key = j * kTile + row;
         const bool valid_k = key < p.T;
         const int q0 = c * kChunk + half * 32;
-        const bool tr = p.trace && blockIdx.x == 0 && it < 16 && warp == 2 && lane == 0;
         mbar_wait(&bar[SF0 + bsel], (it >> 1) & 1);
         tc_fence_after();
-        if (tr) g_trace[it * 8 + 4] = clock64();
         const uint32_t tS = tmem + uint32_t(bsel * 128) + lane_off, tdP = tS + 64;
-        uint32_t sv[32], dp[32];
-        tmem_ld_32x32(tS + uint32_t(half * 32), sv);
-        tmem_ld_32x32(tdP + uint32_t(half * 32), dp);
-        float lq[32], dq[32];
-#pragma unroll
-        for (int v = 0; v < 8; ++v) {
-          const float4 a = *reinterpret_cast<const float4*>(sL + q0 + 4 * v);
-          const float4 d = *reinterpret_cast<const float4*>(sD + q0 + 4 * v);
-          lq[4 * v] = a.x, lq[4 * v + 1] = a.y, lq[4 * v + 2] = a.z, lq[4 * v + 3] = a.w;
-          dq[4 * v] = d.x, dq[4 * v + 1] = d.y, dq[4 * v + 2] = d.z, dq[4 * v + 3] = d.w;
-        }
-        tmem_ld_wait();
-        if (tr) g_trace[it * 8 + 5] = clock64();
-        // both warps of this lane quarter have read their S^T / dP^T columns
-        // before either overwrites the buffer's first 32 columns with bf16 pairs
-        asm volatile("bar.sync %0, 64;" ::"r"(1 + quarter) : "memory");
-        if (tr) g_trace[it * 8 + 6] = clock64();
         // No masking: rows / columns past T hold zero-filled K, V (resp. Q, dO)
         // and lse2 = D = 0, so their P^T is finite and every product that
         // reaches a stored value is zero (dQ += dS K_j with K_j row = 0,
         // dV / dK rows past T are not stored, dS = p (0 - 0) for q >= T).
-        // (Rows of keys past T get p = 0 outright, so an extreme lse can never
-        // turn them into inf * 0 inside the dQ MMA.)
+        // Rows of keys past T get p = 0 outright (koff), so an extreme lse can
+        // never turn them into inf * 0 inside the dQ MMA.
         const float sl2 = p.scale_log2;
         const float koff = valid_k ? 0.f : 1e30f;
-        uint32_t pp[16], pd[16];
-#pragma unroll
-        for (int jj = 0; jj < 16; ++jj) {
-          const float p0 = fast_exp2(fmaf(__uint_as_float(sv[2 * jj]), sl2, -(lq[2 * jj] + koff)));
-          const float p1 =
-              fast_exp2(fmaf(__uint_as_float(sv[2 * jj + 1]), sl2, -(lq[2 * jj + 1] + koff)));
-          pp[jj] = pack_bf16(p0, p1);
-          pd[jj] = pack_bf16(p0 * (__uint_as_float(dp[2 * jj]) - dq[2 * jj]),
-                             p1 * (__uint_as_float(dp[2 * jj + 1]) - dq[2 * jj + 1]));
-        }
-        tmem_st_32x32_x16(tS + uint32_t(half * 16), pp);
-        tmem_st_32x32_x16(tdP + uint32_t(half * 16), pd);
-        // dS^T row -> staging buffer (tile parity), chunk c&1, pieces half*4 .. +3
         const uint32_t chunk = smem_addr(sS) +
                                uint32_t(((it >> 1) & 1) * 2 + (c & 1)) * uint32_t(kDsChunk) +
                                uint32_t(row >> 3) * 1024u;
+        // Two passes of 16 query columns.  The bf16 P^T / dS^T of this warp's
+        // 32 queries stay inside its own 32 S^T / dP^T columns (pass hh writes
+        // columns 32*half + 8*hh, already read), so the two warps sharing a
+        // lane quarter never wait on each other; the MMAs address the pieces.
 #pragma unroll
-        for (int v = 0; v < 4; ++v)
-          st_shared_v4(chunk + uint32_t(swz128(row & 7, half * 4 + v)), pd[4 * v], pd[4 * v + 1],
-                       pd[4 * v + 2], pd[4 * v + 3]);
+        for (int hh = 0; hh < 2; ++hh) {
+          const uint32_t col = uint32_t(half * 32 + hh * 16);
+          uint32_t sv[16], dp[16];
+          tmem_ld_32x32_x16(tS + col, sv);
+          tmem_ld_32x32_x16(tdP + col, dp);
+          float nl[16], dq[16];
+          const int qb = q0 + hh * 16;
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            const float4 a = *reinterpret_cast<const float4*>(sL + qb + 4 * v);
+            const float4 d = *reinterpret_cast<const float4*>(sD + qb + 4 * v);
+            nl[4 * v] = -(a.x + koff), nl[4 * v + 1] = -(a.y + koff);
+            nl[4 * v + 2] = -(a.z + koff), nl[4 * v + 3] = -(a.w + koff);
+            dq[4 * v] = d.x, dq[4 * v + 1] = d.y, dq[4 * v + 2] = d.z, dq[4 * v + 3] = d.w;
+          }
+          tmem_ld_wait();
+          uint32_t pp[8], pd[8];
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj) {
+            const float p0 = fast_exp2(fmaf(__uint_as_float(sv[2 * jj]), sl2, nl[2 * jj]));
+            const float p1 = fast_exp2(fmaf(__uint_as_float(sv[2 * jj + 1]), sl2, nl[2 * jj + 1]));
+            pp[jj] = pack_bf16(p0, p1);
+            pd[jj] = pack_bf16(p0 * (__uint_as_float(dp[2 * jj]) - dq[2 * jj]),
+                               p1 * (__uint_as_float(dp[2 * jj + 1]) - dq[2 * jj + 1]));
+          }
+          tmem_st_32x32_x8(tS + uint32_t(half * 32 + hh * 8), pp);
+          tmem_st_32x32_x8(tdP + uint32_t(half * 32 + hh * 8), pd);
+          // dS^T row -> staging buffer (tile parity), chunk c&1, pieces half*4 + 2*hh ..
+#pragma unroll
+          for (int v = 0; v < 2; ++v)
+            st_shared_v4(chunk + uint32_t(swz128(row & 7, half * 4 + hh * 2 + v)), pd[4 * v],
+                         pd[4 * v + 1], pd[4 * v + 2], pd[4 * v + 3]);
+        }
         fence_proxy_async_smem();
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&bar[PF0 + bsel]);
-        if (tr) g_trace[it * 8 + 7] = clock64();
         if (c == nc - 1) {
           // dV_j (half 0) / dK_j (half 1) complete: store + bias column sums
           mbar_wait(&bar[KVF], kt & 1);
@@ -1080,7 +1070,6 @@ int attn_fwd_tc(const void* qkv, void* out, float* lse, int B, int T, int H, flo
   return cudaGetLastError() == cudaSuccess ? EPS_OK : EPS_ECUDA;
 }
 
-int g_trace_on = 0;
 
 int attn_bwd_tc(const void* qkv, const void* out, const void* dout, const float* lse, void* dqkv,
                 float* dbias, float* dsum, int B, int T, int H, float scale, cudaStream_t st) {
@@ -1103,7 +1092,6 @@ int attn_bwd_tc(const void* qkv, const void* out, const void* dout, const float*
   p.dsum = dsum;
   p.dqkv = static_cast<uint16_t*>(dqkv);
   p.dbias = dbias;
-  p.trace = g_trace_on;
   if (T <= 2 * kTile) {
     const size_t sf = bwd_fused_smem(T);
     if (!ensure_smem(attn_bwd_fused_tc_kernel, sf)) return EPS_ECUDA;
@@ -1125,15 +1113,3 @@ int attn_bwd_tc(const void* qkv, const void* out, const void* dout, const float*
 }
 
 }  // namespace eps_k
-
-// Profiling aid: phase timestamps of the fused attention backward (CTA 0).
-extern "C" int eps_attn_trace_enable(int on) {
-  eps_k::g_trace_on = on;
-  return EPS_OK;
-}
-extern "C" int eps_attn_trace_read(long long* out, int n) {
-  if (n > 16 * 8) n = 16 * 8;
-  return cudaMemcpyFromSymbol(out, eps_k::attn_tc::g_trace, sizeof(long long) * n) == cudaSuccess
-             ? EPS_OK
-             : EPS_ECUDA;
-}
