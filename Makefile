@@ -29,7 +29,7 @@ $(OBJDIR)/%.o: %.cpp $(wildcard include/eps/*.hpp) include/eps_capi.h
 	@mkdir -p $(dir $@)
 	$(CXX) $(CXXFLAGS) -c $< -o $@
 
-$(OBJDIR)/%.o: %.cu $(wildcard $(PKG)/csrc/kernels/*.cuh) include/eps_capi.h
+$(OBJDIR)/%.o: %.cu $(wildcard $(PKG)/csrc/kernels/*.cuh) include/eps_capi.h $(wildcard include/eps/*.hpp)
 	@mkdir -p $(dir $@)
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $@.ptxas.log || (cat $@.ptxas.log; false)
 

@@ -16,9 +16,13 @@ device and reports the measured end-to-end speedup vs no-freeze
 (runner.cpp:298 semantics: baseline total time / freeze total time).
 
 N > 1 (torchrun, one rank per GPU, NCCL): the ranks execute the planner's
-plan -- K-stage GPipe pipelines (cut activations / gradients over NCCL
-point-to-point on NVLink) times R AutoDP replicas (per-stage NCCL all-reduce
-of the active gradients).  At epoch 0 the reference plans K = N, R = 1, so
+plan -- K-stage GPipe pipelines times R AutoDP replicas (per-stage NCCL
+all-reduce of the active gradients in 25 MB buckets during the drain).  The
+stage hand-off (--p2p ipc, default) is fused into the producing kernels: the
+last GEMM / LayerNorm of a stage stores the cut activation straight into the
+next stage's buffer over CUDA-IPC peer memory (NVLink), and the gradient
+flows back the same way, ordered by stream flags; --p2p nccl uses NCCL
+send / recv instead.  At epoch 0 the reference plans K = N, R = 1, so
 the per-step work is one 400-image batch at every N ("scaling": "strong");
 the freeze schedule forks replicas as layers freeze.
 
@@ -58,6 +62,9 @@ def parse():
     ap.add_argument("--no-schedule", action="store_true", help="skip the freeze-schedule replay")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--p2p", default="ipc", choices=["ipc", "nccl"],
+                    help="stage hand-off: producer kernels write the neighbour's buffers over "
+                         "CUDA-IPC peer memory (default) or NCCL send/recv")
     ap.add_argument("--gloo-one-gpu", action="store_true",
                     help="test mode: all ranks share cuda:0, gloo with host-staged transfers")
     return ap.parse_args()
@@ -237,7 +244,8 @@ def main_ours(args, world, rank, local):
     plan0 = StagePlan.from_decision(decisions[0], g.layers)
 
     ex = VitExecutor(g, max_batch=batch, seed=17, device=dev)
-    runner = StageRunner(ex, rank, world, Transport(host_staged=one_gpu))
+    runner = StageRunner(ex, rank, world, Transport(host_staged=one_gpu),
+                         peer=(args.p2p == "ipc"))
     runner.set_plan(plan0)
     pipe, stage = plan0.role(rank)
     gen = torch.Generator(device=dev).manual_seed(1234 + pipe)

@@ -447,6 +447,22 @@ int eps_scatter_rows(const void* src, void* dst, int64_t dst_stride_rows, int ro
                      int64_t offset_rows, void* stream);
 int eps_colsum_bf16(const void* x, float* out, int64_t rows, int64_t cols, void* stream);
 
+/* ---- peer memory (csrc/runtime/peer.cu) ---------------------------------- */
+/* CUDA IPC export of the allocation holding dev_ptr: 64-byte handle + byte
+ * offset of dev_ptr inside it. */
+int eps_ipc_export(const void* dev_ptr, void* handle, int64_t* offset);
+/* Map a peer allocation: *base for eps_ipc_close, *dev_ptr = base + offset. */
+int eps_ipc_open(const void* handle, int64_t offset, void** base, void** dev_ptr);
+int eps_ipc_close(void* base);
+/* Stream-ordered flag protocol: signal = system-scope release store of
+ * `value` to `flag` (may be a peer address) after all prior work on the
+ * stream; wait = the stream blocks (cuStreamWaitValue32, GEQ) until the local
+ * `flag` reaches `value`. */
+int eps_peer_signal(void* flag, uint32_t value, void* stream);
+int eps_peer_wait(const void* flag, uint32_t value, void* stream);
+/* Stream-ordered device copy (peer addresses allowed, UVA). */
+int eps_copy_async(void* dst, const void* src, int64_t bytes, void* stream);
+
 /* Kernels launched by this library in this process (launch accounting). */
 unsigned long long eps_launch_count(void);
 
@@ -496,6 +512,11 @@ int eps_vit_stage_backward_part(eps_vit_t* h, int b0, int b, int g0, int g1, int
 /* Residual-stream buffer [max_batch*T, d] bf16 at the cut before global
  * sublayer g (g == 2L: the stack output), or (grad = 1) the dX scratch. */
 void* eps_vit_cut(eps_vit_t* h, int g, int grad);
+/* Stage hand-off over peer memory: write the output cut `out_g` into
+ * out_ptr (the next stage's cut buffer, IPC-mapped) and the gradient at the
+ * input cut `dx_g` into dx_ptr (the previous stage's dX buffer) directly from
+ * the producing kernel.  NULL pointers restore local writes. */
+int eps_vit_set_redirect(eps_vit_t* h, int out_g, void* out_ptr, int dx_g, void* dx_ptr);
 /* Parameter elements [begin, end) of global sublayers [g0, g1) (embedding in
  * sublayer 0, final LN + head in sublayer 2L-1); contiguous by layout. */
 int eps_vit_param_range(eps_vit_t* h, int g0, int g1, int64_t* begin, int64_t* end);
@@ -564,6 +585,7 @@ int eps_bert_stage_backward(eps_bert_t* h, int b0, int b, int g0, int g1, int l_
 int eps_bert_stage_backward_part(eps_bert_t* h, int b0, int b, int g0, int g1, int stage_g0,
                                  int l_frozen, int cut_out, void* stream);
 void* eps_bert_cut(eps_bert_t* h, int g, int grad);
+int eps_bert_set_redirect(eps_bert_t* h, int out_g, void* out_ptr, int dx_g, void* dx_ptr);
 int eps_bert_param_range(eps_bert_t* h, int g0, int g1, int64_t* begin, int64_t* end);
 int eps_bert_sgd_range(eps_bert_t* h, int64_t begin, int64_t end, float lr, float momentum,
                        float weight_decay, void* stream);

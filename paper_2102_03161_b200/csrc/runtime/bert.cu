@@ -175,6 +175,14 @@ struct eps_bert {
   float* g32;
   float* mom;
   float* loss_sum = nullptr;
+  // Stage hand-off over peer memory (see the ViT executor).
+  int out_g = -1, dx_g = -1;
+  uint16_t* out_to = nullptr;
+  uint16_t* dx_to = nullptr;
+  uint16_t* out_buf(int gs, uint16_t* local) const {
+    return (gs == out_g && out_to != nullptr) ? out_to : local;
+  }
+  uint16_t* dx_buf(int gs) const { return (gs == dx_g && dx_to != nullptr) ? dx_to : act.dX; }
   eps_bert(const Geometry& geom, float* p, uint16_t* pb, float* gr, float* m, uint8_t* ws)
       : g(geom), lay(geom), act(geom, lay.total, ws), p32(p), p16(pb), g32(gr), mom(m) {}
   ~eps_bert() {
@@ -279,8 +287,8 @@ struct eps_bert {
     });
     mm(0, 0, EPS_EPI_BIAS_RESID_BF16, act.A[l] + r0 * d, W(s.wp), act.S1[l] + r0 * d, P(s.bp),
        act.X[l] + r0 * d, nullptr, R, d, d, d, d, d, 1, st);
-    layernorm(act.S1[l] + r0 * d, s.ln1g, s.ln1b, act.X1[l] + r0 * d, act.mean1[l] + r0,
-              act.rstd1[l] + r0, R, st);
+    layernorm(act.S1[l] + r0 * d, s.ln1g, s.ln1b, out_buf(2 * l + 1, act.X1[l]) + r0 * d,
+              act.mean1[l] + r0, act.rstd1[l] + r0, R, st);
   }
 
   void mlp_fwd(int l, int b0, int b, cudaStream_t st) {
@@ -290,8 +298,8 @@ struct eps_bert {
        act.U[l] + r0 * f, nullptr, R, f, d, d, d, f, 1, st);
     mm(0, 0, EPS_EPI_BIAS_RESID_BF16, act.G[l] + r0 * f, W(s.w2), act.S2[l] + r0 * d, P(s.b2),
        act.X1[l] + r0 * d, nullptr, R, d, f, f, f, d, 1, st);
-    layernorm(act.S2[l] + r0 * d, s.ln2g, s.ln2b, act.X[l + 1] + r0 * d, act.mean2[l] + r0,
-              act.rstd2[l] + r0, R, st);
+    layernorm(act.S2[l] + r0 * d, s.ln2g, s.ln2b, out_buf(2 * l + 2, act.X[l + 1]) + r0 * d,
+              act.mean2[l] + r0, act.rstd2[l] + r0, R, st);
   }
 
   void sub_fwd(int gs, int b0, int b, cudaStream_t st) {
@@ -379,7 +387,8 @@ struct eps_bert {
     mm(1, 1, EPS_EPI_ACCUM_F32, Gm, act.X1[l] + r0 * d, Gr(s.w1), nullptr, nullptr, nullptr, f, d,
        R, f, d, d, split, st);
     // dX1 = dU W1 + dS2 (the residual branch of the post-norm block)
-    mm(0, 1, EPS_EPI_RESID_BF16, Gm, W(s.w1), dX, nullptr, dS, nullptr, R, d, f, f, d, d, 1, st);
+    mm(0, 1, EPS_EPI_RESID_BF16, Gm, W(s.w1), dx_buf(2 * l + 1) + r0 * d, nullptr, dS, nullptr, R,
+       d, f, f, d, d, 1, st);
   }
 
   void att_bwd(int l, int b0, int b, bool need_dx, cudaStream_t st) {
@@ -405,8 +414,8 @@ struct eps_bert {
     mm(1, 1, EPS_EPI_ACCUM_F32, act.dQKV + r0 * 3 * d, act.X[l] + r0 * d, Gr(s.wqkv), nullptr,
        nullptr, nullptr, 3 * d, d, R, 3 * d, d, d, split, st);
     if (need_dx)  // dX = dQKV Wqkv + dS1
-      mm(0, 1, EPS_EPI_RESID_BF16, act.dQKV + r0 * 3 * d, W(s.wqkv), dX, nullptr, dS, nullptr, R,
-         d, 3 * d, 3 * d, d, d, 1, st);
+      mm(0, 1, EPS_EPI_RESID_BF16, act.dQKV + r0 * 3 * d, W(s.wqkv), dx_buf(2 * l) + r0 * d,
+         nullptr, dS, nullptr, R, d, 3 * d, 3 * d, d, d, 1, st);
   }
 
   void embed_bwd(const int64_t* tok, const int64_t* seg, int b0, int b, cudaStream_t st) {
@@ -630,6 +639,16 @@ int eps_bert_stage_backward(eps_bert* h, int b0, int b, int g0, int g1, int l_fr
     h->check_rows(b0, b);
     h->check_span(g0, g1, l_frozen);
     h->stage_bwd(b0, b, g0, g1, l_frozen, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int eps_bert_set_redirect(eps_bert* h, int out_g, void* out_ptr, int dx_g, void* dx_ptr) {
+  return guard([&] {
+    if (h == nullptr) throw int(EPS_EINVAL);
+    h->out_g = out_g;
+    h->out_to = static_cast<uint16_t*>(out_ptr);
+    h->dx_g = dx_g;
+    h->dx_to = static_cast<uint16_t*>(dx_ptr);
   });
 }
 

@@ -172,6 +172,16 @@ struct eps_vit {
   float* g32;
   float* mom;
   float* loss_sum;  // device scalar owned by caller
+  // Stage hand-off over peer memory: the output cut `out_g` is written to
+  // `out_to` (the next stage's buffer) and the gradient at the input cut
+  // `dx_g` to `dx_to` (the previous stage's dX), both [max_batch*T, d].
+  int out_g = -1, dx_g = -1;
+  uint16_t* out_to = nullptr;
+  uint16_t* dx_to = nullptr;
+  uint16_t* out_buf(int gs, uint16_t* local) const {
+    return (gs == out_g && out_to != nullptr) ? out_to : local;
+  }
+  uint16_t* dx_buf(int gs) const { return (gs == dx_g && dx_to != nullptr) ? dx_to : act.dX; }
   eps_vit(const Geometry& geom, float* p, uint16_t* pb, float* gr, float* m, uint8_t* ws)
       : g(geom), lay(geom), act(geom, lay.total, ws), p32(p), p16(pb), g32(gr), mom(m),
         loss_sum(nullptr) {}
@@ -298,8 +308,9 @@ struct eps_vit {
                           act.lse[l] + int64_t(b0) * g.heads * g.tokens, b, g.tokens, g.heads,
                           g.head_dim(), scale(), st);
     });
-    mm(0, 0, EPS_EPI_BIAS_RESID_BF16, act.A[l] + r0 * d, W(s.wp), act.X1[l] + r0 * d, P(s.bp),
-       act.X[l] + r0 * d, nullptr, R, d, d, d, d, d, 1, st);
+    mm(0, 0, EPS_EPI_BIAS_RESID_BF16, act.A[l] + r0 * d, W(s.wp),
+       out_buf(2 * l + 1, act.X1[l]) + r0 * d, P(s.bp), act.X[l] + r0 * d, nullptr, R, d, d, d,
+       d, d, 1, st);
   }
 
   void mlp_fwd(int l, int b0, int b, cudaStream_t st) {
@@ -309,8 +320,9 @@ struct eps_vit {
               act.rstd2[l] + r0, R, st);
     mm(0, 0, EPS_EPI_BIAS_GELU_BF16, act.H2[l] + r0 * d, W(s.w1), act.G[l] + r0 * f, P(s.b1),
        act.U[l] + r0 * f, nullptr, R, f, d, d, d, f, 1, st);
-    mm(0, 0, EPS_EPI_BIAS_RESID_BF16, act.G[l] + r0 * f, W(s.w2), act.X[l + 1] + r0 * d, P(s.b2),
-       act.X1[l] + r0 * d, nullptr, R, d, f, f, f, d, 1, st);
+    mm(0, 0, EPS_EPI_BIAS_RESID_BF16, act.G[l] + r0 * f, W(s.w2),
+       out_buf(2 * l + 2, act.X[l + 1]) + r0 * d, P(s.b2), act.X1[l] + r0 * d, nullptr, R, d, f,
+       f, f, d, 1, st);
   }
 
   void sub_fwd(int gs, int b0, int b, cudaStream_t st) {
@@ -369,7 +381,7 @@ struct eps_vit {
     mm(0, 1, EPS_EPI_STORE_BF16, Gm, W(s.w1), act.dH + r0 * d, nullptr, nullptr, nullptr, R, d,
        f, f, d, d, 1, st);
     layernorm_bwd(act.dH + r0 * d, act.X1[l] + r0 * d, s.ln2g, s.ln2b, act.mean2[l] + r0,
-                  act.rstd2[l] + r0, dX, dX, colsum_prev, R, st);
+                  act.rstd2[l] + r0, dX, dx_buf(2 * l + 1) + r0 * d, colsum_prev, R, st);
   }
 
   // need_dx: write dL/dX[l] (false for the lowest trainable layer when the
@@ -396,8 +408,8 @@ struct eps_vit {
     mm(0, 1, EPS_EPI_STORE_BF16, act.dQKV + r0 * 3 * d, W(s.wqkv), act.dH + r0 * d, nullptr,
        nullptr, nullptr, R, d, 3 * d, 3 * d, d, d, 1, st);
     layernorm_bwd(act.dH + r0 * d, act.X[l] + r0 * d, s.ln1g, s.ln1b, act.mean1[l] + r0,
-                  act.rstd1[l] + r0, dX, need_dx ? dX : nullptr, need_dx ? colsum_prev : nullptr,
-                  R, st);
+                  act.rstd1[l] + r0, dX, need_dx ? dx_buf(2 * l) + r0 * d : nullptr,
+                  need_dx ? colsum_prev : nullptr, R, st);
   }
 
   void embed_bwd(int b0, int b, cudaStream_t st) {
@@ -667,6 +679,16 @@ int eps_vit_stage_backward_part(eps_vit* h, int b0, int b, int g0, int g1, int s
     h->check_span(stage_g0, g1, l_frozen);
     h->stage_bwd(b0, b, g0, g1, stage_g0, l_frozen, cut_out != 0,
                  static_cast<cudaStream_t>(stream));
+  });
+}
+
+int eps_vit_set_redirect(eps_vit* h, int out_g, void* out_ptr, int dx_g, void* dx_ptr) {
+  return guard([&] {
+    if (h == nullptr) throw int(EPS_EINVAL);
+    h->out_g = out_g;
+    h->out_to = static_cast<uint16_t*>(out_ptr);
+    h->dx_g = dx_g;
+    h->dx_to = static_cast<uint16_t*>(dx_ptr);
   });
 }
 

@@ -28,6 +28,7 @@ choreography runs over NCCL (device tensors) or over gloo with host staging
 from __future__ import annotations
 
 import ctypes as C
+import pickle
 from dataclasses import dataclass
 from typing import Dict, List, Optional, Sequence, Tuple
 
@@ -144,6 +145,116 @@ class Transport:
 BUCKET_BYTES = 25.0e6  # CostModel::allreduce_bucket_bytes (cost_model.hpp:16)
 
 
+class PeerLink:
+    """Stage-to-stage hand-off over peer memory (NVLink) for one plan.
+
+    Each rank exports, as CUDA IPC handles, the buffer its first sublayer
+    reads (the input cut), its activation-gradient buffer and a small flag
+    array.  The previous stage's executor then writes its output cut straight
+    into our input buffer from the producing kernel (eps_*_set_redirect), the
+    next stage writes the gradient of our output straight into our dX, and a
+    monotone counter per direction -- bumped with a system-scope release store
+    after the producer, awaited with cuStreamWaitValue32 on the consumer's
+    stream -- orders the two.  A third counter, bumped at the end of each of
+    the receiver's iterations, keeps a relay stage 0 (no backward) from
+    overwriting rows the receiver still uses."""
+
+    FWD, BWD, FREE = 0, 1, 2
+
+    def __init__(self, ex, runner: "StageRunner"):
+        from . import ops
+        self.lib = ops.api().lib
+        self.ex, self.r = ex, runner
+        self.flags = torch.zeros(16, dtype=torch.int32, device=ex.g32.device)
+        self.opened: List[int] = []
+        self.next_flags = self.prev_flags = None
+        self.copy_out = None
+        self.fwd = self.bwd = self.iters = 0
+        for n, args in {"eps_ipc_export": [C.c_void_p, C.c_void_p, C.c_void_p],
+                        "eps_ipc_open": [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p],
+                        "eps_ipc_close": [C.c_void_p],
+                        "eps_peer_signal": [C.c_void_p, C.c_uint32, C.c_void_p],
+                        "eps_peer_wait": [C.c_void_p, C.c_uint32, C.c_void_p],
+                        "eps_copy_async": [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]}.items():
+            getattr(self.lib, n).argtypes = args
+            getattr(self.lib, n).restype = C.c_int
+
+    def _export(self, t: torch.Tensor):
+        h = (C.c_char * 64)()
+        off = C.c_int64()
+        if self.lib.eps_ipc_export(C.c_void_p(t.data_ptr()), h, C.byref(off)) != 0:
+            raise RuntimeError("eps_ipc_export failed")
+        return bytes(h), off.value
+
+    def _open(self, handle) -> int:
+        h = (C.c_char * 64).from_buffer_copy(handle[0])
+        base, ptr = C.c_void_p(), C.c_void_p()
+        if self.lib.eps_ipc_open(h, handle[1], C.byref(base), C.byref(ptr)) != 0:
+            raise RuntimeError("eps_ipc_open failed")
+        self.opened.append(base.value)
+        return ptr.value
+
+    def close(self):
+        for b in self.opened:
+            self.lib.eps_ipc_close(C.c_void_p(b))
+        self.opened = []
+        self.ex.set_redirect(-1, None, -1, None)
+
+    def setup(self, plan: StagePlan, stage: int, g0: int, g1: int):
+        """Collective over the world: exchange handles, map the neighbours."""
+        self.close()
+        self.flags.zero_()
+        torch.cuda.synchronize()
+        mb = self.ex.max_batch
+        mine = {"cut": self._export(self.ex.cut_rows(g0, 0, mb)),
+                "dx": self._export(self.ex.cut_rows(0, 0, mb, grad=True)),
+                "flags": self._export(self.flags)}
+        allh = [None] * self.r.world
+        dist.all_gather_object(allh, pickle.dumps(mine))
+        allh = [pickle.loads(x) for x in allh]
+        K, rank = plan.K, self.r.rank
+        out_g, out_ptr, dx_g, dx_ptr = -1, None, -1, None
+        self.next_flags = self.prev_flags = None
+        self.copy_out = None
+        if stage < K - 1:
+            nxt = allh[rank + 1]
+            peer_cut = self._open(nxt["cut"])
+            self.next_flags = self._open(nxt["flags"])
+            if g1 > g0:  # the stage's last kernel writes the peer buffer itself
+                out_g, out_ptr = g1, peer_cut
+            else:  # relay stage (frozen prefix / cache only): copy its output rows
+                self.copy_out = peer_cut
+        if stage > 0:
+            prv = allh[rank - 1]
+            self.prev_flags = self._open(prv["flags"])
+            if plan.upstream_needs_grad(stage):
+                dx_g, dx_ptr = g0, self._open(prv["dx"])
+        self.ex.set_redirect(out_g, out_ptr, dx_g, dx_ptr)
+        self.fwd = self.bwd = self.iters = 0
+
+    def _stream(self):
+        return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+    def copy(self, dst_ptr: int, src: torch.Tensor):
+        """Stream-ordered copy of `src` to a (peer) device address."""
+        if self.lib.eps_copy_async(C.c_void_p(dst_ptr), C.c_void_p(src.data_ptr()),
+                                   C.c_int64(src.numel() * src.element_size()),
+                                   self._stream()) != 0:
+            raise RuntimeError("eps_copy_async failed")
+
+    def _flag(self, base: int, which: int) -> C.c_void_p:
+        return C.c_void_p(base + 4 * which)
+
+    def signal(self, base, which, value):
+        if self.lib.eps_peer_signal(self._flag(base, which), value, self._stream()) != 0:
+            raise RuntimeError("eps_peer_signal failed")
+
+    def wait(self, which, value):
+        if self.lib.eps_peer_wait(self._flag(self.flags.data_ptr(), which), value,
+                                  self._stream()) != 0:
+            raise RuntimeError("eps_peer_wait failed")
+
+
 class StageRunner:
     """Executes the iterations of one rank (one pipeline stage of one replica)
     over a stage executor exposing the eps_vit_stage_* operations.
@@ -155,8 +266,9 @@ class StageRunner:
     the rest of the drain."""
 
     def __init__(self, ex, rank: int, world: int, transport: Transport,
-                 bucket_bytes: float = BUCKET_BYTES):
+                 bucket_bytes: float = BUCKET_BYTES, peer: bool = False):
         self.ex = ex
+        self.peer = PeerLink(ex, self) if peer else None
         self.rank = rank
         self.world = world
         self.tp = transport
@@ -188,6 +300,8 @@ class StageRunner:
         self.groups = self._dp_groups(plan)
         self.range = self.ex.param_range(*plan.owner_spans()[self.stage])
         self.buckets = self._plan_buckets() if plan.R > 1 else []
+        if self.peer is not None and self.world > 1:
+            self.peer.setup(plan, self.stage, self.g0, self.g1)
 
     def _plan_buckets(self) -> List[Tuple[int, int]]:
         """Sublayer pieces [g_lo, g_hi) of this stage, top first, each closed
@@ -223,22 +337,40 @@ class StageRunner:
         ex, lf = self.ex, p.l_frozen
         mbs = microbatch_offsets(batch, p.M)
         prev, nxt = self.rank - 1, self.rank + 1
+        pl = self.peer if (self.peer is not None and K > 1) else None
         ex.loss_sum.zero_()
+        if pl is not None and s < K - 1 and pl.iters > 0:
+            pl.wait(PeerLink.FREE, pl.iters)  # receiver done with last iteration's rows
         for b0, b in mbs:
-            if s > 0:
+            if pl is not None:
+                if s > 0:
+                    pl.wait(PeerLink.FWD, pl.fwd + 1)
+            elif s > 0:
                 self.tp.recv(ex.cut_rows(self.g0, b0, b), prev)
             ex.stage_forward(images if s == 0 else None, b0, b, self.g0, self.g1, lf,
                              front=(s == 0), cache_mode=cache_mode if s == 0 else 0,
                              cache_old=cache_old, store=store if s == 0 else None,
                              ids=ids if s == 0 else None)
             if s < K - 1:
-                self.tp.send(ex.cut_rows(self.g1, b0, b), nxt)
+                if pl is not None:
+                    if pl.copy_out is not None:
+                        rows = ex.cut_rows(self.g1, b0, b)
+                        pl.copy(pl.copy_out + rows.data_ptr() - ex.cut_rows(self.g1, 0, 1).data_ptr(),
+                                rows)
+                    pl.signal(pl.next_flags, PeerLink.FWD, pl.fwd + 1)
+                else:
+                    self.tp.send(ex.cut_rows(self.g1, b0, b), nxt)
             else:
                 ex.stage_head(labels, b0, b, batch)
+            if pl is not None:
+                pl.fwd += 1
         if p.trainable(s):
             for i, (b0, b) in enumerate(reversed(mbs)):
                 if s < K - 1:
-                    self.tp.recv(ex.cut_rows(0, b0, b, grad=True), nxt)
+                    if pl is not None:
+                        pl.wait(PeerLink.BWD, pl.bwd + 1)
+                    else:
+                        self.tp.recv(ex.cut_rows(0, b0, b, grad=True), nxt)
                 if self.buckets and i == len(mbs) - 1:
                     # last micro-batch of the drain: walk the stage bucket by bucket
                     # and start each bucket's all-reduce once its grads are final
@@ -251,7 +383,16 @@ class StageRunner:
                 else:
                     ex.stage_backward(b0, b, self.g0, self.g1, lf, cut_out=s < K - 1)
                 if p.upstream_needs_grad(s):
-                    self.tp.send(ex.cut_rows(0, b0, b, grad=True), prev)
+                    if pl is not None:
+                        pl.signal(pl.prev_flags, PeerLink.BWD, pl.bwd + 1)
+                    else:
+                        self.tp.send(ex.cut_rows(0, b0, b, grad=True), prev)
+                if pl is not None:
+                    pl.bwd += 1
+        if pl is not None:
+            pl.iters += 1
+            if s > 0:
+                pl.signal(pl.prev_flags, PeerLink.FREE, pl.iters)
         return ex.loss_sum
 
     def sync_grads(self):

@@ -75,7 +75,7 @@ class Trainer:
     def __init__(self, scenario: dict, geometry: Geometry, *, iterations_per_epoch: int,
                  seed: int = 17, lr: float = 1e-3, momentum: float = 0.9,
                  rank: int = 0, world: int = 1, device=None, host_staged: bool = False,
-                 device_norms: bool = True, cache_tier: str = "hbm"):
+                 device_norms: bool = True, cache_tier: str = "hbm", peer: bool = False):
         self.g = geometry
         self.api = EpsApi(LIB_PATH, "eps_")
         self.planner = Planner(self.api, scenario)
@@ -92,7 +92,8 @@ class Trainer:
         self.device = torch.device(device or "cuda")
         self.device_norms = device_norms
         self.ex = VitExecutor(geometry, max_batch=self.batch, seed=seed, device=self.device)
-        self.runner = StageRunner(self.ex, rank, world, Transport(host_staged=host_staged))
+        self.runner = StageRunner(self.ex, rank, world, Transport(host_staged=host_staged),
+                                  peer=peer)
         self.tp = self.runner.tp
         # dataset = iterations x batch x initial replica count (runner.cpp:103-104)
         k0 = scenario.get("initial_pipeline_length", 0) or self.cluster.gpus_per_node

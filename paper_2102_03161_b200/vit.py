@@ -249,6 +249,12 @@ class VitExecutor:
         base = self.ws[off:off + 2 * self.max_batch * T * d].view(torch.bfloat16)
         return base.view(self.max_batch * T, d)[b0 * T:(b0 + b) * T]
 
+    def set_redirect(self, out_g: int, out_ptr, dx_g: int, dx_ptr):
+        """Write the output cut `out_g` / the gradient at cut `dx_g` straight
+        into peer buffers (device addresses, e.g. IPC-mapped); None = local."""
+        self._call(self.PREFIX + "set_redirect", out_g, C.c_void_p(out_ptr or 0), dx_g,
+                   C.c_void_p(dx_ptr or 0))
+
     def param_range(self, g0: int, g1: int):
         """Parameter elements [begin, end) of global sublayers [g0, g1)."""
         a, e = C.c_int64(), C.c_int64()

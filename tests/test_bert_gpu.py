@@ -113,14 +113,14 @@ def _port():
     return p
 
 
-def _worker(rank, world, port, out):
+def _worker(rank, world, port, out, peer=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         torch.cuda.set_device(0)
         g = GEOMETRIES["tiny-bert-qa"]
         ex = BertExecutor(g, max_batch=4, params=init_params(g, seed=11), device="cuda:0")
-        run = StageRunner(ex, rank, world, Transport(host_staged=True))
+        run = StageRunner(ex, rank, world, Transport(host_staged=True), peer=peer)
         plan = StagePlan(2, 1, 2, 0, g.layers, ((0, 1), (1, 4)))  # cut between ATT and MLP
         run.set_plan(plan)
         tok, seg, lab = _data(g, 4, seed=3)
@@ -133,8 +133,9 @@ def _worker(rank, world, port, out):
         dist.destroy_process_group()
 
 
-def test_bert_two_stage_pipeline(cuda, tmp_path):
-    mp.spawn(_worker, args=(2, _port(), str(tmp_path)), nprocs=2, join=True)
+@pytest.mark.parametrize("peer", [False, True])
+def test_bert_two_stage_pipeline(cuda, tmp_path, peer):
+    mp.spawn(_worker, args=(2, _port(), str(tmp_path), peer), nprocs=2, join=True)
     g = GEOMETRIES["tiny-bert-qa"]
     ref = BertExecutor(g, max_batch=4, params=init_params(g, seed=11))
     tok, seg, lab = _data(g, 4, seed=3)

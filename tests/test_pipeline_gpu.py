@@ -70,7 +70,7 @@ PLANS = {
 }
 
 
-def _worker(rank, world, port, name, out):
+def _worker(rank, world, port, name, out, peer=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -80,12 +80,17 @@ def _worker(rank, world, port, name, out):
         ex = VitExecutor(g, max_batch=BATCH, params=init_params(g, seed=3), device="cuda:0")
         # small buckets: the replicated plans walk the last micro-batch's drain in
         # several pieces, each all-reduced as soon as it is final
-        run = StageRunner(ex, rank, world, Transport(host_staged=True), bucket_bytes=200_000)
+        run = StageRunner(ex, rank, world, Transport(host_staged=True), bucket_bytes=200_000,
+                          peer=peer)
         run.set_plan(plan)
         pipe, stage = plan.role(rank)
         x, y = _data(seeds[pipe], g)
-        loss = run.iteration(x.cuda(), y.cuda(), BATCH)
-        run.sync_grads()
+        iters = 2 if peer else 1  # peer mode: also exercise the cross-iteration counters
+        for _ in range(iters):
+            loss = run.iteration(x.cuda(), y.cuda(), BATCH)
+            run.sync_grads()
+        if iters > 1:
+            ex.g32.mul_(1.0 / iters)  # grads accumulated over identical iterations
         norms = run.layer_sqnorms(ex.segments)
         torch.cuda.synchronize()
         a, b = ex.param_range(*plan.owner_spans()[stage])
@@ -96,10 +101,14 @@ def _worker(rank, world, port, name, out):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("name", list(PLANS))
-def test_two_ranks_on_one_gpu(cuda, name, tmp_path):
+@pytest.mark.parametrize("name,peer", [(n, False) for n in PLANS] +
+                         [(n, True) for n in PLANS if PLANS[n][0].K > 1])
+def test_two_ranks_on_one_gpu(cuda, name, peer, tmp_path):
+    """peer=True: the cut activations / gradients are written by the producing
+    kernels straight into the neighbour's buffers over CUDA IPC (same device
+    here, NVLink peers on a multi-GPU box), ordered by stream flags."""
     plan, seeds = PLANS[name]
-    mp.spawn(_worker, args=(2, _port(), name, str(tmp_path)), nprocs=2, join=True)
+    mp.spawn(_worker, args=(2, _port(), name, str(tmp_path), peer), nprocs=2, join=True)
     g = GEOMETRIES[CFG]
     ref = VitExecutor(g, max_batch=BATCH * len(seeds), params=init_params(g, seed=3))
     data = [_data(s, g) for s in seeds]

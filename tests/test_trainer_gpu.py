@@ -85,7 +85,7 @@ def _port():
     return p
 
 
-def _worker(rank, world, port, out, tier="hbm"):
+def _worker(rank, world, port, out, tier="hbm", peer=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -93,7 +93,7 @@ def _worker(rank, world, port, out, tier="hbm"):
         scen = _elastic_scenario()
         tr = Trainer(scen, configs.GEOMETRIES["tiny-vit"], iterations_per_epoch=2, rank=rank,
                      world=world, device="cuda:0", host_staged=True, device_norms=False,
-                     cache_tier=tier)
+                     cache_tier=tier, peer=peer)
         rows = tr.run()
         torch.save([(r.l_frozen, r.k, r.r, r.m, r.cache_enabled, r.mean_loss) for r in rows],
                    os.path.join(out, f"tr_{rank}.pt"))
@@ -101,9 +101,9 @@ def _worker(rank, world, port, out, tier="hbm"):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("tier", ["hbm", "host"])
-def test_two_rank_elastic_run(cuda, tmp_path, tier):
-    mp.spawn(_worker, args=(2, _port(), str(tmp_path), tier), nprocs=2, join=True)
+@pytest.mark.parametrize("tier,peer", [("hbm", False), ("host", False), ("hbm", True)])
+def test_two_rank_elastic_run(cuda, tmp_path, tier, peer):
+    mp.spawn(_worker, args=(2, _port(), str(tmp_path), tier, peer), nprocs=2, join=True)
     a, b = (torch.load(tmp_path / f"tr_{r}.pt") for r in range(2))
     assert [x[:5] for x in a] == [x[:5] for x in b]
     ks = [x[1] for x in a]
