@@ -358,7 +358,9 @@ int eps_grid_coord(const eps_cluster_t* cluster, int pipeline_length, int global
 /* GEMM C[M,N] = sum_k A(m,k) B(n,k), bf16 in, fp32 accumulate (tcgen05 +
  * TMEM + TMA).  a_mn_major: A stored [K][M] (M contiguous) instead of
  * [M][K]; b_mn_major: B stored [K][N] instead of [N][K].  lda/ldb/ldc in
- * elements.  epilogue: see EPS_EPI_*.  aux/aux2 per epilogue. */
+ * elements.  epilogue: see EPS_EPI_*.  aux/aux2 per epilogue.  split_k: K
+ * splits for EPS_EPI_ACCUM_F32 (0 = choose from the tile count: ~3 units
+ * per SM, each split >= 8 k-blocks). */
 enum {
   EPS_EPI_STORE_BF16 = 0,     /* C = acc                                     */
   EPS_EPI_BIAS_BF16 = 1,      /* C = acc + bias[n]                           */

@@ -19,6 +19,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdio>
 
 #include "eps_capi.h"
@@ -495,6 +496,7 @@ extern "C" int eps_gemm_bf16(int a_mn_major, int b_mn_major, int epilogue, const
   if (M <= 0 || N <= 0 || K <= 0 || N % 8 != 0 || lda % 8 != 0 || ldb % 8 != 0 ||
       ldc % 8 != 0 || M > (int64_t(1) << 31) || epilogue < 0 || epilogue > EPS_EPI_RESID_BF16)
     return EPS_EINVAL;
+  const bool auto_split = split_k == 0 && epilogue == EPS_EPI_ACCUM_F32;
   if (split_k < 1) split_k = 1;
   const bool needs_aux = epilogue == EPS_EPI_BIAS_GELU_BF16 || epilogue == EPS_EPI_BIAS_RESID_BF16 ||
                          epilogue == EPS_EPI_DGELU_BF16 || epilogue == EPS_EPI_RESID_BF16;
@@ -515,6 +517,24 @@ extern "C" int eps_gemm_bf16(int a_mn_major, int b_mn_major, int epilogue, const
   args.aux = aux;
   args.colsum = colsum;
   const int kblocks = int((K + kBK - 1) / kBK);
+  if (auto_split) {
+    // wgrad: few output tiles, long contraction over token rows.  Pick the
+    // split s minimising waves(s) * (k-blocks per split + 1): one k-block of
+    // MMA is about the cost of a unit's fp32 tile reduce-add.  Each split
+    // keeps >= 4 k-blocks.
+    const int64_t tiles = ((M + kBM - 1) / kBM) * ((N + 255) / 256);
+    const int64_t sms = sm_count();
+    const int cap = std::max(1, std::min(16, kblocks / 4));
+    double best = 1e30;
+    for (int sk = 1; sk <= cap; ++sk) {
+      const double waves = double((tiles * sk + sms - 1) / sms);
+      const double cost = waves * (double(kblocks) / sk + 1.0);
+      if (cost < best - 1e-12) {
+        best = cost;
+        split_k = sk;
+      }
+    }
+  }
   if (split_k > kblocks) split_k = kblocks;
   args.k_blocks_per_split = (kblocks + split_k - 1) / split_k;
   args.splits = (kblocks + args.k_blocks_per_split - 1) / args.k_blocks_per_split;

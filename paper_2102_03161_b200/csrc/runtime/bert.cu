@@ -326,7 +326,7 @@ struct eps_bert {
                              Gr(lay.bc), b, g.tokens, int(C), gs, st);
       });
       mm(1, 1, EPS_EPI_ACCUM_F32, dlg, xl, Gr(lay.wc), nullptr, nullptr, nullptr, C, d, R, C, d, d,
-         split_for(R), st);
+         0, st);
       mm(0, 1, EPS_EPI_STORE_BF16, dlg, W(lay.wc), dX, nullptr, nullptr, nullptr, R, d, C, C, d, d,
          1, st);
       return;
@@ -377,7 +377,7 @@ struct eps_bert {
     uint16_t* dX = act.dX + r0 * d;
     uint16_t* dS = act.dS + r0 * d;
     uint16_t* Gm = act.G[l] + r0 * f;
-    const int split = split_for(R);
+    const int split = 0;  // auto split-K (eps_gemm_bf16)
     layernorm_bwd(dX, act.S2[l] + r0 * d, s.ln2g, s.ln2b, act.mean2[l] + r0, act.rstd2[l] + r0, dS,
                   Gr(s.b2), R, st);
     mm(1, 1, EPS_EPI_ACCUM_F32, dS, Gm, Gr(s.w2), nullptr, nullptr, nullptr, d, f, R, d, f, f,
@@ -396,7 +396,7 @@ struct eps_bert {
     const int64_t d = g.d, r0 = int64_t(b0) * g.tokens, R = int64_t(b) * g.tokens;
     uint16_t* dX = act.dX + r0 * d;
     uint16_t* dS = act.dS + r0 * d;
-    const int split = split_for(R);
+    const int split = 0;  // auto split-K (eps_gemm_bf16)
     layernorm_bwd(dX, act.S1[l] + r0 * d, s.ln1g, s.ln1b, act.mean1[l] + r0, act.rstd1[l] + r0, dS,
                   Gr(s.bp), R, st);
     mm(1, 1, EPS_EPI_ACCUM_F32, dS, act.A[l] + r0 * d, Gr(s.wp), nullptr, nullptr, nullptr, d, d,

@@ -370,7 +370,7 @@ struct eps_vit {
     const int64_t d = g.d, f = g.f, r0 = int64_t(b0) * g.tokens, R = int64_t(b) * g.tokens;
     uint16_t* dX = act.dX + r0 * d;
     uint16_t* Gm = act.G[l] + r0 * f;
-    const int split = split_for(R);
+    const int split = 0;  // auto split-K (eps_gemm_bf16)
     mm(1, 1, EPS_EPI_ACCUM_F32, dX, Gm, Gr(s.w2), nullptr, nullptr, nullptr, d, f, R, d, f, f,
        split, st);
     // du overwrites G (its last reader was the dW2 GEMM above)
@@ -390,7 +390,7 @@ struct eps_vit {
     const LayerSlots& s = lay.layer[l];
     const int64_t d = g.d, r0 = int64_t(b0) * g.tokens, R = int64_t(b) * g.tokens;
     uint16_t* dX = act.dX + r0 * d;
-    const int split = split_for(R);
+    const int split = 0;  // auto split-K (eps_gemm_bf16)
     mm(1, 1, EPS_EPI_ACCUM_F32, dX, act.A[l] + r0 * d, Gr(s.wp), nullptr, nullptr, nullptr, d, d,
        R, d, d, d, split, st);
     mm(0, 1, EPS_EPI_STORE_BF16, dX, W(s.wp), act.dA + r0 * d, nullptr, nullptr, nullptr, R, d, d,
@@ -421,7 +421,7 @@ struct eps_vit {
     });
     eltwise(st, [&] { return eps_colsum_bf16(dptok, Gr(lay.bpe), int64_t(b) * np, d, st); });
     mm(1, 1, EPS_EPI_ACCUM_F32, dptok, act.patches + int64_t(b0) * np * pl, Gr(lay.wpe), nullptr,
-       nullptr, nullptr, d, pl, int64_t(b) * np, d, pl, pl, split_for(int64_t(b) * np), st);
+       nullptr, nullptr, d, pl, int64_t(b) * np, d, pl, pl, 0, st);
   }
 
   // Backward of sublayer gs; `first` = lowest sublayer held by this stage.
