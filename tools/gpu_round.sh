@@ -14,5 +14,5 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemm
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:attn_ -s 2 -c 2 -o gpurun_out/prof_attn -f $B > gpurun_out/ncu_attn.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:ln_ -s 4 -c 2 -o gpurun_out/prof_ln -f $B > gpurun_out/ncu_ln.log 2>&1
 fi
-tail -3 gpurun_out/pytest_gpu.log gpurun_out/smoke.log gpurun_out/bench.err
+tail -n 3 gpurun_out/pytest_gpu.log gpurun_out/smoke.log gpurun_out/bench.err
 cat gpurun_out/bench.json
