@@ -369,7 +369,11 @@ enum {
   EPS_EPI_DGELU_BF16 = 4,     /* C = acc * gelu'(aux[m,n]); colsum -> bias   */
   EPS_EPI_STORE_F32 = 5,      /* Cf32 = acc (beta 0)                         */
   EPS_EPI_ACCUM_F32 = 6,      /* Cf32 += acc (split-K / micro-batch accum)   */
-  EPS_EPI_RESID_BF16 = 7      /* C = acc + aux[m,n] (residual-gradient add)  */
+  EPS_EPI_RESID_BF16 = 7,     /* C = acc + aux[m,n] (residual-gradient add)  */
+  EPS_EPI_ROWDOT_BF16 = 8     /* C = acc; colsum[m*(N/64) + n/64] += sum over
+                                 each 64-column group of bf16(acc)*aux[m,n]
+                                 (attention D = rowsum(dO * O) per head, fused
+                                 into the dO-producing GEMM; colsum pre-zeroed) */
 };
 int eps_gemm_bf16(int a_mn_major, int b_mn_major, int epilogue, const void* A, const void* B,
                   void* C, const float* bias, void* aux, float* colsum, int64_t M, int64_t N,
@@ -397,6 +401,22 @@ int eps_attn_fwd(const void* qkv, void* out, float* lse, int batch, int tokens, 
 int eps_attn_bwd_ws(const void* qkv, const void* out, const void* dout, const float* lse,
                     void* dqkv, float* dbias_qkv, float* dsum_workspace, int batch, int tokens,
                     int heads, int head_dim, float scale, void* stream);
+
+/* Backward with D = rowsum(dO * O) precomputed per (row, head) as fp32
+ * [batch*tokens, heads] (e.g. by EPS_EPI_ROWDOT_BF16 on the GEMM producing
+ * dout).  Used by the fused persistent kernel (head_dim 64, tokens <= 256);
+ * other shapes ignore dsum_rows and use dsum_workspace as eps_attn_bwd_ws. */
+int eps_attn_bwd_rowdot(const void* qkv, const void* out, const void* dout, const float* lse,
+                        const float* dsum_rows, void* dqkv, float* dbias_qkv,
+                        float* dsum_workspace, int batch, int tokens, int heads, int head_dim,
+                        float scale, void* stream);
+/* 1 if eps_attn_bwd_rowdot consumes dsum_rows for this shape. */
+int eps_attn_bwd_uses_rowdot(int tokens, int head_dim);
+
+/* Profiling aid: clock64 phase stamps of CTA 0 of the fused attention
+ * backward (layout documented in attention_tc.cu); off unless enabled. */
+int eps_attn_trace_enable(int on);
+int eps_attn_trace_read(long long* out, int n);
 
 /* Flat-arena form: segment s = flat[seg_offsets[s], seg_offsets[s+1]) (host
  * offsets, <= 64 segments); out: device double[n_segments]; workspace >=

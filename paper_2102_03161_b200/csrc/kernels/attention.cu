@@ -575,7 +575,9 @@ bool attn_tc_supported(int T, int head_dim);
 int attn_fwd_tc(const void* qkv, void* out, float* lse, int B, int T, int H, float scale,
                 cudaStream_t st);
 int attn_bwd_tc(const void* qkv, const void* out, const void* dout, const float* lse, void* dqkv,
-                float* dbias, float* dsum, int B, int T, int H, float scale, cudaStream_t st);
+                float* dbias, float* dsum, const float* drow, int B, int T, int H, float scale,
+                cudaStream_t st);
+bool attn_bwd_fused_supported(int T, int head_dim);
 
 }  // namespace eps_k
 
@@ -604,8 +606,8 @@ extern "C" int eps_attn_bwd_ws(const void* qkv, const void* out, const void* dou
   auto st = static_cast<cudaStream_t>(stream);
   if (batch < 1 || tokens < 1 || heads < 1) return EPS_EINVAL;
   if (attn_tc_supported(tokens, head_dim))
-    return attn_bwd_tc(qkv, out, dout, lse, dqkv, dbias_qkv, dsum_workspace, batch, tokens, heads,
-                       scale, st);
+    return attn_bwd_tc(qkv, out, dout, lse, dqkv, dbias_qkv, dsum_workspace, nullptr, batch,
+                       tokens, heads, scale, st);
   switch (head_dim) {
     case 32:
       return attn_bwd_launch<32>(qkv, out, dout, lse, dqkv, dbias_qkv, dsum_workspace, batch,
@@ -616,4 +618,22 @@ extern "C" int eps_attn_bwd_ws(const void* qkv, const void* out, const void* dou
     default:
       return EPS_EINVAL;
   }
+}
+
+extern "C" int eps_attn_bwd_uses_rowdot(int tokens, int head_dim) {
+  return eps_k::attn_bwd_fused_supported(tokens, head_dim) ? 1 : 0;
+}
+
+extern "C" int eps_attn_bwd_rowdot(const void* qkv, const void* out, const void* dout,
+                                   const float* lse, const float* dsum_rows, void* dqkv,
+                                   float* dbias_qkv, float* dsum_workspace, int batch, int tokens,
+                                   int heads, int head_dim, float scale, void* stream) {
+  using namespace eps_k;
+  if (batch < 1 || tokens < 1 || heads < 1) return EPS_EINVAL;
+  if (!attn_bwd_fused_supported(tokens, head_dim))
+    return eps_attn_bwd_ws(qkv, out, dout, lse, dqkv, dbias_qkv, dsum_workspace, batch, tokens,
+                           heads, head_dim, scale, stream);
+  if (dsum_rows == nullptr) return EPS_EINVAL;
+  return attn_bwd_tc(qkv, out, dout, lse, dqkv, dbias_qkv, dsum_workspace, dsum_rows, batch,
+                     tokens, heads, scale, static_cast<cudaStream_t>(stream));
 }

@@ -92,9 +92,11 @@ __device__ __forceinline__ void load_tmem_row64(uint32_t taddr, float (&v)[64]) 
 }
 
 struct Params {
+  int trace;  // record phase stamps of CTA 0 (eps_attn_trace_*)
   int T, H, Tp, n_split;
   float scale, scale_log2;
   const uint16_t* out;  // forward output (bwd: for D = rowsum(dO * O))
+  const float* drow;  // bwd (fused): D = rowsum(dO * O), fp32 [B*T, H]
   uint16_t* out_w;      // forward: written
   float* lse;
   float* dsum;
@@ -525,23 +527,45 @@ __global__ void __launch_bounds__(kThreads, 2)
 }
 
 // ---------------------------------------------------------------------------
+// Profiling aid: clock64 phase stamps of CTA 0 of the fused backward (off
+// unless eps_attn_trace_enable(1)).  Layout: [it*8 + e] for the first 64
+// iterations (e: 0 S issued, 1 PF seen by MMA, 2 post issued, 3 SF seen by
+// exp warp 2, 4 PF arrive by exp warp 2), [512 + kt*2 + e] per key tile
+// (KVF seen, KVE arrive), [640 + hi*4 + e] per head (DQF seen, DQE arrive,
+// FULL seen by MMA, table ready seen by exp).
+__device__ long long g_attn_trace[1024];
+#define EPS_TRACE(cond, idx) \
+  do {                        \
+    if (p.trace && blockIdx.x == 0 && (cond)) g_attn_trace[(idx)] = clock64(); \
+  } while (0)
+
 // Fused, persistent backward for T <= 256.  One CTA per SM walks the (b, h)
 // heads; per head Q, dO, K, V (<= 256 rows each) sit in smem and the
 // (128-key tile j, 64-query chunk c) pairs are visited once, so every exp is
 // evaluated once:
 //   S^T = K_j Q_c^T, dP^T = V_j dO_c^T                 (SS MMAs -> TMEM)
 //   P^T = exp2(S^T*scale*log2e - lse2[q]), dS^T = P^T (dP^T - D[q])
-//        (8 warps: key row per lane, 32 queries per warp; P^T / dS^T back
-//         into TMEM as bf16, dS^T also into a smem staging tile)
+//        (8 exp warps: key row per lane, 32 queries per warp; P^T / dS^T
+//         back into TMEM as bf16, dS^T also into a smem staging tile)
 //   dV_j += P^T dO_c, dK_j += dS^T Q_c                 (TS MMAs, A in TMEM)
 //   dQ_t += dS_t K_j once both 64-query halves of 128-query tile t are staged
 //                                                     (SS MMA, A MN-major)
-// S^T / dP^T are double-buffered in TMEM and the MMA issue runs one chunk
-// ahead of the exp work; dS staging is double-buffered in smem.
-// TMEM (512 cols): [S^T 64 | dP^T 64] x 2 | dV 64 | dK 64 | dQ_0 64 | dQ_1 64.
-// The next head's tiles are prefetched into L2 while this one computes.
+// Roles (448 threads):
+//   warp 0       TMA: the head's Q, dO, K, V; L2 prefetch two heads ahead
+//   warp 1       TMEM alloc + single-thread MMA issue, one chunk ahead of exp
+//   warps 2-9    exp / dS only: they never wait on an epilogue
+//   warps 10-13  epilogue: the NEXT head's per-query (-lse*log2e, D) into a
+//                double-buffered smem table (D = rowsum(dO * O) arrives
+//                precomputed, fused into the GEMM that produced dO); dV / dK
+//                per key tile and dQ per head: TMEM -> bf16 -> global, plus
+//                the QKV bias column sums
+// S^T / dP^T are double-buffered in TMEM, dS staging is double-buffered in
+// smem.  TMEM (512 cols): [S^T 64 | dP^T 64] x 2 | dV 64 | dK 64 | dQ_t 64 x NT.
+// NT (= ceil(T / 128)) is a template parameter so the iteration bookkeeping
+// is shifts and masks.
 constexpr int kDsChunk = kTile * kRowBytes;  // [128 keys][64 queries] bf16 = 16 KB
-constexpr int kBwdThreads = 64 + 8 * 32;
+constexpr int kBwdExpWarps = 8, kBwdEpiWarps = 4;
+constexpr int kBwdThreads = 64 + 32 * (kBwdExpWarps + kBwdEpiWarps);
 
 __device__ __forceinline__ void tma_prefetch_3d(const void* tmap, int c0, int c1, int c2) {
   asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];" ::"l"(
@@ -550,25 +574,69 @@ __device__ __forceinline__ void tma_prefetch_3d(const void* tmap, int c0, int c1
                : "memory");
 }
 
+// One row of 64 fp32 TMEM columns -> scaled, bf16-rounded pairs (the stored
+// values; bias column sums are taken from the same rounded values).
+__device__ __forceinline__ void load_tmem_packed64(uint32_t taddr, float sc, uint32_t (&pk)[32]) {
+  uint32_t a[32];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    tmem_ld_32x32(taddr + uint32_t(h * 32), a);
+    tmem_ld_wait();
+#pragma unroll
+    for (int d = 0; d < 16; ++d)
+      pk[h * 16 + d] = pack_bf16(__uint_as_float(a[2 * d]) * sc, __uint_as_float(a[2 * d + 1]) * sc);
+  }
+}
+
+__device__ __forceinline__ void zero32(uint32_t (&pk)[32]) {
+#pragma unroll
+  for (int d = 0; d < 32; ++d) pk[d] = 0u;
+}
+
+__device__ __forceinline__ void store_packed64(uint16_t* dst, const uint32_t (&pk)[32]) {
+  uint4* d4 = reinterpret_cast<uint4*>(dst);
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+    d4[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+}
+
+// colsum64 of the 64 bf16 values packed in pk (32 unpacked at a time).
+__device__ __forceinline__ void colsum_packed64(const uint32_t (&pk)[32], float* dbias) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int half = 0; half < 2; ++half) {
+    float t[32];
+#pragma unroll
+    for (int d = 0; d < 16; ++d) {
+      t[2 * d] = bf16_lo(pk[half * 16 + d]);
+      t[2 * d + 1] = bf16_hi(pk[half * 16 + d]);
+    }
+    atomicAdd(dbias + half * 32 + lane, warp_transpose_sum32(t));
+  }
+}
+
+template <int NT>
 __global__ void __launch_bounds__(kBwdThreads, 1)
     attn_bwd_fused_tc_kernel(const __grid_constant__ CUtensorMap map_qkv,
-                             const __grid_constant__ CUtensorMap map_do, const Params p,
+                             const __grid_constant__ CUtensorMap map_do,
+                             const __grid_constant__ CUtensorMap map_dq, const Params p,
                              int n_heads) {
+  constexpr int Tr = NT * kTile;   // rows loaded per operand (zero-filled past T)
+  constexpr int NC = Tr / kChunk;  // 64-query chunks per key tile (2 or 4)
+  constexpr int LNC = NC == 2 ? 1 : 2;
+  constexpr int NIT = NT * NC;     // iterations per head (2 or 8, even)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
-  const int nt = (p.T + kTile - 1) / kTile;  // 128-row tiles of keys / queries (1 or 2)
-  const int Tr = nt * kTile;                 // rows loaded (zero-filled past T)
-  const int nc = Tr / kChunk;                // 64-query chunks per key tile
-  const int n_it = nt * nc;                  // iterations per head (even)
   uint8_t* sQ = smem;
-  uint8_t* sO = sQ + Tr * kRowBytes;
+  uint8_t* sO = sQ + Tr * kRowBytes;  // dO
   uint8_t* sK = sO + Tr * kRowBytes;
   uint8_t* sV = sK + Tr * kRowBytes;
   uint8_t* sS = sV + Tr * kRowBytes;  // dS staging: 2 buffers x 2 chunks x 16 KB
-  float* sL = reinterpret_cast<float*>(sS + 4 * kDsChunk);
-  float* sD = sL + Tr;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sD + Tr);
-  enum { FULL = 0, EMPTY, SF0, SF1, PF0, PF1, AC0, AC1, KVF, KVE, DQF, DQE, NBAR };
+  uint8_t* sStage = sS + 4 * kDsChunk;  // epilogue: one 128x64 bf16 output tile
+  float2* sLD = reinterpret_cast<float2*>(sStage + kDsChunk);  // [2][Tr] (-lse2, D)
+  float* sRed = reinterpret_cast<float*>(sLD + 2 * Tr);  // [64] bias column sums of a head
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sRed + 64);
+  enum { FULL = 0, EMPTY, SF0, SF1, PF0, PF1, AC0, AC1, KVF, KVE, DQF, DQE, LF0, LF1, LE0, LE1, NBAR };
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + NBAR);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int HD = p.H * kD;
@@ -576,8 +644,16 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   if (threadIdx.x == 0) {
     tma_prefetch(&map_qkv);
     tma_prefetch(&map_do);
-    for (int i = 0; i < NBAR; ++i)
-      mbar_init(&bar[i], (i == PF0 || i == PF1 || i == KVE || i == DQE) ? 8 : 1);
+    tma_prefetch(&map_dq);
+    for (int i = 0; i < NBAR; ++i) {
+      uint32_t cnt = 1;
+      if (i == PF0 || i == PF1) cnt = kBwdExpWarps;
+      if (i == KVE || i == DQE) cnt = kBwdEpiWarps;
+      if (i == LF0 || i == LF1) cnt = 32 * kBwdEpiWarps;
+      if (i == LE0 || i == LE1) cnt = 32 * kBwdExpWarps;
+      if (i == EMPTY) cnt = 2;  // MMA warp's commit + the epilogue's dO-sum
+      mbar_init(&bar[i], cnt);
+    }
     mbar_fence_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, 512);
@@ -598,9 +674,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         load_rows(sO, &map_do, &bar[FULL], h * kD, 0, Tr, b);
         load_rows(sK, &map_qkv, &bar[FULL], HD + h * kD, 0, Tr, b);
         load_rows(sV, &map_qkv, &bar[FULL], 2 * HD + h * kD, 0, Tr, b);
-        const int nb = bh + gridDim.x;  // warm L2 with the next head
+        // warm L2 with the next head's tiles
+        const int nb = bh + gridDim.x;
         if (nb < n_heads) {
           const int b2 = nb / p.H, h2 = nb % p.H;
+#pragma unroll
           for (int r = 0; r < Tr; r += kChunk) {
             tma_prefetch_3d(&map_qkv, h2 * kD, r, b2);
             tma_prefetch_3d(&map_do, h2 * kD, r, b2);
@@ -611,217 +689,318 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      const uint32_t q_s = smem_addr(sQ), o_s = smem_addr(sO), k_s = smem_addr(sK),
-                     v_s = smem_addr(sV), ds_s = smem_addr(sS);
-      const uint32_t idesc_kk = umma_idesc_bf16(128, kChunk, false, false);
-      const uint32_t idesc_km = umma_idesc_bf16(128, kD, false, true);
-      const uint32_t idesc_mm = umma_idesc_bf16(128, kD, true, true);
-      int it0 = 0, kt = 0, hi = 0;
-      // dV / dK / dQ work of iteration `it` (k-th of its head)
-      auto post = [&](int it, int k) {
-        const int bsel = it & 1, j = k / nc, c = k % nc;
-        mbar_wait(&bar[PF0 + bsel], (it >> 1) & 1);
+    // The whole warp runs the issue loop (warp-uniform descriptors held in
+    // uniform registers); one elected lane issues each MMA / commit.
+    // Descriptor arithmetic: +2 per 16-element K slice of a K-major operand
+    // (32 B), +128 per 16 K-rows of an MN-major one (2 KB), +8 per row (128 B).
+    const uint64_t dQ0 = umma_sdesc(smem_addr(sQ), 16, 1024), dO0 = umma_sdesc(smem_addr(sO), 16, 1024);
+    const uint64_t dK0 = umma_sdesc(smem_addr(sK), 16, 1024), dV0 = umma_sdesc(smem_addr(sV), 16, 1024);
+    const uint64_t mQ0 = umma_sdesc(smem_addr(sQ), 64 * 128, 1024);
+    const uint64_t mO0 = umma_sdesc(smem_addr(sO), 64 * 128, 1024);
+    const uint64_t mK0 = umma_sdesc(smem_addr(sK), 64 * 128, 1024);
+    const uint64_t mS0 = umma_sdesc(smem_addr(sS), kDsChunk, 1024);
+    constexpr uint32_t idesc_kk = umma_idesc_bf16(128, kChunk, false, false);
+    constexpr uint32_t idesc_km = umma_idesc_bf16(128, kD, false, true);
+    constexpr uint32_t idesc_mm = umma_idesc_bf16(128, kD, true, true);
+    int kt = 0, hi = 0;
+    // dV / dK / dQ work of global iteration `it` (k-th of head hi)
+    auto post = [&](int it, int k) {
+      const int bsel = it & 1, j = k >> LNC, c = k & (NC - 1);
+      mbar_wait(&bar[PF0 + bsel], (it >> 1) & 1);
+      tc_fence_after();
+      EPS_TRACE(it < 64 && lane == 0, it * 8 + 1);
+      if (c == 0 && kt > 0) {  // dK / dV of the previous key tile read out
+        mbar_wait(&bar[KVE], (kt - 1) & 1);
         tc_fence_after();
-        if (c == 0 && kt > 0) {  // dK / dV of the previous key tile read out
-          mbar_wait(&bar[KVE], (kt - 1) & 1);
+      }
+      const uint32_t tS = tmem + uint32_t(bsel * 128), tdP = tS + 64;
+      const uint64_t qc = mQ0 + uint64_t(c * kChunk * 8), oc = mO0 + uint64_t(c * kChunk * 8);
+#pragma unroll
+      for (int kk = 0; kk < kChunk / 16; ++kk) {
+        const uint32_t acc = (c > 0 || kk > 0) ? 1u : 0u;
+        // 16-query slice kk sits at column 32*(kk/2) + 8*(kk%2) (see the exp loop)
+        const uint32_t pcol = uint32_t(32 * (kk >> 1) + 8 * (kk & 1));
+        tc_mma_ts_ws(tdV, tS + pcol, oc + uint64_t(kk * 128), idesc_km, acc);
+        tc_mma_ts_ws(tdK, tdP + pcol, qc + uint64_t(kk * 128), idesc_km, acc);
+      }
+      if (c & 1) {  // both halves of 128-query tile c/2 staged: dQ_t += dS_t K_j
+        const int t = c >> 1;
+        if (j == 0 && t == 0 && hi > 0) {
+          mbar_wait(&bar[DQE], (hi - 1) & 1);
+          tc_fence_after();
+        }
+        const uint64_t stg = mS0 + uint64_t(((it >> 1) & 1) * 2 * (kDsChunk >> 4));
+        const uint64_t kj = mK0 + uint64_t(j * kTile * 8);
+#pragma unroll
+        for (int kk = 0; kk < kTile / 16; ++kk)
+          tc_mma_ss_ws(tdQ + uint32_t(t * kD), stg + uint64_t(kk * 128), kj + uint64_t(kk * 128),
+                       idesc_mm, (j > 0 || kk > 0) ? 1u : 0u);
+      }
+      tc_commit_ws(&bar[AC0 + bsel]);
+      EPS_TRACE(it < 64 && lane == 0, it * 8 + 2);
+      if (c == NC - 1) {
+        tc_commit_ws(&bar[KVF]);
+        ++kt;
+      }
+    };
+    for (int bh = blockIdx.x; bh < n_heads; bh += gridDim.x, ++hi) {
+      const int it0 = hi * NIT;
+      mbar_wait(&bar[FULL], hi & 1);
+      tc_fence_after();
+      EPS_TRACE(hi < 16 && lane == 0, 640 + hi * 4 + 2);
+      for (int k = 0; k < NIT; ++k) {
+        const int it = it0 + k, bsel = k & 1, j = k >> LNC, c = k & (NC - 1);
+        if (it >= 2) {  // post(it - 2) finished reading this S^T / dP^T buffer
+          mbar_wait(&bar[AC0 + bsel], ((it >> 1) - 1) & 1);
           tc_fence_after();
         }
         const uint32_t tS = tmem + uint32_t(bsel * 128), tdP = tS + 64;
-        const uint32_t qc = q_s + uint32_t(c * kChunk) * kRowBytes;
-        const uint32_t oc = o_s + uint32_t(c * kChunk) * kRowBytes;
+        const uint64_t kj = dK0 + uint64_t(j * kTile * 8), vj = dV0 + uint64_t(j * kTile * 8);
+        const uint64_t qc = dQ0 + uint64_t(c * kChunk * 8), oc = dO0 + uint64_t(c * kChunk * 8);
 #pragma unroll
-        for (int kk = 0; kk < kChunk / 16; ++kk) {
-          const uint32_t acc = (c > 0 || kk > 0) ? 1u : 0u;
-          // 16-query slice kk sits at column 32*(kk/2) + 8*(kk%2) (see the exp loop)
-          const uint32_t pcol = uint32_t(32 * (kk >> 1) + 8 * (kk & 1));
-          tc_mma_bf16_ts(tdV, tS + pcol, mndesc(oc + uint32_t(kk * 16) * kRowBytes), idesc_km, acc);
-          tc_mma_bf16_ts(tdK, tdP + pcol, mndesc(qc + uint32_t(kk * 16) * kRowBytes), idesc_km, acc);
-        }
-        if (c & 1) {  // both halves of 128-query tile c/2 staged: dQ_t += dS_t K_j
-          const int t = c >> 1;
-          if (j == 0 && t == 0 && hi > 0) {
-            mbar_wait(&bar[DQE], (hi - 1) & 1);
-            tc_fence_after();
-          }
-          const uint32_t stg = ds_s + uint32_t(((it >> 1) & 1) * 2) * uint32_t(kDsChunk);
-          const uint32_t kj = k_s + uint32_t(j * kTile) * kRowBytes;
+        for (int kk = 0; kk < kD / 16; ++kk)
+          tc_mma_ss_ws(tS, kj + uint64_t(2 * kk), qc + uint64_t(2 * kk), idesc_kk, kk > 0 ? 1u : 0u);
 #pragma unroll
-          for (int kk = 0; kk < kTile / 16; ++kk)
-            tc_mma_bf16(tdQ + uint32_t(t * kD), umma_sdesc(stg + uint32_t(kk) * 2048u, kDsChunk, 1024),
-                        mndesc(kj + uint32_t(kk * 16) * kRowBytes), idesc_mm,
-                        (j > 0 || kk > 0) ? 1u : 0u);
-        }
-        tc_commit(&bar[AC0 + bsel]);
-        if (c == nc - 1) {
-          tc_commit(&bar[KVF]);
-          ++kt;
-        }
-      };
-      for (int bh = blockIdx.x; bh < n_heads; bh += gridDim.x, ++hi) {
-        mbar_wait(&bar[FULL], hi & 1);
-        tc_fence_after();
-        for (int k = 0; k < n_it; ++k) {
-          const int it = it0 + k, bsel = it & 1, j = k / nc, c = k % nc;
-          if (it >= 2) {  // post(it - 2) finished reading this S^T / dP^T buffer
-            mbar_wait(&bar[AC0 + bsel], ((it >> 1) - 1) & 1);
-            tc_fence_after();
-          }
-          const uint32_t tS = tmem + uint32_t(bsel * 128), tdP = tS + 64;
-          const uint32_t kj = k_s + uint32_t(j * kTile) * kRowBytes;
-          const uint32_t vj = v_s + uint32_t(j * kTile) * kRowBytes;
-          const uint32_t qc = q_s + uint32_t(c * kChunk) * kRowBytes;
-          const uint32_t oc = o_s + uint32_t(c * kChunk) * kRowBytes;
-#pragma unroll
-          for (int kk = 0; kk < kD / 16; ++kk)
-            tc_mma_bf16(tS, kdesc(kj, kk), kdesc(qc, kk), idesc_kk, kk > 0 ? 1u : 0u);
-#pragma unroll
-          for (int kk = 0; kk < kD / 16; ++kk)
-            tc_mma_bf16(tdP, kdesc(vj, kk), kdesc(oc, kk), idesc_kk, kk > 0 ? 1u : 0u);
-          tc_commit(&bar[SF0 + bsel]);
-          if (k > 0) post(it - 1, k - 1);
-        }
-        post(it0 + n_it - 1, n_it - 1);
-        tc_commit(&bar[DQF]);
-        tc_commit(&bar[EMPTY]);
-        it0 += n_it;
+        for (int kk = 0; kk < kD / 16; ++kk)
+          tc_mma_ss_ws(tdP, vj + uint64_t(2 * kk), oc + uint64_t(2 * kk), idesc_kk, kk > 0 ? 1u : 0u);
+        tc_commit_ws(&bar[SF0 + bsel]);
+        EPS_TRACE(it < 64 && lane == 0, it * 8 + 0);
+        if (k > 0) post(it - 1, k - 1);
       }
+      post(it0 + NIT - 1, NIT - 1);
+      tc_commit_ws(&bar[DQF]);
+      tc_commit_ws(&bar[EMPTY]);
     }
-  } else {
+  } else if (warp < 2 + kBwdExpWarps) {
+    // ---- exp / dS warps --------------------------------------------------
     const int half = (warp - 2) >> 2;  // which 32 of the chunk's 64 queries
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;
-    const uint32_t lane_off = uint32_t(quarter * 32) << 16;
-    const int tid = threadIdx.x - 64;  // 0..255
-    int it0 = 0, kt = 0, hi = 0;
+    const float sl2 = p.scale_log2;
+    int hi = 0;
     for (int bh = blockIdx.x; bh < n_heads; bh += gridDim.x, ++hi) {
-      const int b = bh / p.H, h = bh % p.H;
-      mbar_wait(&bar[FULL], hi & 1);
-      // prologue: lse (log2 domain) and D = rowsum(dO * O) per query
-      for (int q = tid; q < Tr; q += 256) {
-        float Dq = 0.f, l2 = 0.f;
-        if (q < p.T) {
-          const uint4* o4 =
-              reinterpret_cast<const uint4*>(p.out + (int64_t(b) * p.T + q) * HD + h * kD);
-          const uint32_t rowa = smem_addr(sO) + uint32_t(q >> 3) * 1024u;
-#pragma unroll
-          for (int v = 0; v < 8; ++v) {
-            const uint4 a = __ldg(o4 + v);
-            const uint4 d = ld_shared_v4(rowa + uint32_t(swz128(q & 7, v)));
-            Dq += bf16_lo(a.x) * bf16_lo(d.x) + bf16_hi(a.x) * bf16_hi(d.x) +
-                  bf16_lo(a.y) * bf16_lo(d.y) + bf16_hi(a.y) * bf16_hi(d.y) +
-                  bf16_lo(a.z) * bf16_lo(d.z) + bf16_hi(a.z) * bf16_hi(d.z) +
-                  bf16_lo(a.w) * bf16_lo(d.w) + bf16_hi(a.w) * bf16_hi(d.w);
-          }
-          l2 = p.lse[int64_t(bh) * p.T + q] * kLog2e;
-        }
-        sL[q] = l2;
-        sD[q] = Dq;
-      }
-      asm volatile("bar.sync 5, 256;" ::: "memory");
-      for (int k = 0; k < n_it; ++k) {
-        const int it = it0 + k, bsel = it & 1, j = k / nc, c = k % nc;
-        const int key = j * kTile + row;
-        const bool valid_k = key < p.T;
+      const int lb = hi & 1;
+      mbar_wait(&bar[LF0 + lb], (hi >> 1) & 1);
+      EPS_TRACE(hi < 16 && warp == 2 && lane == 0, 640 + hi * 4 + 3);
+      const uint32_t ld = smem_addr(sLD + lb * Tr);
+#pragma unroll 1
+      for (int k = 0; k < NIT; ++k) {
+        const int it = hi * NIT + k, bsel = k & 1, j = k >> LNC, c = k & (NC - 1);
+        const int kbase = j * kTile + quarter * 32;  // this warp's 32 keys
         const int q0 = c * kChunk + half * 32;
         mbar_wait(&bar[SF0 + bsel], (it >> 1) & 1);
         tc_fence_after();
-        const uint32_t tS = tmem + uint32_t(bsel * 128) + lane_off, tdP = tS + 64;
-        // No masking: rows / columns past T hold zero-filled K, V (resp. Q, dO)
-        // and lse2 = D = 0, so their P^T is finite and every product that
-        // reaches a stored value is zero (dQ += dS K_j with K_j row = 0,
-        // dV / dK rows past T are not stored, dS = p (0 - 0) for q >= T).
-        // Rows of keys past T get p = 0 outright (koff), so an extreme lse can
-        // never turn them into inf * 0 inside the dQ MMA.
-        const float sl2 = p.scale_log2;
-        const float koff = valid_k ? 0.f : 1e30f;
+        EPS_TRACE(it < 64 && warp == 2 && lane == 0, it * 8 + 3);
+        const uint32_t tS = tmem + uint32_t(bsel * 128) + (uint32_t(quarter * 32) << 16);
+        const uint32_t tdP = tS + 64;
         const uint32_t chunk = smem_addr(sS) +
                                uint32_t(((it >> 1) & 1) * 2 + (c & 1)) * uint32_t(kDsChunk) +
                                uint32_t(row >> 3) * 1024u;
-        // Two passes of 16 query columns.  The bf16 P^T / dS^T of this warp's
-        // 32 queries stay inside its own 32 S^T / dP^T columns (pass hh writes
-        // columns 32*half + 8*hh, already read), so the two warps sharing a
-        // lane quarter never wait on each other; the MMAs address the pieces.
+        // Query columns past T need no mask: their Q / dO rows are zero-filled
+        // and -lse2 = D = 0, so P^T = 1 and dS^T = 0, and dV += P^T dO adds
+        // zero rows.  Keys past T are masked per warp (P^T = dS^T = 0, so an
+        // extreme lse can never reach the dQ MMA as inf * 0).
+        if (kbase >= p.T) {
+          const uint32_t z[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
-          const uint32_t col = uint32_t(half * 32 + hh * 16);
-          uint32_t sv[16], dp[16];
-          tmem_ld_32x32_x16(tS + col, sv);
-          tmem_ld_32x32_x16(tdP + col, dp);
-          float nl[16], dq[16];
-          const int qb = q0 + hh * 16;
+          for (int hh = 0; hh < 2; ++hh) {
+            tmem_st_32x32_x8(tS + uint32_t(half * 32 + hh * 8), z);
+            tmem_st_32x32_x8(tdP + uint32_t(half * 32 + hh * 8), z);
 #pragma unroll
-          for (int v = 0; v < 4; ++v) {
-            const float4 a = *reinterpret_cast<const float4*>(sL + qb + 4 * v);
-            const float4 d = *reinterpret_cast<const float4*>(sD + qb + 4 * v);
-            nl[4 * v] = -(a.x + koff), nl[4 * v + 1] = -(a.y + koff);
-            nl[4 * v + 2] = -(a.z + koff), nl[4 * v + 3] = -(a.w + koff);
-            dq[4 * v] = d.x, dq[4 * v + 1] = d.y, dq[4 * v + 2] = d.z, dq[4 * v + 3] = d.w;
+            for (int v = 0; v < 2; ++v)
+              st_shared_v4(chunk + uint32_t(swz128(row & 7, half * 4 + hh * 2 + v)), 0u, 0u, 0u, 0u);
           }
+        } else {
+          const bool mixed = kbase + 32 > p.T;
+          const bool kvalid = kbase + lane < p.T;
+          // The bf16 P^T / dS^T of this warp's 32 queries stay inside its own
+          // 32 S^T / dP^T columns (pass hh writes columns 32*half + 8*hh,
+          // already read), so the two warps sharing a lane quarter never wait
+          // on each other; the MMAs address the pieces.
+          uint32_t sv[2][16], dp[2][16];
+          tmem_ld_32x32_x16(tS + uint32_t(half * 32), sv[0]);
+          tmem_ld_32x32_x16(tdP + uint32_t(half * 32), dp[0]);
+          tmem_ld_32x32_x16(tS + uint32_t(half * 32 + 16), sv[1]);
+          tmem_ld_32x32_x16(tdP + uint32_t(half * 32 + 16), dp[1]);
           tmem_ld_wait();
-          uint32_t pp[8], pd[8];
 #pragma unroll
-          for (int jj = 0; jj < 8; ++jj) {
-            const float p0 = fast_exp2(fmaf(__uint_as_float(sv[2 * jj]), sl2, nl[2 * jj]));
-            const float p1 = fast_exp2(fmaf(__uint_as_float(sv[2 * jj + 1]), sl2, nl[2 * jj + 1]));
-            pp[jj] = pack_bf16(p0, p1);
-            pd[jj] = pack_bf16(p0 * (__uint_as_float(dp[2 * jj]) - dq[2 * jj]),
-                               p1 * (__uint_as_float(dp[2 * jj + 1]) - dq[2 * jj + 1]));
+          for (int hh = 0; hh < 2; ++hh) {
+            const uint32_t l4 = ld + uint32_t(q0 + hh * 16) * 8u;
+            uint32_t pp[8], pd[8];
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj) {
+              const uint4 w = ld_shared_v4(l4 + 16u * jj);  // (-lse2, D) of queries 2jj, 2jj+1
+              const float4 a = make_float4(__uint_as_float(w.x), __uint_as_float(w.y),
+                                           __uint_as_float(w.z), __uint_as_float(w.w));
+              float p0 = fast_exp2(fmaf(__uint_as_float(sv[hh][2 * jj]), sl2, a.x));
+              float p1 = fast_exp2(fmaf(__uint_as_float(sv[hh][2 * jj + 1]), sl2, a.z));
+              if (mixed) {
+                p0 = kvalid ? p0 : 0.f;
+                p1 = kvalid ? p1 : 0.f;
+              }
+              pp[jj] = pack_bf16(p0, p1);
+              pd[jj] = pack_bf16(p0 * (__uint_as_float(dp[hh][2 * jj]) - a.y),
+                                 p1 * (__uint_as_float(dp[hh][2 * jj + 1]) - a.w));
+            }
+            tmem_st_32x32_x8(tS + uint32_t(half * 32 + hh * 8), pp);
+            tmem_st_32x32_x8(tdP + uint32_t(half * 32 + hh * 8), pd);
+#pragma unroll
+            for (int v = 0; v < 2; ++v)
+              st_shared_v4(chunk + uint32_t(swz128(row & 7, half * 4 + hh * 2 + v)), pd[4 * v],
+                           pd[4 * v + 1], pd[4 * v + 2], pd[4 * v + 3]);
           }
-          tmem_st_32x32_x8(tS + uint32_t(half * 32 + hh * 8), pp);
-          tmem_st_32x32_x8(tdP + uint32_t(half * 32 + hh * 8), pd);
-          // dS^T row -> staging buffer (tile parity), chunk c&1, pieces half*4 + 2*hh ..
-#pragma unroll
-          for (int v = 0; v < 2; ++v)
-            st_shared_v4(chunk + uint32_t(swz128(row & 7, half * 4 + hh * 2 + v)), pd[4 * v],
-                         pd[4 * v + 1], pd[4 * v + 2], pd[4 * v + 3]);
         }
         fence_proxy_async_smem();
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&bar[PF0 + bsel]);
-        if (c == nc - 1) {
-          // dV_j (half 0) / dK_j (half 1) complete: store + bias column sums
-          mbar_wait(&bar[KVF], kt & 1);
-          tc_fence_after();
-          float v[64];
-          load_tmem_row64((half ? tdK : tdV) + lane_off, v);
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&bar[KVE]);
-          const float sc = half ? p.scale : 1.f;
-#pragma unroll
-          for (int d = 0; d < 64; ++d)
-            v[d] = valid_k ? __bfloat162float(__float2bfloat16_rn(v[d] * sc)) : 0.f;
-          const int col = (half ? HD : 2 * HD) + h * kD;
-          if (valid_k) store_row64(p.dqkv + (int64_t(b) * p.T + key) * (3 * HD) + col, v);
-          if (p.dbias != nullptr) colsum64(v, p.dbias + col);
-          ++kt;
-        }
+        EPS_TRACE(it < 64 && warp == 2 && lane == 0, it * 8 + 4);
       }
-      // dQ tiles: warp half t stores 128-query tile t
+      mbar_arrive(&bar[LE0 + lb]);  // done reading this head's (-lse2, D) table
+    }
+  } else {
+    // ---- epilogue warps ----------------------------------------------------
+    const int quarter = warp & 3;
+    const int row = quarter * 32 + lane;
+    const uint32_t lane_off = uint32_t(quarter * 32) << 16;
+    const int te = threadIdx.x - (64 + 32 * kBwdExpWarps);  // 0..127
+    // (-lse * log2e, D = rowsum(dO * O)) of every query of head `bh` into
+    // table hi & 1, once the exp warps released it (head hi - 2).
+    auto fill_table = [&](int bh, int hi) {
+      const int lb = hi & 1, b = bh / p.H, h = bh % p.H;
+      if (hi >= 2) mbar_wait(&bar[LE0 + lb], ((hi >> 1) - 1) & 1);
+      EPS_TRACE(hi < 16 && warp == 10 && lane == 0, 704 + hi * 2);
+#pragma unroll
+      for (int r = 0; r < Tr / 128; ++r) {
+        const int q = te + 128 * r;
+        // queries past T: -lse2 = D = 0 (see the exp loop)
+        float2 e = make_float2(0.f, 0.f);
+        if (q < p.T)
+          e = make_float2(-__ldg(p.lse + int64_t(bh) * p.T + q) * kLog2e,
+                          __ldg(p.drow + (int64_t(b) * p.T + q) * p.H + h));
+        sLD[lb * Tr + q] = e;
+      }
+      mbar_arrive(&bar[LF0 + lb]);
+      EPS_TRACE(hi < 16 && warp == 10 && lane == 0, 704 + hi * 2 + 1);
+    };
+    // Tiles leave through a swizzled 16 KB staging buffer and TMA stores
+    // (coalesced, asynchronous); `te == 0` owns the bulk groups.
+    const uint32_t stage_s = smem_addr(sStage);
+    auto epi_sync = [] { asm volatile("bar.sync 1, 128;" ::: "memory"); };
+    auto store_tile = [&](const uint32_t (&pk)[32], int col, int row0, int b) {
+      if (te == 0) bulk_wait_read<0>();  // previous tile read out of the staging buffer
+      epi_sync();
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        st_shared_v4(stage_s + swz128(row, c), pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+      fence_proxy_async_smem();
+      epi_sync();
+      if (te == 0) {
+        tma_store_3d(&map_dq, sStage, col, row0, b);
+        tma_store_3d(&map_dq, sStage + 64 * kRowBytes, col, row0 + 64, b);
+        bulk_commit();
+      }
+    };
+    // Column sums of a tile (one row per thread) into sRed[64] (per head).
+    auto colsum_tile = [&](const uint32_t (&pk)[32]) {
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        float t[32];
+#pragma unroll
+        for (int d = 0; d < 16; ++d) {
+          t[2 * d] = bf16_lo(pk[half * 16 + d]);
+          t[2 * d + 1] = bf16_hi(pk[half * 16 + d]);
+        }
+        atomicAdd(&sRed[half * 32 + lane], warp_transpose_sum32(t));
+      }
+    };
+    int hi = 0, kt = 0;
+    if (int(blockIdx.x) < n_heads) fill_table(blockIdx.x, 0);
+    for (int bh = blockIdx.x; bh < n_heads; bh += gridDim.x, ++hi) {
+      const int b = bh / p.H, h = bh % p.H;
+      if (p.dbias != nullptr) {
+        // V bias gradient = sum_q dO[q, :] (rows of P sum to one), from the
+        // dO tile in smem; then the tile may be overwritten (EMPTY has two
+        // arrivals: the MMA warp's commit and this one).  The K bias
+        // gradient is exactly zero (softmax is shift-invariant per query).
+        mbar_wait(&bar[FULL], hi & 1);
+        const int g = te & 7, rs = te >> 3;  // 16-byte column group, 16-row set
+        float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        const uint32_t o_s = smem_addr(sO);
+#pragma unroll 4
+        for (int r = rs * (Tr / 16); r < (rs + 1) * (Tr / 16); ++r) {
+          const uint4 w = ld_shared_v4(o_s + swz128(r, g));
+          acc[0] += bf16_lo(w.x), acc[1] += bf16_hi(w.x), acc[2] += bf16_lo(w.y);
+          acc[3] += bf16_hi(w.y), acc[4] += bf16_lo(w.z), acc[5] += bf16_hi(w.z);
+          acc[6] += bf16_lo(w.w), acc[7] += bf16_hi(w.w);
+        }
+        if (te < 64) sRed[te] = 0.f;  // (dQ sums of this head accumulate here)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], 8);
+          acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], 16);
+        }
+        epi_sync();  // every thread is past its sO reads; sRed zeroed
+        if (te == 0) mbar_arrive(&bar[EMPTY]);
+        if (lane < 8) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) atomicAdd(&sRed[g * 8 + i], acc[i]);
+        }
+        epi_sync();
+        if (te < 64) {
+          atomicAdd(p.dbias + 2 * HD + h * kD + te, sRed[te]);
+          sRed[te] = 0.f;
+        }
+        epi_sync();
+      } else {
+        if (te == 0) mbar_arrive(&bar[EMPTY]);
+      }
+      // TMEM is read out and released first (the MMA warp is waiting for
+      // it); stores work from the packed registers.
+      for (int j = 0; j < NT; ++j, ++kt) {
+        mbar_wait(&bar[KVF], kt & 1);
+        tc_fence_after();
+        EPS_TRACE(kt < 64 && warp == 10 && lane == 0, 512 + kt * 2);
+        uint32_t pv[32], pk[32];
+        load_tmem_packed64(tdV + lane_off, 1.f, pv);
+        load_tmem_packed64(tdK + lane_off, p.scale, pk);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bar[KVE]);
+        EPS_TRACE(kt < 64 && warp == 10 && lane == 0, 512 + kt * 2 + 1);
+        store_tile(pv, 2 * HD + h * kD, j * kTile, b);
+        store_tile(pk, HD + h * kD, j * kTile, b);
+        // the next head's table, off the key-tile hand-off path (its exp work
+        // starts only after this head's remaining iterations)
+        if (j == 0 && bh + int(gridDim.x) < n_heads) fill_table(bh + gridDim.x, hi + 1);
+      }
       mbar_wait(&bar[DQF], hi & 1);
       tc_fence_after();
-      float v[64];
-      if (half < nt) load_tmem_row64(tdQ + uint32_t(half * kD) + lane_off, v);
+      EPS_TRACE(hi < 16 && warp == 10 && lane == 0, 640 + hi * 4);
+      uint32_t pq[NT][32];
+#pragma unroll
+      for (int t = 0; t < NT; ++t) load_tmem_packed64(tdQ + uint32_t(t * kD) + lane_off, p.scale, pq[t]);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bar[DQE]);
-      if (half < nt) {
-        const int q = half * kTile + row;
-        const bool valid_q = q < p.T;
+      EPS_TRACE(hi < 16 && warp == 10 && lane == 0, 640 + hi * 4 + 1);
 #pragma unroll
-        for (int d = 0; d < 64; ++d)
-          v[d] = valid_q ? __bfloat162float(__float2bfloat16_rn(v[d] * p.scale)) : 0.f;
-        if (valid_q) store_row64(p.dqkv + (int64_t(b) * p.T + q) * (3 * HD) + h * kD, v);
-        if (p.dbias != nullptr) colsum64(v, p.dbias + h * kD);
+      for (int t = 0; t < NT; ++t) {
+        if (t * kTile + row >= p.T) zero32(pq[t]);
+        store_tile(pq[t], h * kD, t * kTile, b);
+        if (p.dbias != nullptr) colsum_tile(pq[t]);
       }
-      // sL / sD are rewritten by the next head's prologue only after all
-      // 256 exp threads are done with them
-      asm volatile("bar.sync 5, 256;" ::: "memory");
-      it0 += n_it;
+      if (p.dbias != nullptr) {
+        epi_sync();
+        if (te < 64) {
+          atomicAdd(p.dbias + h * kD + te, sRed[te]);
+          sRed[te] = 0.f;
+        }
+        epi_sync();
+      }
     }
+    if (te == 0) bulk_wait<0>();
   }
   tc_fence_before();
   __syncthreads();
@@ -833,7 +1012,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 
 size_t bwd_fused_smem(int T) {
   const int Tr = (T + kTile - 1) / kTile * kTile;
-  return size_t(4 * Tr) * kRowBytes + 4 * size_t(kDsChunk) + size_t(2 * Tr) * 4 + 1024 + 256;
+  return size_t(4 * Tr) * kRowBytes + 5 * size_t(kDsChunk) + size_t(2 * Tr) * 8 + 256 + 1024 + 256;
 }
 
 // ---------------------------------------------------------------------------
@@ -1071,8 +1250,43 @@ int attn_fwd_tc(const void* qkv, void* out, float* lse, int B, int T, int H, flo
 }
 
 
+// D = rowsum(dO * O) per (row, head) -> drow [rows, H] (one warp per row).
+__global__ void attn_rowdot_kernel(const uint16_t* __restrict__ out,
+                                   const uint16_t* __restrict__ dout, float* __restrict__ drow,
+                                   int64_t rows, int H) {
+  const int64_t row = int64_t(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const int nv = H * 8;  // 16-byte vectors per row (8 per head)
+  const uint4* o4 = reinterpret_cast<const uint4*>(out + row * H * attn_tc::kD);
+  const uint4* d4 = reinterpret_cast<const uint4*>(dout + row * H * attn_tc::kD);
+  for (int i0 = 0; i0 < nv; i0 += 32) {
+    const int i = i0 + lane;
+    float s = 0.f;
+    if (i < nv) {
+      const uint4 a = __ldg(o4 + i), d = __ldg(d4 + i);
+      s = bf16_lo(a.x) * bf16_lo(d.x) + bf16_hi(a.x) * bf16_hi(d.x) + bf16_lo(a.y) * bf16_lo(d.y) +
+          bf16_hi(a.y) * bf16_hi(d.y) + bf16_lo(a.z) * bf16_lo(d.z) + bf16_hi(a.z) * bf16_hi(d.z) +
+          bf16_lo(a.w) * bf16_lo(d.w) + bf16_hi(a.w) * bf16_hi(d.w);
+    }
+    s += __shfl_xor_sync(0xffffffffu, s, 1);
+    s += __shfl_xor_sync(0xffffffffu, s, 2);
+    s += __shfl_xor_sync(0xffffffffu, s, 4);
+    if (i < nv && (lane & 7) == 0) drow[row * H + (i >> 3)] = s;
+  }
+}
+
+static int g_trace_on = 0;
+
+bool attn_bwd_fused_supported(int T, int head_dim) {
+  return head_dim == 64 && T >= 1 && T <= 2 * attn_tc::kTile;
+}
+
+// drow: precomputed D [B*T, H] (fused path) or nullptr (computed here into
+// dsum, which then holds it in the same layout).
 int attn_bwd_tc(const void* qkv, const void* out, const void* dout, const float* lse, void* dqkv,
-                float* dbias, float* dsum, int B, int T, int H, float scale, cudaStream_t st) {
+                float* dbias, float* dsum, const float* drow, int B, int T, int H, float scale,
+                cudaStream_t st) {
   using namespace attn_tc;
   const int Tp = pad64(T);
   const int64_t W = int64_t(3) * H * kD, WO = int64_t(H) * kD;
@@ -1093,12 +1307,25 @@ int attn_bwd_tc(const void* qkv, const void* out, const void* dout, const float*
   p.dqkv = static_cast<uint16_t*>(dqkv);
   p.dbias = dbias;
   if (T <= 2 * kTile) {
+    if (drow == nullptr) {
+      const int64_t rows = int64_t(B) * T;
+      count_launch();
+      attn_rowdot_kernel<<<unsigned((rows + 7) / 8), 256, 0, st>>>(
+          static_cast<const uint16_t*>(out), static_cast<const uint16_t*>(dout), dsum, rows, H);
+      drow = dsum;
+    }
+    p.drow = drow;
+    p.trace = g_trace_on;
+    CUtensorMap mdq;
+    if (!make_map_3d(&mdq, dqkv, W, T, B, W, int64_t(T) * W, kD, kChunk, CU_TENSOR_MAP_SWIZZLE_128B))
+      return EPS_ECUDA;
     const size_t sf = bwd_fused_smem(T);
-    if (!ensure_smem(attn_bwd_fused_tc_kernel, sf)) return EPS_ECUDA;
     const int heads = B * H;
+    const int grid = heads < sm_count() ? heads : sm_count();
+    auto kern = T <= kTile ? attn_bwd_fused_tc_kernel<1> : attn_bwd_fused_tc_kernel<2>;
+    if (!ensure_smem(kern, sf)) return EPS_ECUDA;
     count_launch();
-    attn_bwd_fused_tc_kernel<<<heads < sm_count() ? heads : sm_count(), kBwdThreads, sf, st>>>(
-        mq, mo, p, heads);
+    kern<<<grid, kBwdThreads, sf, st>>>(mq, mo, mdq, p, heads);
     return cudaGetLastError() == cudaSuccess ? EPS_OK : EPS_ECUDA;
   }
   const size_t s1 = bwd_dq_smem(Tp), s2 = bwd_dkdv_smem(Tp);
@@ -1113,3 +1340,16 @@ int attn_bwd_tc(const void* qkv, const void* out, const void* dout, const float*
 }
 
 }  // namespace eps_k
+
+extern "C" int eps_attn_trace_enable(int on) {
+  eps_k::g_trace_on = on;
+  return EPS_OK;
+}
+
+extern "C" int eps_attn_trace_read(long long* out, int n) {
+  if (n > 1024) n = 1024;
+  return cudaMemcpyFromSymbol(out, eps_k::attn_tc::g_attn_trace, size_t(n) * sizeof(long long)) ==
+                 cudaSuccess
+             ? EPS_OK
+             : EPS_ECUDA;
+}

@@ -101,7 +101,7 @@ constexpr int kChunkBf16 = 2048;  // 32x32 bf16
 
 __device__ __forceinline__ bool epi_reads_aux(int epi) {
   return epi == EPS_EPI_BIAS_RESID_BF16 || epi == EPS_EPI_DGELU_BF16 ||
-         epi == EPS_EPI_RESID_BF16;
+         epi == EPS_EPI_RESID_BF16 || epi == EPS_EPI_ROWDOT_BF16;
 }
 
 __device__ __forceinline__ void stage_bf16(uint32_t base, int lane, const float (&v)[32]) {
@@ -406,6 +406,21 @@ __global__ void __launch_bounds__(kThreads, 1)
               v[j] = __bfloat162float(__float2bfloat16_rn(v[j] * gelu_grad_f(x[j])));
             stage_bf16(out_s, lane, v);
             break;
+          case EPS_EPI_ROWDOT_BF16: {
+            // this lane's row: partial dot of the stored (bf16) values with
+            // aux over the chunk's 32 columns; the two chunks of a 64-column
+            // group come from the two warps of this lane quarter
+            float dot = 0.f;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              v[j] = __bfloat162float(__float2bfloat16_rn(v[j]));
+              dot = fmaf(v[j], x[j], dot);
+            }
+            stage_bf16(out_s, lane, v);
+            if (my_row < args.M)
+              atomicAdd(args.colsum + int64_t(my_row) * (args.N >> 6) + (col0 >> 6), dot);
+            break;
+          }
           default:
             if (f32_out) stage_f32(out_s, lane, v);
             else stage_bf16(out_s, lane, v);
@@ -494,12 +509,14 @@ extern "C" int eps_gemm_bf16(int a_mn_major, int b_mn_major, int epilogue, const
                              int64_t ldb, int64_t ldc, int split_k, void* stream) {
   using namespace eps_k;
   if (M <= 0 || N <= 0 || K <= 0 || N % 8 != 0 || lda % 8 != 0 || ldb % 8 != 0 ||
-      ldc % 8 != 0 || M > (int64_t(1) << 31) || epilogue < 0 || epilogue > EPS_EPI_RESID_BF16)
+      ldc % 8 != 0 || M > (int64_t(1) << 31) || epilogue < 0 || epilogue > EPS_EPI_ROWDOT_BF16)
     return EPS_EINVAL;
+  if (epilogue == EPS_EPI_ROWDOT_BF16 && (N % 64 != 0 || colsum == nullptr)) return EPS_EINVAL;
   const bool auto_split = split_k == 0 && epilogue == EPS_EPI_ACCUM_F32;
   if (split_k < 1) split_k = 1;
   const bool needs_aux = epilogue == EPS_EPI_BIAS_GELU_BF16 || epilogue == EPS_EPI_BIAS_RESID_BF16 ||
-                         epilogue == EPS_EPI_DGELU_BF16 || epilogue == EPS_EPI_RESID_BF16;
+                         epilogue == EPS_EPI_DGELU_BF16 || epilogue == EPS_EPI_RESID_BF16 ||
+                         epilogue == EPS_EPI_ROWDOT_BF16;
   if (needs_aux && aux == nullptr) return EPS_EINVAL;
   if ((epilogue == EPS_EPI_BIAS_BF16 || epilogue == EPS_EPI_BIAS_GELU_BF16 ||
        epilogue == EPS_EPI_BIAS_RESID_BF16) && bias == nullptr)
@@ -544,7 +561,7 @@ extern "C" int eps_gemm_bf16(int a_mn_major, int b_mn_major, int epilogue, const
   // Epilogues that read an aux input (residual, GELU pre-activation) are
   // latency-bound on it: BN = 192 tiles free smem for a 3-deep TMA aux ring.
   const bool aux_epi = epilogue == EPS_EPI_BIAS_RESID_BF16 || epilogue == EPS_EPI_DGELU_BF16 ||
-                       epilogue == EPS_EPI_RESID_BF16;
+                       epilogue == EPS_EPI_RESID_BF16 || epilogue == EPS_EPI_ROWDOT_BF16;
   if (aux_epi && N >= 192) {
     args.tiles_n = int((N + 191) / 192);
     switch (key) {

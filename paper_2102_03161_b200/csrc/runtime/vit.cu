@@ -104,6 +104,7 @@ struct Acts {
   float *meanf = nullptr, *rstdf = nullptr;
   uint16_t *dX = nullptr, *dH = nullptr, *dA = nullptr, *dQKV = nullptr, *dptok = nullptr;
   float* dsum = nullptr;
+  float* drow = nullptr;  // attention D = rowsum(dO * O) [rows, heads] (ROWDOT epilogue)
   double* sq_ws = nullptr;
   size_t sq_ws_bytes = 0;
   size_t bytes = 0;
@@ -150,6 +151,7 @@ struct Acts {
     dQKV = bf(R * 3 * d);
     dptok = bf(BP * d);
     dsum = fp(B * g.heads * g.tokens);
+    drow = fp(B * g.heads * g.tokens);
     sq_ws_bytes = size_t((param_total + 65535) / 65536 + 64) * 8;
     sq_ws = reinterpret_cast<double*>(take(sq_ws_bytes));
     bytes = at;
@@ -393,15 +395,21 @@ struct eps_vit {
     const int split = 0;  // auto split-K (eps_gemm_bf16)
     mm(1, 1, EPS_EPI_ACCUM_F32, dX, act.A[l] + r0 * d, Gr(s.wp), nullptr, nullptr, nullptr, d, d,
        R, d, d, d, split, st);
-    mm(0, 1, EPS_EPI_STORE_BF16, dX, W(s.wp), act.dA + r0 * d, nullptr, nullptr, nullptr, R, d, d,
-       d, d, d, 1, st);
+    // dA = dX1 W_o; for the fused attention backward its epilogue also forms
+    // D = rowsum(dA * A) per (row, head) (EPS_EPI_ROWDOT_BF16)
+    const bool rowdot = eps_attn_bwd_uses_rowdot(g.tokens, g.head_dim()) != 0;
+    float* drow = act.drow + r0 * g.heads;
+    if (rowdot) cudaMemsetAsync(drow, 0, size_t(R) * g.heads * sizeof(float), st);
+    mm(0, 1, rowdot ? EPS_EPI_ROWDOT_BF16 : EPS_EPI_STORE_BF16, dX, W(s.wp), act.dA + r0 * d,
+       nullptr, rowdot ? act.A[l] + r0 * d : nullptr, rowdot ? drow : nullptr, R, d, d, d, d, d, 1,
+       st);
     const double t = g.tokens, hd = double(g.heads) * g.head_dim();
     run(EPS_TC_ATTN, 8.0 * b * t * t * hd, 18.0 * b * t * hd, st, [&] {
-      return eps_attn_bwd_ws(act.QKV[l] + r0 * 3 * d, act.A[l] + r0 * d, act.dA + r0 * d,
-                             act.lse[l] + int64_t(b0) * g.heads * g.tokens,
-                             act.dQKV + r0 * 3 * d, Gr(s.bqkv),
-                             act.dsum + int64_t(b0) * g.heads * g.tokens, b, g.tokens, g.heads,
-                             g.head_dim(), scale(), st);
+      return eps_attn_bwd_rowdot(act.QKV[l] + r0 * 3 * d, act.A[l] + r0 * d, act.dA + r0 * d,
+                                 act.lse[l] + int64_t(b0) * g.heads * g.tokens, drow,
+                                 act.dQKV + r0 * 3 * d, Gr(s.bqkv),
+                                 act.dsum + int64_t(b0) * g.heads * g.tokens, b, g.tokens,
+                                 g.heads, g.head_dim(), scale(), st);
     });
     mm(1, 1, EPS_EPI_ACCUM_F32, act.dQKV + r0 * 3 * d, act.H1[l] + r0 * d, Gr(s.wqkv), nullptr,
        nullptr, nullptr, 3 * d, d, R, 3 * d, d, d, split, st);

@@ -22,6 +22,8 @@ EPI_BIAS_RESID_BF16 = 3
 EPI_DGELU_BF16 = 4
 EPI_STORE_F32 = 5
 EPI_ACCUM_F32 = 6
+EPI_RESID_BF16 = 7
+EPI_ROWDOT_BF16 = 8
 
 _api: Optional[EpsApi] = None
 
@@ -43,6 +45,8 @@ def _declare(lib):
         "eps_layernorm_bwd": [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, i64, i64, vp, vp],
         "eps_attn_fwd": [vp, vp, vp, i32, i32, i32, i32, f32, vp],
         "eps_attn_bwd_ws": [vp, vp, vp, vp, vp, vp, vp, i32, i32, i32, i32, f32, vp],
+        "eps_attn_bwd_rowdot": [vp, vp, vp, vp, vp, vp, vp, vp, i32, i32, i32, i32, f32, vp],
+        "eps_attn_bwd_uses_rowdot": [i32, i32],
         "eps_grad_sqnorm_flat": [vp, vp, i32, vp, vp, C.c_size_t, vp],
         "eps_softmax_xent_bias": [vp, vp, vp, vp, vp, i32, i32, i32, f32, vp],
         "eps_grad_sqnorm_segmented": [vp, vp, vp, i32, vp, i32, vp, C.c_size_t, vp],

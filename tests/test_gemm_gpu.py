@@ -69,6 +69,24 @@ def test_gemm_epilogues(cuda):
     _close(colsum, refd.sum(0), rtol=2e-2)
 
 
+@pytest.mark.parametrize("M,N", [(1000, 768), (77, 128), (4000, 1024)])
+def test_gemm_rowdot(cuda, M, N):
+    """C = acc; D[m, g] = sum over 64-column group g of bf16(acc) * aux (attention D)."""
+    K = 768
+    g = torch.Generator(device=cuda).manual_seed(M + N)
+    a = torch.randn(M, K, device=cuda, generator=g).bfloat16()
+    b = (torch.randn(N, K, device=cuda, generator=g) * 0.05).bfloat16()
+    aux = torch.randn(M, N, device=cuda, generator=g).bfloat16()
+    out = torch.empty(M, N, device=cuda, dtype=torch.bfloat16)
+    drow = torch.zeros(M, N // 64, device=cuda)
+    ops.gemm(a, b, out, epilogue=ops.EPI_ROWDOT_BF16, aux=aux, colsum=drow)
+    torch.cuda.synchronize()
+    ref = _ref(a, b, False, False)
+    _close(out, ref)
+    want = (out.float() * aux.float()).reshape(M, N // 64, 64).sum(-1)
+    assert (drow - want).abs().max().item() <= 1e-3 * want.abs().max().item() + 1e-3
+
+
 @pytest.mark.parametrize("split", [1, 4, 9])
 def test_gemm_wgrad_f32(cuda, split):
     R, out_f, in_f = 7880, 768, 2304  # dW[out,in] = dY^T X over R token rows
