@@ -565,7 +565,8 @@ __device__ long long g_attn_trace[1024];
 // is shifts and masks.
 constexpr int kDsChunk = kTile * kRowBytes;  // [128 keys][64 queries] bf16 = 16 KB
 constexpr int kBwdExpWarps = 8, kBwdEpiWarps = 4;
-constexpr int kBwdThreads = 64 + 32 * (kBwdExpWarps + kBwdEpiWarps);
+constexpr int kBwdPostWarp = 2 + kBwdExpWarps + kBwdEpiWarps;  // second MMA issuer
+constexpr int kBwdThreads = 32 * (kBwdPostWarp + 1);
 
 __device__ __forceinline__ void tma_prefetch_3d(const void* tmap, int c0, int c1, int c2) {
   asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global [%0, {%1, %2, %3}];" ::"l"(
@@ -657,6 +658,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     mbar_fence_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, 512);
+  if (threadIdx.x < 64) sRed[threadIdx.x] = 0.f;
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -664,11 +666,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   const uint32_t tdV = tmem + 256, tdK = tmem + 320, tdQ = tmem + 384;
 
   if (warp == 0) {
-    if (lane == 0) {
-      int hi = 0;
-      for (int bh = blockIdx.x; bh < n_heads; bh += gridDim.x, ++hi) {
-        const int b = bh / p.H, h = bh % p.H;
-        mbar_wait(&bar[EMPTY], (hi & 1) ^ 1);
+    int hi = 0;
+    for (int bh = blockIdx.x; bh < n_heads; bh += gridDim.x, ++hi) {
+      const int b = bh / p.H, h = bh % p.H;
+      mbar_wait(&bar[EMPTY], (hi & 1) ^ 1);
+      if (lane == 0) {
         mbar_expect_tx(&bar[FULL], uint32_t(4 * Tr) * kRowBytes);
         load_rows(sQ, &map_qkv, &bar[FULL], h * kD, 0, Tr, b);
         load_rows(sO, &map_do, &bar[FULL], h * kD, 0, Tr, b);
@@ -687,89 +689,132 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           }
         }
       }
+      __syncwarp();
+      // V bias gradient = sum_q dO[q, :] of the head (rows of P sum to one),
+      // from the dO tile in smem by this warp's 32 lanes; then the tiles may
+      // be overwritten (EMPTY has two arrivals: the MMA warp's commit and
+      // this one).  The K bias gradient is exactly zero (softmax is
+      // shift-invariant per query), so no K column sums are formed.
+      if (p.dbias != nullptr) {
+        mbar_wait(&bar[FULL], hi & 1);
+        const int g = lane & 7, rs = lane >> 3;  // 16-byte column group, 64-row set
+        float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        const uint32_t o_s = smem_addr(sO);
+#pragma unroll 4
+        for (int r = rs * (Tr / 4); r < (rs + 1) * (Tr / 4); ++r) {
+          const uint4 w = ld_shared_v4(o_s + swz128(r, g));
+          acc[0] += bf16_lo(w.x), acc[1] += bf16_hi(w.x), acc[2] += bf16_lo(w.y);
+          acc[3] += bf16_hi(w.y), acc[4] += bf16_lo(w.z), acc[5] += bf16_hi(w.z);
+          acc[6] += bf16_lo(w.w), acc[7] += bf16_hi(w.w);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bar[EMPTY]);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], 8);
+          acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], 16);
+        }
+        if (lane < 8) {
+          float* dst = p.dbias + 2 * HD + (bh % p.H) * kD + g * 8;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) atomicAdd(dst + i, acc[i]);
+        }
+      } else if (lane == 0) {
+        mbar_arrive(&bar[EMPTY]);
+      }
+      __syncwarp();
     }
-  } else if (warp == 1) {
-    // The whole warp runs the issue loop (warp-uniform descriptors held in
-    // uniform registers); one elected lane issues each MMA / commit.
+  } else if (warp == 1 || warp == kBwdPostWarp) {
+    // Two MMA issuers: warp 1 issues S^T / dP^T of each iteration, warp
+    // kBwdPostWarp the dV / dK / dQ work that follows the exp warps, so the
+    // next iteration's S^T / dP^T never queues behind a post.  Each issuer
+    // runs converged (warp-uniform descriptors in uniform registers) and one
+    // elected lane issues each MMA / commit; a commit tracks its own
+    // thread's MMAs, so AC / KVF / DQF / EMPTY come from the post issuer.
     // Descriptor arithmetic: +2 per 16-element K slice of a K-major operand
     // (32 B), +128 per 16 K-rows of an MN-major one (2 KB), +8 per row (128 B).
-    const uint64_t dQ0 = umma_sdesc(smem_addr(sQ), 16, 1024), dO0 = umma_sdesc(smem_addr(sO), 16, 1024);
-    const uint64_t dK0 = umma_sdesc(smem_addr(sK), 16, 1024), dV0 = umma_sdesc(smem_addr(sV), 16, 1024);
-    const uint64_t mQ0 = umma_sdesc(smem_addr(sQ), 64 * 128, 1024);
-    const uint64_t mO0 = umma_sdesc(smem_addr(sO), 64 * 128, 1024);
-    const uint64_t mK0 = umma_sdesc(smem_addr(sK), 64 * 128, 1024);
-    const uint64_t mS0 = umma_sdesc(smem_addr(sS), kDsChunk, 1024);
     constexpr uint32_t idesc_kk = umma_idesc_bf16(128, kChunk, false, false);
     constexpr uint32_t idesc_km = umma_idesc_bf16(128, kD, false, true);
     constexpr uint32_t idesc_mm = umma_idesc_bf16(128, kD, true, true);
-    int kt = 0, hi = 0;
-    // dV / dK / dQ work of global iteration `it` (k-th of head hi)
-    auto post = [&](int it, int k) {
-      const int bsel = it & 1, j = k >> LNC, c = k & (NC - 1);
-      mbar_wait(&bar[PF0 + bsel], (it >> 1) & 1);
-      tc_fence_after();
-      EPS_TRACE(it < 64 && lane == 0, it * 8 + 1);
-      if (c == 0 && kt > 0) {  // dK / dV of the previous key tile read out
-        mbar_wait(&bar[KVE], (kt - 1) & 1);
+    if (warp == 1) {
+      const uint64_t dQ0 = umma_sdesc(smem_addr(sQ), 16, 1024);
+      const uint64_t dO0 = umma_sdesc(smem_addr(sO), 16, 1024);
+      const uint64_t dK0 = umma_sdesc(smem_addr(sK), 16, 1024);
+      const uint64_t dV0 = umma_sdesc(smem_addr(sV), 16, 1024);
+      int hi = 0;
+      for (int bh = blockIdx.x; bh < n_heads; bh += gridDim.x, ++hi) {
+        const int it0 = hi * NIT;
+        mbar_wait(&bar[FULL], hi & 1);
         tc_fence_after();
-      }
-      const uint32_t tS = tmem + uint32_t(bsel * 128), tdP = tS + 64;
-      const uint64_t qc = mQ0 + uint64_t(c * kChunk * 8), oc = mO0 + uint64_t(c * kChunk * 8);
+        EPS_TRACE(hi < 16 && lane == 0, 640 + hi * 4 + 2);
+        for (int k = 0; k < NIT; ++k) {
+          const int it = it0 + k, bsel = k & 1, j = k >> LNC, c = k & (NC - 1);
+          if (it >= 2) {  // post(it - 2) finished reading this S^T / dP^T buffer
+            mbar_wait(&bar[AC0 + bsel], ((it >> 1) - 1) & 1);
+            tc_fence_after();
+          }
+          const uint32_t tS = tmem + uint32_t(bsel * 128), tdP = tS + 64;
+          const uint64_t kj = dK0 + uint64_t(j * kTile * 8), vj = dV0 + uint64_t(j * kTile * 8);
+          const uint64_t qc = dQ0 + uint64_t(c * kChunk * 8), oc = dO0 + uint64_t(c * kChunk * 8);
 #pragma unroll
-      for (int kk = 0; kk < kChunk / 16; ++kk) {
-        const uint32_t acc = (c > 0 || kk > 0) ? 1u : 0u;
-        // 16-query slice kk sits at column 32*(kk/2) + 8*(kk%2) (see the exp loop)
-        const uint32_t pcol = uint32_t(32 * (kk >> 1) + 8 * (kk & 1));
-        tc_mma_ts_ws(tdV, tS + pcol, oc + uint64_t(kk * 128), idesc_km, acc);
-        tc_mma_ts_ws(tdK, tdP + pcol, qc + uint64_t(kk * 128), idesc_km, acc);
-      }
-      if (c & 1) {  // both halves of 128-query tile c/2 staged: dQ_t += dS_t K_j
-        const int t = c >> 1;
-        if (j == 0 && t == 0 && hi > 0) {
-          mbar_wait(&bar[DQE], (hi - 1) & 1);
-          tc_fence_after();
+          for (int kk = 0; kk < kD / 16; ++kk)
+            tc_mma_ss_ws(tS, kj + uint64_t(2 * kk), qc + uint64_t(2 * kk), idesc_kk, kk > 0 ? 1u : 0u);
+#pragma unroll
+          for (int kk = 0; kk < kD / 16; ++kk)
+            tc_mma_ss_ws(tdP, vj + uint64_t(2 * kk), oc + uint64_t(2 * kk), idesc_kk, kk > 0 ? 1u : 0u);
+          tc_commit_ws(&bar[SF0 + bsel]);
+          EPS_TRACE(it < 64 && lane == 0, it * 8 + 0);
         }
-        const uint64_t stg = mS0 + uint64_t(((it >> 1) & 1) * 2 * (kDsChunk >> 4));
-        const uint64_t kj = mK0 + uint64_t(j * kTile * 8);
-#pragma unroll
-        for (int kk = 0; kk < kTile / 16; ++kk)
-          tc_mma_ss_ws(tdQ + uint32_t(t * kD), stg + uint64_t(kk * 128), kj + uint64_t(kk * 128),
-                       idesc_mm, (j > 0 || kk > 0) ? 1u : 0u);
       }
-      tc_commit_ws(&bar[AC0 + bsel]);
-      EPS_TRACE(it < 64 && lane == 0, it * 8 + 2);
-      if (c == NC - 1) {
-        tc_commit_ws(&bar[KVF]);
-        ++kt;
-      }
-    };
-    for (int bh = blockIdx.x; bh < n_heads; bh += gridDim.x, ++hi) {
-      const int it0 = hi * NIT;
-      mbar_wait(&bar[FULL], hi & 1);
-      tc_fence_after();
-      EPS_TRACE(hi < 16 && lane == 0, 640 + hi * 4 + 2);
-      for (int k = 0; k < NIT; ++k) {
-        const int it = it0 + k, bsel = k & 1, j = k >> LNC, c = k & (NC - 1);
-        if (it >= 2) {  // post(it - 2) finished reading this S^T / dP^T buffer
-          mbar_wait(&bar[AC0 + bsel], ((it >> 1) - 1) & 1);
+    } else {
+      const uint64_t mQ0 = umma_sdesc(smem_addr(sQ), 64 * 128, 1024);
+      const uint64_t mO0 = umma_sdesc(smem_addr(sO), 64 * 128, 1024);
+      const uint64_t mK0 = umma_sdesc(smem_addr(sK), 64 * 128, 1024);
+      const uint64_t mS0 = umma_sdesc(smem_addr(sS), kDsChunk, 1024);
+      int kt = 0, hi = 0;
+      for (int bh = blockIdx.x; bh < n_heads; bh += gridDim.x, ++hi) {
+        for (int k = 0; k < NIT; ++k) {
+          const int it = hi * NIT + k, bsel = k & 1, j = k >> LNC, c = k & (NC - 1);
+          mbar_wait(&bar[PF0 + bsel], (it >> 1) & 1);
           tc_fence_after();
+          EPS_TRACE(it < 64 && lane == 0, it * 8 + 1);
+          if (c == 0 && kt > 0) {  // dK / dV of the previous key tile read out
+            mbar_wait(&bar[KVE], (kt - 1) & 1);
+            tc_fence_after();
+          }
+          const uint32_t tS = tmem + uint32_t(bsel * 128), tdP = tS + 64;
+          const uint64_t qc = mQ0 + uint64_t(c * kChunk * 8), oc = mO0 + uint64_t(c * kChunk * 8);
+#pragma unroll
+          for (int kk = 0; kk < kChunk / 16; ++kk) {
+            const uint32_t acc = (c > 0 || kk > 0) ? 1u : 0u;
+            // 16-query slice kk sits at column 32*(kk/2) + 8*(kk%2) (see the exp loop)
+            const uint32_t pcol = uint32_t(32 * (kk >> 1) + 8 * (kk & 1));
+            tc_mma_ts_ws(tdV, tS + pcol, oc + uint64_t(kk * 128), idesc_km, acc);
+            tc_mma_ts_ws(tdK, tdP + pcol, qc + uint64_t(kk * 128), idesc_km, acc);
+          }
+          if (c & 1) {  // both halves of 128-query tile c/2 staged: dQ_t += dS_t K_j
+            const int t = c >> 1;
+            if (j == 0 && t == 0 && hi > 0) {
+              mbar_wait(&bar[DQE], (hi - 1) & 1);
+              tc_fence_after();
+            }
+            const uint64_t stg = mS0 + uint64_t(((it >> 1) & 1) * 2 * (kDsChunk >> 4));
+            const uint64_t kj = mK0 + uint64_t(j * kTile * 8);
+#pragma unroll
+            for (int kk = 0; kk < kTile / 16; ++kk)
+              tc_mma_ss_ws(tdQ + uint32_t(t * kD), stg + uint64_t(kk * 128), kj + uint64_t(kk * 128),
+                           idesc_mm, (j > 0 || kk > 0) ? 1u : 0u);
+          }
+          tc_commit_ws(&bar[AC0 + bsel]);
+          EPS_TRACE(it < 64 && lane == 0, it * 8 + 2);
+          if (c == NC - 1) {
+            tc_commit_ws(&bar[KVF]);
+            ++kt;
+          }
         }
-        const uint32_t tS = tmem + uint32_t(bsel * 128), tdP = tS + 64;
-        const uint64_t kj = dK0 + uint64_t(j * kTile * 8), vj = dV0 + uint64_t(j * kTile * 8);
-        const uint64_t qc = dQ0 + uint64_t(c * kChunk * 8), oc = dO0 + uint64_t(c * kChunk * 8);
-#pragma unroll
-        for (int kk = 0; kk < kD / 16; ++kk)
-          tc_mma_ss_ws(tS, kj + uint64_t(2 * kk), qc + uint64_t(2 * kk), idesc_kk, kk > 0 ? 1u : 0u);
-#pragma unroll
-        for (int kk = 0; kk < kD / 16; ++kk)
-          tc_mma_ss_ws(tdP, vj + uint64_t(2 * kk), oc + uint64_t(2 * kk), idesc_kk, kk > 0 ? 1u : 0u);
-        tc_commit_ws(&bar[SF0 + bsel]);
-        EPS_TRACE(it < 64 && lane == 0, it * 8 + 0);
-        if (k > 0) post(it - 1, k - 1);
+        tc_commit_ws(&bar[DQF]);
+        tc_commit_ws(&bar[EMPTY]);
       }
-      post(it0 + NIT - 1, NIT - 1);
-      tc_commit_ws(&bar[DQF]);
-      tc_commit_ws(&bar[EMPTY]);
     }
   } else if (warp < 2 + kBwdExpWarps) {
     // ---- exp / dS warps --------------------------------------------------
@@ -859,7 +904,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       }
       mbar_arrive(&bar[LE0 + lb]);  // done reading this head's (-lse2, D) table
     }
-  } else {
+  } else if (warp < 2 + kBwdExpWarps + kBwdEpiWarps) {
     // ---- epilogue warps ----------------------------------------------------
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;
@@ -902,60 +947,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         bulk_commit();
       }
     };
-    // Column sums of a tile (one row per thread) into sRed[64] (per head).
-    auto colsum_tile = [&](const uint32_t (&pk)[32]) {
-#pragma unroll
-      for (int half = 0; half < 2; ++half) {
-        float t[32];
-#pragma unroll
-        for (int d = 0; d < 16; ++d) {
-          t[2 * d] = bf16_lo(pk[half * 16 + d]);
-          t[2 * d + 1] = bf16_hi(pk[half * 16 + d]);
-        }
-        atomicAdd(&sRed[half * 32 + lane], warp_transpose_sum32(t));
-      }
-    };
     int hi = 0, kt = 0;
     if (int(blockIdx.x) < n_heads) fill_table(blockIdx.x, 0);
     for (int bh = blockIdx.x; bh < n_heads; bh += gridDim.x, ++hi) {
       const int b = bh / p.H, h = bh % p.H;
-      if (p.dbias != nullptr) {
-        // V bias gradient = sum_q dO[q, :] (rows of P sum to one), from the
-        // dO tile in smem; then the tile may be overwritten (EMPTY has two
-        // arrivals: the MMA warp's commit and this one).  The K bias
-        // gradient is exactly zero (softmax is shift-invariant per query).
-        mbar_wait(&bar[FULL], hi & 1);
-        const int g = te & 7, rs = te >> 3;  // 16-byte column group, 16-row set
-        float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        const uint32_t o_s = smem_addr(sO);
-#pragma unroll 4
-        for (int r = rs * (Tr / 16); r < (rs + 1) * (Tr / 16); ++r) {
-          const uint4 w = ld_shared_v4(o_s + swz128(r, g));
-          acc[0] += bf16_lo(w.x), acc[1] += bf16_hi(w.x), acc[2] += bf16_lo(w.y);
-          acc[3] += bf16_hi(w.y), acc[4] += bf16_lo(w.z), acc[5] += bf16_hi(w.z);
-          acc[6] += bf16_lo(w.w), acc[7] += bf16_hi(w.w);
-        }
-        if (te < 64) sRed[te] = 0.f;  // (dQ sums of this head accumulate here)
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], 8);
-          acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], 16);
-        }
-        epi_sync();  // every thread is past its sO reads; sRed zeroed
-        if (te == 0) mbar_arrive(&bar[EMPTY]);
-        if (lane < 8) {
-#pragma unroll
-          for (int i = 0; i < 8; ++i) atomicAdd(&sRed[g * 8 + i], acc[i]);
-        }
-        epi_sync();
-        if (te < 64) {
-          atomicAdd(p.dbias + 2 * HD + h * kD + te, sRed[te]);
-          sRed[te] = 0.f;
-        }
-        epi_sync();
-      } else {
-        if (te == 0) mbar_arrive(&bar[EMPTY]);
-      }
       // TMEM is read out and released first (the MMA warp is waiting for
       // it); stores work from the packed registers.
       for (int j = 0; j < NT; ++j, ++kt) {
@@ -971,6 +966,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         EPS_TRACE(kt < 64 && warp == 10 && lane == 0, 512 + kt * 2 + 1);
         store_tile(pv, 2 * HD + h * kD, j * kTile, b);
         store_tile(pk, HD + h * kD, j * kTile, b);
+        EPS_TRACE(hi < 16 && j == 0 && warp == 10 && lane == 0, 760 + hi * 4 + 2);
         // the next head's table, off the key-tile hand-off path (its exp work
         // starts only after this head's remaining iterations)
         if (j == 0 && bh + int(gridDim.x) < n_heads) fill_table(bh + gridDim.x, hi + 1);
@@ -989,9 +985,23 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       for (int t = 0; t < NT; ++t) {
         if (t * kTile + row >= p.T) zero32(pq[t]);
         store_tile(pq[t], h * kD, t * kTile, b);
-        if (p.dbias != nullptr) colsum_tile(pq[t]);
       }
-      if (p.dbias != nullptr) {
+      if (p.dbias != nullptr) {  // Q bias gradient: column sums of dQ
+        float u[64];
+#pragma unroll
+        for (int d = 0; d < 32; ++d) {
+          u[2 * d] = bf16_lo(pq[0][d]);
+          u[2 * d + 1] = bf16_hi(pq[0][d]);
+#pragma unroll
+          for (int t = 1; t < NT; ++t) u[2 * d] += bf16_lo(pq[t][d]), u[2 * d + 1] += bf16_hi(pq[t][d]);
+        }
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          float t32[32];
+#pragma unroll
+          for (int d = 0; d < 32; ++d) t32[d] = u[half * 32 + d];
+          atomicAdd(&sRed[half * 32 + lane], warp_transpose_sum32(t32));
+        }
         epi_sync();
         if (te < 64) {
           atomicAdd(p.dbias + h * kD + te, sRed[te]);
@@ -999,6 +1009,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         }
         epi_sync();
       }
+      EPS_TRACE(hi < 16 && warp == 10 && lane == 0, 760 + hi * 4);
     }
     if (te == 0) bulk_wait<0>();
   }

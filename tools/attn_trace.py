@@ -45,6 +45,6 @@ for it in range(8, 32):
 print("kt  KVF_seen KVE_arr")
 for kt in range(2, 8):
     print(kt, r(t[512 + kt * 2]), r(t[512 + kt * 2 + 1]))
-print("hi  DQF DQE FULL_mma table_exp fill_start fill_end")
+print("hi  DQF DQE FULL_mma table_exp fill_start fill_end dq_stored dOsum_done tile0_stored")
 for hi in range(1, 4):
-    print(hi, *[r(t[640 + hi * 4 + k]) for k in range(4)], r(t[704 + hi * 2]), r(t[705 + hi * 2]))
+    print(hi, *[r(t[640 + hi * 4 + k]) for k in range(4)], r(t[704 + hi * 2]), r(t[705 + hi * 2]), r(t[760 + hi * 4]), r(t[761 + hi * 4]), r(t[762 + hi * 4]))
