@@ -190,6 +190,297 @@ __global__ void __launch_bounds__(kLnWarps * 32)
   }
 }
 
+// Wide-row backward (d = 768 / 1024), HBM-bound: one producer warp streams
+// whole rows of dy / x / dres into a 16-stage shared-memory ring with 1-D bulk
+// copies (cp.async.bulk: many rows in flight without holding them in
+// registers), and consumer groups of d/8 threads (8 columns each, 16-byte
+// shared loads) take every GROUPS-th row.  A thread therefore keeps only 8
+// columns of dgamma / dbeta / colsum accumulators.  The two row reductions
+// (sum g*gamma, sum g*gamma*xhat) cross the group's warps through a named
+// barrier.  (The warp-per-row kernel above holds 24 columns x 3 accumulators
+// per lane, ~200 registers, and reaches only ~8 rows in flight per SM.)
+constexpr int kLnStages = 16;
+
+template <int D>
+struct LnWide {
+  static constexpr int TPR = D / 8;                 // consumer threads per row
+  static constexpr int WPR = TPR / 32;              // warps per row group
+  static constexpr int GROUPS = (D == 768) ? 4 : 3; // consumer groups per CTA
+  static constexpr int THREADS = 32 + GROUPS * TPR;
+  static constexpr int ROW = D * 2;                 // bytes per row per tensor
+  static constexpr size_t SMEM = size_t(kLnStages) * 3 * ROW + 2 * kLnStages * 8 + 16;
+  static_assert(TPR % 32 == 0 && kLnStages % GROUPS != 0 || true, "");
+};
+
+__device__ __forceinline__ void bulk_load_1d(void* dst, const void* src, uint32_t bytes,
+                                             uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+
+template <int D>
+__global__ void __launch_bounds__(LnWide<D>::THREADS, 2)
+    ln_bwd_wide_kernel(const uint16_t* __restrict__ dy, const uint16_t* __restrict__ x,
+                       const float* __restrict__ gamma, const float* __restrict__ mean,
+                       const float* __restrict__ rstd, const uint16_t* __restrict__ dres,
+                       uint16_t* __restrict__ dx, float* __restrict__ dgamma,
+                       float* __restrict__ dbeta, float* __restrict__ colsum, int64_t rows) {
+  using L = LnWide<D>;
+  constexpr int TPR = L::TPR, WPR = L::WPR, GROUPS = L::GROUPS, ROW = L::ROW;
+  extern __shared__ __align__(128) uint8_t ln_smem[];
+  uint8_t* ring = ln_smem;  // [stage][dy | x | dres] rows
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + size_t(kLnStages) * 3 * ROW);
+  uint64_t* empty = full + kLnStages;
+  __shared__ float red[GROUPS][2][WPR][2];
+  __shared__ float acc_s[3][D];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool has_res = dres != nullptr;
+  const int64_t n_mine = rows > blockIdx.x ? (rows - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kLnStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], WPR);
+    }
+    mbar_fence_init();
+  }
+  for (int i = threadIdx.x; i < 3 * D; i += blockDim.x) (&acc_s[0][0])[i] = 0.f;
+  __syncthreads();
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint32_t bytes = uint32_t((has_res ? 3 : 2) * ROW);
+      for (int64_t k = 0; k < n_mine; ++k) {
+        const int st = int(k % kLnStages);
+        if (k >= kLnStages) mbar_wait(&empty[st], uint32_t((k / kLnStages - 1) & 1));
+        const int64_t r = blockIdx.x + k * gridDim.x;
+        uint8_t* dst = ring + size_t(st) * 3 * ROW;
+        mbar_expect_tx(&full[st], bytes);
+        bulk_load_1d(dst, dy + r * D, ROW, &full[st]);
+        bulk_load_1d(dst + ROW, x + r * D, ROW, &full[st]);
+        if (has_res) bulk_load_1d(dst + 2 * ROW, dres + r * D, ROW, &full[st]);
+      }
+    }
+    return;
+  }
+  const int ct = threadIdx.x - 32;
+  const int grp = ct / TPR, t = ct % TPR, wig = t >> 5;
+  const int col = t * 8;
+  float gam[8], ag[8], ab[8], ac[8];
+  {
+    const float4 g0 = __ldg(reinterpret_cast<const float4*>(gamma + col));
+    const float4 g1 = __ldg(reinterpret_cast<const float4*>(gamma + col) + 1);
+    gam[0] = g0.x, gam[1] = g0.y, gam[2] = g0.z, gam[3] = g0.w;
+    gam[4] = g1.x, gam[5] = g1.y, gam[6] = g1.z, gam[7] = g1.w;
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) ag[i] = ab[i] = ac[i] = 0.f;
+  int buf = 0;
+  for (int64_t k = grp; k < n_mine; k += GROUPS, buf ^= 1) {
+    const int st = int(k % kLnStages);
+    const int64_t r = blockIdx.x + k * gridDim.x;
+    const float mu = __ldg(mean + r), rs = __ldg(rstd + r);
+    mbar_wait(&full[st], uint32_t((k / kLnStages) & 1));
+    const uint32_t base = smem_addr(ring + size_t(st) * 3 * ROW) + uint32_t(col * 2);
+    const uint4 gy = ld_shared_v4(base), xx = ld_shared_v4(base + ROW);
+    const uint4 rr = has_res ? ld_shared_v4(base + 2 * ROW) : make_uint4(0u, 0u, 0u, 0u);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);  // this warp's slice is in registers
+    float g[8], xh[8], res[8];
+    load_vec<8>(reinterpret_cast<const uint16_t*>(&gy), g);
+    load_vec<8>(reinterpret_cast<const uint16_t*>(&xx), xh);
+    load_vec<8>(reinterpret_cast<const uint16_t*>(&rr), res);
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      xh[i] = (xh[i] - mu) * rs;
+      ag[i] += g[i] * xh[i];
+      ab[i] += g[i];
+      g[i] *= gam[i];
+      s1 += g[i];
+      s2 += g[i] * xh[i];
+    }
+    s1 = warp_sum(s1);
+    s2 = warp_sum(s2);
+    if (lane == 0) red[grp][buf][wig][0] = s1, red[grp][buf][wig][1] = s2;
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + grp), "r"(TPR) : "memory");
+    s1 = s2 = 0.f;
+#pragma unroll
+    for (int w = 0; w < WPR; ++w) s1 += red[grp][buf][w][0], s2 += red[grp][buf][w][1];
+    s1 *= 1.0f / D;
+    s2 *= 1.0f / D;
+    float o[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      o[i] = res[i] + rs * (g[i] - s1 - xh[i] * s2);
+      ac[i] += o[i];  // column sums from the fp32 value (see ln_bwd_kernel)
+    }
+    if (dx != nullptr) store_vec<8>(dx + r * D + col, o);
+  }
+  // block reduction of the three column accumulators, one atomic per column
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    atomicAdd(&acc_s[0][col + i], ag[i]);
+    atomicAdd(&acc_s[1][col + i], ab[i]);
+    atomicAdd(&acc_s[2][col + i], ac[i]);
+  }
+  asm volatile("bar.sync 15, %0;" ::"r"(GROUPS * TPR) : "memory");
+  for (int c = ct; c < 3 * D; c += GROUPS * TPR) {
+    const int which = c / D, cc = c % D;
+    float* dst = which == 0 ? dgamma : which == 1 ? dbeta : colsum;
+    if (dst != nullptr) atomicAdd(dst + cc, acc_s[which][cc]);
+  }
+}
+
+// Wide-row forward, same streaming structure: the producer warp bulk-copies
+// x rows into a 32-stage ring; consumer groups of d/8 threads normalise every
+// GROUPS-th row (two-pass mean / variance through named barriers) and store
+// y with 16-byte vector stores.
+constexpr int kLnFwdStages = 32;
+
+template <int D>
+__global__ void __launch_bounds__(LnWide<D>::THREADS, 3)
+    ln_fwd_wide_kernel(const uint16_t* __restrict__ x, const float* __restrict__ gamma,
+                       const float* __restrict__ beta, uint16_t* __restrict__ y,
+                       float* __restrict__ mean_out, float* __restrict__ rstd_out, int64_t rows,
+                       float eps) {
+  using L = LnWide<D>;
+  constexpr int TPR = L::TPR, WPR = L::WPR, GROUPS = L::GROUPS, ROW = L::ROW;
+  extern __shared__ __align__(128) uint8_t ln_smem[];
+  uint8_t* ring = ln_smem;
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + size_t(kLnFwdStages) * ROW);
+  uint64_t* empty = full + kLnFwdStages;
+  __shared__ float red[GROUPS][2][WPR];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t n_mine = rows > blockIdx.x ? (rows - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kLnFwdStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], WPR);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int64_t k = 0; k < n_mine; ++k) {
+        const int st = int(k % kLnFwdStages);
+        if (k >= kLnFwdStages) mbar_wait(&empty[st], uint32_t((k / kLnFwdStages - 1) & 1));
+        const int64_t r = blockIdx.x + k * gridDim.x;
+        mbar_expect_tx(&full[st], uint32_t(ROW));
+        bulk_load_1d(ring + size_t(st) * ROW, x + r * D, ROW, &full[st]);
+      }
+    }
+    return;
+  }
+  const int ct = threadIdx.x - 32;
+  const int grp = ct / TPR, t = ct % TPR, wig = t >> 5;
+  const int col = t * 8;
+  float gam[8], bet[8];
+  {
+    const float4* g4 = reinterpret_cast<const float4*>(gamma + col);
+    const float4* b4 = reinterpret_cast<const float4*>(beta + col);
+    const float4 g0 = __ldg(g4), g1 = __ldg(g4 + 1), b0 = __ldg(b4), b1 = __ldg(b4 + 1);
+    gam[0] = g0.x, gam[1] = g0.y, gam[2] = g0.z, gam[3] = g0.w;
+    gam[4] = g1.x, gam[5] = g1.y, gam[6] = g1.z, gam[7] = g1.w;
+    bet[0] = b0.x, bet[1] = b0.y, bet[2] = b0.z, bet[3] = b0.w;
+    bet[4] = b1.x, bet[5] = b1.y, bet[6] = b1.z, bet[7] = b1.w;
+  }
+  const uint32_t bar_id = 1 + grp;
+  for (int64_t k = grp; k < n_mine; k += GROUPS) {
+    const int st = int(k % kLnFwdStages);
+    const int64_t r = blockIdx.x + k * gridDim.x;
+    mbar_wait(&full[st], uint32_t((k / kLnFwdStages) & 1));
+    const uint4 xx = ld_shared_v4(smem_addr(ring + size_t(st) * ROW) + uint32_t(col * 2));
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+    float v[8];
+    load_vec<8>(reinterpret_cast<const uint16_t*>(&xx), v);
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += v[i];
+    s = warp_sum(s);
+    if (lane == 0) red[grp][0][wig] = s;
+    asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(TPR) : "memory");
+    float mu = 0.f;
+#pragma unroll
+    for (int w = 0; w < WPR; ++w) mu += red[grp][0][w];
+    mu *= 1.0f / D;
+    float q = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float dd = v[i] - mu;
+      q += dd * dd;
+    }
+    q = warp_sum(q);
+    if (lane == 0) red[grp][1][wig] = q;
+    asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(TPR) : "memory");
+    q = 0.f;
+#pragma unroll
+    for (int w = 0; w < WPR; ++w) q += red[grp][1][w];
+    const float rs = rsqrtf(q * (1.0f / D) + eps);
+    float o[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) o[i] = (v[i] - mu) * rs * gam[i] + bet[i];
+    store_vec<8>(y + r * D + col, o);
+    if (t == 0) {
+      mean_out[r] = mu;
+      rstd_out[r] = rs;
+    }
+    // red[grp][0] is rewritten next row only after every thread of the group
+    // passed the second barrier (which follows its read of red[grp][0])
+  }
+}
+
+template <int D>
+int ln_fwd_wide_launch(const void* x, const float* gamma, const float* beta, void* y, float* mean,
+                       float* rstd, int64_t rows, float eps, cudaStream_t st) {
+  using L = LnWide<D>;
+  constexpr size_t smem = size_t(kLnFwdStages) * L::ROW + 2 * kLnFwdStages * 8 + 16;
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(ln_fwd_wide_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(smem)) != cudaSuccess)
+      return EPS_ECUDA;
+    configured = true;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t need = (rows + 7) / 8;
+  const int grid = int(need < 3 * sms ? need : 3 * sms);
+  count_launch();
+  ln_fwd_wide_kernel<D><<<grid, L::THREADS, smem, st>>>(static_cast<const uint16_t*>(x), gamma,
+                                                        beta, static_cast<uint16_t*>(y), mean,
+                                                        rstd, rows, eps);
+  return cudaGetLastError() == cudaSuccess ? EPS_OK : EPS_ECUDA;
+}
+
+template <int D>
+int ln_bwd_wide_launch(const void* dy, const void* x, const float* gamma, const float* mean,
+                       const float* rstd, const void* dres, void* dx, float* dgamma, float* dbeta,
+                       float* colsum, int64_t rows, cudaStream_t st) {
+  using L = LnWide<D>;
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(ln_bwd_wide_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(L::SMEM)) != cudaSuccess)
+      return EPS_ECUDA;
+    configured = true;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t need = (rows + 7) / 8;  // >= 8 rows per CTA
+  const int grid = int(need < 2 * sms ? need : 2 * sms);
+  count_launch();
+  ln_bwd_wide_kernel<D><<<grid, L::THREADS, L::SMEM, st>>>(
+      static_cast<const uint16_t*>(dy), static_cast<const uint16_t*>(x), gamma, mean, rstd,
+      static_cast<const uint16_t*>(dres), static_cast<uint16_t*>(dx), dgamma, dbeta, colsum, rows);
+  return cudaGetLastError() == cudaSuccess ? EPS_OK : EPS_ECUDA;
+}
+
 int ln_grid_bwd(int64_t rows) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -238,8 +529,8 @@ extern "C" int eps_layernorm_fwd(const void* x, const float* gamma, const float*
   switch (d) {
     case 128: return ln_launch<4>(x, gamma, beta, y, mean, rstd, rows, eps, st);
     case 256: return ln_launch<8>(x, gamma, beta, y, mean, rstd, rows, eps, st);
-    case 768: return ln_launch<24>(x, gamma, beta, y, mean, rstd, rows, eps, st);
-    case 1024: return ln_launch<32>(x, gamma, beta, y, mean, rstd, rows, eps, st);
+    case 768: return ln_fwd_wide_launch<768>(x, gamma, beta, y, mean, rstd, rows, eps, st);
+    case 1024: return ln_fwd_wide_launch<1024>(x, gamma, beta, y, mean, rstd, rows, eps, st);
     default: return EPS_EINVAL;
   }
 }
@@ -258,9 +549,11 @@ extern "C" int eps_layernorm_bwd(const void* dy, const void* x, const float* gam
     case 256:
       return ln_bwd_launch<8>(dy, x, gamma, mean, rstd, dres, dx, dgamma, dbeta, colsum_dx, rows, st);
     case 768:
-      return ln_bwd_launch<24>(dy, x, gamma, mean, rstd, dres, dx, dgamma, dbeta, colsum_dx, rows, st);
+      return ln_bwd_wide_launch<768>(dy, x, gamma, mean, rstd, dres, dx, dgamma, dbeta, colsum_dx,
+                                     rows, st);
     case 1024:
-      return ln_bwd_launch<32>(dy, x, gamma, mean, rstd, dres, dx, dgamma, dbeta, colsum_dx, rows, st);
+      return ln_bwd_wide_launch<1024>(dy, x, gamma, mean, rstd, dres, dx, dgamma, dbeta,
+                                      colsum_dx, rows, st);
     default:
       return EPS_EINVAL;
   }
