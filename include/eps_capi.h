@@ -370,14 +370,23 @@ enum {
   EPS_EPI_STORE_F32 = 5,      /* Cf32 = acc (beta 0)                         */
   EPS_EPI_ACCUM_F32 = 6,      /* Cf32 += acc (split-K / micro-batch accum)   */
   EPS_EPI_RESID_BF16 = 7,     /* C = acc + aux[m,n] (residual-gradient add)  */
-  EPS_EPI_ROWDOT_BF16 = 8     /* C = acc; colsum[m*(N/64) + n/64] += sum over
+  EPS_EPI_ROWDOT_BF16 = 8,    /* C = acc; colsum[m*(N/64) + n/64] += sum over
                                  each 64-column group of bf16(acc)*aux[m,n]
                                  (attention D = rowsum(dO * O) per head, fused
                                  into the dO-producing GEMM; colsum pre-zeroed) */
+  EPS_EPI_BIAS_GELU2_BF16 = 9,/* u = acc + bias: C = gelu(u), aux = gelu'(u)
+                                 (one tanh for both; the backward then needs
+                                 only a product, EPS_EPI_MUL_BF16)             */
+  EPS_EPI_MUL_BF16 = 10       /* C = acc * aux[m,n]; colsum -> bias (dGELU
+                                 with gelu' stored by EPS_EPI_BIAS_GELU2_BF16) */
 };
 int eps_gemm_bf16(int a_mn_major, int b_mn_major, int epilogue, const void* A, const void* B,
                   void* C, const float* bias, void* aux, float* colsum, int64_t M, int64_t N,
                   int64_t K, int64_t lda, int64_t ldb, int64_t ldc, int split_k, void* stream);
+
+/* CTA-pair (cta_group::2, 256-row) GEMM tiles: mode 1 on (default), 0 off;
+ * mode < 0 only queries.  Returns the mode in effect. */
+int eps_gemm_pair_mode(int mode);
 
 /* LayerNorm over rows of width d (fp32 statistics). */
 int eps_layernorm_fwd(const void* x, const float* gamma, const float* beta, void* y,

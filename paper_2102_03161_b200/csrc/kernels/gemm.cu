@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdio>
 
 #include "eps_capi.h"
@@ -50,16 +51,22 @@ struct GemmArgs {
 // come through registers); 8 KB: 2 KB output + a 3-deep 2 KB TMA ring for the
 // aux input (residual / GELU pre-activation), used with BN = 192 so the
 // mainloop ring still keeps 4 stages.
-template <int BN, int STAGES, bool A_MN, bool B_MN, int EPIB>
+//
+// PAIR: a cluster of two CTAs computes one 256 x BN tile with cta_group::2
+// MMAs (M = 256): each CTA stages its 128 rows of A and BN/2 rows of B, so a
+// stage is 16 KB + BN*64 B per CTA instead of 16 KB + BN*128 B, and the even
+// CTA issues the MMAs for both.
+template <int BN, int STAGES, bool A_MN, bool B_MN, int EPIB, bool PAIR = false>
 struct GemmCfg {
+  static constexpr int kBRows = PAIR ? BN / 2 : BN;  // B rows staged by this CTA
   static constexpr int kABytes = kBM * kBK * 2;
-  static constexpr int kBBytes = BN * kBK * 2;
+  static constexpr int kBBytes = kBRows * kBK * 2;
   static constexpr int kStageBytes = kABytes + kBBytes;
   // double-buffered accumulator (2 x BN columns), allocation rounded to a power of two
   static constexpr int kTmemCols = 2 * BN <= 256 ? 256 : 512;
   static constexpr size_t kSmem = size_t(STAGES) * kStageBytes + 8 * size_t(EPIB) /*epilogue*/ +
                                   1024 /*align*/ + 512 /*barriers*/;
-  static constexpr uint32_t kIdesc = umma_idesc_bf16(kBM, BN, A_MN, B_MN);
+  static constexpr uint32_t kIdesc = umma_idesc_bf16(PAIR ? 2 * kBM : kBM, BN, A_MN, B_MN);
 };
 
 // Byte offset of the UMMA_K=16 slice kk inside one k-block tile.
@@ -89,6 +96,19 @@ __device__ __forceinline__ void load_operand(void* dst, const CUtensorMap* map, 
   }
 }
 
+template <int ROWS, bool MN>
+__device__ __forceinline__ void load_operand_pair(void* dst, const CUtensorMap* map,
+                                                  uint32_t bar_leader, int row0, int k0) {
+  if constexpr (MN) {
+#pragma unroll
+    for (int j = 0; j < ROWS / kMnChunk; ++j)
+      tma_load_2d_pair(static_cast<char*>(dst) + j * (kBK * 128), map, bar_leader,
+                       row0 + j * kMnChunk, k0);
+  } else {
+    tma_load_2d_pair(dst, map, bar_leader, k0, row0);
+  }
+}
+
 // ---- epilogue ----------------------------------------------------------------
 // Two warps per TMEM lane quarter (32 output rows) walk alternate 32-column
 // chunks of each tile.  Outputs are staged in a per-warp swizzled 4 KB smem
@@ -101,7 +121,7 @@ constexpr int kChunkBf16 = 2048;  // 32x32 bf16
 
 __device__ __forceinline__ bool epi_reads_aux(int epi) {
   return epi == EPS_EPI_BIAS_RESID_BF16 || epi == EPS_EPI_DGELU_BF16 ||
-         epi == EPS_EPI_RESID_BF16 || epi == EPS_EPI_ROWDOT_BF16;
+         epi == EPS_EPI_RESID_BF16 || epi == EPS_EPI_ROWDOT_BF16 || epi == EPS_EPI_MUL_BF16;
 }
 
 __device__ __forceinline__ void stage_bf16(uint32_t base, int lane, const float (&v)[32]) {
@@ -163,13 +183,21 @@ __device__ __forceinline__ void unpack_aux(const uint4 (&w)[4], float (&a)[32]) 
 
 constexpr int kAuxDepth = 3;
 
-template <int BN, int STAGES, bool A_MN, bool B_MN, int EPIB>
+std::atomic<int>& gemm_pair_mode();
+
+template <int BN, int STAGES, bool A_MN, bool B_MN, int EPIB, bool PAIR>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
                    const __grid_constant__ CUtensorMap map_b,
                    const __grid_constant__ CUtensorMap map_c,
                    const __grid_constant__ CUtensorMap map_x, const GemmArgs args) {
-  using Cfg = GemmCfg<BN, STAGES, A_MN, B_MN, EPIB>;
+  using Cfg = GemmCfg<BN, STAGES, A_MN, B_MN, EPIB, PAIR>;
+  // PAIR: rank 0 / 1 of the CTA pair; work is distributed over pairs.
+  const int rank = PAIR ? int(cluster_ctarank()) : 0;
+  const bool leader = rank == 0;
+  const int cta0 = PAIR ? int(blockIdx.x) >> 1 : int(blockIdx.x);
+  const int ncta = PAIR ? int(gridDim.x) >> 1 : int(gridDim.x);
+  constexpr int kTileM = PAIR ? 2 * kBM : kBM;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -196,14 +224,18 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tmem_full[s], 1);
-      mbar_init(&tmem_empty[s], kEpiWarps);
+      mbar_init(&tmem_empty[s], PAIR ? 2 * kEpiWarps : kEpiWarps);  // both CTAs' epilogues
     }
     for (int s = 0; s < kAuxDepth * kEpiWarps; ++s) mbar_init(&aux_full[s], 1);
     mbar_fence_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, Cfg::kTmemCols);
+  if (warp == 1) {
+    if constexpr (PAIR) tmem_alloc_pair(tmem_slot, Cfg::kTmemCols);
+    else tmem_alloc(tmem_slot, Cfg::kTmemCols);
+  }
   tc_fence_before();
   __syncthreads();
+  if constexpr (PAIR) cluster_sync_all();  // the peer's barriers are initialised
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -215,20 +247,28 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      for (int u = cta0; u < units; u += ncta) {
         const int split = u / tiles;
         const int t = u - split * tiles;
-        const int m0 = (t / args.tiles_n) * kBM;
-        const int n0 = (t % args.tiles_n) * BN;
+        const int m0 = (t / args.tiles_n) * kTileM + rank * kBM;
+        const int n0 = (t % args.tiles_n) * BN + rank * Cfg::kBRows;
         const int kb0 = split * args.k_blocks_per_split;
         const int kb1 = min(kb0 + args.k_blocks_per_split, kblocks_total);
         for (int kb = kb0; kb < kb1; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = ring + stage * Cfg::kStageBytes;
           uint8_t* sb = sa + Cfg::kABytes;
-          mbar_expect_tx(&full[stage], Cfg::kStageBytes);
-          load_operand<kBM, A_MN>(sa, &map_a, &full[stage], m0, kb * kBK);
-          load_operand<BN, B_MN>(sb, &map_b, &full[stage], n0, kb * kBK);
+          if constexpr (PAIR) {
+            // both CTAs' bytes land on the leader's full barrier
+            if (leader) mbar_expect_tx(&full[stage], 2 * Cfg::kStageBytes);
+            load_operand_pair<kBM, A_MN>(sa, &map_a, leader_addr(&full[stage]), m0, kb * kBK);
+            load_operand_pair<Cfg::kBRows, B_MN>(sb, &map_b, leader_addr(&full[stage]), n0,
+                                                 kb * kBK);
+          } else {
+            mbar_expect_tx(&full[stage], Cfg::kStageBytes);
+            load_operand<kBM, A_MN>(sa, &map_a, &full[stage], m0, kb * kBK);
+            load_operand<BN, B_MN>(sb, &map_b, &full[stage], n0, kb * kBK);
+          }
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -237,12 +277,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    if (lane == 0 && leader) {  // PAIR: the even CTA issues for both
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      for (int u = cta0; u < units; u += ncta) {
         const int split = u / tiles;
         const int kb0 = split * args.k_blocks_per_split;
         const int kb1 = min(kb0 + args.k_blocks_per_split, kblocks_total);
@@ -255,16 +295,23 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t sa = smem_addr(ring + stage * Cfg::kStageBytes);
           const uint32_t sb = sa + Cfg::kABytes;
 #pragma unroll
-          for (int kk = 0; kk < kBK / 16; ++kk)
-            tc_mma_bf16(d_tmem, operand_desc<A_MN>(sa, kk), operand_desc<B_MN>(sb, kk),
-                        Cfg::kIdesc, (kb > kb0 || kk > 0) ? 1u : 0u);
-          tc_commit(&empty[stage]);
+          for (int kk = 0; kk < kBK / 16; ++kk) {
+            if constexpr (PAIR)
+              tc_mma_pair(d_tmem, operand_desc<A_MN>(sa, kk), operand_desc<B_MN>(sb, kk),
+                          Cfg::kIdesc, (kb > kb0 || kk > 0) ? 1u : 0u);
+            else
+              tc_mma_bf16(d_tmem, operand_desc<A_MN>(sa, kk), operand_desc<B_MN>(sb, kk),
+                          Cfg::kIdesc, (kb > kb0 || kk > 0) ? 1u : 0u);
+          }
+          if constexpr (PAIR) tc_commit_pair(&empty[stage]);
+          else tc_commit(&empty[stage]);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        tc_commit(&tmem_full[acc]);
+        if constexpr (PAIR) tc_commit_pair(&tmem_full[acc]);
+        else tc_commit(&tmem_full[acc]);
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
@@ -281,13 +328,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     const bool f32_out = epi == EPS_EPI_STORE_F32 || epi == EPS_EPI_ACCUM_F32;
     // Per-warp out ring: GELU (2 outputs) and fp32 chunks take 4 KB, bf16 2 KB;
     // with the aux TMA ring: one 2 KB out slot + kAuxDepth 2 KB aux slots.
-    const int out_bytes = (epi == EPS_EPI_BIAS_GELU_BF16 || f32_out) ? 4096 : 2048;
-    const int n_out = aux_tma ? 1 : kEpiWarpBytes / out_bytes;
+    const bool two_out = epi == EPS_EPI_BIAS_GELU_BF16 || epi == EPS_EPI_BIAS_GELU2_BF16;
+    const int out_bytes = (two_out || f32_out) ? 4096 : 2048;
+    const int n_out = aux_tma ? 1 : EPIB / out_bytes;
     const uint16_t* auxp = static_cast<const uint16_t*>(args.aux);
     uint64_t* my_aux_bar = aux_full + kAuxDepth * ew;
     const uint32_t aux_s = area_s + kChunkBf16;
     // TMA prefetch cursor over this warp's (tile, chunk) stream: c = part, part+2, ...
-    int pf_u = blockIdx.x, pf_c = part;
+    int pf_u = cta0, pf_c = part;
     uint32_t pf_n = 0, use_n = 0;
     auto chunks_of = [&](int uu) {
       const int tt = uu % tiles;
@@ -296,12 +344,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     auto tma_prefetch_until = [&](uint32_t limit) {
       while (pf_n < limit) {
         while (pf_u < units && pf_c >= chunks_of(pf_u)) {
-          pf_u += gridDim.x;
+          pf_u += ncta;
           pf_c = part;
         }
         if (pf_u >= units) return;
         const int tt = pf_u % tiles;
-        const int row = (tt / args.tiles_n) * kBM + quarter * 32;
+        const int row = (tt / args.tiles_n) * kTileM + rank * kBM + quarter * 32;
         const int col = (tt % args.tiles_n) * BN + pf_c * 32;
         const uint32_t slot = pf_n % kAuxDepth;
         fence_proxy_async_smem();
@@ -319,25 +367,25 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (!aux_in || aux_tma || uu >= units) return;
       const int tt = uu % tiles;
       const int pn0 = (tt % args.tiles_n) * BN;
-      const int prow = (tt / args.tiles_n) * kBM + quarter * 32 + lane;
+      const int prow = (tt / args.tiles_n) * kTileM + rank * kBM + quarter * 32 + lane;
       if (prow >= args.M) return;
       const int pch = min(BN / 32, (args.N - pn0 + 31) / 32);
       for (int c = part; c < pch; c += 2) prefetch_l2(auxp + int64_t(prow) * args.ldc + pn0 + c * 32);
     };
-    prefetch_aux(blockIdx.x);
+    prefetch_aux(cta0);
 
     uint32_t out_n = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    for (int u = cta0; u < units; u += ncta) {
       const int split = u / tiles;
       const int t = u - split * tiles;
-      const int m0 = (t / args.tiles_n) * kBM;
+      const int m0 = (t / args.tiles_n) * kTileM + rank * kBM;
       const int n0 = (t % args.tiles_n) * BN;
       const int row0 = m0 + quarter * 32;
       const int my_row = row0 + lane;
       const int chunks = min(BN / 32, (args.N - n0 + 31) / 32);
-      prefetch_aux(u + gridDim.x);
+      prefetch_aux(u + ncta);
       uint4 xa[4];
       if (aux_in && !aux_tma && part < chunks)
         load_aux_row(auxp, args.ldc, my_row, args.M, n0 + part * 32, args.N, xa);
@@ -400,10 +448,21 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int j = 0; j < 32; ++j) v[j] += x[j];
             stage_bf16(out_s, lane, v);
             break;
+          case EPS_EPI_BIAS_GELU2_BF16:
+#pragma unroll
+            for (int j = 0; j < 32; ++j) gelu_and_grad_f(v[j], v[j], x[j]);
+            stage_bf16(out_s + kChunkBf16, lane, x);  // gelu' -> map_x
+            stage_bf16(out_s, lane, v);
+            break;
           case EPS_EPI_DGELU_BF16:
 #pragma unroll
             for (int j = 0; j < 32; ++j)
               v[j] = __bfloat162float(__float2bfloat16_rn(v[j] * gelu_grad_f(x[j])));
+            stage_bf16(out_s, lane, v);
+            break;
+          case EPS_EPI_MUL_BF16:
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = __bfloat162float(__float2bfloat16_rn(v[j] * x[j]));
             stage_bf16(out_s, lane, v);
             break;
           case EPS_EPI_ROWDOT_BF16: {
@@ -433,13 +492,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_reduce_add_2d(&map_c, my_area + out_off, col0, row0);
           } else {
             tma_store_2d(&map_c, my_area + out_off, col0, row0);
-            if (epi == EPS_EPI_BIAS_GELU_BF16)
-              tma_store_2d(&map_x, my_area + out_off + kChunkBf16, col0, row0);
+            if (two_out) tma_store_2d(&map_x, my_area + out_off + kChunkBf16, col0, row0);
           }
           bulk_commit();
         }
         ++out_n;
-        if (epi == EPS_EPI_DGELU_BF16 && args.colsum != nullptr) {
+        if ((epi == EPS_EPI_DGELU_BF16 || epi == EPS_EPI_MUL_BF16) && args.colsum != nullptr) {
           // rows past M were zero-filled by TMA (and aux zeroed), so they contribute 0
           const float s = warp_transpose_sum32(v);
           if (lane < valid) atomicAdd(args.colsum + col0 + lane, s);
@@ -451,7 +509,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&tmem_empty[acc]);
+      if (lane == 0) {
+        if constexpr (PAIR) mbar_arrive_cluster(leader_addr(&tmem_empty[acc]));
+        else mbar_arrive(&tmem_empty[acc]);
+      }
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
@@ -460,19 +521,21 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   tc_fence_before();
   __syncthreads();
+  if constexpr (PAIR) cluster_sync_all();  // no remote traffic targets an exited CTA
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem_base, Cfg::kTmemCols);
+    if constexpr (PAIR) tmem_dealloc_pair(tmem_base, Cfg::kTmemCols);
+    else tmem_dealloc(tmem_base, Cfg::kTmemCols);
   }
 }
 
 // ---- host side -------------------------------------------------------------
 
-template <int BN, int STAGES, bool A_MN, bool B_MN, int EPIB = 4096>
+template <int BN, int STAGES, bool A_MN, bool B_MN, int EPIB = 4096, bool PAIR = false>
 int launch(const void* A, const void* B, int64_t lda, int64_t ldb, GemmArgs args,
            cudaStream_t stream) {
-  using Cfg = GemmCfg<BN, STAGES, A_MN, B_MN, EPIB>;
-  auto kern = gemm_tc_kernel<BN, STAGES, A_MN, B_MN, EPIB>;
+  using Cfg = GemmCfg<BN, STAGES, A_MN, B_MN, EPIB, PAIR>;
+  auto kern = gemm_tc_kernel<BN, STAGES, A_MN, B_MN, EPIB, PAIR>;
   static bool configured = false;
   if (!configured) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -487,7 +550,7 @@ int launch(const void* A, const void* B, int64_t lda, int64_t ldb, GemmArgs args
   const bool ok_a = A_MN ? make_map(&ma, A, false, args.M, args.K, lda, 64, kBK, SW128)
                          : make_map(&ma, A, false, args.K, args.M, lda, 64, kBM, SW128);
   const bool ok_b = B_MN ? make_map(&mb, B, false, args.N, args.K, ldb, 64, kBK, SW128)
-                         : make_map(&mb, B, false, args.K, args.N, ldb, 64, BN, SW128);
+                         : make_map(&mb, B, false, args.K, args.N, ldb, 64, Cfg::kBRows, SW128);
   const bool f32 = args.epi == EPS_EPI_STORE_F32 || args.epi == EPS_EPI_ACCUM_F32;
   const bool ok_c = make_map(&mc, args.C, f32, args.N, args.M, args.ldc, 32, 32, f32 ? SW128 : SW64);
   // aux: GELU pre-activation output (TMA store); residual / pre-activation
@@ -496,12 +559,45 @@ int launch(const void* A, const void* B, int64_t lda, int64_t ldb, GemmArgs args
   const bool ok_x = make_map(&mx, xptr, false, args.N, args.M, args.ldc, 32, 32, SW64);
   if (!ok_a || !ok_b || !ok_c || !ok_x) return EPS_ECUDA;
   const int units = args.tiles_m * args.tiles_n * args.splits;
+  if constexpr (PAIR) {
+    const int pairs = units < sm_count() / 2 ? units : sm_count() / 2;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2 * pairs);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = Cfg::kSmem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    count_launch();
+    if (cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, mx, args) != cudaSuccess) return EPS_ECUDA;
+    return cudaGetLastError() == cudaSuccess ? EPS_OK : EPS_ECUDA;
+  }
   const int grid = units < sm_count() ? units : sm_count();
   count_launch(); kern<<<grid, kThreads, Cfg::kSmem, stream>>>(ma, mb, mc, mx, args);
   return cudaGetLastError() == cudaSuccess ? EPS_OK : EPS_ECUDA;
 }
 
+// CTA-pair tiles on (1, default; EPS_GEMM_PAIR=0 in the environment or
+// eps_gemm_pair_mode(0) turns them off for A/B comparisons).
+std::atomic<int>& gemm_pair_mode() {
+  static std::atomic<int> mode{[] {
+    const char* e = std::getenv("EPS_GEMM_PAIR");
+    return e == nullptr ? 1 : std::atoi(e);
+  }()};
+  return mode;
+}
+
 }  // namespace eps_k
+
+extern "C" int eps_gemm_pair_mode(int mode) {
+  if (mode >= 0) eps_k::gemm_pair_mode().store(mode);
+  return eps_k::gemm_pair_mode().load();
+}
 
 extern "C" int eps_gemm_bf16(int a_mn_major, int b_mn_major, int epilogue, const void* A,
                              const void* B, void* C, const float* bias, void* aux,
@@ -509,16 +605,18 @@ extern "C" int eps_gemm_bf16(int a_mn_major, int b_mn_major, int epilogue, const
                              int64_t ldb, int64_t ldc, int split_k, void* stream) {
   using namespace eps_k;
   if (M <= 0 || N <= 0 || K <= 0 || N % 8 != 0 || lda % 8 != 0 || ldb % 8 != 0 ||
-      ldc % 8 != 0 || M > (int64_t(1) << 31) || epilogue < 0 || epilogue > EPS_EPI_ROWDOT_BF16)
+      ldc % 8 != 0 || M > (int64_t(1) << 31) || epilogue < 0 || epilogue > EPS_EPI_MUL_BF16)
     return EPS_EINVAL;
   if (epilogue == EPS_EPI_ROWDOT_BF16 && (N % 64 != 0 || colsum == nullptr)) return EPS_EINVAL;
   const bool auto_split = split_k == 0 && epilogue == EPS_EPI_ACCUM_F32;
   if (split_k < 1) split_k = 1;
   const bool needs_aux = epilogue == EPS_EPI_BIAS_GELU_BF16 || epilogue == EPS_EPI_BIAS_RESID_BF16 ||
+                         epilogue == EPS_EPI_BIAS_GELU2_BF16 || epilogue == EPS_EPI_MUL_BF16 ||
                          epilogue == EPS_EPI_DGELU_BF16 || epilogue == EPS_EPI_RESID_BF16 ||
                          epilogue == EPS_EPI_ROWDOT_BF16;
   if (needs_aux && aux == nullptr) return EPS_EINVAL;
   if ((epilogue == EPS_EPI_BIAS_BF16 || epilogue == EPS_EPI_BIAS_GELU_BF16 ||
+       epilogue == EPS_EPI_BIAS_GELU2_BF16 ||
        epilogue == EPS_EPI_BIAS_RESID_BF16) && bias == nullptr)
     return EPS_EINVAL;
   if (split_k > 1 && epilogue != EPS_EPI_ACCUM_F32) return EPS_EINVAL;
@@ -530,17 +628,23 @@ extern "C" int eps_gemm_bf16(int a_mn_major, int b_mn_major, int epilogue, const
   args.C = C;
   args.ldc = ldc;
   args.bias = (epilogue == EPS_EPI_BIAS_BF16 || epilogue == EPS_EPI_BIAS_GELU_BF16 ||
+               epilogue == EPS_EPI_BIAS_GELU2_BF16 ||
                epilogue == EPS_EPI_BIAS_RESID_BF16) ? bias : nullptr;
   args.aux = aux;
   args.colsum = colsum;
   const int kblocks = int((K + kBK - 1) / kBK);
+  // CTA pairs (256-row tiles, cta_group::2) for every GEMM with at least two
+  // pair tiles of rows and a 256-multiple N (all ViT-B / BERT block GEMMs);
+  // EPS_GEMM_PAIR=0 forces single-CTA tiles (A/B comparisons).
+  const bool pair = gemm_pair_mode() != 0 && M >= 512 && N % 256 == 0;
+  const int64_t tile_m = pair ? 2 * kBM : kBM;
   if (auto_split) {
     // wgrad: few output tiles, long contraction over token rows.  Pick the
     // split s minimising waves(s) * (k-blocks per split + 1): one k-block of
     // MMA is about the cost of a unit's fp32 tile reduce-add.  Each split
     // keeps >= 4 k-blocks.
-    const int64_t tiles = ((M + kBM - 1) / kBM) * ((N + 255) / 256);
-    const int64_t sms = sm_count();
+    const int64_t tiles = ((M + tile_m - 1) / tile_m) * ((N + 255) / 256);
+    const int64_t sms = pair ? sm_count() / 2 : sm_count();  // concurrent tile workers
     const int cap = std::max(1, std::min(16, kblocks / 4));
     double best = 1e30;
     for (int sk = 1; sk <= cap; ++sk) {
@@ -555,14 +659,40 @@ extern "C" int eps_gemm_bf16(int a_mn_major, int b_mn_major, int epilogue, const
   if (split_k > kblocks) split_k = kblocks;
   args.k_blocks_per_split = (kblocks + split_k - 1) / split_k;
   args.splits = (kblocks + args.k_blocks_per_split - 1) / args.k_blocks_per_split;
-  args.tiles_m = int((M + kBM - 1) / kBM);
+  args.tiles_m = int((M + tile_m - 1) / tile_m);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const int key = (a_mn_major ? 2 : 0) | (b_mn_major ? 1 : 0);
+  const bool aux_or_two = epilogue == EPS_EPI_BIAS_RESID_BF16 || epilogue == EPS_EPI_DGELU_BF16 ||
+                          epilogue == EPS_EPI_RESID_BF16 || epilogue == EPS_EPI_ROWDOT_BF16 ||
+                          epilogue == EPS_EPI_MUL_BF16 || epilogue == EPS_EPI_BIAS_GELU2_BF16;
+  if (pair) {
+    // 256 x 256 pair tiles; a CTA stages 32 KB per k-block, so 6 stages fit
+    // beside the 4 KB-per-warp epilogue staging, or 5 beside the 8 KB aux ring.
+    args.tiles_n = int(N / 256);
+    if (aux_or_two) {
+      switch (key) {
+        case 0: return launch<256, 5, false, false, 8192, true>(A, B, lda, ldb, args, st);
+        case 1: return launch<256, 5, false, true, 8192, true>(A, B, lda, ldb, args, st);
+        case 2: return launch<256, 5, true, false, 8192, true>(A, B, lda, ldb, args, st);
+        default: return launch<256, 5, true, true, 8192, true>(A, B, lda, ldb, args, st);
+      }
+    }
+    switch (key) {
+      case 0: return launch<256, 6, false, false, 4096, true>(A, B, lda, ldb, args, st);
+      case 1: return launch<256, 6, false, true, 4096, true>(A, B, lda, ldb, args, st);
+      case 2: return launch<256, 6, true, false, 4096, true>(A, B, lda, ldb, args, st);
+      default: return launch<256, 6, true, true, 4096, true>(A, B, lda, ldb, args, st);
+    }
+  }
   // Epilogues that read an aux input (residual, GELU pre-activation) are
   // latency-bound on it: BN = 192 tiles free smem for a 3-deep TMA aux ring.
   const bool aux_epi = epilogue == EPS_EPI_BIAS_RESID_BF16 || epilogue == EPS_EPI_DGELU_BF16 ||
-                       epilogue == EPS_EPI_RESID_BF16 || epilogue == EPS_EPI_ROWDOT_BF16;
-  if (aux_epi && N >= 192) {
+                       epilogue == EPS_EPI_RESID_BF16 || epilogue == EPS_EPI_ROWDOT_BF16 ||
+                       epilogue == EPS_EPI_MUL_BF16;
+  // Two-output GELU forward: BN = 192 leaves 8 KB per epilogue warp, i.e. two
+  // 4 KB (gelu, gelu') staging slots, so a chunk's stores drain while the
+  // next chunk is computed.
+  if ((aux_epi || epilogue == EPS_EPI_BIAS_GELU2_BF16) && N >= 192) {
     args.tiles_n = int((N + 191) / 192);
     switch (key) {
       case 0: return launch<192, 4, false, false, 8192>(A, B, lda, ldb, args, st);

@@ -172,6 +172,15 @@ __device__ __forceinline__ float gelu_grad_f(float x) {
   return fmaf(0.5f, t, 0.5f) + (0.5f * x) * fmaf(-t, t, 1.0f) * fmaf(3.0f * kGeluC1, u, kGeluC0);
 }
 
+// gelu(x) and gelu'(x) from one tanh.
+__device__ __forceinline__ void gelu_and_grad_f(float x, float& g, float& gp) {
+  const float u = x * x;
+  const float t = tanh_approx(x * fmaf(kGeluC1, u, kGeluC0));
+  const float h = 0.5f * x;
+  g = fmaf(h, t, h);
+  gp = fmaf(0.5f, t, 0.5f) + h * fmaf(-t, t, 1.0f) * fmaf(3.0f * kGeluC1, u, kGeluC0);
+}
+
 // After this, lane j holds sum over the warp's 32 lanes of v[j] (31 shuffles).
 __device__ __forceinline__ float warp_transpose_sum32(float (&v)[32]) {
   const int lane = threadIdx.x & 31;
@@ -365,5 +374,70 @@ __device__ __forceinline__ void tc_commit_ws(uint64_t* bar) {
       "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
       "}\n" ::"r"(smem_addr(bar))
       : "memory");
+}
+}  // namespace eps_k
+
+// ---- CTA pairs (cluster of 2, tcgen05 cta_group::2) -------------------------
+// A pair computes one 256-row tile: each CTA stages its 128 rows of A and
+// half of B; the even ("leader") CTA issues M=256 MMAs that read both CTAs'
+// shared memory and accumulate into both CTAs' TMEM.
+namespace eps_k {
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+// The leader CTA's copy of a shared-memory object, as a shared::cluster
+// address (rank bit cleared), for TMA completion and remote arrivals.
+__device__ __forceinline__ uint32_t leader_addr(const void* p) { return smem_addr(p) & 0xFEFFFFFFu; }
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const void* tmap, uint32_t bar_leader,
+                                                 int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_addr(dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(bar_leader), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
+__device__ __forceinline__ void tc_mma_pair(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                            uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// Arrive on the barrier at this offset in both CTAs of the pair once the
+// issuing thread's MMAs complete.
+__device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "{\n"
+      ".reg .b16 m;\n"
+      "mov.b16 m, 3;\n"
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], m;\n"
+      "}\n" ::"r"(smem_addr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tmem_alloc_pair(uint32_t* slot, uint32_t cols) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                   smem_addr(slot)),
+               "r"(cols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc_pair(uint32_t taddr, uint32_t cols) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(cols)
+               : "memory");
 }
 }  // namespace eps_k

@@ -296,7 +296,7 @@ struct eps_bert {
   void mlp_fwd(int l, int b0, int b, cudaStream_t st) {
     const LayerSlots& s = lay.layer[l];
     const int64_t d = g.d, f = g.f, r0 = int64_t(b0) * g.tokens, R = int64_t(b) * g.tokens;
-    mm(0, 0, EPS_EPI_BIAS_GELU_BF16, act.X1[l] + r0 * d, W(s.w1), act.G[l] + r0 * f, P(s.b1),
+    mm(0, 0, EPS_EPI_BIAS_GELU2_BF16, act.X1[l] + r0 * d, W(s.w1), act.G[l] + r0 * f, P(s.b1),
        act.U[l] + r0 * f, nullptr, R, f, d, d, d, f, 1, st);
     mm(0, 0, EPS_EPI_BIAS_RESID_BF16, act.G[l] + r0 * f, W(s.w2), act.S2[l] + r0 * d, P(s.b2),
        act.X1[l] + r0 * d, nullptr, R, d, f, f, f, d, 1, st);
@@ -384,7 +384,7 @@ struct eps_bert {
                   Gr(s.b2), R, st);
     mm(1, 1, EPS_EPI_ACCUM_F32, dS, Gm, Gr(s.w2), nullptr, nullptr, nullptr, d, f, R, d, f, f,
        split, st);
-    mm(0, 1, EPS_EPI_DGELU_BF16, dS, W(s.w2), Gm, nullptr, act.U[l] + r0 * f, Gr(s.b1), R, f, d, d,
+    mm(0, 1, EPS_EPI_MUL_BF16, dS, W(s.w2), Gm, nullptr, act.U[l] + r0 * f, Gr(s.b1), R, f, d, d,
        f, f, 1, st);
     mm(1, 1, EPS_EPI_ACCUM_F32, Gm, act.X1[l] + r0 * d, Gr(s.w1), nullptr, nullptr, nullptr, f, d,
        R, f, d, d, split, st);

@@ -320,7 +320,7 @@ struct eps_vit {
     const int64_t d = g.d, f = g.f, r0 = int64_t(b0) * g.tokens, R = int64_t(b) * g.tokens;
     layernorm(act.X1[l] + r0 * d, s.ln2g, s.ln2b, act.H2[l] + r0 * d, act.mean2[l] + r0,
               act.rstd2[l] + r0, R, st);
-    mm(0, 0, EPS_EPI_BIAS_GELU_BF16, act.H2[l] + r0 * d, W(s.w1), act.G[l] + r0 * f, P(s.b1),
+    mm(0, 0, EPS_EPI_BIAS_GELU2_BF16, act.H2[l] + r0 * d, W(s.w1), act.G[l] + r0 * f, P(s.b1),
        act.U[l] + r0 * f, nullptr, R, f, d, d, d, f, 1, st);
     mm(0, 0, EPS_EPI_BIAS_RESID_BF16, act.G[l] + r0 * f, W(s.w2),
        out_buf(2 * l + 2, act.X[l + 1]) + r0 * d, P(s.b2), act.X1[l] + r0 * d, nullptr, R, d, f,
@@ -376,7 +376,7 @@ struct eps_vit {
     mm(1, 1, EPS_EPI_ACCUM_F32, dX, Gm, Gr(s.w2), nullptr, nullptr, nullptr, d, f, R, d, f, f,
        split, st);
     // du overwrites G (its last reader was the dW2 GEMM above)
-    mm(0, 1, EPS_EPI_DGELU_BF16, dX, W(s.w2), Gm, nullptr, act.U[l] + r0 * f, Gr(s.b1), R, f, d,
+    mm(0, 1, EPS_EPI_MUL_BF16, dX, W(s.w2), Gm, nullptr, act.U[l] + r0 * f, Gr(s.b1), R, f, d,
        d, f, f, 1, st);
     mm(1, 1, EPS_EPI_ACCUM_F32, Gm, act.H2[l] + r0 * d, Gr(s.w1), nullptr, nullptr, nullptr, f,
        d, R, f, d, d, split, st);

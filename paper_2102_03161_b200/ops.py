@@ -24,6 +24,8 @@ EPI_STORE_F32 = 5
 EPI_ACCUM_F32 = 6
 EPI_RESID_BF16 = 7
 EPI_ROWDOT_BF16 = 8
+EPI_BIAS_GELU2_BF16 = 9
+EPI_MUL_BF16 = 10
 
 _api: Optional[EpsApi] = None
 

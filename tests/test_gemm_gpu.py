@@ -21,8 +21,11 @@ def _close(out, ref, rtol=RTOL):
     assert err <= rtol * scale + 1e-3, f"max err {err} vs scale {scale}"
 
 
+# (3546, 2304), (600, 512), (2000, 768): CTA-pair (256-row, cta_group::2)
+# tiles, including pairs whose second CTA is partly / wholly past M.
 @pytest.mark.parametrize("M,N,K", [(128, 256, 64), (3546, 2304, 768), (300, 768, 3072),
-                                   (1000, 1000, 768), (77, 768, 768), (400, 1000, 777)])
+                                   (1000, 1000, 768), (77, 768, 768), (400, 1000, 777),
+                                   (600, 512, 192), (2000, 768, 3072)])
 @pytest.mark.parametrize("a_mn,b_mn", [(False, False), (False, True), (True, False),
                                        (True, True)])
 def test_gemm_store(cuda, M, N, K, a_mn, b_mn):
@@ -65,6 +68,30 @@ def test_gemm_epilogues(cuda):
     uf = u.float()
     gprime = 0.5 * (1 + torch.erf(uf / 2 ** 0.5)) + uf * torch.exp(-0.5 * uf * uf) / (2 * torch.pi) ** 0.5
     refd = _ref(a, b, False, False) * gprime
+    _close(d, refd)
+    _close(colsum, refd.sum(0), rtol=2e-2)
+
+
+def test_gemm_gelu2_mul(cuda):
+    """FC1 forward stores gelu(u) and gelu'(u); the FC2 dgrad multiplies by gelu'."""
+    M, N, K = 1000, 3072, 768
+    g = torch.Generator(device=cuda).manual_seed(9)
+    a = torch.randn(M, K, device=cuda, generator=g).bfloat16()
+    b = (torch.randn(N, K, device=cuda, generator=g) * 0.05).bfloat16()
+    bias = torch.randn(N, device=cuda, generator=g)
+    u = _ref(a, b, False, False) + bias
+    out = torch.empty(M, N, device=cuda, dtype=torch.bfloat16)
+    gp = torch.empty_like(out)
+    ops.gemm(a, b, out, epilogue=ops.EPI_BIAS_GELU2_BF16, bias=bias, aux=gp)
+    torch.cuda.synchronize()
+    _close(out, torch.nn.functional.gelu(u))
+    want_gp = 0.5 * (1 + torch.erf(u / 2 ** 0.5)) + u * torch.exp(-0.5 * u * u) / (2 * torch.pi) ** 0.5
+    _close(gp, want_gp)
+    colsum = torch.zeros(N, device=cuda)
+    d = torch.empty_like(out)
+    ops.gemm(a, b, d, epilogue=ops.EPI_MUL_BF16, aux=gp, colsum=colsum)
+    torch.cuda.synchronize()
+    refd = _ref(a, b, False, False) * gp.float()
     _close(d, refd)
     _close(colsum, refd.sum(0), rtol=2e-2)
 
