@@ -474,7 +474,10 @@ struct eps_vit {
         start = cache_old;
       }
       if (start == 0 && cache_mode != 1) embed_fwd(images, b0, b, st);
-      for (int l = start; l < l_frozen; ++l) {
+      // frozen layers below the span (a span starting below 2*L_f -- AutoPipe
+      // off, frozen layers on their stage -- runs them itself)
+      const int prefix_end = g0 / 2 < l_frozen ? g0 / 2 : l_frozen;
+      for (int l = start; l < prefix_end; ++l) {
         att_fwd(l, b0, b, st);
         mlp_fwd(l, b0, b, st);
       }
@@ -490,6 +493,9 @@ struct eps_vit {
   // may walk a stage's span in pieces, e.g. to launch gradient buckets early).
   void stage_bwd(int b0, int b, int g0, int g1, int stage_g0, int l_frozen, bool cut_out,
                  cudaStream_t st) {
+    // frozen sublayers inside the span have no backward
+    if (g0 < 2 * l_frozen) g0 = 2 * l_frozen;
+    if (stage_g0 < 2 * l_frozen) stage_g0 = 2 * l_frozen;
     if (g1 <= g0) return;
     const int64_t d = g.d, R = int64_t(b) * g.tokens;
     if (cut_out) {
@@ -519,8 +525,7 @@ struct eps_vit {
     if (b0 < 0 || b < 1 || b0 + b > g.max_batch) throw int(EPS_EINVAL);
   }
   void check_span(int g0, int g1, int l_frozen) const {
-    if (l_frozen < 0 || l_frozen >= g.layers || g0 < 2 * l_frozen || g1 < g0 ||
-        g1 > 2 * g.layers)
+    if (l_frozen < 0 || l_frozen >= g.layers || g0 < 0 || g1 < g0 || g1 > 2 * g.layers)
       throw int(EPS_EINVAL);
   }
 };
@@ -651,7 +656,8 @@ int eps_vit_stage_forward(eps_vit* h, const float* images, int b0, int b, int g0
     h->check_rows(b0, b);
     h->check_span(g0, g1, l_frozen);
     if (front && images == nullptr && cache_mode != 1) throw int(EPS_EINVAL);
-    if (cache_mode != 0 && (!front || store == nullptr || ids == nullptr || l_frozen == 0))
+    if (cache_mode != 0 &&
+        (!front || store == nullptr || ids == nullptr || l_frozen == 0 || g0 < 2 * l_frozen))
       throw int(EPS_EINVAL);
     h->stage_fwd(images, b0, b, g0, g1, l_frozen, front != 0, cache_mode, cache_old, store, ids,
                  static_cast<cudaStream_t>(stream));

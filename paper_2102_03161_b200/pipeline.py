@@ -49,7 +49,7 @@ class StagePlan:
 
     @staticmethod
     def from_decision(d, layers: int) -> "StagePlan":
-        base = 2 * d.l_frozen
+        base = getattr(d, "span_base", 2 * d.l_frozen)
         spans = tuple((base + b, base + e) for b, e in d.spans)
         return StagePlan(d.pipeline_length, d.replica_width, d.micro_batches, d.l_frozen,
                          layers, spans)
@@ -59,8 +59,13 @@ class StagePlan:
         return rank // self.K, rank % self.K
 
     def trainable(self, s: int) -> bool:
-        g0, g1 = self.spans[s]
-        return g1 > g0
+        return self.spans[s][1] > self.first_active(s)
+
+    def first_active(self, s: int) -> int:
+        """First trainable sublayer of stage s: with AutoPipe off the epoch-0
+        partition is kept and frozen sublayers stay on their stage (forward
+        only), so a span may start below 2 * L_f."""
+        return max(self.spans[s][0], 2 * self.l_frozen)
 
     def upstream_needs_grad(self, s: int) -> bool:
         """Stage s sends dX to s-1 iff some earlier stage holds trainable
@@ -279,6 +284,7 @@ class StageRunner:
         self.range = (0, 0)
         self.buckets: List[Tuple[int, int]] = []
         self.pending: List[Tuple[object, int, int]] = []
+        self.trace: Optional[list] = None  # [] records the next iteration's blocks
 
     # -- plan changes ------------------------------------------------------------
     def _dp_groups(self, plan: StagePlan):
@@ -297,6 +303,7 @@ class StageRunner:
         self.plan = plan
         self.pipe, self.stage = plan.role(self.rank)
         self.g0, self.g1 = plan.spans[self.stage]
+        self.a0 = plan.first_active(self.stage)  # trainable sublayers: [a0, g1)
         self.groups = self._dp_groups(plan)
         self.range = self.ex.param_range(*plan.owner_spans()[self.stage])
         self.buckets = self._plan_buckets() if plan.R > 1 else []
@@ -307,10 +314,10 @@ class StageRunner:
         """Sublayer pieces [g_lo, g_hi) of this stage, top first, each closed
         once its fp32 gradients reach the bucket size."""
         out, hi, acc = [], self.g1, 0
-        for g in range(self.g1 - 1, self.g0 - 1, -1):
+        for g in range(self.g1 - 1, self.a0 - 1, -1):
             a, b = self.ex.param_range(g, g + 1)
             acc += 4 * (b - a)
-            if acc >= self.bucket_bytes or g == self.g0:
+            if acc >= self.bucket_bytes or g == self.a0:
                 out.append((g, hi))
                 hi, acc = g, 0
         return out
@@ -339,6 +346,10 @@ class StageRunner:
         prev, nxt = self.rank - 1, self.rank + 1
         pl = self.peer if (self.peer is not None and K > 1) else None
         ex.loss_sum.zero_()
+        tr = self.trace
+        if tr is not None:
+            tr.clear()
+            t_iter = self._mark()
         if pl is not None and s < K - 1 and pl.iters > 0:
             pl.wait(PeerLink.FREE, pl.iters)  # receiver done with last iteration's rows
         for b0, b in mbs:
@@ -347,10 +358,13 @@ class StageRunner:
                     pl.wait(PeerLink.FWD, pl.fwd + 1)
             elif s > 0:
                 self.tp.recv(ex.cut_rows(self.g0, b0, b), prev)
+            t0 = self._mark() if tr is not None else None
             ex.stage_forward(images if s == 0 else None, b0, b, self.g0, self.g1, lf,
                              front=(s == 0), cache_mode=cache_mode if s == 0 else 0,
                              cache_old=cache_old, store=store if s == 0 else None,
                              ids=ids if s == 0 else None)
+            if tr is not None:
+                tr.append(("F", f"mb{len(tr)}", t0, self._mark()))
             if s < K - 1:
                 if pl is not None:
                     if pl.copy_out is not None:
@@ -366,6 +380,7 @@ class StageRunner:
                 pl.fwd += 1
         if p.trainable(s):
             for i, (b0, b) in enumerate(reversed(mbs)):
+                t0 = self._mark() if tr is not None else None
                 if s < K - 1:
                     if pl is not None:
                         pl.wait(PeerLink.BWD, pl.bwd + 1)
@@ -382,6 +397,8 @@ class StageRunner:
                         self.pending.append((work, a, e))
                 else:
                     ex.stage_backward(b0, b, self.g0, self.g1, lf, cut_out=s < K - 1)
+                if tr is not None:
+                    tr.append(("B", f"mb{len(mbs) - 1 - i}", t0, self._mark()))
                 if p.upstream_needs_grad(s):
                     if pl is not None:
                         pl.signal(pl.prev_flags, PeerLink.BWD, pl.bwd + 1)
@@ -393,7 +410,29 @@ class StageRunner:
             pl.iters += 1
             if s > 0:
                 pl.signal(pl.prev_flags, PeerLink.FREE, pl.iters)
+        if tr is not None:
+            tr.insert(0, ("iteration", "", t_iter, None))
         return ex.loss_sum
+
+    # -- measured timeline (report bundle) -------------------------
+    @staticmethod
+    def _mark():
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        return e
+
+    def timeline(self):
+        """Blocks of the last traced iteration in the reference's timeline schema
+        (runner.cpp:357-367: device, kind, start_s, end_s, tag), from CUDA events
+        on this rank's stream, relative to the iteration start; `trace = []`
+        turns tracing on."""
+        if not self.trace:
+            return []
+        torch.cuda.synchronize()
+        t_iter = self.trace[0][2]
+        return [{"device": self.rank, "kind": k, "start_s": t_iter.elapsed_time(a) / 1e3,
+                 "end_s": t_iter.elapsed_time(b) / 1e3, "tag": tag}
+                for k, tag, a, b in self.trace[1:]]
 
     def sync_grads(self):
         """Finish the bucket all-reduces of this iteration and average this
@@ -408,7 +447,7 @@ class StageRunner:
 
     def step(self, lr: float, momentum: float = 0.9, weight_decay: float = 0.0):
         if self.plan.trainable(self.stage):
-            a, b = self.ex.param_range(self.g0, self.g1)
+            a, b = self.ex.param_range(self.a0, self.g1)
             self.ex.sgd_range(a, b, lr, momentum, weight_decay)
 
     def layer_sqnorms(self, segments: Sequence[int]) -> torch.Tensor:
@@ -420,7 +459,7 @@ class StageRunner:
         L = len(segments) - 1
         out = torch.zeros(L, dtype=torch.float64, device=self.ex.g32.device)
         if p.trainable(self.stage):
-            a, b = self.ex.param_range(self.g0, self.g1)
+            a, b = self.ex.param_range(self.a0, self.g1)
             cuts = sorted({a, b} | {x for x in segments if a < x < b})
             part = torch.zeros(len(cuts) - 1, dtype=torch.float64, device=out.device)
             self.ex.sqnorm_ranges(cuts, part)

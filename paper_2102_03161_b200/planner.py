@@ -30,8 +30,13 @@ class EpochDecision:
     cache_old_boundary: int
     cache_moved: bool
     n_messages: int
-    spans: List[Tuple[int, int]]      # active-sublayer spans per stage
+    spans: List[Tuple[int, int]]      # spans per stage, indices into the planned sequence
     param_sums: List[int]
+    # global index of the planned sequence's first sublayer: 2 * L_f when
+    # AutoPipe repartitions the active sublayers, 0 when it is off and the
+    # epoch-0 partition of the whole model is kept (runner.cpp begin_epoch:
+    # frozen layers then still occupy their stage)
+    span_base: int = 0
 
 
 class Planner:
@@ -42,6 +47,7 @@ class Planner:
         api.call("planner_create", self.scenario.h, C.byref(h))
         self.h = h
         self.layers = self._layers()
+        self.elastic = bool(self.scenario.to_json().get("features", {}).get("autopipe", True))
 
     def _layers(self) -> int:
         n, bpp = C.c_int(), C.c_int()
@@ -68,4 +74,5 @@ class Planner:
                              d.micro_batches, bool(d.plan_changed), bool(d.cache_enabled),
                              d.cache_boundary, d.cache_old_boundary, bool(d.cache_moved),
                              d.n_messages, [(d.plan.begin[i], d.plan.end[i]) for i in range(k)],
-                             [d.plan.param_sums[i] for i in range(k)])
+                             [d.plan.param_sums[i] for i in range(k)],
+                             2 * d.l_frozen if self.elastic else 0)

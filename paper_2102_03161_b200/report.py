@@ -1,0 +1,171 @@
+"""Measured report bundle.
+
+The reference *models* every epoch (runner.cpp:94-305) and writes a CSV
+(runner.cpp:340-355), a timeline (runner.cpp:357-367) and a feature ladder
+(speedup_breakdown, runner.cpp:307-338) from its cost model.  This module puts
+the *measured* B200 numbers beside the modeled ones:
+
+* `calibrate_c_fwd`: fit the cost model's forward rate `c_fwd`
+  (cost_model.hpp:12, seconds per parameter-sample) so the modeled epoch-0
+  iteration equals the measured one -- the reference's constants describe RTX
+  5000s; a calibrated scenario replays the planner with B200 costs;
+* `compare`: per-epoch modeled vs measured iteration time (same decisions);
+* `ladder`: measured rungs of the feature ladder next to the modeled ones;
+* `bundle`: writes epochs.csv (reference schema, measured), timeline.json
+  (reference schema, measured CUDA-event blocks), calibration / comparison /
+  ladder JSON.
+
+Transition overheads (8(f) row 4) are measured by Trainer.run_epoch (CUDA
+events around StageRunner.set_plan: migration + regroup + store hand-over) and
+land in the CSV's transition_overhead_s column; `transition_table` lists them
+next to the reference's Table-3 constants (runner.cpp:24-28).
+"""
+from __future__ import annotations
+
+import copy
+import json
+import math
+import os
+from typing import Callable, Dict, List, Sequence
+
+from .capi import EpsApi, Scenario
+
+# The feature-ladder rungs of runner.cpp:312-319 (freeze, autopipe, autodp, autocache).
+LADDER = [
+    ("baseline", (False, False, False, False)),
+    ("freeze", (True, False, False, False)),
+    ("autopipe", (True, True, False, False)),
+    ("autopipe+autocache", (True, True, False, True)),
+    ("autopipe+autodp", (True, True, True, False)),
+    ("all", (True, True, True, True)),
+]
+
+
+def with_features(scenario: dict, flags: Sequence[bool]) -> dict:
+    s = copy.deepcopy(scenario)
+    s["features"] = dict(zip(("freeze", "autopipe", "autodp", "autocache"), map(bool, flags)))
+    return s
+
+
+def modeled(api: EpsApi, scenario: dict):
+    """The reference's modeled run (simulate_run): per-epoch rows + summary."""
+    return Scenario(api, scenario).simulate()
+
+
+def calibrate_c_fwd(api: EpsApi, scenario: dict, measured_iteration_s: float,
+                    epoch: int = 0, iters: int = 60) -> dict:
+    """Bisect (in log space) the cost model's c_fwd so the modeled iteration
+    time of `epoch` equals `measured_iteration_s`.  The modeled time is
+    monotone in c_fwd (every F/B block scales with it; comm and per-micro-batch
+    overheads do not).  Returns {c_fwd, modeled_iteration_s, scenario}."""
+    if measured_iteration_s <= 0:
+        raise ValueError("measured iteration time must be positive")
+
+    def t_of(c):
+        s = copy.deepcopy(scenario)
+        s["cost_model"]["c_fwd"] = c
+        rows, _ = modeled(api, s)
+        return rows[epoch]["iteration_time"], s
+
+    lo, hi = 1e-18, 1e-6
+    t_lo, _ = t_of(lo)
+    if t_lo >= measured_iteration_s:  # overheads alone exceed the measurement
+        return {"c_fwd": lo, "modeled_iteration_s": t_lo, "scenario": t_of(lo)[1],
+                "note": "fixed overheads exceed the measured iteration"}
+    for _ in range(iters):
+        mid = math.sqrt(lo * hi)
+        t, _ = t_of(mid)
+        if t < measured_iteration_s:
+            lo = mid
+        else:
+            hi = mid
+    c = math.sqrt(lo * hi)
+    t, s = t_of(c)
+    return {"c_fwd": c, "modeled_iteration_s": t, "scenario": s}
+
+
+def compare(modeled_rows: List[dict], measured_rows) -> List[dict]:
+    """Epoch-by-epoch: decisions must agree; iteration times side by side."""
+    out = []
+    for m, r in zip(modeled_rows, measured_rows):
+        same = (m["l_frozen"], m["pipeline_length"], m["replica_width"], m["micro_batches"]) == (
+            r.l_frozen, r.k, r.r, r.m)
+        out.append({"epoch": r.epoch, "l_frozen": r.l_frozen, "k": r.k, "r": r.r, "m": r.m,
+                    "decisions_match": same,
+                    "modeled_iteration_s": m["iteration_time"],
+                    "measured_iteration_s": r.iteration_time_s,
+                    "measured_over_modeled": r.iteration_time_s / m["iteration_time"]
+                    if m["iteration_time"] > 0 else None,
+                    "modeled_transition_s": m["transition_overhead"],
+                    "measured_transition_s": r.transition_time_s})
+    return out
+
+
+def ladder(api: EpsApi, scenario: dict, run_rung: Callable[[dict], float],
+           rungs: Sequence[str] = ("baseline", "freeze", "all")) -> List[dict]:
+    """Measured total time of each rung (run_rung(scenario) -> seconds) with
+    speedups vs the measured baseline, beside the reference's modeled ladder."""
+    model = {name: (t, sps, sp) for name, t, sps, sp in Scenario(api, scenario).speedup_breakdown()}
+    flags = dict(LADDER)
+    out, base = [], None
+    for name in rungs:
+        t = run_rung(with_features(scenario, flags[name]))
+        base = t if name == "baseline" else base
+        out.append({"rung": name, "measured_total_s": t,
+                    "measured_speedup": (base / t) if base else None,
+                    "modeled_total_s": model[name][0], "modeled_speedup": model[name][2]})
+    return out
+
+
+def transition_table(scenario: dict, measured_rows) -> List[dict]:
+    """Measured plan-change overheads beside the scenario's Table-3 constants."""
+    consts = scenario.get("cost_model", {}).get("transition_overheads", {})
+    out, prev_k = [], None
+    for r in measured_rows:
+        if prev_k is not None and r.k != prev_k:
+            key = f"{prev_k}->{r.k}"
+            out.append({"epoch": r.epoch, "transition": key,
+                        "measured_s": r.transition_time_s, "reference_constant_s": consts.get(key)})
+        prev_k = r.k
+    return out
+
+
+def bundle(out_dir: str, api: EpsApi, scenario: dict, measured_rows, timeline: List[dict],
+           ladder_rows: List[dict] = None, extra: Dict = None) -> Dict[str, str]:
+    """Write the measured report bundle; returns {name: path}."""
+    from .trainer import Trainer  # local: trainer imports torch
+
+    os.makedirs(out_dir, exist_ok=True)
+    rows_mod, summ = modeled(api, scenario)
+    cal = calibrate_c_fwd(api, scenario, measured_rows[0].iteration_time_s)
+    rows_cal, summ_cal = modeled(api, cal["scenario"])
+    files = {}
+
+    def dump(name, obj):
+        path = os.path.join(out_dir, name)
+        with open(path, "w") as f:
+            if isinstance(obj, str):
+                f.write(obj)
+            else:
+                json.dump(obj, f, indent=1)
+        files[name] = path
+
+    dump("epochs.csv", Trainer.report_csv(measured_rows))
+    dump("timeline.json", timeline)
+    measured_total = sum(r.epoch_time_s + r.transition_time_s for r in measured_rows)
+    dump("modeled_vs_measured.json", {
+        "reference_constants": {"epochs": compare(rows_mod, measured_rows),
+                                "modeled_total_s": summ["total_seconds"],
+                                "modeled_speedup": summ["speedup"]},
+        "calibrated": {"c_fwd": cal["c_fwd"],
+                       "reference_c_fwd": scenario["cost_model"]["c_fwd"],
+                       "epochs": compare(rows_cal, measured_rows),
+                       "modeled_total_s": summ_cal["total_seconds"],
+                       "modeled_speedup": summ_cal["speedup"]},
+        "measured_total_s": measured_total,
+        "transitions": transition_table(scenario, measured_rows),
+        **(extra or {})})
+    dump("calibrated_scenario.json", cal["scenario"])
+    if ladder_rows is not None:
+        dump("ladder.json", ladder_rows)
+    return files

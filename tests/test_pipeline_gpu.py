@@ -61,6 +61,35 @@ def test_single_stage_runner_equals_train_step(cuda):
     assert abs(a.loss_sum.item() - b.loss_sum.item()) <= 1e-6 * abs(a.loss_sum.item())
 
 
+def test_freeze_only_span_equals_elastic_span(cuda):
+    """AutoPipe off: the epoch-0 partition is kept and frozen sublayers stay on
+    their stage (span (0, 2L) with L_f = 1 runs layer 0 forward-only inside
+    the span); the math equals the elastic span (2, 2L), and the frozen
+    parameters are not updated."""
+    g = GEOMETRIES[CFG]
+    params = init_params(g, seed=5)
+    x, y = _data(6, g)
+    x, y = x.cuda(), y.cuda()
+    a = VitExecutor(g, max_batch=BATCH, params=params)
+    ra = StageRunner(a, 0, 1, Transport(host_staged=True))
+    ra.set_plan(StagePlan(1, 1, 2, 1, g.layers, ((2, 2 * g.layers),)))
+    b = VitExecutor(g, max_batch=BATCH, params=params)
+    rb = StageRunner(b, 0, 1, Transport(host_staged=True))
+    plan_b = StagePlan(1, 1, 2, 1, g.layers, ((0, 2 * g.layers),))
+    assert plan_b.first_active(0) == 2 and plan_b.trainable(0)
+    rb.set_plan(plan_b)
+    p0 = b.p32.clone()
+    for r in (ra, rb):
+        r.iteration(x, y, BATCH)
+        r.step(lr=0.1)
+    torch.cuda.synchronize()
+    assert _rel(b.g32, a.g32) < 1e-5
+    assert abs(a.loss_sum.item() - b.loss_sum.item()) <= 1e-5 * abs(a.loss_sum.item())
+    lo, hi = b.param_range(0, 2)
+    assert torch.equal(b.p32[lo:hi], p0[lo:hi])  # frozen layer 0 + embedding untouched
+    assert _rel(b.p32, a.p32) < 1e-5
+
+
 PLANS = {
     # L=4 -> 8 sublayers; cut inside a layer (ATT | MLP) and between layers
     "pipe2": (StagePlan(2, 1, 2, 0, 4, ((0, 3), (3, 8))), [5]),

@@ -120,3 +120,16 @@ def test_two_rank_elastic_run(cuda, tmp_path, tier, peer):
     for x in a + b:
         if x[5] == x[5]:  # last-stage ranks report a loss
             assert 0 < x[5] < 20
+
+
+def test_measured_timeline_blocks(cuda):
+    """StageRunner.trace: the last iteration's F / B blocks in the reference's
+    timeline schema (runner.cpp:357-367), ordered and non-overlapping."""
+    scen = _tiny_scenario(epochs=1)
+    tr = Trainer(scen, configs.GEOMETRIES["tiny-vit"], iterations_per_epoch=2)
+    tr.runner.trace = []
+    tr.run(1)
+    tl = tr.runner.timeline()
+    assert [b["kind"] for b in tl] == ["F", "B"]
+    assert set(tl[0]) == {"device", "kind", "start_s", "end_s", "tag"}
+    assert 0.0 <= tl[0]["start_s"] < tl[0]["end_s"] <= tl[1]["start_s"] < tl[1]["end_s"]
