@@ -11,6 +11,7 @@ the *measured* B200 numbers beside the modeled ones:
   5000s; a calibrated scenario replays the planner with B200 costs;
 * `compare`: per-epoch modeled vs measured iteration time (same decisions);
 * `ladder`: measured rungs of the feature ladder next to the modeled ones;
+* `alpha_sweep`: the freeze-aggressiveness sweep (cli.cpp:75-135) measured;
 * `bundle`: writes epochs.csv (reference schema, measured), timeline.json
   (reference schema, measured CUDA-event blocks), calibration / comparison /
   ladder JSON.
@@ -117,6 +118,26 @@ def ladder(api: EpsApi, scenario: dict, run_rung: Callable[[dict], float],
     return out
 
 
+def alpha_sweep(api: EpsApi, scenario: dict, run_total: Callable[[dict], float],
+                alphas: Sequence[float] = (0.2, 1.0 / 3.0, 0.4, 0.5),
+                baseline_total_s: float = None) -> List[dict]:
+    """The freeze-aggressiveness sweep of cli.cpp:75-135 (Eq. 1's alpha) run on
+    the device: measured total time and speedup vs the no-freeze baseline per
+    alpha, beside the modeled speedup and the frozen-layer trajectory."""
+    base = baseline_total_s if baseline_total_s is not None else run_total(
+        with_features(scenario, dict(LADDER)["baseline"]))
+    out = []
+    for a in alphas:
+        s = copy.deepcopy(scenario)
+        s["training"]["alpha"] = a
+        rows, summ = modeled(api, s)
+        t = run_total(s)
+        out.append({"alpha": a, "frozen_trajectory": [r["l_frozen"] for r in rows],
+                    "measured_total_s": t, "measured_speedup": base / t,
+                    "modeled_speedup": summ["speedup"]})
+    return out
+
+
 def transition_table(scenario: dict, measured_rows) -> List[dict]:
     """Measured plan-change overheads beside the scenario's Table-3 constants."""
     consts = scenario.get("cost_model", {}).get("transition_overheads", {})
@@ -131,7 +152,8 @@ def transition_table(scenario: dict, measured_rows) -> List[dict]:
 
 
 def bundle(out_dir: str, api: EpsApi, scenario: dict, measured_rows, timeline: List[dict],
-           ladder_rows: List[dict] = None, extra: Dict = None) -> Dict[str, str]:
+           ladder_rows: List[dict] = None, extra: Dict = None,
+           sweep_rows: List[dict] = None) -> Dict[str, str]:
     """Write the measured report bundle; returns {name: path}."""
     from .trainer import Trainer  # local: trainer imports torch
 
@@ -168,4 +190,6 @@ def bundle(out_dir: str, api: EpsApi, scenario: dict, measured_rows, timeline: L
     dump("calibrated_scenario.json", cal["scenario"])
     if ladder_rows is not None:
         dump("ladder.json", ladder_rows)
+    if sweep_rows is not None:
+        dump("alpha_sweep.json", sweep_rows)
     return files

@@ -68,3 +68,12 @@ def test_ladder_and_bundle(tmp_path):
     assert mvm["calibrated"]["c_fwd"] > 0
     assert all(e["decisions_match"] for e in mvm["calibrated"]["epochs"])
     assert os.path.exists(files["timeline.json"])
+
+
+def test_alpha_sweep_is_monotone_in_the_model():
+    scen = configs.scenario("vit-b16", 1)
+    rows = report.alpha_sweep(API, scen, lambda s: 1.0 / (1.0 + s["training"]["alpha"]),
+                              alphas=(0.2, 0.5), baseline_total_s=1.0)
+    assert [r["alpha"] for r in rows] == [0.2, 0.5]
+    assert rows[1]["modeled_speedup"] >= rows[0]["modeled_speedup"]
+    assert sum(rows[1]["frozen_trajectory"]) >= sum(rows[0]["frozen_trajectory"])

@@ -5,8 +5,8 @@ real epoch loop with the scenario's own norm source (so every decision equals
 the modeled one), then writes gpurun_out/<tag>_report/ (copied to profiles/): epochs.csv (reference
 schema, measured), timeline.json (measured F/B blocks of the last iteration),
 modeled_vs_measured.json (reference constants and B200-calibrated c_fwd),
-calibrated_scenario.json and ladder.json (baseline / freeze / all, measured
-beside the modeled ladder).
+calibrated_scenario.json, ladder.json (baseline / freeze / all, measured
+beside the modeled ladder) and alpha_sweep.json (Eq. 1's alpha, measured).
 
     python tools/measured_report.py [tag] [iterations_per_epoch]
 """
@@ -55,10 +55,12 @@ def rung(s):
 
 
 lad = report.ladder(api, scen, rung)
-files = report.bundle(out, api, scen, rows, timeline, lad,
+sweep = report.alpha_sweep(api, scen, rung, baseline_total_s=lad[0]["measured_total_s"])
+files = report.bundle(out, api, scen, rows, timeline, lad, sweep_rows=sweep,
                       extra={"device": torch.cuda.get_device_name(),
                              "iterations_per_epoch": iters,
                              "note": "measured epochs run `iterations_per_epoch` iterations; "
                                      "per-iteration times compare directly with the model"})
 print(json.dumps({k: os.path.relpath(v) for k, v in files.items()}))
 print(json.dumps(lad))
+print(json.dumps(sweep))
