@@ -132,6 +132,31 @@ __device__ __forceinline__ void stage_bf16(uint32_t base, int lane, const float 
                  pack_bf16(v[8 * q + 6], v[8 * q + 7]));
 }
 
+// Column sums of a staged 32x32 bf16 chunk (SWIZZLE_64B rows), read back
+// column-wise: lane l sums columns 2(l%16), 2(l%16)+1 over rows 16(l/16)..+16;
+// the two row halves meet with one shuffle.  Cheaper than a register
+// transpose (16 shared loads instead of 31 shuffles + 62 selects) and sums
+// exactly the stored (rounded) values.  Result valid in lanes 0..15.
+__device__ __forceinline__ float2 staged_colsum_bf16(uint32_t base, int lane) {
+  const int p = lane & 15, h = lane >> 4;
+  const uint32_t col_off = uint32_t((p & 3) * 4);
+  const int q = p >> 2;
+  float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int r = h * 16 + i;
+    uint32_t w;
+    asm volatile("ld.shared.b32 %0, [%1];"
+                 : "=r"(w)
+                 : "r"(base + uint32_t(r * 64 + ((q ^ ((r >> 1) & 3)) << 4)) + col_off));
+    s0 += bf16_lo(w);
+    s1 += bf16_hi(w);
+  }
+  s0 += __shfl_xor_sync(0xffffffffu, s0, 16);
+  s1 += __shfl_xor_sync(0xffffffffu, s1, 16);
+  return make_float2(s0, s1);
+}
+
 __device__ __forceinline__ void stage_f32(uint32_t base, int lane, const float (&v)[32]) {
 #pragma unroll
   for (int q = 0; q < 8; ++q)
@@ -335,26 +360,31 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* my_aux_bar = aux_full + kAuxDepth * ew;
     const uint32_t aux_s = area_s + kChunkBf16;
     // TMA prefetch cursor over this warp's (tile, chunk) stream: c = part, part+2, ...
-    int pf_u = cta0, pf_c = part;
+    // Tile coordinates are decoded once per tile (integer division is a
+    // ~20-instruction sequence and lane 0 runs this once per chunk).
+    int pf_u = cta0, pf_c = part, pf_row = 0, pf_col = 0, pf_chunks = -1;
     uint32_t pf_n = 0, use_n = 0;
-    auto chunks_of = [&](int uu) {
-      const int tt = uu % tiles;
-      return min(BN / 32, (args.N - (tt % args.tiles_n) * BN + 31) / 32);
+    auto pf_decode = [&]() {
+      const int tt = pf_u % tiles;
+      const int mt = tt / args.tiles_n, nt = tt - mt * args.tiles_n;
+      pf_row = mt * kTileM + rank * kBM + quarter * 32;
+      pf_col = nt * BN;
+      pf_chunks = min(BN / 32, (args.N - pf_col + 31) / 32);
     };
     auto tma_prefetch_until = [&](uint32_t limit) {
       while (pf_n < limit) {
-        while (pf_u < units && pf_c >= chunks_of(pf_u)) {
+        if (pf_chunks < 0 && pf_u < units) pf_decode();
+        while (pf_u < units && pf_c >= pf_chunks) {
           pf_u += ncta;
           pf_c = part;
+          if (pf_u < units) pf_decode();
         }
         if (pf_u >= units) return;
-        const int tt = pf_u % tiles;
-        const int row = (tt / args.tiles_n) * kTileM + rank * kBM + quarter * 32;
-        const int col = (tt % args.tiles_n) * BN + pf_c * 32;
         const uint32_t slot = pf_n % kAuxDepth;
         fence_proxy_async_smem();
         mbar_expect_tx(&my_aux_bar[slot], kChunkBf16);
-        tma_load_2d(my_area + kChunkBf16 * (1 + slot), &map_x, &my_aux_bar[slot], col, row);
+        tma_load_2d(my_area + kChunkBf16 * (1 + slot), &map_x, &my_aux_bar[slot],
+                    pf_col + pf_c * 32, pf_row);
         ++pf_n;
         pf_c += 2;
       }
@@ -456,13 +486,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             break;
           case EPS_EPI_DGELU_BF16:
 #pragma unroll
-            for (int j = 0; j < 32; ++j)
-              v[j] = __bfloat162float(__float2bfloat16_rn(v[j] * gelu_grad_f(x[j])));
-            stage_bf16(out_s, lane, v);
+            for (int j = 0; j < 32; ++j) v[j] *= gelu_grad_f(x[j]);
+            stage_bf16(out_s, lane, v);  // bias-gradient sums read the staged values back
             break;
           case EPS_EPI_MUL_BF16:
 #pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = __bfloat162float(__float2bfloat16_rn(v[j] * x[j]));
+            for (int j = 0; j < 32; ++j) v[j] *= x[j];
             stage_bf16(out_s, lane, v);
             break;
           case EPS_EPI_ROWDOT_BF16: {
@@ -470,12 +499,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             // aux over the chunk's 32 columns; the two chunks of a 64-column
             // group come from the two warps of this lane quarter
             float dot = 0.f;
+            uint32_t pk[16];
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              v[j] = __bfloat162float(__float2bfloat16_rn(v[j]));
-              dot = fmaf(v[j], x[j], dot);
+            for (int j = 0; j < 16; ++j) {
+              pk[j] = pack_bf16(v[2 * j], v[2 * j + 1]);
+              dot = fmaf(bf16_lo(pk[j]), x[2 * j], dot);
+              dot = fmaf(bf16_hi(pk[j]), x[2 * j + 1], dot);
             }
-            stage_bf16(out_s, lane, v);
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              st_shared_v4(out_s + swz64(lane, q), pk[4 * q], pk[4 * q + 1], pk[4 * q + 2],
+                           pk[4 * q + 3]);
             if (my_row < args.M)
               atomicAdd(args.colsum + int64_t(my_row) * (args.N >> 6) + (col0 >> 6), dot);
             break;
@@ -499,8 +533,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         ++out_n;
         if ((epi == EPS_EPI_DGELU_BF16 || epi == EPS_EPI_MUL_BF16) && args.colsum != nullptr) {
           // rows past M were zero-filled by TMA (and aux zeroed), so they contribute 0
-          const float s = warp_transpose_sum32(v);
-          if (lane < valid) atomicAdd(args.colsum + col0 + lane, s);
+          const float2 cs = staged_colsum_bf16(out_s, lane);
+          if (lane < 16) {
+            if (2 * lane < valid) atomicAdd(args.colsum + col0 + 2 * lane, cs.x);
+            if (2 * lane + 1 < valid) atomicAdd(args.colsum + col0 + 2 * lane + 1, cs.y);
+          }
         }
         if (aux_in && !aux_tma) {
 #pragma unroll
@@ -510,7 +547,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
-        if constexpr (PAIR) mbar_arrive_cluster(leader_addr(&tmem_empty[acc]));
+        if constexpr (PAIR) mbar_arrive_remote(&tmem_empty[acc], 0u);
         else mbar_arrive(&tmem_empty[acc]);
       }
       acc ^= 1;

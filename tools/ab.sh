@@ -1,3 +1,4 @@
 cd $GRAFT_REPO_ROOT
-timeout 900 python -m pytest tests/test_pipeline_gpu.py tests/test_trainer_gpu.py tests/test_vit_gpu.py -x -q 2>&1 | tail -n 3
-timeout 900 python tools/measured_report.py r01e 3 > gpurun_out/mr.log 2>&1; grep -v Warn gpurun_out/mr.log | tail -n 3
+timeout 300 python -m pytest tests/test_gemm_gpu.py -x -q 2>&1 | tail -n 2
+python tools/gemm_bench.py dgrad_fc2_mul fwd_fc1_gelu2 dgrad_proj_rowdot fwd_proj fwd_fc1_store dgrad_qkv wgrad_fc2
+ncu --set full --clock-control none --import-source on -k regex:gemm_tc -s 3 -c 1 -o gpurun_out/prof_mul -f python tools/gemm_bench.py dgrad_fc2_mul > /dev/null 2>&1
