@@ -37,9 +37,16 @@ python tools/launch_summary.py gpurun_out/launches.csv
 echo
 echo "## ncu --set full"
 echo
-for f in gemm attn ln; do
+for f in gemm attn attnb ln lnb; do
   [ -f gpurun_out/prof_$f.ncu-rep ] && python tools/ncu_summary.py gpurun_out/prof_$f.ncu-rep && echo
 done
+echo "## Step timeline (CUPTI, uninstrumented step) and per-role kernel times"
+echo
+echo '```'
+grep -A16 "step span" gpurun_out/timeline.txt
+echo
+cat gpurun_out/step_breakdown.txt
+echo '```'
 } > profiles/${tag}_summary.md
 cp gpurun_out/bench.json profiles/${tag}_bench.json
 cp gpurun_out/launches.csv profiles/${tag}_launches.csv
