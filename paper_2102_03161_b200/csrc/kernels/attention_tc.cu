@@ -1027,13 +1027,20 @@ size_t bwd_fused_smem(int T) {
 }
 
 // ---------------------------------------------------------------------------
-// Persistent forward for T <= 256: one CTA per SM walks the (b, h) heads;
-// Q, K, V of a head (<= 256 rows each) are double-buffered in smem so the
-// TMA load of the next head overlaps this head's math.  Two softmax
-// warpgroups own the two 128-query tiles (S_c in TMEM columns [256c, +Tp),
-// P_c written back in place, O_c at 256c + 128), so both tiles' exp work and
-// the MMAs of the other tile proceed concurrently.
-constexpr int kFwdThreads = 64 + 8 * 32;
+// Persistent forward for T <= 256, two ping-pong pipelines per CTA.  One CTA
+// per SM walks the (b, h) heads; pipeline c (one MMA-issuer warp + one
+// softmax warpgroup + smem buffer c + TMEM context c) takes every other head
+// and runs both of its 128-query tiles in turn:
+//   S = Q_t K^T -> TMEM context c (N = Tp <= 256 columns)
+//   row max, exp2, row sum; P written back as bf16 into the S columns
+//   O = P V, a TS-form MMA (A = P from TMEM) into columns 128..191 of c
+//   O / rowsum -> bf16 -> global, lse
+// The two pipelines are decoupled, so one's MMAs and latencies overlap the
+// other's exp work (the SFU is the floor: T*Tp exp2 per head).  (The
+// previous design ran both tiles of one head in lock step, so the two
+// warpgroups waited on the same MMAs and competed for the SFU at the same
+// time.)  A single TMA warp loads head i into buffer i & 1.
+constexpr int kFwdThreads = 12 * 32;  // TMA, MMA0, MMA1, (alloc), WG0 (4-7), WG1 (8-11)
 
 __global__ void __launch_bounds__(kFwdThreads, 1)
     attn_fwd_persistent_tc_kernel(const __grid_constant__ CUtensorMap map_qkv, const Params p,
@@ -1045,17 +1052,19 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   const int Tp = p.Tp;  // S columns (pad64(T) <= 256)
   const size_t buf_bytes = size_t(3 * Tr) * kRowBytes;
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 2 * buf_bytes);
-  // 0-1 full[buf], 2-3 empty[buf], 4-5 s[c], 6-7 p[c], 8-9 o[c], 10-11 tfree[c]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 12);
+  // per pipeline c: FULL, EMPTY, SF (S ready), PF (P written), OF (O ready), TF (O read out)
+  enum { FULL = 0, EMPTY, SF, PF, OF, TF, NB };
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 2 * NB);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int HD = p.H * kD;
 
   if (threadIdx.x == 0) {
     tma_prefetch(&map_qkv);
-    for (int i = 0; i < 12; ++i) mbar_init(&bar[i], (i >= 6 && i < 8) || i >= 10 ? 4 : 1);
+    for (int c = 0; c < 2; ++c)
+      for (int i = 0; i < NB; ++i) mbar_init(&bar[c * NB + i], (i == PF || i == TF) ? 4 : 1);
     mbar_fence_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  if (warp == 3) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -1065,89 +1074,90 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     if (lane == 0) {
       int i = 0;
       for (int bh = blockIdx.x; bh < n_heads; bh += gridDim.x, ++i) {
-        const int buf = i & 1, b = bh / p.H, h = bh % p.H;
-        mbar_wait(&bar[2 + buf], ((i >> 1) & 1) ^ 1);
-        uint8_t* base = smem + buf * buf_bytes;
-        mbar_expect_tx(&bar[buf], uint32_t(3 * Tr) * kRowBytes);
-        load_rows(base, &map_qkv, &bar[buf], h * kD, 0, Tr, b);
-        load_rows(base + Tr * kRowBytes, &map_qkv, &bar[buf], HD + h * kD, 0, Tr, b);
-        load_rows(base + 2 * Tr * kRowBytes, &map_qkv, &bar[buf], 2 * HD + h * kD, 0, Tr, b);
+        const int c = i & 1, b = bh / p.H, h = bh % p.H;
+        uint64_t* pb = bar + c * NB;
+        mbar_wait(&pb[EMPTY], ((i >> 1) & 1) ^ 1);
+        uint8_t* base = smem + c * buf_bytes;
+        mbar_expect_tx(&pb[FULL], uint32_t(3 * Tr) * kRowBytes);
+        load_rows(base, &map_qkv, &pb[FULL], h * kD, 0, Tr, b);
+        load_rows(base + Tr * kRowBytes, &map_qkv, &pb[FULL], HD + h * kD, 0, Tr, b);
+        load_rows(base + 2 * Tr * kRowBytes, &map_qkv, &pb[FULL], 2 * HD + h * kD, 0, Tr, b);
       }
     }
-  } else if (warp == 1) {
-    if (lane == 0) {
-      const int nsplit = Tp > 256 ? 2 : 1;  // (Tp <= 256 here)
-      const int nc = Tp / nsplit;
-      const uint32_t idesc_s = umma_idesc_bf16(128, nc, false, false);
-      const uint32_t idesc_o = umma_idesc_bf16(128, kD, false, true);
-      int i = 0;
-      for (int bh = blockIdx.x; bh < n_heads; bh += gridDim.x, ++i) {
-        const int buf = i & 1;
-        mbar_wait(&bar[buf], (i >> 1) & 1);
-        tc_fence_after();
-        const uint32_t q_s = smem_addr(smem + buf * buf_bytes);
-        const uint32_t k_s = q_s + uint32_t(Tr * kRowBytes), v_s = k_s + uint32_t(Tr * kRowBytes);
-        for (int c = 0; c < nt; ++c) {
-          mbar_wait(&bar[10 + c], (i & 1) ^ 1);  // WG c done with last head's S/O
+  } else if (warp == 1 || warp == 2) {
+    // MMA issuer of pipeline c, warp-converged (one elected lane issues)
+    const int c = warp - 1;
+    uint64_t* pb = bar + c * NB;
+    const uint32_t tS = tmem + uint32_t(256 * c);
+    const uint32_t idesc_s = umma_idesc_bf16(128, Tp, false, false);
+    const uint32_t idesc_o = umma_idesc_bf16(128, kD, false, true);
+    int i = 0, k = 0;  // k: tiles done by this pipeline
+    for (int bh = blockIdx.x; bh < n_heads; bh += gridDim.x, ++i) {
+      if ((i & 1) != c) continue;
+      const int n = i >> 1;  // this pipeline's head count
+      mbar_wait(&pb[FULL], n & 1);
+      tc_fence_after();
+      const uint64_t q0 = umma_sdesc(smem_addr(smem + c * buf_bytes), 16, 1024);
+      const uint64_t k0 = q0 + uint64_t((Tr * kRowBytes) >> 4);
+      const uint64_t v0 = umma_sdesc(smem_addr(smem + c * buf_bytes + 2 * Tr * kRowBytes),
+                                     64 * 128, 1024);
+      for (int t = 0; t < nt; ++t, ++k) {
+        if (k > 0) {  // the warpgroup has read out the previous tile's O
+          mbar_wait(&pb[TF], (k - 1) & 1);
           tc_fence_after();
-          const uint32_t tS = tmem + uint32_t(256 * c);
-          const uint32_t qc = q_s + uint32_t(c * kTile) * kRowBytes;
-          for (int sp = 0; sp < nsplit; ++sp)
+        }
+        const uint64_t qt = q0 + uint64_t((t * kTile * kRowBytes) >> 4);
 #pragma unroll
-            for (int kk = 0; kk < kD / 16; ++kk)
-              tc_mma_bf16(tS + uint32_t(sp * nc), kdesc(qc, kk),
-                          kdesc(k_s + uint32_t(sp * nc) * kRowBytes, kk), idesc_s,
-                          kk > 0 ? 1u : 0u);
-          tc_commit(&bar[4 + c]);
-        }
-        for (int c = 0; c < nt; ++c) {
-          mbar_wait(&bar[6 + c], i & 1);
-          tc_fence_after();
-          const uint32_t tS = tmem + uint32_t(256 * c);
-          for (int kk = 0; kk < Tp / 16; ++kk)
-            tc_mma_bf16_ts(tS + 128, tS + uint32_t(kk * 8),
-                           mndesc(v_s + uint32_t(kk * 16) * kRowBytes), idesc_o, kk > 0 ? 1u : 0u);
-          tc_commit(&bar[8 + c]);
-        }
-        tc_commit(&bar[2 + buf]);  // smem buffer free once every MMA above is done
+        for (int kk = 0; kk < kD / 16; ++kk)
+          tc_mma_ss_ws(tS, qt + uint64_t(2 * kk), k0 + uint64_t(2 * kk), idesc_s, kk > 0 ? 1u : 0u);
+        tc_commit_ws(&pb[SF]);
+        mbar_wait(&pb[PF], k & 1);
+        tc_fence_after();
+        for (int kk = 0; kk < Tp / 16; ++kk)
+          tc_mma_ts_ws(tS + 128, tS + uint32_t(kk * 8), v0 + uint64_t(kk * 128), idesc_o,
+                       kk > 0 ? 1u : 0u);
+        tc_commit_ws(&pb[OF]);
       }
+      tc_commit_ws(&pb[EMPTY]);  // smem buffer free once this head's MMAs are done
     }
-  } else {
-    const int wg = (warp - 2) >> 2;  // query tile of this warpgroup
+  } else if (warp >= 4) {
+    const int c = (warp - 4) >> 2;  // pipeline of this warpgroup
+    uint64_t* pb = bar + c * NB;
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;
     const uint32_t lane_off = uint32_t(quarter * 32) << 16;
-    const uint32_t tS = tmem + uint32_t(256 * wg) + lane_off;
-    if (wg < nt) {
-      int i = 0;
-      const int nch = (p.T + 31) / 32;  // S chunks holding valid keys
-      for (int bh = blockIdx.x; bh < n_heads; bh += gridDim.x, ++i) {
-        const int b = bh / p.H, h = bh % p.H;
-        const int q = wg * kTile + row;
-        mbar_wait(&bar[4 + wg], i & 1);
+    const uint32_t tS = tmem + uint32_t(256 * c) + lane_off;
+    const int nch = (p.T + 31) / 32;  // S chunks holding valid keys
+    const float sl2 = p.scale_log2;
+    int i = 0, k = 0;
+    for (int bh = blockIdx.x; bh < n_heads; bh += gridDim.x, ++i) {
+      if ((i & 1) != c) continue;
+      const int b = bh / p.H, h = bh % p.H;
+      for (int t = 0; t < nt; ++t, ++k) {
+        const int q = t * kTile + row;
+        mbar_wait(&pb[SF], k & 1);
         tc_fence_after();
         float m = -FLT_MAX;
-        for (int c = 0; c < nch; ++c) {
+        for (int ch = 0; ch < nch; ++ch) {
           uint32_t r[32];
-          tmem_ld_32x32(tS + uint32_t(c * 32), r);
+          tmem_ld_32x32(tS + uint32_t(ch * 32), r);
           tmem_ld_wait();
-          if (c * 32 + 32 <= p.T) {
+          if (ch * 32 + 32 <= p.T) {
 #pragma unroll
             for (int j = 0; j < 32; ++j) m = fmaxf(m, __uint_as_float(r[j]));
           } else {
 #pragma unroll
             for (int j = 0; j < 32; ++j)
-              if (c * 32 + j < p.T) m = fmaxf(m, __uint_as_float(r[j]));
+              if (ch * 32 + j < p.T) m = fmaxf(m, __uint_as_float(r[j]));
           }
         }
-        const float sl2 = p.scale_log2;
         const float ms = m * sl2;
         float sum = 0.f;
-        for (int c = 0; c < Tp / 32; ++c) {
+        for (int ch = 0; ch < Tp / 32; ++ch) {
           uint32_t pk[16];
-          if (c * 32 + 32 <= p.T) {  // full chunk: no key mask
+          if (ch * 32 + 32 <= p.T) {  // full chunk: no key mask
             uint32_t r[32];
-            tmem_ld_32x32(tS + uint32_t(c * 32), r);
+            tmem_ld_32x32(tS + uint32_t(ch * 32), r);
             tmem_ld_wait();
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
@@ -1156,16 +1166,16 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
               sum += e0 + e1;
               pk[j] = pack_bf16(e0, e1);
             }
-          } else if (c < nch) {
+          } else if (ch < nch) {
             uint32_t r[32];
-            tmem_ld_32x32(tS + uint32_t(c * 32), r);
+            tmem_ld_32x32(tS + uint32_t(ch * 32), r);
             tmem_ld_wait();
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
-              const int k = c * 32 + 2 * j;
-              const float e0 = k < p.T ? fast_exp2(fmaf(__uint_as_float(r[2 * j]), sl2, -ms)) : 0.f;
+              const int kk = ch * 32 + 2 * j;
+              const float e0 = kk < p.T ? fast_exp2(fmaf(__uint_as_float(r[2 * j]), sl2, -ms)) : 0.f;
               const float e1 =
-                  k + 1 < p.T ? fast_exp2(fmaf(__uint_as_float(r[2 * j + 1]), sl2, -ms)) : 0.f;
+                  kk + 1 < p.T ? fast_exp2(fmaf(__uint_as_float(r[2 * j + 1]), sl2, -ms)) : 0.f;
               sum += e0 + e1;
               pk[j] = pack_bf16(e0, e1);
             }
@@ -1173,20 +1183,20 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 #pragma unroll
             for (int j = 0; j < 16; ++j) pk[j] = 0u;  // keys past T: P = 0
           }
-          tmem_st_32x32_x16(tS + uint32_t(c * 16), pk);
+          tmem_st_32x32_x16(tS + uint32_t(ch * 16), pk);
         }
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&bar[6 + wg]);
+        if (lane == 0) mbar_arrive(&pb[PF]);
         if (q < p.T) p.lse[int64_t(bh) * p.T + q] = (ms + __log2f(sum)) * kLn2;
-        mbar_wait(&bar[8 + wg], i & 1);
+        mbar_wait(&pb[OF], k & 1);
         tc_fence_after();
         float o[64];
         load_tmem_row64(tS + 128, o);
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&bar[10 + wg]);
+        if (lane == 0) mbar_arrive(&pb[TF]);
         if (q < p.T) {
           const float inv = 1.f / sum;
 #pragma unroll
@@ -1198,7 +1208,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) {
+  if (warp == 3) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
@@ -1206,7 +1216,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 
 size_t fwd_persistent_smem(int T) {
   const int Tr = (T + kTile - 1) / kTile * kTile;
-  return 2 * size_t(3 * Tr) * kRowBytes + 1024 + 128;
+  return 2 * size_t(3 * Tr) * kRowBytes + 1024 + 256;
 }
 
 size_t fwd_smem(int Tp) { return size_t(kTile + 2 * Tp) * kRowBytes + 1024 + 64; }
