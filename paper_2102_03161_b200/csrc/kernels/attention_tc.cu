@@ -792,6 +792,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             tc_mma_ts_ws(tdV, tS + pcol, oc + uint64_t(kk * 128), idesc_km, acc);
             tc_mma_ts_ws(tdK, tdP + pcol, qc + uint64_t(kk * 128), idesc_km, acc);
           }
+          // P^T / dS^T in this TMEM buffer are consumed: release it to the S
+          // issuer before the dQ MMAs (they read dS from the smem staging)
+          tc_commit_ws(&bar[AC0 + bsel]);
+          if (c == NC - 1) tc_commit_ws(&bar[KVF]);
           if (c & 1) {  // both halves of 128-query tile c/2 staged: dQ_t += dS_t K_j
             const int t = c >> 1;
             if (j == 0 && t == 0 && hi > 0) {
@@ -805,12 +809,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
               tc_mma_ss_ws(tdQ + uint32_t(t * kD), stg + uint64_t(kk * 128), kj + uint64_t(kk * 128),
                            idesc_mm, (j > 0 || kk > 0) ? 1u : 0u);
           }
-          tc_commit_ws(&bar[AC0 + bsel]);
           EPS_TRACE(it < 64 && lane == 0, it * 8 + 2);
-          if (c == NC - 1) {
-            tc_commit_ws(&bar[KVF]);
-            ++kt;
-          }
+          if (c == NC - 1) ++kt;
         }
         tc_commit_ws(&bar[DQF]);
         tc_commit_ws(&bar[EMPTY]);
