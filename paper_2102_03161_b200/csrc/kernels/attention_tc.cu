@@ -637,10 +637,21 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   float2* sLD = reinterpret_cast<float2*>(sStage + kDsChunk);  // [2][Tr] (-lse2, D)
   float* sRed = reinterpret_cast<float*>(sLD + 2 * Tr);  // [64] bias column sums of a head
   uint64_t* bar = reinterpret_cast<uint64_t*>(sRed + 64);
-  enum { FULL = 0, EMPTY, SF0, SF1, PF0, PF1, AC0, AC1, KVF, KVE, DQF, DQE, LF0, LF1, LE0, LE1, NBAR };
+  // Operand regions, each with its own full / empty barrier pair so a head's
+  // tiles are reloaded as soon as their last reader is done: KV_j = rows of
+  // key tile j of K and V; QO_t = rows of query tile t of Q and dO.
+  //   region r: 0 = KV0, 1 = KV1, 2 = QO0, 3 = QO1   (FR + r, ER + r)
+  enum { FR = 0, ER = 4, SF0 = 8, SF1, PF0, PF1, AC0, AC1, KVF, KVE, DQF, DQE, LF0, LF1, LE0, LE1,
+         NBAR };
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + NBAR);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int HD = p.H * kD;
+  // last iteration of a head that reads region r: KV_j is read by S (key
+  // tile j) and by the dQ MMAs of its odd chunks; QO_t by the S and post MMAs
+  // of chunks 2t, 2t+1 of the last key tile
+  auto last_use = [](int r) {
+    return r < 2 ? r * NC + NC - 1 : (NT - 1) * NC + 2 * (r - 2) + 1;
+  };
 
   if (threadIdx.x == 0) {
     tma_prefetch(&map_qkv);
@@ -652,7 +663,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       if (i == KVE || i == DQE) cnt = kBwdEpiWarps;
       if (i == LF0 || i == LF1) cnt = 32 * kBwdEpiWarps;
       if (i == LE0 || i == LE1) cnt = 32 * kBwdExpWarps;
-      if (i == EMPTY) cnt = 2;  // MMA warp's commit + the epilogue's dO-sum
+      if (i == ER + 2 || i == ER + 3) cnt = 2;  // post issuer's commit + the TMA warp's dO sums
       mbar_init(&bar[i], cnt);
     }
     mbar_fence_init();
@@ -669,13 +680,28 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     int hi = 0;
     for (int bh = blockIdx.x; bh < n_heads; bh += gridDim.x, ++hi) {
       const int b = bh / p.H, h = bh % p.H;
-      mbar_wait(&bar[EMPTY], (hi & 1) ^ 1);
+      // regions in the order the previous head releases them: KV0, QO0, KV1, QO1
+      const int order[4] = {0, 2, 1, 3};
+      for (int oi = 0; oi < 2 * NT; ++oi) {
+        const int r = order[oi];  // NT == 1: KV0, QO0
+        const int t = r & 1;  // key tile (KV) or query tile (QO)
+        mbar_wait(&bar[ER + r], (hi & 1) ^ 1);
+        if (lane == 0) {
+          mbar_expect_tx(&bar[FR + r], uint32_t(2 * kTile * kRowBytes));
+          if (r < 2) {
+            load_rows(sK + t * kTile * kRowBytes, &map_qkv, &bar[FR + r], HD + h * kD, t * kTile,
+                      kTile, b);
+            load_rows(sV + t * kTile * kRowBytes, &map_qkv, &bar[FR + r], 2 * HD + h * kD,
+                      t * kTile, kTile, b);
+          } else {
+            load_rows(sQ + t * kTile * kRowBytes, &map_qkv, &bar[FR + r], h * kD, t * kTile,
+                      kTile, b);
+            load_rows(sO + t * kTile * kRowBytes, &map_do, &bar[FR + r], h * kD, t * kTile, kTile,
+                      b);
+          }
+        }
+      }
       if (lane == 0) {
-        mbar_expect_tx(&bar[FULL], uint32_t(4 * Tr) * kRowBytes);
-        load_rows(sQ, &map_qkv, &bar[FULL], h * kD, 0, Tr, b);
-        load_rows(sO, &map_do, &bar[FULL], h * kD, 0, Tr, b);
-        load_rows(sK, &map_qkv, &bar[FULL], HD + h * kD, 0, Tr, b);
-        load_rows(sV, &map_qkv, &bar[FULL], 2 * HD + h * kD, 0, Tr, b);
         // warm L2 with the next head's tiles
         const int nb = bh + gridDim.x;
         if (nb < n_heads) {
@@ -691,36 +717,38 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       }
       __syncwarp();
       // V bias gradient = sum_q dO[q, :] of the head (rows of P sum to one),
-      // from the dO tile in smem by this warp's 32 lanes; then the tiles may
-      // be overwritten (EMPTY has two arrivals: the MMA warp's commit and
-      // this one).  The K bias gradient is exactly zero (softmax is
-      // shift-invariant per query), so no K column sums are formed.
-      if (p.dbias != nullptr) {
-        mbar_wait(&bar[FULL], hi & 1);
-        const int g = lane & 7, rs = lane >> 3;  // 16-byte column group, 64-row set
-        float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-        const uint32_t o_s = smem_addr(sO);
+      // from the dO tiles in smem by this warp's 32 lanes; the QO regions are
+      // released by two arrivals (the post issuer's commit and this one).
+      // The K bias gradient is exactly zero (softmax is shift-invariant per
+      // query), so no K column sums are formed.
+      float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      const int g = lane & 7, rs = lane >> 3;  // 16-byte column group, row set
+      for (int t = 0; t < NT; ++t) {
+        mbar_wait(&bar[FR + 2 + t], hi & 1);
+        if (p.dbias != nullptr) {
+          const uint32_t o_s = smem_addr(sO);
 #pragma unroll 4
-        for (int r = rs * (Tr / 4); r < (rs + 1) * (Tr / 4); ++r) {
-          const uint4 w = ld_shared_v4(o_s + swz128(r, g));
-          acc[0] += bf16_lo(w.x), acc[1] += bf16_hi(w.x), acc[2] += bf16_lo(w.y);
-          acc[3] += bf16_hi(w.y), acc[4] += bf16_lo(w.z), acc[5] += bf16_hi(w.z);
-          acc[6] += bf16_lo(w.w), acc[7] += bf16_hi(w.w);
+          for (int r = t * kTile + rs * 32; r < t * kTile + rs * 32 + 32; ++r) {
+            const uint4 w = ld_shared_v4(o_s + swz128(r, g));
+            acc[0] += bf16_lo(w.x), acc[1] += bf16_hi(w.x), acc[2] += bf16_lo(w.y);
+            acc[3] += bf16_hi(w.y), acc[4] += bf16_lo(w.z), acc[5] += bf16_hi(w.z);
+            acc[6] += bf16_lo(w.w), acc[7] += bf16_hi(w.w);
+          }
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&bar[EMPTY]);
+        if (lane == 0) mbar_arrive(&bar[ER + 2 + t]);
+      }
+      if (p.dbias != nullptr) {
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], 8);
           acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], 16);
         }
         if (lane < 8) {
-          float* dst = p.dbias + 2 * HD + (bh % p.H) * kD + g * 8;
+          float* dst = p.dbias + 2 * HD + h * kD + g * 8;
 #pragma unroll
           for (int i = 0; i < 8; ++i) atomicAdd(dst + i, acc[i]);
         }
-      } else if (lane == 0) {
-        mbar_arrive(&bar[EMPTY]);
       }
       __syncwarp();
     }
@@ -744,15 +772,15 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       int hi = 0;
       for (int bh = blockIdx.x; bh < n_heads; bh += gridDim.x, ++hi) {
         const int it0 = hi * NIT;
-        mbar_wait(&bar[FULL], hi & 1);
-        tc_fence_after();
-        EPS_TRACE(hi < 16 && lane == 0, 640 + hi * 4 + 2);
         for (int k = 0; k < NIT; ++k) {
           const int it = it0 + k, bsel = k & 1, j = k >> LNC, c = k & (NC - 1);
+          mbar_wait(&bar[FR + j], hi & 1);             // K_j, V_j of this head
+          mbar_wait(&bar[FR + 2 + (c >> 1)], hi & 1);  // Q, dO rows of chunk c
+          if (k == 0) EPS_TRACE(hi < 16 && lane == 0, 640 + hi * 4 + 2);
           if (it >= 2) {  // post(it - 2) finished reading this S^T / dP^T buffer
             mbar_wait(&bar[AC0 + bsel], ((it >> 1) - 1) & 1);
-            tc_fence_after();
           }
+          tc_fence_after();
           const uint32_t tS = tmem + uint32_t(bsel * 128), tdP = tS + 64;
           const uint64_t kj = dK0 + uint64_t(j * kTile * 8), vj = dV0 + uint64_t(j * kTile * 8);
           const uint64_t qc = dQ0 + uint64_t(c * kChunk * 8), oc = dO0 + uint64_t(c * kChunk * 8);
@@ -811,9 +839,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           }
           EPS_TRACE(it < 64 && lane == 0, it * 8 + 2);
           if (c == NC - 1) ++kt;
+          // operand regions whose last reader this was (tracks the dQ MMAs too)
+#pragma unroll
+          for (int r = 0; r < 4; ++r)
+            if ((r & 1) < NT && last_use(r) == k) tc_commit_ws(&bar[ER + r]);
         }
         tc_commit_ws(&bar[DQF]);
-        tc_commit_ws(&bar[EMPTY]);
       }
     }
   } else if (warp < 2 + kBwdExpWarps) {
