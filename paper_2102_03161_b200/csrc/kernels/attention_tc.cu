@@ -565,6 +565,14 @@ __device__ long long g_attn_trace[1024];
 // is shifts and masks.
 constexpr int kDsChunk = kTile * kRowBytes;  // [128 keys][64 queries] bf16 = 16 KB
 constexpr int kBwdExpWarps = 8, kBwdEpiWarps = 4;
+// queries of a 64-query chunk per exp warp (4 warps per TMEM lane quarter)
+constexpr int kBwdQPW = kChunk / (kBwdExpWarps / 4);
+constexpr int kBwdPasses = kBwdQPW / 16;  // 16-query passes per warp
+// TMEM column (within an S^T / dP^T buffer) of the packed bf16 P^T / dS^T of
+// 16-query slice g: inside the columns of the warp that owns the slice
+__host__ __device__ constexpr int pk_col(int g) {
+  return (g / kBwdPasses) * kBwdQPW + (g % kBwdPasses) * 8;
+}
 constexpr int kBwdPostWarp = 2 + kBwdExpWarps + kBwdEpiWarps;  // second MMA issuer
 constexpr int kBwdThreads = 32 * (kBwdPostWarp + 1);
 
@@ -815,8 +823,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 #pragma unroll
           for (int kk = 0; kk < kChunk / 16; ++kk) {
             const uint32_t acc = (c > 0 || kk > 0) ? 1u : 0u;
-            // 16-query slice kk sits at column 32*(kk/2) + 8*(kk%2) (see the exp loop)
-            const uint32_t pcol = uint32_t(32 * (kk >> 1) + 8 * (kk & 1));
+            const uint32_t pcol = uint32_t(pk_col(kk));  // see the exp loop
             tc_mma_ts_ws(tdV, tS + pcol, oc + uint64_t(kk * 128), idesc_km, acc);
             tc_mma_ts_ws(tdK, tdP + pcol, qc + uint64_t(kk * 128), idesc_km, acc);
           }
@@ -849,7 +856,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     }
   } else if (warp < 2 + kBwdExpWarps) {
     // ---- exp / dS warps --------------------------------------------------
-    const int half = (warp - 2) >> 2;  // which 32 of the chunk's 64 queries
+    // 4 warps per TMEM lane quarter; warp `sub` of a quarter owns queries
+    // [sub*QPW, +QPW) of each 64-query chunk and S^T / dP^T columns of the
+    // same range, and writes its packed bf16 P^T / dS^T inside that range
+    // (already read), so warps never wait on each other; the MMAs address
+    // the pieces (pk_col).
+    const int sub = (warp - 2) >> 2;
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;
     const float sl2 = p.scale_log2;
@@ -863,7 +875,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       for (int k = 0; k < NIT; ++k) {
         const int it = hi * NIT + k, bsel = k & 1, j = k >> LNC, c = k & (NC - 1);
         const int kbase = j * kTile + quarter * 32;  // this warp's 32 keys
-        const int q0 = c * kChunk + half * 32;
+        const int q0 = c * kChunk + sub * kBwdQPW;
         mbar_wait(&bar[SF0 + bsel], (it >> 1) & 1);
         tc_fence_after();
         EPS_TRACE(it < 64 && warp == 2 && lane == 0, it * 8 + 3);
@@ -879,28 +891,26 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         if (kbase >= p.T) {
           const uint32_t z[8] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
 #pragma unroll
-          for (int hh = 0; hh < 2; ++hh) {
-            tmem_st_32x32_x8(tS + uint32_t(half * 32 + hh * 8), z);
-            tmem_st_32x32_x8(tdP + uint32_t(half * 32 + hh * 8), z);
+          for (int hh = 0; hh < kBwdPasses; ++hh) {
+            tmem_st_32x32_x8(tS + uint32_t(pk_col(sub * kBwdPasses + hh)), z);
+            tmem_st_32x32_x8(tdP + uint32_t(pk_col(sub * kBwdPasses + hh)), z);
 #pragma unroll
             for (int v = 0; v < 2; ++v)
-              st_shared_v4(chunk + uint32_t(swz128(row & 7, half * 4 + hh * 2 + v)), 0u, 0u, 0u, 0u);
+              st_shared_v4(chunk + uint32_t(swz128(row & 7, (sub * kBwdQPW + hh * 16) / 8 + v)),
+                           0u, 0u, 0u, 0u);
           }
         } else {
           const bool mixed = kbase + 32 > p.T;
           const bool kvalid = kbase + lane < p.T;
-          // The bf16 P^T / dS^T of this warp's 32 queries stay inside its own
-          // 32 S^T / dP^T columns (pass hh writes columns 32*half + 8*hh,
-          // already read), so the two warps sharing a lane quarter never wait
-          // on each other; the MMAs address the pieces.
-          uint32_t sv[2][16], dp[2][16];
-          tmem_ld_32x32_x16(tS + uint32_t(half * 32), sv[0]);
-          tmem_ld_32x32_x16(tdP + uint32_t(half * 32), dp[0]);
-          tmem_ld_32x32_x16(tS + uint32_t(half * 32 + 16), sv[1]);
-          tmem_ld_32x32_x16(tdP + uint32_t(half * 32 + 16), dp[1]);
+          uint32_t sv[kBwdPasses][16], dp[kBwdPasses][16];
+#pragma unroll
+          for (int hh = 0; hh < kBwdPasses; ++hh) {
+            tmem_ld_32x32_x16(tS + uint32_t(sub * kBwdQPW + hh * 16), sv[hh]);
+            tmem_ld_32x32_x16(tdP + uint32_t(sub * kBwdQPW + hh * 16), dp[hh]);
+          }
           tmem_ld_wait();
 #pragma unroll
-          for (int hh = 0; hh < 2; ++hh) {
+          for (int hh = 0; hh < kBwdPasses; ++hh) {
             const uint32_t l4 = ld + uint32_t(q0 + hh * 16) * 8u;
             uint32_t pp[8], pd[8];
 #pragma unroll
@@ -918,12 +928,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
               pd[jj] = pack_bf16(p0 * (__uint_as_float(dp[hh][2 * jj]) - a.y),
                                  p1 * (__uint_as_float(dp[hh][2 * jj + 1]) - a.w));
             }
-            tmem_st_32x32_x8(tS + uint32_t(half * 32 + hh * 8), pp);
-            tmem_st_32x32_x8(tdP + uint32_t(half * 32 + hh * 8), pd);
+            tmem_st_32x32_x8(tS + uint32_t(pk_col(sub * kBwdPasses + hh)), pp);
+            tmem_st_32x32_x8(tdP + uint32_t(pk_col(sub * kBwdPasses + hh)), pd);
 #pragma unroll
             for (int v = 0; v < 2; ++v)
-              st_shared_v4(chunk + uint32_t(swz128(row & 7, half * 4 + hh * 2 + v)), pd[4 * v],
-                           pd[4 * v + 1], pd[4 * v + 2], pd[4 * v + 3]);
+              st_shared_v4(chunk + uint32_t(swz128(row & 7, (sub * kBwdQPW + hh * 16) / 8 + v)),
+                           pd[4 * v], pd[4 * v + 1], pd[4 * v + 2], pd[4 * v + 3]);
           }
         }
         fence_proxy_async_smem();
@@ -946,7 +956,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     auto fill_table = [&](int bh, int hi) {
       const int lb = hi & 1, b = bh / p.H, h = bh % p.H;
       if (hi >= 2) mbar_wait(&bar[LE0 + lb], ((hi >> 1) - 1) & 1);
-      EPS_TRACE(hi < 16 && warp == 10 && lane == 0, 704 + hi * 2);
+      EPS_TRACE(hi < 16 && warp == 2 + kBwdExpWarps && lane == 0, 704 + hi * 2);
 #pragma unroll
       for (int r = 0; r < Tr / 128; ++r) {
         const int q = te + 128 * r;
@@ -958,7 +968,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         sLD[lb * Tr + q] = e;
       }
       mbar_arrive(&bar[LF0 + lb]);
-      EPS_TRACE(hi < 16 && warp == 10 && lane == 0, 704 + hi * 2 + 1);
+      EPS_TRACE(hi < 16 && warp == 2 + kBwdExpWarps && lane == 0, 704 + hi * 2 + 1);
     };
     // Tiles leave through a swizzled 16 KB staging buffer and TMA stores
     // (coalesced, asynchronous); `te == 0` owns the bulk groups.
@@ -987,31 +997,31 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       for (int j = 0; j < NT; ++j, ++kt) {
         mbar_wait(&bar[KVF], kt & 1);
         tc_fence_after();
-        EPS_TRACE(kt < 64 && warp == 10 && lane == 0, 512 + kt * 2);
+        EPS_TRACE(kt < 64 && warp == 2 + kBwdExpWarps && lane == 0, 512 + kt * 2);
         uint32_t pv[32], pk[32];
         load_tmem_packed64(tdV + lane_off, 1.f, pv);
         load_tmem_packed64(tdK + lane_off, p.scale, pk);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&bar[KVE]);
-        EPS_TRACE(kt < 64 && warp == 10 && lane == 0, 512 + kt * 2 + 1);
+        EPS_TRACE(kt < 64 && warp == 2 + kBwdExpWarps && lane == 0, 512 + kt * 2 + 1);
         store_tile(pv, 2 * HD + h * kD, j * kTile, b);
         store_tile(pk, HD + h * kD, j * kTile, b);
-        EPS_TRACE(hi < 16 && j == 0 && warp == 10 && lane == 0, 760 + hi * 4 + 2);
+        EPS_TRACE(hi < 16 && j == 0 && warp == 2 + kBwdExpWarps && lane == 0, 760 + hi * 4 + 2);
         // the next head's table, off the key-tile hand-off path (its exp work
         // starts only after this head's remaining iterations)
         if (j == 0 && bh + int(gridDim.x) < n_heads) fill_table(bh + gridDim.x, hi + 1);
       }
       mbar_wait(&bar[DQF], hi & 1);
       tc_fence_after();
-      EPS_TRACE(hi < 16 && warp == 10 && lane == 0, 640 + hi * 4);
+      EPS_TRACE(hi < 16 && warp == 2 + kBwdExpWarps && lane == 0, 640 + hi * 4);
       uint32_t pq[NT][32];
 #pragma unroll
       for (int t = 0; t < NT; ++t) load_tmem_packed64(tdQ + uint32_t(t * kD) + lane_off, p.scale, pq[t]);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bar[DQE]);
-      EPS_TRACE(hi < 16 && warp == 10 && lane == 0, 640 + hi * 4 + 1);
+      EPS_TRACE(hi < 16 && warp == 2 + kBwdExpWarps && lane == 0, 640 + hi * 4 + 1);
 #pragma unroll
       for (int t = 0; t < NT; ++t) {
         if (t * kTile + row >= p.T) zero32(pq[t]);
@@ -1040,7 +1050,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         }
         epi_sync();
       }
-      EPS_TRACE(hi < 16 && warp == 10 && lane == 0, 760 + hi * 4);
+      EPS_TRACE(hi < 16 && warp == 2 + kBwdExpWarps && lane == 0, 760 + hi * 4);
     }
     if (te == 0) bulk_wait<0>();
   }
