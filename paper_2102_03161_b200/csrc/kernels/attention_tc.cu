@@ -913,6 +913,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           for (int hh = 0; hh < kBwdPasses; ++hh) {
             const uint32_t l4 = ld + uint32_t(q0 + hh * 16) * 8u;
             uint32_t pp[8], pd[8];
+            if (q0 + hh * 16 >= p.T) {
+              // 16 query columns wholly past T (up to 23 % of a ViT head's
+              // columns): their dO rows are zero, so P^T = dS^T = 0 is exact
+              // and the exps are skipped
+#pragma unroll
+              for (int jj = 0; jj < 8; ++jj) pp[jj] = pd[jj] = 0u;
+            } else {
 #pragma unroll
             for (int jj = 0; jj < 8; ++jj) {
               const uint4 w = ld_shared_v4(l4 + 16u * jj);  // (-lse2, D) of queries 2jj, 2jj+1
@@ -927,6 +934,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
               pp[jj] = pack_bf16(p0, p1);
               pd[jj] = pack_bf16(p0 * (__uint_as_float(dp[hh][2 * jj]) - a.y),
                                  p1 * (__uint_as_float(dp[hh][2 * jj + 1]) - a.w));
+            }
             }
             tmem_st_32x32_x8(tS + uint32_t(pk_col(sub * kBwdPasses + hh)), pp);
             tmem_st_32x32_x8(tdP + uint32_t(pk_col(sub * kBwdPasses + hh)), pd);
@@ -1093,8 +1101,11 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   const int Tp = p.Tp;  // S columns (pad64(T) <= 256)
   const size_t buf_bytes = size_t(3 * Tr) * kRowBytes;
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 2 * buf_bytes);
-  // per pipeline c: FULL, EMPTY, SF (S ready), PF (P written), OF (O ready), TF (O read out)
-  enum { FULL = 0, EMPTY, SF, PF, OF, TF, NB };
+  // per pipeline c: full / empty of the operand regions Q_0, Q_1, K, V (so the
+  // next head's Q_0 loads once S(tile 0) is done, K and Q_1 after S(tile 1),
+  // V after the last PV), SF (S ready), PF (P written), OF (O ready), TF (O
+  // read out)
+  enum { FQ0 = 0, FQ1, FK, FV, EQ0, EQ1, EK, EV, SF, PF, OF, TF, NB };
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 2 * NB);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int HD = p.H * kD;
@@ -1111,18 +1122,32 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0) {
+  if (warp == 0 || warp == 3) {
+    // TMA producer of pipeline c (warp 0: c = 0, warp 3: c = 1), region by
+    // region in the order the previous head of the pipeline releases them
+    const int c = warp == 0 ? 0 : 1;
+    uint64_t* pb = bar + c * NB;
+    uint8_t* base = smem + c * buf_bytes;
     if (lane == 0) {
       int i = 0;
       for (int bh = blockIdx.x; bh < n_heads; bh += gridDim.x, ++i) {
-        const int c = i & 1, b = bh / p.H, h = bh % p.H;
-        uint64_t* pb = bar + c * NB;
-        mbar_wait(&pb[EMPTY], ((i >> 1) & 1) ^ 1);
-        uint8_t* base = smem + c * buf_bytes;
-        mbar_expect_tx(&pb[FULL], uint32_t(3 * Tr) * kRowBytes);
-        load_rows(base, &map_qkv, &pb[FULL], h * kD, 0, Tr, b);
-        load_rows(base + Tr * kRowBytes, &map_qkv, &pb[FULL], HD + h * kD, 0, Tr, b);
-        load_rows(base + 2 * Tr * kRowBytes, &map_qkv, &pb[FULL], 2 * HD + h * kD, 0, Tr, b);
+        if ((i & 1) != c) continue;
+        const int b = bh / p.H, h = bh % p.H;
+        const uint32_t par = ((i >> 1) & 1) ^ 1;
+        for (int t = 0; t < nt; ++t) {
+          mbar_wait(&pb[EQ0 + t], par);
+          mbar_expect_tx(&pb[FQ0 + t], uint32_t(kTile * kRowBytes));
+          load_rows(base + t * kTile * kRowBytes, &map_qkv, &pb[FQ0 + t], h * kD, t * kTile,
+                    kTile, b);
+          if (t == 0) {
+            mbar_wait(&pb[EK], par);
+            mbar_expect_tx(&pb[FK], uint32_t(Tr * kRowBytes));
+            load_rows(base + Tr * kRowBytes, &map_qkv, &pb[FK], HD + h * kD, 0, Tr, b);
+          }
+        }
+        mbar_wait(&pb[EV], par);
+        mbar_expect_tx(&pb[FV], uint32_t(Tr * kRowBytes));
+        load_rows(base + 2 * Tr * kRowBytes, &map_qkv, &pb[FV], 2 * HD + h * kD, 0, Tr, b);
       }
     }
   } else if (warp == 1 || warp == 2) {
@@ -1136,30 +1161,33 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     for (int bh = blockIdx.x; bh < n_heads; bh += gridDim.x, ++i) {
       if ((i & 1) != c) continue;
       const int n = i >> 1;  // this pipeline's head count
-      mbar_wait(&pb[FULL], n & 1);
-      tc_fence_after();
       const uint64_t q0 = umma_sdesc(smem_addr(smem + c * buf_bytes), 16, 1024);
       const uint64_t k0 = q0 + uint64_t((Tr * kRowBytes) >> 4);
       const uint64_t v0 = umma_sdesc(smem_addr(smem + c * buf_bytes + 2 * Tr * kRowBytes),
                                      64 * 128, 1024);
       for (int t = 0; t < nt; ++t, ++k) {
-        if (k > 0) {  // the warpgroup has read out the previous tile's O
+        if (k > 0)  // the warpgroup has read out the previous tile's O
           mbar_wait(&pb[TF], (k - 1) & 1);
-          tc_fence_after();
-        }
+        mbar_wait(&pb[FQ0 + t], n & 1);
+        mbar_wait(&pb[FK], n & 1);
+        tc_fence_after();
         const uint64_t qt = q0 + uint64_t((t * kTile * kRowBytes) >> 4);
 #pragma unroll
         for (int kk = 0; kk < kD / 16; ++kk)
           tc_mma_ss_ws(tS, qt + uint64_t(2 * kk), k0 + uint64_t(2 * kk), idesc_s, kk > 0 ? 1u : 0u);
         tc_commit_ws(&pb[SF]);
+        tc_commit_ws(&pb[EQ0 + t]);             // Q_t read
+        if (t == nt - 1) tc_commit_ws(&pb[EK]);  // K read by the last S
+        EPS_TRACE(c == 0 && k < 32 && lane == 0, 832 + k * 5);
         mbar_wait(&pb[PF], k & 1);
+        if (t == 0) mbar_wait(&pb[FV], n & 1);
         tc_fence_after();
         for (int kk = 0; kk < Tp / 16; ++kk)
           tc_mma_ts_ws(tS + 128, tS + uint32_t(kk * 8), v0 + uint64_t(kk * 128), idesc_o,
                        kk > 0 ? 1u : 0u);
         tc_commit_ws(&pb[OF]);
       }
-      tc_commit_ws(&pb[EMPTY]);  // smem buffer free once this head's MMAs are done
+      tc_commit_ws(&pb[EV]);  // V read by the last PV
     }
   } else if (warp >= 4) {
     const int c = (warp - 4) >> 2;  // pipeline of this warpgroup
@@ -1178,6 +1206,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         const int q = t * kTile + row;
         mbar_wait(&pb[SF], k & 1);
         tc_fence_after();
+        EPS_TRACE(c == 0 && k < 32 && warp == 4 && lane == 0, 832 + k * 5 + 1);
         float m = -FLT_MAX;
         for (int ch = 0; ch < nch; ++ch) {
           uint32_t r[32];
@@ -1207,6 +1236,22 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
               sum += e0 + e1;
               pk[j] = pack_bf16(e0, e1);
             }
+          } else if (ch < nch && p.T - ch * 32 <= 16) {
+            // tail chunk with <= 16 valid keys: half the loads and exps
+            uint32_t r[16];
+            tmem_ld_32x32_x16(tS + uint32_t(ch * 32), r);
+            tmem_ld_wait();
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const int kk = ch * 32 + 2 * j;
+              const float e0 = kk < p.T ? fast_exp2(fmaf(__uint_as_float(r[2 * j]), sl2, -ms)) : 0.f;
+              const float e1 =
+                  kk + 1 < p.T ? fast_exp2(fmaf(__uint_as_float(r[2 * j + 1]), sl2, -ms)) : 0.f;
+              sum += e0 + e1;
+              pk[j] = pack_bf16(e0, e1);
+            }
+#pragma unroll
+            for (int j = 8; j < 16; ++j) pk[j] = 0u;
           } else if (ch < nch) {
             uint32_t r[32];
             tmem_ld_32x32(tS + uint32_t(ch * 32), r);
@@ -1230,14 +1275,17 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&pb[PF]);
+        EPS_TRACE(c == 0 && k < 32 && warp == 4 && lane == 0, 832 + k * 5 + 2);
         if (q < p.T) p.lse[int64_t(bh) * p.T + q] = (ms + __log2f(sum)) * kLn2;
         mbar_wait(&pb[OF], k & 1);
         tc_fence_after();
+        EPS_TRACE(c == 0 && k < 32 && warp == 4 && lane == 0, 832 + k * 5 + 3);
         float o[64];
         load_tmem_row64(tS + 128, o);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&pb[TF]);
+        EPS_TRACE(c == 0 && k < 32 && warp == 4 && lane == 0, 832 + k * 5 + 4);
         if (q < p.T) {
           const float inv = 1.f / sum;
 #pragma unroll
@@ -1277,6 +1325,8 @@ bool ensure_smem(K kern, size_t bytes) {
 // Entry points used by attention.cu's C ABI for head_dim 64, T <= 384.
 bool attn_tc_supported(int T, int head_dim) { return head_dim == 64 && T >= 1 && T <= 384; }
 
+static int g_trace_on = 0;
+
 int attn_fwd_tc(const void* qkv, void* out, float* lse, int B, int T, int H, float scale,
                 cudaStream_t st) {
   using namespace attn_tc;
@@ -1294,6 +1344,7 @@ int attn_fwd_tc(const void* qkv, void* out, float* lse, int B, int T, int H, flo
   p.scale_log2 = scale * kLog2e;
   p.out_w = static_cast<uint16_t*>(out);
   p.lse = lse;
+  p.trace = g_trace_on;
   if (T <= 2 * kTile) {
     const size_t sp = fwd_persistent_smem(T);
     if (!ensure_smem(attn_fwd_persistent_tc_kernel, sp)) return EPS_ECUDA;
@@ -1338,7 +1389,6 @@ __global__ void attn_rowdot_kernel(const uint16_t* __restrict__ out,
   }
 }
 
-static int g_trace_on = 0;
 
 bool attn_bwd_fused_supported(int T, int head_dim) {
   return head_dim == 64 && T >= 1 && T <= 2 * attn_tc::kTile;
