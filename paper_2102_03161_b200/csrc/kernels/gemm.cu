@@ -65,7 +65,7 @@ struct GemmCfg {
   // double-buffered accumulator (2 x BN columns), allocation rounded to a power of two
   static constexpr int kTmemCols = 2 * BN <= 256 ? 256 : 512;
   static constexpr size_t kSmem = size_t(STAGES) * kStageBytes + 8 * size_t(EPIB) /*epilogue*/ +
-                                  1024 /*align*/ + 512 /*barriers*/;
+                                  1024 /*align*/ + 1024 /*barriers*/;
   static constexpr uint32_t kIdesc = umma_idesc_bf16(PAIR ? 2 * kBM : kBM, BN, A_MN, B_MN);
 };
 
@@ -206,7 +206,7 @@ __device__ __forceinline__ void unpack_aux(const uint4 (&w)[4], float (&a)[32]) 
   }
 }
 
-constexpr int kAuxDepth = 3;
+constexpr int kAuxDepthMax = 7;  // barrier slots per epilogue warp
 
 std::atomic<int>& gemm_pair_mode();
 
@@ -217,6 +217,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                    const __grid_constant__ CUtensorMap map_c,
                    const __grid_constant__ CUtensorMap map_x, const GemmArgs args) {
   using Cfg = GemmCfg<BN, STAGES, A_MN, B_MN, EPIB, PAIR>;
+  // aux TMA ring depth: the per-warp epilogue area minus one 2 KB out slot
+  constexpr int kAuxDepth = EPIB >= 8192 ? (EPIB - 2048) / 2048 : 1;
+  static_assert(kAuxDepth <= kAuxDepthMax, "aux ring");
   // PAIR: rank 0 / 1 of the CTA pair; work is distributed over pairs.
   const int rank = PAIR ? int(cluster_ctarank()) : 0;
   const bool leader = rank == 0;
@@ -232,8 +235,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* tmem_full = empty + STAGES;
   uint64_t* tmem_empty = tmem_full + 2;
-  uint64_t* aux_full = tmem_empty + 2;  // [kEpiWarps][kAuxDepth]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aux_full + kAuxDepth * kEpiWarps);
+  uint64_t* aux_full = tmem_empty + 2;  // [kEpiWarps][kAuxDepthMax]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aux_full + kAuxDepthMax * kEpiWarps);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -251,7 +254,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&tmem_full[s], 1);
       mbar_init(&tmem_empty[s], PAIR ? 2 * kEpiWarps : kEpiWarps);  // both CTAs' epilogues
     }
-    for (int s = 0; s < kAuxDepth * kEpiWarps; ++s) mbar_init(&aux_full[s], 1);
+    for (int s = 0; s < kAuxDepthMax * kEpiWarps; ++s) mbar_init(&aux_full[s], 1);
     mbar_fence_init();
   }
   if (warp == 1) {
@@ -357,7 +360,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int out_bytes = (two_out || f32_out) ? 4096 : 2048;
     const int n_out = aux_tma ? 1 : EPIB / out_bytes;
     const uint16_t* auxp = static_cast<const uint16_t*>(args.aux);
-    uint64_t* my_aux_bar = aux_full + kAuxDepth * ew;
+    uint64_t* my_aux_bar = aux_full + kAuxDepthMax * ew;
     const uint32_t aux_s = area_s + kChunkBf16;
     // TMA prefetch cursor over this warp's (tile, chunk) stream: c = part, part+2, ...
     // Tile coordinates are decoded once per tile (integer division is a

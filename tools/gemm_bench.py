@@ -16,6 +16,10 @@ SHAPES = {  # name: (M, N, K, a_mn, b_mn, epi, split)
     "dgrad_fc2": (R, 3072, 768, False, True, ops.EPI_DGELU_BF16, 1),
     "dgrad_fc2_nocolsum": (R, 3072, 768, False, True, ops.EPI_DGELU_BF16, 1),
     "dgrad_fc2_mul": (R, 3072, 768, False, True, ops.EPI_MUL_BF16, 1),
+    "dgrad_fc2_mul_nocolsum": (R, 3072, 768, False, True, ops.EPI_MUL_BF16, 1),
+    "dgrad_fc2_resid": (R, 3072, 768, False, True, ops.EPI_RESID_BF16, 1),
+    "dgrad_fc2_store": (R, 3072, 768, False, True, ops.EPI_STORE_BF16, 1),
+    "fwd_fc1_bias": (R, 3072, 768, False, False, ops.EPI_BIAS_BF16, 1),
     "fwd_fc1_gelu2": (R, 3072, 768, False, False, ops.EPI_BIAS_GELU2_BF16, 1),
     "dgrad_proj_rowdot": (R, 768, 768, False, True, ops.EPI_ROWDOT_BF16, 1),
     "fwd_fc1_store": (R, 3072, 768, False, False, ops.EPI_STORE_BF16, 1),
@@ -34,7 +38,7 @@ def run(name, M, N, K, a_mn, b_mn, epi, split, iters=20):
     f32 = epi in (ops.EPI_STORE_F32, ops.EPI_ACCUM_F32)
     out = torch.zeros(M, N, device=dev, dtype=torch.float32 if f32 else torch.bfloat16)
     bias = torch.randn(N, device=dev)
-    aux = torch.randn(M, N, device=dev).bfloat16() if epi in (2, 3, 4, 8, 9, 10) else None
+    aux = torch.randn(M, N, device=dev).bfloat16() if epi in (2, 3, 4, 7, 8, 9, 10) else None
     colsum = (torch.zeros(N, device=dev) if epi in (4, 10) and "nocolsum" not in name else
               torch.zeros(M * N // 64, device=dev) if epi == 8 else None)
     kw = dict(a_mn=a_mn, b_mn=b_mn, epilogue=epi, bias=bias, aux=aux, colsum=colsum,
