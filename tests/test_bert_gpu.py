@@ -146,3 +146,32 @@ def test_bert_two_stage_pipeline(cuda, tmp_path, peer):
     for o in outs:
         a, b = o["range"]
         assert _rel(o["g"], ref.g32[a:b]) < 1e-3
+
+
+@pytest.mark.parametrize("cfg", ["bert-base-384", "bert-large-128"])
+def test_bert_full_size_step_properties(cuda, cfg):
+    """BASELINE configs 4 and 5 at full size (batch 64): micro-batch invariance
+    of the loss and every gradient (one pass vs 4 micro-batches -- different
+    GEMM / attention tilings; the 2-kernel T=384 and the fused T=128
+    attention backward), and additivity of the loss sum over two halves."""
+    g = GEOMETRIES[cfg]
+    batch = 64
+    params = init_params(g, seed=13)
+    tok, seg, lab = _data(g, batch, seed=7)
+    inputs = torch.stack([tok, seg]).cuda()
+    labels = lab.reshape(-1).cuda() if g.head == "qa" else lab.cuda()
+    ex = BertExecutor(g, max_batch=batch, params=params)
+    loss1 = ex.train_step(inputs, labels, micro_batches=1).item()
+    g1 = ex.g32.clone()
+    ex.g32.zero_()
+    loss4 = ex.train_step(inputs, labels, micro_batches=4).item()
+    torch.cuda.synchronize()
+    assert torch.isfinite(g1).all()
+    assert abs(loss4 - loss1) <= 1e-3 * abs(loss1)
+    assert _rel(ex.g32, g1) < 1e-2
+    halves = 0.0
+    for lo in (0, 32):
+        ex.g32.zero_()
+        lab_h = lab[:, lo:lo + 32].reshape(-1).cuda() if g.head == "qa" else lab[lo:lo + 32].cuda()
+        halves += ex.train_step(inputs[:, lo:lo + 32].contiguous(), lab_h).item()
+    assert abs(halves - loss1) <= 1e-3 * abs(loss1)

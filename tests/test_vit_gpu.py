@@ -142,3 +142,36 @@ def test_cache_host_tier(cuda):
     torch.cuda.synchronize()
     assert abs(a - b) <= 1e-6 * abs(a)  # loss sum uses fp32 atomics
     assert torch.allclose(ga, ex.g32, rtol=1e-5, atol=1e-7)
+
+
+def test_full_size_step_properties(cuda):
+    """BASELINE config 2 at full size (ViT-B/16, batch 400 -- 78,800 token rows,
+    CTA-pair GEMM tiles with a partial last pair, every attention / LN path):
+    size-independent properties instead of a CPU oracle at this size.
+    (1) micro-batch invariance (GPipe's contract): one pass == 5 micro-batches
+    (different GEMM / attention tilings) for the loss and every gradient;
+    (2) additivity: the loss sum of the batch == the sums of its two halves;
+    (3) its first 4 samples alone match the fp32 oracle."""
+    g = GEOMETRIES["vit-b16"]
+    batch = 400
+    params = init_params(g, seed=23)
+    images, labels = _data(g, batch, seed=9)
+    x, y = images.cuda(), labels.cuda()
+    ex = VitExecutor(g, max_batch=batch, params=params)
+    loss1 = ex.train_step(x, y, micro_batches=1).item()
+    g1 = ex.g32.clone()
+    ex.g32.zero_()
+    loss5 = ex.train_step(x, y, micro_batches=5).item()
+    torch.cuda.synchronize()
+    assert abs(loss5 - loss1) <= 1e-3 * abs(loss1)
+    assert _rel(ex.g32, g1) < 1e-2
+    assert torch.isfinite(g1).all()
+    halves = 0.0
+    for lo in (0, 200):
+        ex.g32.zero_()
+        halves += ex.train_step(x[lo:lo + 200], y[lo:lo + 200]).item()
+    assert abs(halves - loss1) <= 1e-3 * abs(loss1)
+    ref_loss, _, _ = vit_fp32.train_step(params, images[:4], labels[:4], g, 0)
+    ex.g32.zero_()
+    l4 = ex.train_step(x[:4], y[:4]).item() / 4
+    assert abs(l4 - ref_loss.item()) <= LOSS_RTOL * abs(ref_loss.item())
