@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 
 #include <cfloat>
+#include <unordered_map>
 
 #include "eps_capi.h"
 #include "ptx.cuh"
@@ -1316,8 +1317,16 @@ size_t bwd_dkdv_smem(int Tp) {
 
 template <typename K>
 bool ensure_smem(K kern, size_t bytes) {
-  return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)) ==
-         cudaSuccess;
+  // the attribute is per kernel; set it once per (host thread, kernel, size)
+  thread_local std::unordered_map<const void*, size_t> done;
+  const void* key = reinterpret_cast<const void*>(kern);
+  auto it = done.find(key);
+  if (it != done.end() && it->second >= bytes) return true;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)) !=
+      cudaSuccess)
+    return false;
+  done[key] = bytes;
+  return true;
 }
 
 }  // namespace attn_tc

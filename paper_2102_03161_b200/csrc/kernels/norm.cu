@@ -9,6 +9,7 @@
 
 #include "eps_capi.h"
 #include "ptx.cuh"
+#include "tma_host.cuh"
 
 namespace eps_k {
 
@@ -445,9 +446,7 @@ int ln_fwd_wide_launch(const void* x, const float* gamma, const float* beta, voi
       return EPS_ECUDA;
     configured = true;
   }
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int sms = sm_count();
   const int64_t need = (rows + 7) / 8;
   const int grid = int(need < 3 * sms ? need : 3 * sms);
   count_launch();
@@ -469,9 +468,7 @@ int ln_bwd_wide_launch(const void* dy, const void* x, const float* gamma, const 
       return EPS_ECUDA;
     configured = true;
   }
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int sms = sm_count();
   const int64_t need = (rows + 7) / 8;  // >= 8 rows per CTA
   const int grid = int(need < 2 * sms ? need : 2 * sms);
   count_launch();
@@ -482,9 +479,7 @@ int ln_bwd_wide_launch(const void* dy, const void* x, const float* gamma, const 
 }
 
 int ln_grid_bwd(int64_t rows) {
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int sms = sm_count();
   const int64_t need = (rows + kLnWarps - 1) / kLnWarps;
   return int(need < 2 * sms ? need : 2 * sms);
 }
