@@ -387,6 +387,10 @@ int eps_gemm_bf16(int a_mn_major, int b_mn_major, int epilogue, const void* A, c
 /* CTA-pair (cta_group::2, 256-row) GEMM tiles: mode 1 on (default), 0 off;
  * mode < 0 only queries.  Returns the mode in effect. */
 int eps_gemm_pair_mode(int mode);
+/* Programmatic dependent launch of the GEMM / attention / LayerNorm kernels
+ * (each overlaps its launch and prologue with its predecessor's tail): mode
+ * 1 on (default), 0 off; mode < 0 only queries. */
+int eps_pdl_mode(int mode);
 
 /* LayerNorm over rows of width d (fp32 statistics). */
 int eps_layernorm_fwd(const void* x, const float* gamma, const float* beta, void* y,

@@ -679,10 +679,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   }
   if (warp == 1) tmem_alloc(tmem_slot, 512);
   if (threadIdx.x < 64) sRed[threadIdx.x] = 0.f;
+  pdl_launch_dependents();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();  // the predecessor grid's outputs are complete (PDL launch)
   const uint32_t tdV = tmem + 256, tdK = tmem + 320, tdQ = tmem + 384;
 
   if (warp == 0) {
@@ -1118,10 +1120,12 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     mbar_fence_init();
   }
   if (warp == 3) tmem_alloc(tmem_slot, 512);
+  pdl_launch_dependents();
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();  // the predecessor grid's outputs are complete (PDL launch)
 
   if (warp == 0 || warp == 3) {
     // TMA producer of pipeline c (warp 0: c = 0, warp 3: c = 1), region by
@@ -1360,7 +1364,9 @@ int attn_fwd_tc(const void* qkv, void* out, float* lse, int B, int T, int H, flo
     const int heads = B * H;
     const int grid = heads < sm_count() ? heads : sm_count();
     count_launch();
-    attn_fwd_persistent_tc_kernel<<<grid, kFwdThreads, sp, st>>>(m, p, heads);
+    if (launch_k(attn_fwd_persistent_tc_kernel, dim3(grid), dim3(kFwdThreads), sp, st, 1, m, p,
+                 heads) != cudaSuccess)
+      return EPS_ECUDA;
     return cudaGetLastError() == cudaSuccess ? EPS_OK : EPS_ECUDA;
   }
   const size_t smem = fwd_smem(Tp);
@@ -1446,7 +1452,9 @@ int attn_bwd_tc(const void* qkv, const void* out, const void* dout, const float*
     auto kern = T <= kTile ? attn_bwd_fused_tc_kernel<1> : attn_bwd_fused_tc_kernel<2>;
     if (!ensure_smem(kern, sf)) return EPS_ECUDA;
     count_launch();
-    kern<<<grid, kBwdThreads, sf, st>>>(mq, mo, mdq, p, heads);
+    if (launch_k(kern, dim3(grid), dim3(kBwdThreads), sf, st, 1, mq, mo, mdq, p, heads) !=
+        cudaSuccess)
+      return EPS_ECUDA;
     return cudaGetLastError() == cudaSuccess ? EPS_OK : EPS_ECUDA;
   }
   const size_t s1 = bwd_dq_smem(Tp), s2 = bwd_dkdv_smem(Tp);

@@ -240,6 +240,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  pdl_launch_dependents();
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&map_a);
@@ -266,6 +267,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if constexpr (PAIR) cluster_sync_all();  // the peer's barriers are initialised
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_wait();  // the predecessor grid's outputs are complete (PDL launch)
 
   const int tiles = args.tiles_m * args.tiles_n;
   const int units = tiles * args.splits;
@@ -599,26 +601,12 @@ int launch(const void* A, const void* B, int64_t lda, int64_t ldb, GemmArgs args
   const bool ok_x = make_map(&mx, xptr, false, args.N, args.M, args.ldc, 32, 32, SW64);
   if (!ok_a || !ok_b || !ok_c || !ok_x) return EPS_ECUDA;
   const int units = args.tiles_m * args.tiles_n * args.splits;
-  if constexpr (PAIR) {
-    const int pairs = units < sm_count() / 2 ? units : sm_count() / 2;
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(2 * pairs);
-    cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = Cfg::kSmem;
-    cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    count_launch();
-    if (cudaLaunchKernelEx(&cfg, kern, ma, mb, mc, mx, args) != cudaSuccess) return EPS_ECUDA;
-    return cudaGetLastError() == cudaSuccess ? EPS_OK : EPS_ECUDA;
-  }
-  const int grid = units < sm_count() ? units : sm_count();
-  count_launch(); kern<<<grid, kThreads, Cfg::kSmem, stream>>>(ma, mb, mc, mx, args);
+  const int workers = PAIR ? sm_count() / 2 : sm_count();
+  const int grid = (units < workers ? units : workers) * (PAIR ? 2 : 1);
+  count_launch();
+  if (launch_k(kern, dim3(grid), dim3(kThreads), Cfg::kSmem, stream, PAIR ? 2 : 1, ma, mb, mc, mx,
+               args) != cudaSuccess)
+    return EPS_ECUDA;
   return cudaGetLastError() == cudaSuccess ? EPS_OK : EPS_ECUDA;
 }
 
@@ -633,6 +621,11 @@ std::atomic<int>& gemm_pair_mode() {
 }
 
 }  // namespace eps_k
+
+extern "C" int eps_pdl_mode(int mode) {
+  if (mode >= 0) eps_k::pdl_mode().store(mode);
+  return eps_k::pdl_mode().load();
+}
 
 extern "C" int eps_gemm_pair_mode(int mode) {
   if (mode >= 0) eps_k::gemm_pair_mode().store(mode);

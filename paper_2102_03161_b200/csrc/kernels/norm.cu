@@ -248,7 +248,9 @@ __global__ void __launch_bounds__(LnWide<D>::THREADS, 2)
     mbar_fence_init();
   }
   for (int i = threadIdx.x; i < 3 * D; i += blockDim.x) (&acc_s[0][0])[i] = 0.f;
+  pdl_launch_dependents();
   __syncthreads();
+  pdl_wait();  // the predecessor grid's outputs are complete (PDL launch)
   if (warp == 0) {
     if (lane == 0) {
       const uint32_t bytes = uint32_t((has_res ? 3 : 2) * ROW);
@@ -362,7 +364,9 @@ __global__ void __launch_bounds__(LnWide<D>::THREADS, 3)
     }
     mbar_fence_init();
   }
+  pdl_launch_dependents();
   __syncthreads();
+  pdl_wait();  // the predecessor grid's outputs are complete (PDL launch)
   if (warp == 0) {
     if (lane == 0) {
       for (int64_t k = 0; k < n_mine; ++k) {
@@ -450,9 +454,10 @@ int ln_fwd_wide_launch(const void* x, const float* gamma, const float* beta, voi
   const int64_t need = (rows + 7) / 8;
   const int grid = int(need < 3 * sms ? need : 3 * sms);
   count_launch();
-  ln_fwd_wide_kernel<D><<<grid, L::THREADS, smem, st>>>(static_cast<const uint16_t*>(x), gamma,
-                                                        beta, static_cast<uint16_t*>(y), mean,
-                                                        rstd, rows, eps);
+  if (launch_k(ln_fwd_wide_kernel<D>, dim3(grid), dim3(L::THREADS), smem, st, 1,
+               static_cast<const uint16_t*>(x), gamma, beta, static_cast<uint16_t*>(y), mean, rstd,
+               rows, eps) != cudaSuccess)
+    return EPS_ECUDA;
   return cudaGetLastError() == cudaSuccess ? EPS_OK : EPS_ECUDA;
 }
 
@@ -472,9 +477,11 @@ int ln_bwd_wide_launch(const void* dy, const void* x, const float* gamma, const 
   const int64_t need = (rows + 7) / 8;  // >= 8 rows per CTA
   const int grid = int(need < 2 * sms ? need : 2 * sms);
   count_launch();
-  ln_bwd_wide_kernel<D><<<grid, L::THREADS, L::SMEM, st>>>(
-      static_cast<const uint16_t*>(dy), static_cast<const uint16_t*>(x), gamma, mean, rstd,
-      static_cast<const uint16_t*>(dres), static_cast<uint16_t*>(dx), dgamma, dbeta, colsum, rows);
+  if (launch_k(ln_bwd_wide_kernel<D>, dim3(grid), dim3(L::THREADS), L::SMEM, st, 1,
+               static_cast<const uint16_t*>(dy), static_cast<const uint16_t*>(x), gamma, mean, rstd,
+               static_cast<const uint16_t*>(dres), static_cast<uint16_t*>(dx), dgamma, dbeta,
+               colsum, rows) != cudaSuccess)
+    return EPS_ECUDA;
   return cudaGetLastError() == cudaSuccess ? EPS_OK : EPS_ECUDA;
 }
 

@@ -451,3 +451,18 @@ __device__ __forceinline__ void tmem_dealloc_pair(uint32_t taddr, uint32_t cols)
                : "memory");
 }
 }  // namespace eps_k
+
+// ---- programmatic dependent launch -------------------------------------------
+// Kernels launched with the PDL attribute (eps_k::launch_k) may start while
+// their predecessor in the stream is still finishing: each CTA first lets its
+// own dependents launch, runs its prologue (barrier init, TMEM allocation,
+// tensor-map prefetch), then waits for the predecessor grid's completion and
+// memory flush before touching global memory.  That hides the launch latency
+// and the prologue behind the predecessor's tail (~2 us per kernel boundary,
+// ~10 % of a small-micro-batch pipeline stage).
+namespace eps_k {
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+}  // namespace eps_k

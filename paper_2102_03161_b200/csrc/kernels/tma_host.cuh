@@ -121,3 +121,50 @@ inline int sm_count() {
 }
 
 }  // namespace eps_k
+
+#include <atomic>
+#include <cstdlib>
+#include <utility>
+
+namespace eps_k {
+
+// PDL on (1, default) / off (0): EPS_PDL in the environment or eps_pdl_mode().
+inline std::atomic<int>& pdl_mode() {
+  static std::atomic<int> mode{[] {
+    const char* e = std::getenv("EPS_PDL");
+    return e == nullptr ? 1 : std::atoi(e);
+  }()};
+  return mode;
+}
+
+// cudaLaunchKernelEx with programmatic stream serialization (the kernel must
+// call pdl_wait() before reading or writing global memory) and an optional
+// cluster width.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                     int cluster_x, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  int n = 0;
+  if (pdl_mode().load() != 0) {
+    attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  if (cluster_x > 1) {
+    attr[n].id = cudaLaunchAttributeClusterDimension;
+    attr[n].val.clusterDim.x = unsigned(cluster_x);
+    attr[n].val.clusterDim.y = 1;
+    attr[n].val.clusterDim.z = 1;
+    ++n;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = unsigned(n);
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
+}  // namespace eps_k
