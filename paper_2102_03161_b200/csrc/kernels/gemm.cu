@@ -666,10 +666,15 @@ extern "C" int eps_gemm_bf16(int a_mn_major, int b_mn_major, int epilogue, const
   args.aux = aux;
   args.colsum = colsum;
   const int kblocks = int((K + kBK - 1) / kBK);
-  // CTA pairs (256-row tiles, cta_group::2) for every GEMM with at least two
-  // pair tiles of rows and a 256-multiple N (all ViT-B / BERT block GEMMs);
+  // CTA pairs (256-row tiles, cta_group::2) for every GEMM with enough rows
+  // and a 256-multiple N (all ViT-B / BERT block GEMMs at full batch);
   // EPS_GEMM_PAIR=0 forces single-CTA tiles (A/B comparisons).
-  const bool pair = gemm_pair_mode() != 0 && M >= 512 && N % 256 == 0;
+  // Below ~4K rows without a K split (a pipeline micro-batch of <= 20 ViT
+  // samples) single CTAs balance the few tiles better (measured at 17 and 34
+  // samples); weight gradients (split-K over the token rows) always have
+  // enough units.
+  const bool pair = gemm_pair_mode() != 0 && N % 256 == 0 &&
+                    (M >= 4096 || (auto_split && M >= 512));
   const int64_t tile_m = pair ? 2 * kBM : kBM;
   if (auto_split) {
     // wgrad: few output tiles, long contraction over token rows.  Pick the

@@ -21,11 +21,11 @@ def _close(out, ref, rtol=RTOL):
     assert err <= rtol * scale + 1e-3, f"max err {err} vs scale {scale}"
 
 
-# (3546, 2304), (600, 512), (2000, 768): CTA-pair (256-row, cta_group::2)
+# (4100, 512), (4500, 2304), (5000, 768): CTA-pair (256-row, cta_group::2)
 # tiles, including pairs whose second CTA is partly / wholly past M.
 @pytest.mark.parametrize("M,N,K", [(128, 256, 64), (3546, 2304, 768), (300, 768, 3072),
                                    (1000, 1000, 768), (77, 768, 768), (400, 1000, 777),
-                                   (600, 512, 192), (2000, 768, 3072)])
+                                   (4100, 512, 192), (4500, 2304, 768), (5000, 768, 3072)])
 @pytest.mark.parametrize("a_mn,b_mn", [(False, False), (False, True), (True, False),
                                        (True, True)])
 def test_gemm_store(cuda, M, N, K, a_mn, b_mn):
