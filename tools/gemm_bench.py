@@ -28,6 +28,12 @@ SHAPES = {  # name: (M, N, K, a_mn, b_mn, epi, split)
     "wgrad_qkv": (2304, 768, R, True, True, ops.EPI_ACCUM_F32, 8),
     "wgrad_fc2": (768, 3072, R, True, True, ops.EPI_ACCUM_F32, 8),
     "square8k": (8192, 8192, 8192, False, False, ops.EPI_STORE_BF16, 1),
+    # a K = 8 pipeline micro-batch (17 samples = 3349 token rows)
+    "mb17_qkv": (17 * 197, 2304, 768, False, False, ops.EPI_BIAS_BF16, 1),
+    "mb17_fc1": (17 * 197, 3072, 768, False, False, ops.EPI_BIAS_GELU2_BF16, 1),
+    "mb17_fc2": (17 * 197, 768, 3072, False, False, ops.EPI_BIAS_RESID_BF16, 1),
+    "mb17_dgrad_fc2": (17 * 197, 3072, 768, False, True, ops.EPI_MUL_BF16, 1),
+    "mb17_dgrad_qkv": (17 * 197, 768, 2304, False, True, ops.EPI_STORE_BF16, 1),
 }
 
 
