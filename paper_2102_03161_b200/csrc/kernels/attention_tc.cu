@@ -603,27 +603,6 @@ __device__ __forceinline__ void zero32(uint32_t (&pk)[32]) {
   for (int d = 0; d < 32; ++d) pk[d] = 0u;
 }
 
-__device__ __forceinline__ void store_packed64(uint16_t* dst, const uint32_t (&pk)[32]) {
-  uint4* d4 = reinterpret_cast<uint4*>(dst);
-#pragma unroll
-  for (int i = 0; i < 8; ++i)
-    d4[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
-}
-
-// colsum64 of the 64 bf16 values packed in pk (32 unpacked at a time).
-__device__ __forceinline__ void colsum_packed64(const uint32_t (&pk)[32], float* dbias) {
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int half = 0; half < 2; ++half) {
-    float t[32];
-#pragma unroll
-    for (int d = 0; d < 16; ++d) {
-      t[2 * d] = bf16_lo(pk[half * 16 + d]);
-      t[2 * d + 1] = bf16_hi(pk[half * 16 + d]);
-    }
-    atomicAdd(dbias + half * 32 + lane, warp_transpose_sum32(t));
-  }
-}
 
 template <int NT>
 __global__ void __launch_bounds__(kBwdThreads, 1)

@@ -111,12 +111,12 @@ __device__ __forceinline__ void load_operand_pair(void* dst, const CUtensorMap* 
 
 // ---- epilogue ----------------------------------------------------------------
 // Two warps per TMEM lane quarter (32 output rows) walk alternate 32-column
-// chunks of each tile.  Outputs are staged in a per-warp swizzled 4 KB smem
-// ring and written with TMA stores (TMA reduce-add for fp32 accumulation):
-// coalesced, asynchronous global traffic.  Element-wise inputs (residual /
-// GELU pre-activation) are loaded straight into registers one chunk ahead of
-// use, so their latency hides behind the current chunk's math.
-constexpr int kEpiWarpBytes = 4096;
+// chunks of each tile.  Outputs are staged in a per-warp swizzled smem ring
+// (EPIB bytes per warp) and written with TMA stores (TMA reduce-add for fp32
+// accumulation): coalesced, asynchronous global traffic.  Element-wise inputs
+// (residual / gelu' / attention output) arrive through a per-warp TMA ring
+// (EPIB >= 8 KB) or, on the 4 KB configurations, straight into registers one
+// chunk ahead of use.
 constexpr int kChunkBf16 = 2048;  // 32x32 bf16
 
 __device__ __forceinline__ bool epi_reads_aux(int epi) {

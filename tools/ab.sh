@@ -1,4 +1,5 @@
 cd $GRAFT_REPO_ROOT
-for i in 1 2; do
-for pr in 0 1; do echo "PAIR=$pr"; for b in 17 34 100; do EPS_GEMM_PAIR=$pr python tools/timeline.py $b 2>&1 | grep "step span"; done; done
-done
+timeout 300 python -m pytest tests/test_kernels_gpu.py -x -q -k attention 2>&1 | tail -n 2
+python tools/attn_bench.py vit-b16 bert-large-128
+EPS_LIB_PATH=$PWD/tools/_cmp/libeps_b200_base.so python tools/attn_bench.py vit-b16 bert-large-128
+python tools/attn_bench.py vit-b16 bert-large-128
