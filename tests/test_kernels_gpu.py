@@ -68,7 +68,8 @@ def _attn_ref(qkv, B, T, H, dh):
 @pytest.mark.parametrize("B,T,H,dh", [(3, 197, 12, 64), (5, 65, 4, 32), (2, 128, 16, 64),
                                       (1, 384, 12, 64), (2, 50, 2, 64), (30, 197, 12, 64),
                                       (64, 128, 16, 64), (3, 256, 4, 64), (7, 129, 3, 64),
-                                      (5, 1, 2, 64)])
+                                      (5, 1, 2, 64), (1, 255, 1, 64), (300, 197, 1, 64),
+                                      (40, 64, 8, 64)])
 def test_attention_fwd_bwd(cuda, B, T, H, dh):
     g = torch.Generator(device=cuda).manual_seed(T * H)
     D = H * dh
