@@ -84,23 +84,7 @@ __global__ void assemble_kernel(const uint16_t* __restrict__ tok, const float* _
 }
 
 // Backward of assemble: dpos[t] += sum_b dx[b,t]; dcls += sum_b dx[b,0];
-// dtok[b*P+p] = dx[b,1+p] (optional).  Block = (token t, 256-col slab).
-__global__ void assemble_bwd_kernel(const uint16_t* __restrict__ dx, float* __restrict__ dcls,
-                                    float* __restrict__ dpos, uint16_t* __restrict__ dtok,
-                                    int batch, int tokens, int d) {
-  const int t = blockIdx.x;
-  const int col = blockIdx.y * blockDim.x + threadIdx.x;
-  if (col >= d) return;
-  float s = 0.f;
-  for (int b = 0; b < batch; ++b) {
-    const uint16_t raw = dx[(int64_t(b) * tokens + t) * d + col];
-    const float g = __uint_as_float(uint32_t(raw) << 16);
-    s += g;
-    if (dtok != nullptr && t > 0) dtok[(int64_t(b) * (tokens - 1) + t - 1) * d + col] = raw;
-  }
-  if (dpos != nullptr) atomicAdd(dpos + int64_t(t) * d + col, s);
-  if (t == 0 && dcls != nullptr) atomicAdd(dcls + col, s);
-}
+// dtok[b*P+p] = dx[b,1+p] (optional) -- assemble_bwd_split_kernel below.
 
 // ---- softmax cross-entropy -------------------------------------------------------
 // One warp per row: loss_sum += lse - z[label]; dz = (softmax - onehot) / B;
@@ -272,6 +256,80 @@ __global__ void colsum_kernel(const uint16_t* __restrict__ x, float* __restrict_
   atomicAdd(out + c, s);
 }
 
+// Row-per-block variants (no 64-bit divisions per element): one block per
+// patch row / token row, one thread per 4 (patchify) or 8 (assemble) columns.
+__global__ void patchify_rows_kernel(const float* __restrict__ img, uint16_t* __restrict__ out,
+                                     int channels, int side, int ps) {
+  const int per_side = side / ps, patches = per_side * per_side;
+  const int row = blockIdx.x;  // b * patches + p
+  const int b = row / patches, p = row - b * patches;
+  const int col = threadIdx.x * 4;  // within channels * ps * ps
+  const int c = col / (ps * ps), rem = col - c * ps * ps, kh = rem / ps, kw0 = rem - kh * ps;
+  const int py = (p / per_side) * ps + kh, px0 = (p % per_side) * ps + kw0;
+  const float4 a = __ldg(reinterpret_cast<const float4*>(
+      img + (int64_t(b) * channels + c) * side * side + int64_t(py) * side + px0));
+  *reinterpret_cast<uint2*>(out + int64_t(row) * channels * ps * ps + col) =
+      make_uint2(pack_bf16(a.x, a.y), pack_bf16(a.z, a.w));
+}
+
+__global__ void assemble_rows_kernel(const uint16_t* __restrict__ tok, const float* __restrict__ cls,
+                                     const float* __restrict__ pos, uint16_t* __restrict__ x,
+                                     int tokens, int d) {
+  const int row = blockIdx.x;  // b * tokens + t
+  const int b = row / tokens, t = row - b * tokens;
+  const int col = threadIdx.x * 8;
+  float v[8];
+  if (t == 0) {
+    const float4 c0 = __ldg(reinterpret_cast<const float4*>(cls + col));
+    const float4 c1 = __ldg(reinterpret_cast<const float4*>(cls + col) + 1);
+    v[0] = c0.x; v[1] = c0.y; v[2] = c0.z; v[3] = c0.w;
+    v[4] = c1.x; v[5] = c1.y; v[6] = c1.z; v[7] = c1.w;
+  } else {
+    const uint4 w = *reinterpret_cast<const uint4*>(tok + (int64_t(b) * (tokens - 1) + t - 1) * d + col);
+    v[0] = bf16_lo(w.x); v[1] = bf16_hi(w.x); v[2] = bf16_lo(w.y); v[3] = bf16_hi(w.y);
+    v[4] = bf16_lo(w.z); v[5] = bf16_hi(w.z); v[6] = bf16_lo(w.w); v[7] = bf16_hi(w.w);
+  }
+  const float4 p0 = __ldg(reinterpret_cast<const float4*>(pos + int64_t(t) * d + col));
+  const float4 p1 = __ldg(reinterpret_cast<const float4*>(pos + int64_t(t) * d + col) + 1);
+  v[0] += p0.x; v[1] += p0.y; v[2] += p0.z; v[3] += p0.w;
+  v[4] += p1.x; v[5] += p1.y; v[6] += p1.z; v[7] += p1.w;
+  *reinterpret_cast<uint4*>(x + int64_t(row) * d + col) =
+      make_uint4(pack_bf16(v[0], v[1]), pack_bf16(v[2], v[3]), pack_bf16(v[4], v[5]),
+                 pack_bf16(v[6], v[7]));
+}
+
+// Backward of assemble (block = token t, 256-col slab, batch slice z), batch split over gridDim.z slices with 4 independent
+// accumulators per thread (the sequential 400-sample loop was latency-bound).
+__global__ void assemble_bwd_split_kernel(const uint16_t* __restrict__ dx, float* __restrict__ dcls,
+                                          float* __restrict__ dpos, uint16_t* __restrict__ dtok,
+                                          int batch, int tokens, int d) {
+  const int t = blockIdx.x;
+  const int col = blockIdx.y * blockDim.x + threadIdx.x;
+  if (col >= d) return;
+  const int per = (batch + gridDim.z - 1) / gridDim.z;
+  const int b0 = blockIdx.z * per, b1 = min(batch, b0 + per);
+  float s[4] = {0.f, 0.f, 0.f, 0.f};
+  int b = b0;
+  for (; b + 4 <= b1; b += 4) {
+    uint16_t raw[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) raw[u] = dx[(int64_t(b + u) * tokens + t) * d + col];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      s[u] += __uint_as_float(uint32_t(raw[u]) << 16);
+      if (dtok != nullptr && t > 0) dtok[(int64_t(b + u) * (tokens - 1) + t - 1) * d + col] = raw[u];
+    }
+  }
+  for (; b < b1; ++b) {
+    const uint16_t raw = dx[(int64_t(b) * tokens + t) * d + col];
+    s[0] += __uint_as_float(uint32_t(raw) << 16);
+    if (dtok != nullptr && t > 0) dtok[(int64_t(b) * (tokens - 1) + t - 1) * d + col] = raw;
+  }
+  const float sum = (s[0] + s[1]) + (s[2] + s[3]);
+  if (dpos != nullptr) atomicAdd(dpos + int64_t(t) * d + col, sum);
+  if (t == 0 && dcls != nullptr) atomicAdd(dcls + col, sum);
+}
+
 }  // namespace eps_k
 
 using namespace eps_k;
@@ -282,6 +340,14 @@ extern "C" int eps_patchify(const float* images, void* patches, int batch, int c
   const int out_side = image & 0xFFFF;
   const int in_side = (image >> 16) ? (image >> 16) : out_side;
   if (patch % 4 != 0 || out_side % patch != 0) return EPS_EINVAL;
+  const int row_len = channels * patch * patch;
+  if (in_side == out_side && row_len / 4 <= 1024) {
+    const int rows = batch * (out_side / patch) * (out_side / patch);
+    count_launch();
+    patchify_rows_kernel<<<rows, row_len / 4, 0, static_cast<cudaStream_t>(stream)>>>(
+        images, static_cast<uint16_t*>(patches), channels, out_side, patch);
+    return ok_or_cuda();
+  }
   count_launch(); patchify_kernel<<<num_sms() * 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(
       images, static_cast<uint16_t*>(patches), batch, channels, in_side, out_side, patch);
   return ok_or_cuda();
@@ -290,6 +356,13 @@ extern "C" int eps_patchify(const float* images, void* patches, int batch, int c
 extern "C" int eps_vit_assemble(const void* patch_tokens, const float* cls, const float* pos,
                                 void* x, int batch, int tokens, int64_t d, void* stream) {
   if (d % 8 != 0) return EPS_EINVAL;
+  if (d / 8 <= 1024) {
+    count_launch();
+    assemble_rows_kernel<<<batch * tokens, int(d / 8), 0, static_cast<cudaStream_t>(stream)>>>(
+        static_cast<const uint16_t*>(patch_tokens), cls, pos, static_cast<uint16_t*>(x), tokens,
+        int(d));
+    return ok_or_cuda();
+  }
   count_launch(); assemble_kernel<<<num_sms() * 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const uint16_t*>(patch_tokens), cls, pos, static_cast<uint16_t*>(x), batch,
       tokens, int(d));
@@ -298,8 +371,10 @@ extern "C" int eps_vit_assemble(const void* patch_tokens, const float* cls, cons
 
 extern "C" int eps_vit_assemble_bwd(const void* dx, float* dcls, float* dpos, void* dpatch_tokens,
                                     int batch, int tokens, int64_t d, void* stream) {
-  dim3 grid(tokens, unsigned((d + 255) / 256));
-  count_launch(); assemble_bwd_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+  const int splits = batch >= 64 ? 8 : 1;
+  dim3 grid(tokens, unsigned((d + 255) / 256), unsigned(splits));
+  count_launch();
+  assemble_bwd_split_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const uint16_t*>(dx), dcls, dpos, static_cast<uint16_t*>(dpatch_tokens), batch,
       tokens, int(d));
   return ok_or_cuda();

@@ -199,3 +199,21 @@ def test_patchify_assemble(cuda):
     torch.cuda.synchronize()
     want = torch.cat([cls.expand(B, 1, d), tok.float().reshape(B, 196, d)], 1) + pos
     assert _rel(x, want) < 1e-2
+
+
+@pytest.mark.parametrize("B", [3, 67, 400])
+def test_assemble_bwd(cuda, B):
+    """dpos = sum_b dx, dcls = sum_b dx[:, 0], dtok = dx[:, 1:] (bit copy); the
+    B >= 64 launch splits the batch over 8 slices with atomics."""
+    d, T = 768, 197
+    g = torch.Generator(device=cuda).manual_seed(B)
+    dx = torch.randn(B, T, d, device=cuda, generator=g).bfloat16()
+    dcls = torch.zeros(d, device=cuda)
+    dpos = torch.zeros(T, d, device=cuda)
+    dtok = torch.empty(B * (T - 1), d, dtype=torch.bfloat16, device=cuda)
+    ops.call("eps_vit_assemble_bwd", dx, dcls, dpos, dtok, B, T, d, _s())
+    torch.cuda.synchronize()
+    want = dx.double().sum(0)
+    assert (dpos.double() - want).abs().max().item() < 1e-4 * max(1.0, B ** 0.5)
+    assert (dcls.double() - want[0]).abs().max().item() < 1e-4 * max(1.0, B ** 0.5)
+    assert torch.equal(dtok, dx[:, 1:].reshape(-1, d))
