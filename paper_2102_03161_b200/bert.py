@@ -127,6 +127,8 @@ class BertExecutor(VitExecutor):
                                  C.byref(h))
         if rc != 0:
             raise RuntimeError(f"eps_bert_create failed ({rc})")
+        self._destroy = lib.eps_bert_destroy
+        self._destroy.restype = None
         self.h = h
 
     def _stored_shape(self, name, shape):

@@ -114,12 +114,15 @@ class VitExecutor:
                                 C.byref(h))
         if rc != 0:
             raise RuntimeError(f"eps_vit_create failed ({rc})")
+        self._destroy = getattr(lib, self.PREFIX + "destroy")
+        self._destroy.restype = None
         self.h = h
 
     def __del__(self):
-        if getattr(self, "h", None):
-            f = getattr(ops.api().lib, self.PREFIX + "destroy")
-            f.restype = None
+        # the destroy entry is bound at construction: module globals may
+        # already be torn down when this runs at interpreter exit
+        f = getattr(self, "_destroy", None)
+        if getattr(self, "h", None) and f is not None:
             f(self.h)
             self.h = None
 
