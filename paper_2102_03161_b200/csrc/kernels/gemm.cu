@@ -451,15 +451,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         } else if (aux_in) {
           unpack_aux(xa, x);
         }
+        // element-wise work on column pairs (packed fp32 pipe, bit-identical to scalar)
+        float2* v2 = reinterpret_cast<float2*>(v);
+        float2* x2 = reinterpret_cast<float2*>(x);
         if (args.bias != nullptr) {
           const float4* b4 = reinterpret_cast<const float4*>(args.bias + col0);
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
             const float4 b = (q * 4 < valid) ? __ldg(b4 + q) : make_float4(0.f, 0.f, 0.f, 0.f);
-            v[4 * q] += b.x;
-            v[4 * q + 1] += b.y;
-            v[4 * q + 2] += b.z;
-            v[4 * q + 3] += b.w;
+            v2[2 * q] = __fadd2_rn(v2[2 * q], make_float2(b.x, b.y));
+            v2[2 * q + 1] = __fadd2_rn(v2[2 * q + 1], make_float2(b.z, b.w));
           }
         }
         // reuse an out slot only after its previous TMA store has read it
@@ -480,12 +481,12 @@ __global__ void __launch_bounds__(kThreads, 1)
           case EPS_EPI_BIAS_RESID_BF16:
           case EPS_EPI_RESID_BF16:
 #pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] += x[j];
+            for (int j = 0; j < 16; ++j) v2[j] = __fadd2_rn(v2[j], x2[j]);
             stage_bf16(out_s, lane, v);
             break;
           case EPS_EPI_BIAS_GELU2_BF16:
 #pragma unroll
-            for (int j = 0; j < 32; ++j) gelu_and_grad_f(v[j], v[j], x[j]);
+            for (int j = 0; j < 16; ++j) gelu_and_grad_f2(v2[j], v2[j], x2[j]);
             stage_bf16(out_s + kChunkBf16, lane, x);  // gelu' -> map_x
             stage_bf16(out_s, lane, v);
             break;
@@ -496,7 +497,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             break;
           case EPS_EPI_MUL_BF16:
 #pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] *= x[j];
+            for (int j = 0; j < 16; ++j) v2[j] = __fmul2_rn(v2[j], x2[j]);
             stage_bf16(out_s, lane, v);
             break;
           case EPS_EPI_ROWDOT_BF16: {

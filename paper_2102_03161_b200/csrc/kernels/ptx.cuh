@@ -181,6 +181,23 @@ __device__ __forceinline__ void gelu_and_grad_f(float x, float& g, float& gp) {
   gp = fmaf(0.5f, t, 0.5f) + h * fmaf(-t, t, 1.0f) * fmaf(3.0f * kGeluC1, u, kGeluC0);
 }
 
+// Two columns at once on the packed fp32 pipe (FFMA2 / FMUL2: one issue slot
+// for two IEEE fp32 operations).  Same function as gelu_and_grad_f with the
+// 0.5 factors folded: a = (1 + t) / 2, g = x a,
+// g' = a + x (1 - t^2) (C0 + 3 C1 x^2) / 2.
+__device__ __forceinline__ void gelu_and_grad_f2(float2 x, float2& g, float2& gp) {
+  const float2 u = __fmul2_rn(x, x);
+  const float2 arg = __fmul2_rn(x, __ffma2_rn(make_float2(kGeluC1, kGeluC1), u,
+                                              make_float2(kGeluC0, kGeluC0)));
+  const float2 t = make_float2(tanh_approx(arg.x), tanh_approx(arg.y));
+  const float2 a = __ffma2_rn(make_float2(0.5f, 0.5f), t, make_float2(0.5f, 0.5f));
+  g = __fmul2_rn(x, a);
+  const float2 b = __ffma2_rn(make_float2(-t.x, -t.y), t, make_float2(1.f, 1.f));
+  const float2 c = __ffma2_rn(make_float2(1.5f * kGeluC1, 1.5f * kGeluC1), u,
+                              make_float2(0.5f * kGeluC0, 0.5f * kGeluC0));
+  gp = __ffma2_rn(__fmul2_rn(x, b), c, a);
+}
+
 // After this, lane j holds sum over the warp's 32 lanes of v[j] (31 shuffles).
 __device__ __forceinline__ float warp_transpose_sum32(float (&v)[32]) {
   const int lane = threadIdx.x & 31;
