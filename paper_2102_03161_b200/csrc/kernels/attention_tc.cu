@@ -1080,7 +1080,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
   uint8_t* smem = align1024(smem_raw);
   const int nt = (p.T + kTile - 1) / kTile;
   const int Tr = nt * kTile;
-  const int Tp = p.Tp;  // S columns (pad64(T) <= 256)
+  // S columns: N = pad16(T) <= 256 (keys T..Tn-1 hit the zero-filled K rows;
+  // their P is written as 0, and the PV contraction stops at Tn)
+  const int Tn = (p.T + 15) / 16 * 16;
   const size_t buf_bytes = size_t(3 * Tr) * kRowBytes;
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 2 * buf_bytes);
   // per pipeline c: full / empty of the operand regions Q_0, Q_1, K, V (so the
@@ -1139,7 +1141,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     const int c = warp - 1;
     uint64_t* pb = bar + c * NB;
     const uint32_t tS = tmem + uint32_t(256 * c);
-    const uint32_t idesc_s = umma_idesc_bf16(128, Tp, false, false);
+    const uint32_t idesc_s = umma_idesc_bf16(128, Tn, false, false);
     const uint32_t idesc_o = umma_idesc_bf16(128, kD, false, true);
     int i = 0, k = 0;  // k: tiles done by this pipeline
     for (int bh = blockIdx.x; bh < n_heads; bh += gridDim.x, ++i) {
@@ -1166,7 +1168,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         mbar_wait(&pb[PF], k & 1);
         if (t == 0) mbar_wait(&pb[FV], n & 1);
         tc_fence_after();
-        for (int kk = 0; kk < Tp / 16; ++kk)
+        for (int kk = 0; kk < Tn / 16; ++kk)
           tc_mma_ts_ws(tS + 128, tS + uint32_t(kk * 8), v0 + uint64_t(kk * 128), idesc_o,
                        kk > 0 ? 1u : 0u);
         tc_commit_ws(&pb[OF]);
@@ -1180,7 +1182,6 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     const int row = quarter * 32 + lane;
     const uint32_t lane_off = uint32_t(quarter * 32) << 16;
     const uint32_t tS = tmem + uint32_t(256 * c) + lane_off;
-    const int nch = (p.T + 31) / 32;  // S chunks holding valid keys
     const float sl2 = p.scale_log2;
     int i = 0, k = 0;
     for (int bh = blockIdx.x; bh < n_heads; bh += gridDim.x, ++i) {
@@ -1191,70 +1192,105 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         mbar_wait(&pb[SF], k & 1);
         tc_fence_after();
         EPS_TRACE(c == 0 && k < 32 && warp == 4 && lane == 0, 832 + k * 5 + 1);
-        float m = -FLT_MAX;
-        for (int ch = 0; ch < nch; ++ch) {
-          uint32_t r[32];
-          tmem_ld_32x32(tS + uint32_t(ch * 32), r);
-          tmem_ld_wait();
-          if (ch * 32 + 32 <= p.T) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) m = fmaxf(m, __uint_as_float(r[j]));
-          } else {
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (ch * 32 + j < p.T) m = fmaxf(m, __uint_as_float(r[j]));
-          }
-        }
-        const float ms = m * sl2;
-        float sum = 0.f;
-        for (int ch = 0; ch < Tp / 32; ++ch) {
+        // One pass over S.  The exponent reference ms is the max of chunk 0,
+        // not the row max: any reference within a few dozen binades of the row
+        // max gives the same P / rowsum in fp32 and bf16 (both scale-free), so
+        // the separate max pass (a second TMEM read of S, the binding
+        // bandwidth here) is skipped.  A chunk whose max exceeds ms by more
+        // than 2^32 rescales the P chunks already written (warp-collective,
+        // rare) and raises ms.
+        float ms = 0.f;
+        const float2 sl2x2 = make_float2(sl2, sl2);
+        float2 sum2 = make_float2(0.f, 0.f);  // two interleaved partial sums (packed FADD2)
+        for (int ch = 0; ch * 32 < Tn; ++ch) {
           uint32_t pk[16];
-          if (ch * 32 + 32 <= p.T) {  // full chunk: no key mask
-            uint32_t r[32];
-            tmem_ld_32x32(tS + uint32_t(ch * 32), r);
-            tmem_ld_wait();
+          const int rem = p.T - ch * 32;  // valid keys in this chunk (>= 1)
+          uint32_t r[32];
+          if (rem <= 16) tmem_ld_32x32_x16(tS + uint32_t(ch * 32), reinterpret_cast<uint32_t(&)[16]>(r));
+          else tmem_ld_32x32(tS + uint32_t(ch * 32), r);
+          tmem_ld_wait();
+          // the chunk max is needed up front only for chunk 0; later chunks
+          // compute exps and max side by side and redo the exps on a rescale
+          auto chunk_max = [&]() {
+            float cm = -FLT_MAX;
+            if (rem >= 32) {
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              const float e0 = fast_exp2(fmaf(__uint_as_float(r[2 * j]), sl2, -ms));
-              const float e1 = fast_exp2(fmaf(__uint_as_float(r[2 * j + 1]), sl2, -ms));
-              sum += e0 + e1;
-              pk[j] = pack_bf16(e0, e1);
+              for (int j = 0; j < 32; ++j) cm = fmaxf(cm, __uint_as_float(r[j]));
+            } else if (rem <= 16) {
+#pragma unroll
+              for (int j = 0; j < 16; ++j)
+                if (j < rem) cm = fmaxf(cm, __uint_as_float(r[j]));
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (j < rem) cm = fmaxf(cm, __uint_as_float(r[j]));
             }
-          } else if (ch < nch && p.T - ch * 32 <= 16) {
-            // tail chunk with <= 16 valid keys: half the loads and exps
-            uint32_t r[16];
-            tmem_ld_32x32_x16(tS + uint32_t(ch * 32), r);
-            tmem_ld_wait();
+            return cm * sl2;
+          };
+          auto chunk_exp = [&](float msr) {
+            const float2 nms2 = make_float2(-msr, -msr);
+            float2 cs = make_float2(0.f, 0.f);
+            if (rem >= 32) {  // full chunk: no key mask
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              const int kk = ch * 32 + 2 * j;
-              const float e0 = kk < p.T ? fast_exp2(fmaf(__uint_as_float(r[2 * j]), sl2, -ms)) : 0.f;
-              const float e1 =
-                  kk + 1 < p.T ? fast_exp2(fmaf(__uint_as_float(r[2 * j + 1]), sl2, -ms)) : 0.f;
-              sum += e0 + e1;
-              pk[j] = pack_bf16(e0, e1);
+              for (int j = 0; j < 16; ++j) {
+                const float2 a = __ffma2_rn(
+                    make_float2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1])), sl2x2, nms2);
+                const float2 e = make_float2(fast_exp2(a.x), fast_exp2(a.y));
+                cs = __fadd2_rn(cs, e);
+                pk[j] = pack_bf16(e.x, e.y);
+              }
+            } else if (rem <= 16) {  // tail chunk with <= 16 valid keys: half the exps
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const float2 a = __ffma2_rn(
+                    make_float2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1])), sl2x2, nms2);
+                const float2 e = make_float2(2 * j < rem ? fast_exp2(a.x) : 0.f,
+                                             2 * j + 1 < rem ? fast_exp2(a.y) : 0.f);
+                cs = __fadd2_rn(cs, e);
+                pk[j] = pack_bf16(e.x, e.y);
+              }
+#pragma unroll
+              for (int j = 8; j < 16; ++j) pk[j] = 0u;
+            } else {
+#pragma unroll
+              for (int j = 0; j < 16; ++j) {
+                const float2 a = __ffma2_rn(
+                    make_float2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1])), sl2x2, nms2);
+                const float2 e = make_float2(2 * j < rem ? fast_exp2(a.x) : 0.f,
+                                             2 * j + 1 < rem ? fast_exp2(a.y) : 0.f);
+                cs = __fadd2_rn(cs, e);
+                pk[j] = pack_bf16(e.x, e.y);
+              }
             }
+            return cs;
+          };
+          if (ch == 0) ms = chunk_max();
+          float2 cs = chunk_exp(ms);
+          if (ch > 0) {
+            const float cms = chunk_max();
+            const bool up = cms > ms + 32.f;
+            if (__any_sync(0xffffffffu, up)) {
+              const float ms_new = up ? cms : ms;
+              const float f = fast_exp2(ms - ms_new);  // 1 on lanes without overflow
+              sum2 = __fmul2_rn(sum2, make_float2(f, f));
+              tmem_st_wait();
+              for (int pc = 0; pc < ch; ++pc) {
+                uint32_t q16[16];
+                tmem_ld_32x32_x16(tS + uint32_t(pc * 16), q16);
+                tmem_ld_wait();
 #pragma unroll
-            for (int j = 8; j < 16; ++j) pk[j] = 0u;
-          } else if (ch < nch) {
-            uint32_t r[32];
-            tmem_ld_32x32(tS + uint32_t(ch * 32), r);
-            tmem_ld_wait();
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              const int kk = ch * 32 + 2 * j;
-              const float e0 = kk < p.T ? fast_exp2(fmaf(__uint_as_float(r[2 * j]), sl2, -ms)) : 0.f;
-              const float e1 =
-                  kk + 1 < p.T ? fast_exp2(fmaf(__uint_as_float(r[2 * j + 1]), sl2, -ms)) : 0.f;
-              sum += e0 + e1;
-              pk[j] = pack_bf16(e0, e1);
+                for (int j = 0; j < 16; ++j)
+                  q16[j] = pack_bf16(bf16_lo(q16[j]) * f, bf16_hi(q16[j]) * f);
+                tmem_st_32x32_x16(tS + uint32_t(pc * 16), q16);
+              }
+              ms = ms_new;
+              cs = chunk_exp(ms);
             }
-          } else {
-#pragma unroll
-            for (int j = 0; j < 16; ++j) pk[j] = 0u;  // keys past T: P = 0
           }
+          sum2 = __fadd2_rn(sum2, cs);
           tmem_st_32x32_x16(tS + uint32_t(ch * 16), pk);
         }
+        const float sum = sum2.x + sum2.y;
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();

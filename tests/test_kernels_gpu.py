@@ -110,6 +110,35 @@ def test_attention_fwd_bwd(cuda, B, T, H, dh):
         assert _rel(dbias2, dbias) < 1e-2
 
 
+@pytest.mark.parametrize("T,spike", [(197, 40), (197, 196), (128, 100), (256, 255)])
+def test_attention_fwd_score_spike(cuda, T, spike):
+    """Keys whose score exceeds every score of the first 32 keys by far more than
+    2^32 (in exp2 units): the forward's one-pass softmax must rescale the P
+    chunks it already wrote.  Rows get spikes of different sizes, some none."""
+    B, H, dh = 2, 3, 64
+    D = H * dh
+    g = torch.Generator(device=cuda).manual_seed(spike)
+    qkv = torch.randn(B * T, 3 * D, device=cuda, generator=g)
+    qkv = qkv.reshape(B, T, 3 * D)
+    q = qkv[:, :, :D].reshape(B, T, H, dh)
+    k = qkv[:, :, D:2 * D].reshape(B, T, H, dh)
+    # queries share a direction u per (sample, head); key `spike` is u scaled
+    # with the head index, so its score leads by ~46 / 92 / 138 exp2 units
+    u = torch.randn(B, 1, H, dh, device=cuda, generator=g)
+    q.mul_(0.5).add_(u)
+    k[:, spike] = u[:, 0] * (4.0 * (torch.arange(H, device=cuda) + 1)).reshape(1, H, 1)
+    q[:, ::3] *= 2.0
+    qkv = qkv.reshape(B * T, 3 * D).bfloat16()
+    out = torch.empty(B * T, D, device=cuda, dtype=torch.bfloat16)
+    lse = torch.empty(B, H, T, device=cuda)
+    ops.call("eps_attn_fwd", qkv, out, lse, B, T, H, dh, C.c_float(dh ** -0.5), _s())
+    ref, ref_lse = _attn_ref(qkv.float(), B, T, H, dh)
+    torch.cuda.synchronize()
+    assert torch.isfinite(out.float()).all() and torch.isfinite(lse).all()
+    assert _rel(out, ref) < 1e-2
+    assert ((lse - ref_lse).abs() / ref_lse.abs().clamp_min(1.0)).max().item() < 1e-3
+
+
 def test_softmax_xent(cuda):
     B, Cn = 37, 1000
     g = torch.Generator(device=cuda).manual_seed(1)
