@@ -137,28 +137,44 @@ __device__ __forceinline__ void stage_bf16(uint32_t base, int lane, const float 
 }
 
 // Column sums of a staged 32x32 bf16 chunk (SWIZZLE_64B rows), read back
-// column-wise: lane l sums columns 2(l%16), 2(l%16)+1 over rows 16(l/16)..+16;
-// the two row halves meet with one shuffle.  Cheaper than a register
-// transpose (16 shared loads instead of 31 shuffles + 62 selects) and sums
-// exactly the stored (rounded) values.  Result valid in lanes 0..15.
-__device__ __forceinline__ float2 staged_colsum_bf16(uint32_t base, int lane) {
-  const int p = lane & 15, h = lane >> 4;
-  const uint32_t col_off = uint32_t((p & 3) * 4);
-  const int q = p >> 2;
-  float s0 = 0.f, s1 = 0.f;
+// column-wise -- cheaper than a register transpose, and it sums exactly the
+// stored (rounded) values.
+// Lane l sums columns 4(l%8)..+3
+// over rows l/8, l/8 + 4, ... (eight 8-byte loads, two wavefronts each), the
+// four row groups meet with two shuffle rounds; lanes 0..7 then add their
+// float4 to global memory with one vector reduction each (8 per chunk
+// instead of 32 scalar atomics -- the bias-gradient targets are shared by
+// every CTA on the same column tile, so fewer L2 atomic ops matter).
+__device__ __forceinline__ float4 staged_colsum4_bf16(uint32_t base, int lane) {
+  const int g = lane & 7, h = lane >> 3;
+  const uint32_t q = uint32_t(g >> 1), half_off = uint32_t((g & 1) * 8);
+  float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    const int r = h * 16 + i;
-    uint32_t w;
-    asm volatile("ld.shared.b32 %0, [%1];"
-                 : "=r"(w)
-                 : "r"(base + uint32_t(r * 64 + ((q ^ ((r >> 1) & 3)) << 4)) + col_off));
-    s0 += bf16_lo(w);
-    s1 += bf16_hi(w);
+  for (int j = 0; j < 8; ++j) {
+    const int r = 4 * j + h;
+    uint32_t w0, w1;
+    asm volatile("ld.shared.v2.b32 {%0, %1}, [%2];"
+                 : "=r"(w0), "=r"(w1)
+                 : "r"(base + uint32_t(r * 64) + ((q ^ uint32_t((r >> 1) & 3)) << 4) + half_off));
+    s.x += bf16_lo(w0);
+    s.y += bf16_hi(w0);
+    s.z += bf16_lo(w1);
+    s.w += bf16_hi(w1);
   }
-  s0 += __shfl_xor_sync(0xffffffffu, s0, 16);
-  s1 += __shfl_xor_sync(0xffffffffu, s1, 16);
-  return make_float2(s0, s1);
+#pragma unroll
+  for (int o = 8; o <= 16; o <<= 1) {
+    s.x += __shfl_xor_sync(0xffffffffu, s.x, o);
+    s.y += __shfl_xor_sync(0xffffffffu, s.y, o);
+    s.z += __shfl_xor_sync(0xffffffffu, s.z, o);
+    s.w += __shfl_xor_sync(0xffffffffu, s.w, o);
+  }
+  return s;
+}
+
+__device__ __forceinline__ void red_add_v4(float* addr, float4 v) {
+  asm volatile("red.relaxed.gpu.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(addr), "f"(v.x),
+               "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
 }
 
 __device__ __forceinline__ void stage_f32(uint32_t base, int lane, const float (&v)[32]) {
@@ -543,10 +559,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         ++out_n;
         if ((epi == EPS_EPI_DGELU_BF16 || epi == EPS_EPI_MUL_BF16) && args.colsum != nullptr) {
           // rows past M were zero-filled by TMA (and aux zeroed), so they contribute 0
-          const float2 cs = staged_colsum_bf16(out_s, lane);
-          if (lane < 16) {
-            if (2 * lane < valid) atomicAdd(args.colsum + col0 + 2 * lane, cs.x);
-            if (2 * lane + 1 < valid) atomicAdd(args.colsum + col0 + 2 * lane + 1, cs.y);
+          const float4 cs = staged_colsum4_bf16(out_s, lane);
+          if (lane < 8) {
+            float* dst = args.colsum + col0 + 4 * lane;
+            if (4 * lane + 3 < valid) {
+              red_add_v4(dst, cs);
+            } else {
+              if (4 * lane < valid) atomicAdd(dst, cs.x);
+              if (4 * lane + 1 < valid) atomicAdd(dst + 1, cs.y);
+              if (4 * lane + 2 < valid) atomicAdd(dst + 2, cs.z);
+            }
           }
         }
         if (aux_in && !aux_tma) {

@@ -72,9 +72,12 @@ def test_gemm_epilogues(cuda):
     _close(colsum, refd.sum(0), rtol=2e-2)
 
 
-def test_gemm_gelu2_mul(cuda):
-    """FC1 forward stores gelu(u) and gelu'(u); the FC2 dgrad multiplies by gelu'."""
-    M, N, K = 1000, 3072, 768
+@pytest.mark.parametrize("M,N", [(1000, 3072), (77, 200), (4096, 1000)])
+def test_gemm_gelu2_mul(cuda, M, N):
+    """FC1 forward stores gelu(u) and gelu'(u); the FC2 dgrad multiplies by gelu'
+    and sums columns (bias gradient; N = 200 / 1000 end in partial 32-column
+    chunks of the vector reduction)."""
+    K = 768
     g = torch.Generator(device=cuda).manual_seed(9)
     a = torch.randn(M, K, device=cuda, generator=g).bfloat16()
     b = (torch.randn(N, K, device=cuda, generator=g) * 0.05).bfloat16()
