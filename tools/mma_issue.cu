@@ -1,6 +1,7 @@
 // Microbenchmark: tcgen05.mma issue rate from one warp, two issue styles.
 //   mode 0: one lane (if lane == 0), descriptors rebuilt per MMA (old style)
 //   mode 1: whole warp converged, elect.sync per MMA, descriptors precomputed
+//   mode 2: one lane, descriptors precomputed
 // nvcc -std=c++17 -gencode arch=compute_100a,code=sm_100a
 //   -I paper_2102_03161_b200/csrc/kernels -Iinclude tools/mma_issue.cu -o tools/mma_issue.bin
 #include <cuda_runtime.h>
@@ -50,6 +51,16 @@ __global__ void mma_bench(int iters, long long* out, int mode) {
                         umma_sdesc(smem_addr(b) + kk * 32, 16, 1024), idesc, (i | kk) ? 1u : 0u);
         tc_commit(&bar);
       }
+    } else if (mode == 2) {
+      // one lane, descriptors precomputed (uniform arithmetic only)
+      const uint64_t da = umma_sdesc(smem_addr(a), 16, 1024), db = umma_sdesc(smem_addr(b), 16, 1024);
+      if (lane == 0) {
+        for (int i = 0; i < iters; ++i)
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            tc_mma_bf16(tmem, da + 2 * kk, db + 2 * kk, idesc, (i | kk) ? 1u : 0u);
+        tc_commit(&bar);
+      }
     } else {
       const uint64_t da = umma_sdesc(smem_addr(a), 16, 1024), db = umma_sdesc(smem_addr(b), 16, 1024);
       for (int i = 0; i < iters; ++i)
@@ -80,7 +91,7 @@ template <int N>
 void run(long long* d) {
   const int smem = (128 + N) * 128 + 2048;
   cudaFuncSetAttribute(mma_bench<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  for (int mode = 0; mode < 2; ++mode) {
+  for (int mode = 0; mode < 3; ++mode) {
     const int iters = 1000;
     mma_bench<N><<<1, 128, smem>>>(iters, d, mode);
     cudaDeviceSynchronize();
