@@ -387,6 +387,12 @@ int eps_gemm_bf16(int a_mn_major, int b_mn_major, int epilogue, const void* A, c
 /* CTA-pair (cta_group::2, 256-row) GEMM tiles: mode 1 on (default), 0 off;
  * mode < 0 only queries.  Returns the mode in effect. */
 int eps_gemm_pair_mode(int mode);
+/* Diagnostics: every GEMM launch adds its per-role wait cycles to
+ * `counters` (device, 7 x uint64: MMA-warp span, its accumulator-empty and
+ * operand-full waits, producer slot waits, epilogue warp 0 accumulator-full
+ * and store-slot waits, epilogue span; leader CTAs / all CTAs summed).
+ * NULL turns it off (the default). */
+int eps_gemm_prof(void* counters);
 /* Programmatic dependent launch of the GEMM / attention / LayerNorm kernels
  * (each overlaps its launch and prologue with its predecessor's tail): mode
  * 1 on (default), 0 off; mode < 0 only queries. */

@@ -49,6 +49,7 @@ struct GemmArgs {
   const float* bias;
   void* aux;
   float* colsum;
+  unsigned long long* prof;  // diagnostics (eps_gemm_prof): wait-cycle counters, else null
 };
 
 // EPIB: per-epilogue-warp smem bytes.  4 KB: output staging only (aux inputs
@@ -293,6 +294,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int units = tiles * args.splits;
   const int kblocks_total = (args.K + kBK - 1) / kBK;
 
+  // diagnostics: cycles each role spends waiting, summed over CTAs (eps_gemm_prof)
+  long long pw_slot = 0, pw_full = 0, pw_empty = 0, pw_tfull = 0, pw_store = 0;
+  const long long p_t0 = args.prof ? clock64() : 0;
   if (warp == kTmaWarp) {
     if (lane == 0) {
       int stage = 0;
@@ -305,7 +309,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int kb0 = split * args.k_blocks_per_split;
         const int kb1 = min(kb0 + args.k_blocks_per_split, kblocks_total);
         for (int kb = kb0; kb < kb1; ++kb) {
+          const long long w0 = args.prof ? clock64() : 0;
           mbar_wait(&empty[stage], phase ^ 1);
+          if (args.prof) pw_slot += clock64() - w0;
           uint8_t* sa = ring + stage * Cfg::kStageBytes;
           uint8_t* sb = sa + Cfg::kABytes;
           if constexpr (PAIR) {
@@ -336,11 +342,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int split = u / tiles;
         const int kb0 = split * args.k_blocks_per_split;
         const int kb1 = min(kb0 + args.k_blocks_per_split, kblocks_total);
+        long long w0 = args.prof ? clock64() : 0;
         mbar_wait(&tmem_empty[acc], acc_phase ^ 1);
+        if (args.prof) pw_empty += clock64() - w0;
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + uint32_t(acc * BN);
         for (int kb = kb0; kb < kb1; ++kb) {
+          if (args.prof) w0 = clock64();
           mbar_wait(&full[stage], phase);
+          if (args.prof) pw_full += clock64() - w0;
           tc_fence_after();
           const uint32_t sa = smem_addr(ring + stage * Cfg::kStageBytes);
           const uint32_t sb = sa + Cfg::kABytes;
@@ -444,7 +454,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint4 xa[4];
       if (aux_in && !aux_tma && part < chunks)
         load_aux_row(auxp, args.ldc, my_row, args.M, n0 + part * 32, args.N, xa);
+      const long long w0 = args.prof ? clock64() : 0;
       mbar_wait(&tmem_full[acc], acc_phase);
+      if (args.prof) pw_tfull += clock64() - w0;
       tc_fence_after();
       const uint32_t taddr = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(acc * BN);
 #pragma unroll 1
@@ -485,8 +497,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         // reuse an out slot only after its previous TMA store has read it
         if (lane == 0) {
+          const long long w0 = args.prof ? clock64() : 0;
           if (n_out == 1) bulk_wait_read<0>();
           else bulk_wait_read<1>();
+          if (args.prof) pw_store += clock64() - w0;
         }
         __syncwarp();
         const uint32_t out_off = (out_n % uint32_t(n_out)) * uint32_t(out_bytes);
@@ -588,6 +602,23 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) bulk_wait<0>();
   }
 
+  if (args.prof != nullptr && lane == 0) {
+    // [0] span of the MMA warp, [1] its tmem_empty waits, [2] its full waits,
+    // [3] producer slot waits, [4] epilogue warp 0 tmem_full waits, [5] its
+    // store-slot waits, [6] epilogue warp 0 span
+    const long long span = clock64() - p_t0;
+    if (warp == kMmaWarp && (!PAIR || leader)) {
+      atomicAdd(args.prof + 0, (unsigned long long)span);
+      atomicAdd(args.prof + 1, (unsigned long long)pw_empty);
+      atomicAdd(args.prof + 2, (unsigned long long)pw_full);
+    } else if (warp == kTmaWarp && (!PAIR || leader)) {
+      atomicAdd(args.prof + 3, (unsigned long long)pw_slot);
+    } else if (warp == 0 && (!PAIR || leader)) {
+      atomicAdd(args.prof + 4, (unsigned long long)pw_tfull);
+      atomicAdd(args.prof + 5, (unsigned long long)pw_store);
+      atomicAdd(args.prof + 6, (unsigned long long)span);
+    }
+  }
   tc_fence_before();
   __syncthreads();
   if constexpr (PAIR) cluster_sync_all();  // no remote traffic targets an exited CTA
@@ -639,6 +670,13 @@ int launch(const void* A, const void* B, int64_t lda, int64_t ldb, GemmArgs args
 
 // CTA-pair tiles on (1, default; EPS_GEMM_PAIR=0 in the environment or
 // eps_gemm_pair_mode(0) turns them off for A/B comparisons).
+// Diagnostics: a device buffer of 7 u64 wait-cycle counters every GEMM launch
+// adds to (eps_gemm_prof; null = off, the default).
+std::atomic<unsigned long long*>& gemm_prof_buf() {
+  static std::atomic<unsigned long long*> buf{nullptr};
+  return buf;
+}
+
 std::atomic<int>& gemm_pair_mode() {
   static std::atomic<int> mode{[] {
     const char* e = std::getenv("EPS_GEMM_PAIR");
@@ -652,6 +690,11 @@ std::atomic<int>& gemm_pair_mode() {
 extern "C" int eps_pdl_mode(int mode) {
   if (mode >= 0) eps_k::pdl_mode().store(mode);
   return eps_k::pdl_mode().load();
+}
+
+extern "C" int eps_gemm_prof(void* counters) {
+  eps_k::gemm_prof_buf().store(static_cast<unsigned long long*>(counters));
+  return EPS_OK;
 }
 
 extern "C" int eps_gemm_pair_mode(int mode) {
@@ -692,6 +735,7 @@ extern "C" int eps_gemm_bf16(int a_mn_major, int b_mn_major, int epilogue, const
                epilogue == EPS_EPI_BIAS_RESID_BF16) ? bias : nullptr;
   args.aux = aux;
   args.colsum = colsum;
+  args.prof = gemm_prof_buf().load();
   const int kblocks = int((K + kBK - 1) / kBK);
   // CTA pairs (256-row tiles, cta_group::2) for every GEMM with enough rows
   // and a 256-multiple N (all ViT-B / BERT block GEMMs at full batch);
