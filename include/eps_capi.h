@@ -452,6 +452,11 @@ int eps_grad_sqnorm_segmented(const float* const* tensors, const int64_t* n, con
 /* AutoCache store: rows of row_bytes, keyed by sample id. */
 int eps_cache_gather(const void* store, const int64_t* ids, int n, int64_t row_bytes,
                      void* dst, void* stream);
+/* Same gather on `ctas` CTAs (grid-stride, four 16-byte loads in flight per
+ * thread): the host tier's prefetch window runs it on a copy stream beside the
+ * compute kernels. */
+int eps_cache_gather_bg(const void* store, const int64_t* ids, int n, int64_t row_bytes,
+                        void* dst, int ctas, void* stream);
 int eps_cache_scatter(void* store, const int64_t* ids, int n, int64_t row_bytes,
                       const void* src, void* stream);
 

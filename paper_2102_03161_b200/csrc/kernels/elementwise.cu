@@ -233,6 +233,37 @@ __global__ void cache_copy_kernel(const uint8_t* __restrict__ src, uint8_t* __re
     d[i] = s[i];
 }
 
+// Background gather for the host tier's prefetch window: a few CTAs walk all
+// (row, 16-byte) pairs with four independent 16-byte loads in flight per
+// thread (enough outstanding host-link reads for full PCIe rate from ~8 SMs),
+// so the copy overlaps the compute kernels instead of flooding every SM.
+__global__ void __launch_bounds__(256) cache_gather_bg_kernel(
+    const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, const int64_t* __restrict__ ids,
+    int n, int64_t row_bytes) {
+  const int64_t n16 = row_bytes / 16, total = n16 * n;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+  for (int64_t base = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; base < total;
+       base += 4 * stride) {
+    uint4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t i = base + u * stride;
+      if (i < total) {
+        const int64_t r = i / n16, c = i - r * n16;
+        v[u] = reinterpret_cast<const uint4*>(src + ids[r] * row_bytes)[c];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t i = base + u * stride;
+      if (i < total) {
+        const int64_t r = i / n16, c = i - r * n16;
+        reinterpret_cast<uint4*>(dst + r * row_bytes)[c] = v[u];
+      }
+    }
+  }
+}
+
 __global__ void rows_copy_kernel(const uint16_t* __restrict__ src, int64_t src_stride,
                                  uint16_t* __restrict__ dst, int64_t dst_stride, int rows,
                                  int64_t d) {
@@ -478,6 +509,16 @@ extern "C" int eps_cache_gather(const void* store, const int64_t* ids, int n, in
   dim3 grid(unsigned(std::min<int64_t>((row_bytes / 16 + 255) / 256, 64)), unsigned(n));
   count_launch(); cache_copy_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const uint8_t*>(store), static_cast<uint8_t*>(dst), ids, row_bytes, true);
+  return ok_or_cuda();
+}
+
+extern "C" int eps_cache_gather_bg(const void* store, const int64_t* ids, int n,
+                                   int64_t row_bytes, void* dst, int ctas, void* stream) {
+  if (n <= 0) return EPS_OK;
+  if (row_bytes % 16 || ctas <= 0) return EPS_EINVAL;
+  count_launch();
+  cache_gather_bg_kernel<<<ctas, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const uint8_t*>(store), static_cast<uint8_t*>(dst), ids, n, row_bytes);
   return ok_or_cuda();
 }
 

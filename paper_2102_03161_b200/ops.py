@@ -53,6 +53,7 @@ def _declare(lib):
         "eps_softmax_xent_bias": [vp, vp, vp, vp, vp, i32, i32, i32, f32, vp],
         "eps_grad_sqnorm_segmented": [vp, vp, vp, i32, vp, i32, vp, C.c_size_t, vp],
         "eps_cache_gather": [vp, vp, i32, i64, vp, vp],
+        "eps_cache_gather_bg": [vp, vp, i32, i64, vp, i32, vp],
         "eps_cache_scatter": [vp, vp, i32, i64, vp, vp],
         "eps_sgd_momentum": [vp, vp, vp, vp, i64, f32, f32, f32, vp],
         "eps_adamw": [vp, vp, vp, vp, vp, i64, f32, f32, f32, f32, f32, i32, vp],

@@ -27,6 +27,7 @@ device times.
 """
 from __future__ import annotations
 
+import ctypes as C
 import math
 import os
 from dataclasses import dataclass, field
@@ -35,7 +36,7 @@ from typing import List, Optional
 import torch
 import torch.distributed as dist
 
-from . import LIB_PATH
+from . import LIB_PATH, ops
 from .capi import ClusterSpec, EpsApi
 from .configs import Geometry
 from .pipeline import StagePlan, StageRunner, Transport
@@ -75,7 +76,8 @@ class Trainer:
     def __init__(self, scenario: dict, geometry: Geometry, *, iterations_per_epoch: int,
                  seed: int = 17, lr: float = 1e-3, momentum: float = 0.9,
                  rank: int = 0, world: int = 1, device=None, host_staged: bool = False,
-                 device_norms: bool = True, cache_tier: str = "hbm", peer: bool = False):
+                 device_norms: bool = True, cache_tier: str = "hbm", peer: bool = False,
+                 cache_prefetch: bool = True):
         self.g = geometry
         self.api = EpsApi(LIB_PATH, "eps_")
         self.planner = Planner(self.api, scenario)
@@ -113,6 +115,9 @@ class Trainer:
         if cache_tier == "host" and world > 1 and not host_staged:
             raise NotImplementedError("host-tier store exchange over NCCL (needs device staging)")
         self.cache_tier = cache_tier
+        self.cache_prefetch = cache_prefetch
+        self.cache_prefetch_ctas = 8  # SMs the background gather borrows
+        self._win_buf = None
         self.store: Optional[torch.Tensor] = None
         self.norms_prev: Optional[List[float]] = None
 
@@ -137,6 +142,20 @@ class Trainer:
         group = self.tp.group([p * plan.K for p in range(plan.R)])
         if self.runner.stage == 0:
             self.tp.all_reduce(self.store, group)
+
+    def _window_setup(self):
+        """Two device staging buffers for the host tier's prefetch window."""
+        if self._win_buf is not None:
+            return
+        shape = (self.batch, self.g.tokens, self.g.hidden)
+        self._win_buf = [torch.empty(shape, dtype=torch.bfloat16, device=self.device)
+                         for _ in range(2)]
+        self._win_ids = torch.arange(self.batch, dtype=torch.int64, device=self.device)
+        self._win_copy = torch.cuda.Stream(device=self.device)
+        self._win_ready = [torch.cuda.Event(), torch.cuda.Event()]
+        self._win_free = [torch.cuda.Event(), torch.cuda.Event()]
+        for e in self._win_free:  # both slots start free
+            e.record(torch.cuda.current_stream(self.device))
 
     # -- one epoch -----------------------------------------------------------------------
     def run_epoch(self, epoch: int) -> EpochResult:
@@ -164,6 +183,28 @@ class Trainer:
         _, shards = self.api.redistribute(self.dataset, self.cluster, plan.K, epoch, self.seed)
         shard = torch.tensor(shards[pipe], dtype=torch.int64, device=self.device)
         iters = len(shards[pipe]) // self.batch
+        # Host-tier gather epochs: a sliding window over the epoch's rows --
+        # iteration it + 1's cached boundary activations are gathered from
+        # pinned host memory into a device staging buffer on a copy stream
+        # while iteration it computes, so the host link overlaps compute
+        # (SURVEY.md 8(f) row 1); the executor then gathers from the staging
+        # buffer (HBM) with identity ids.
+        window = (self.cache_tier == "host" and cache_mode == 1 and stage == 0
+                  and self.cache_prefetch and iters > 0)
+        if window:
+            self._window_setup()
+            stream = torch.cuda.current_stream(self.device)
+
+            def fetch(i):
+                slot = i % 2
+                self._win_copy.wait_event(self._win_free[slot])
+                rows = shard[i * self.batch:(i + 1) * self.batch]
+                ops.call("eps_cache_gather_bg", self.store, rows, self.batch,
+                         self.g.tokens * self.g.hidden * 2, self._win_buf[slot],
+                         self.cache_prefetch_ctas, C.c_void_p(self._win_copy.cuda_stream))
+                self._win_ready[slot].record(self._win_copy)
+
+            fetch(0)
         start.record()
         losses = []
         norms = None
@@ -171,9 +212,17 @@ class Trainer:
             ids = shard[it * self.batch:(it + 1) * self.batch]
             x = self.images.index_select(0, ids) if stage == 0 and cache_mode != 1 else None
             y = self.labels.index_select(0, ids)
+            store, sids = self.store, ids
+            if window:
+                if it + 1 < iters:
+                    fetch(it + 1)
+                stream.wait_event(self._win_ready[it % 2])
+                store, sids = self._win_buf[it % 2], self._win_ids
             loss = self.runner.iteration(x, y, self.batch, cache_mode=cache_mode,
-                                         cache_old=d.cache_old_boundary, store=self.store,
-                                         ids=ids)
+                                         cache_old=d.cache_old_boundary, store=store,
+                                         ids=sids)
+            if window:
+                self._win_free[it % 2].record(stream)
             self.runner.sync_grads()
             if it == iters - 1:
                 norms = self.runner.layer_sqnorms(self.ex.segments).sqrt()

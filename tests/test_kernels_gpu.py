@@ -203,6 +203,18 @@ def test_cache_gather_scatter(cuda):
     assert torch.equal(dst, src)
     assert torch.equal(store[ids], src)
     assert store[1].abs().max().item() == 0
+    # background gather (prefetch window): few CTAs, grid-stride; from a pinned
+    # host store too (read over the host link)
+    for ctas in (1, 3, 8):
+        dst2 = torch.empty_like(src)
+        ops.call("eps_cache_gather_bg", store, ids, 7, T * d * 2, dst2, ctas, _s())
+        torch.cuda.synchronize()
+        assert torch.equal(dst2, src)
+    host = store.cpu().pin_memory()
+    dst3 = torch.empty_like(src)
+    ops.call("eps_cache_gather_bg", host, ids, 7, T * d * 2, dst3, 8, _s())
+    torch.cuda.synchronize()
+    assert torch.equal(dst3, src)
 
 
 def test_patchify_assemble(cuda):

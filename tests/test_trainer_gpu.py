@@ -133,3 +133,30 @@ def test_measured_timeline_blocks(cuda):
     assert [b["kind"] for b in tl] == ["F", "B"]
     assert set(tl[0]) == {"device", "kind", "start_s", "end_s", "tag"}
     assert 0.0 <= tl[0]["start_s"] < tl[0]["end_s"] <= tl[1]["start_s"] < tl[1]["end_s"]
+
+
+def test_host_tier_prefetch_window_matches_hbm_tier(cuda):
+    """the host tier's gather epochs read their cached
+    boundary activations through the prefetch window (copy-stream gathers into
+    HBM staging, one iteration ahead).  Same bytes reach the executor, so every
+    epoch's loss and gradient norms equal the HBM tier's and the unwindowed
+    host tier's exactly."""
+    scen = _tiny_scenario(epochs=5)
+    scen["training"]["alpha"] = 0.5
+    scen["cache"]["policy"] = "always_on"
+    g = configs.GEOMETRIES["tiny-vit"]
+    runs = {}
+    for name, kw in {"hbm": dict(cache_tier="hbm"),
+                     "host": dict(cache_tier="host", cache_prefetch=False),
+                     "host+window": dict(cache_tier="host", cache_prefetch=True)}.items():
+        tr = Trainer(scen, g, iterations_per_epoch=3, device_norms=False, **kw)
+        runs[name] = [(r.l_frozen, r.cache_enabled, r.cache_moved, r.mean_loss, tuple(r.norms))
+                      for r in tr.run()]
+    assert any(r[1] and not r[2] for r in runs["hbm"])  # some epochs are pure gathers
+    for name in ("host", "host+window"):
+        for a, b in zip(runs[name], runs["hbm"]):
+            assert a[:3] == b[:3]
+            # bias-gradient reductions use float atomics (run-to-run order), so
+            # equal inputs agree to rounding, not bit for bit
+            assert abs(a[3] - b[3]) <= 1e-4 * abs(b[3])
+            assert all(abs(x - y) <= 1e-3 * max(abs(y), 1e-6) for x, y in zip(a[4], b[4]))
