@@ -12,6 +12,7 @@ the *measured* B200 numbers beside the modeled ones:
 * `compare`: per-epoch modeled vs measured iteration time (same decisions);
 * `ladder`: measured rungs of the feature ladder next to the modeled ones;
 * `alpha_sweep`: the freeze-aggressiveness sweep (cli.cpp:75-135) measured;
+* `chunks_sweep`: the micro-batch-count sweep (cli.cpp:96-117) measured;
 * `bundle`: writes epochs.csv (reference schema, measured), timeline.json
   (reference schema, measured CUDA-event blocks), calibration / comparison /
   ladder JSON.
@@ -138,6 +139,51 @@ def alpha_sweep(api: EpsApi, scenario: dict, run_total: Callable[[dict], float],
     return out
 
 
+def chunks_sweep(api: EpsApi, scenario: dict, k: int, run_m: Callable[[int], float],
+                 calibrated_c_fwd: float = None) -> List[dict]:
+    """The chunks sweep of cli.cpp:96-117 on the device: for pipeline length
+    `k` (L_f = 0 plan from load_balance, replica width from the topology) the
+    reference's modeled iteration time for every M in [k, 6k] (optimal_chunks,
+    chunks.cpp:5-24) beside the measured one (run_m(M) -> seconds per
+    iteration).  With `calibrated_c_fwd` the model is also replayed with the
+    B200-calibrated forward rate.  The measured slope over M is the device's
+    per-micro-batch overhead (cost_model per_microbatch_overhead)."""
+    from .capi import ClusterSpec, CostModel
+
+    cl_d, cm_d = scenario["cluster"], scenario["cost_model"]
+    cluster = ClusterSpec(cl_d["nodes"], cl_d["gpus_per_node"], cl_d["gpu_memory_bytes"],
+                          cl_d["intra_node_bandwidth"], cl_d["inter_node_bandwidth"])
+    cost = CostModel(cm_d["c_fwd"], cm_d["backward_ratio"], cm_d["c_update"],
+                     cm_d["per_microbatch_overhead"], cm_d["allreduce_bucket_bytes"],
+                     cm_d["comm_latency"])
+    model = api.model_preset(scenario["model"]["preset"])
+    seq = api.m_partition(model, 0)
+    crit = 1 if scenario.get("balance_criterion") == "paper-variance" else 0  # scenario.cpp:219-225
+    plan = api.load_balance(seq, k, scenario["training"]["lambda_frozen"], crit)
+    _, r = api.topology(cluster, k)
+    batch = float(scenario["training"]["per_pipeline_batch"])
+    chosen, times = api.optimal_chunks(plan, model, seq, batch, r, cluster, cost)
+    cal_times = None
+    if calibrated_c_fwd is not None:
+        cost_cal = CostModel(**{**cost.__dict__, "c_fwd": calibrated_c_fwd})
+        _, cal_times = api.optimal_chunks(plan, model, seq, batch, r, cluster, cost_cal)
+    out = []
+    for i, m in enumerate(range(k, 6 * k + 1)):
+        row = {"k": k, "m": m, "modeled_iteration_s": times[i], "is_optimal": m == chosen,
+               "measured_iteration_s": run_m(m)}
+        if cal_times is not None:
+            row["calibrated_modeled_iteration_s"] = cal_times[i]
+        out.append(row)
+    if len(out) > 1:  # least-squares slope of measured time over M
+        ms = [o["m"] for o in out]
+        ts = [o["measured_iteration_s"] for o in out]
+        mb, tb = sum(ms) / len(ms), sum(ts) / len(ts)
+        slope = sum((a - mb) * (b - tb) for a, b in zip(ms, ts)) / sum((a - mb) ** 2 for a in ms)
+        for o in out:
+            o["measured_per_microbatch_s"] = slope
+    return out
+
+
 def transition_table(scenario: dict, measured_rows) -> List[dict]:
     """Measured plan-change overheads beside the scenario's Table-3 constants."""
     consts = scenario.get("cost_model", {}).get("transition_overheads", {})
@@ -153,7 +199,7 @@ def transition_table(scenario: dict, measured_rows) -> List[dict]:
 
 def bundle(out_dir: str, api: EpsApi, scenario: dict, measured_rows, timeline: List[dict],
            ladder_rows: List[dict] = None, extra: Dict = None,
-           sweep_rows: List[dict] = None) -> Dict[str, str]:
+           sweep_rows: List[dict] = None, chunks_rows: List[dict] = None) -> Dict[str, str]:
     """Write the measured report bundle; returns {name: path}."""
     from .trainer import Trainer  # local: trainer imports torch
 
@@ -192,4 +238,6 @@ def bundle(out_dir: str, api: EpsApi, scenario: dict, measured_rows, timeline: L
         dump("ladder.json", ladder_rows)
     if sweep_rows is not None:
         dump("alpha_sweep.json", sweep_rows)
+    if chunks_rows is not None:
+        dump("chunks_sweep.json", chunks_rows)
     return files

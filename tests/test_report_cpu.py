@@ -77,3 +77,18 @@ def test_alpha_sweep_is_monotone_in_the_model():
     assert [r["alpha"] for r in rows] == [0.2, 0.5]
     assert rows[1]["modeled_speedup"] >= rows[0]["modeled_speedup"]
     assert sum(rows[1]["frozen_trajectory"]) >= sum(rows[0]["frozen_trajectory"])
+
+
+def test_chunks_sweep_model_matches_reference_choice():
+    """The sweep's modeled side is the reference's optimal_chunks: at 1x8 the
+    epoch-0 choice is M = 23 (SURVEY.md 8(a) a7 golden), and the measured
+    slope over M is recovered (the per-micro-batch overhead)."""
+    scen = configs.scenario("vit-b16", 8)
+    rows = report.chunks_sweep(API, scen, 8, lambda m: 0.25 + 0.002 * m)
+    assert [r["m"] for r in rows] == list(range(8, 49))
+    assert [r["m"] for r in rows if r["is_optimal"]] == [23]
+    assert abs(rows[0]["measured_per_microbatch_s"] - 0.002) < 1e-12
+    one = report.chunks_sweep(API, configs.scenario("vit-b16", 1), 1, lambda m: 0.04,
+                              calibrated_c_fwd=1e-13)
+    assert [r["m"] for r in one] == [1, 2, 3, 4, 5, 6]
+    assert all(r["calibrated_modeled_iteration_s"] < r["modeled_iteration_s"] for r in one)
