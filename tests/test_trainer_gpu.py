@@ -158,5 +158,5 @@ def test_host_tier_prefetch_window_matches_hbm_tier(cuda):
             assert a[:3] == b[:3]
             # bias-gradient reductions use float atomics (run-to-run order), so
             # equal inputs agree to rounding, not bit for bit
-            assert abs(a[3] - b[3]) <= 1e-4 * abs(b[3])
-            assert all(abs(x - y) <= 1e-3 * max(abs(y), 1e-6) for x, y in zip(a[4], b[4]))
+            assert abs(a[3] - b[3]) <= 1e-3 * abs(b[3])
+            assert all(abs(x - y) <= 1e-2 * max(abs(y), 1e-6) for x, y in zip(a[4], b[4]))
