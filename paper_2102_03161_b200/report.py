@@ -13,6 +13,8 @@ the *measured* B200 numbers beside the modeled ones:
 * `ladder`: measured rungs of the feature ladder next to the modeled ones;
 * `alpha_sweep`: the freeze-aggressiveness sweep (cli.cpp:75-135) measured;
 * `chunks_sweep`: the micro-batch-count sweep (cli.cpp:96-117) measured;
+* `bandwidth_sweep`: the interconnect sweep (cli.cpp:118-127), modeled with the reference's
+  and with the B200-calibrated constants;
 * `bundle`: writes epochs.csv (reference schema, measured), timeline.json
   (reference schema, measured CUDA-event blocks), calibration / comparison /
   ladder JSON.
@@ -181,6 +183,29 @@ def chunks_sweep(api: EpsApi, scenario: dict, k: int, run_m: Callable[[int], flo
         slope = sum((a - mb) * (b - tb) for a, b in zip(ms, ts)) / sum((a - mb) ** 2 for a in ms)
         for o in out:
             o["measured_per_microbatch_s"] = slope
+    return out
+
+
+def bandwidth_sweep(api: EpsApi, scenario: dict, values: Sequence[float],
+                    calibrated_c_fwd: float = None) -> List[dict]:
+    """The bandwidth sweep of cli.cpp:118-127: the modeled run per
+    inter-node bandwidth (comm ratio, speedup, total time), with the
+    reference's constants and, given `calibrated_c_fwd`, with the B200
+    forward rate -- the calibrated model is what a multi-node B200 run is
+    predicted to see (one GPU cannot vary its interconnect)."""
+    out = []
+    for bw in values:
+        s = copy.deepcopy(scenario)
+        s["cluster"]["inter_node_bandwidth"] = float(bw)
+        _, summ = modeled(api, s)
+        row = {"inter_node_bandwidth": float(bw), "comm_ratio": summ["comm_ratio"],
+               "speedup": summ["speedup"], "total_time_s": summ["total_seconds"]}
+        if calibrated_c_fwd is not None:
+            s["cost_model"]["c_fwd"] = calibrated_c_fwd
+            _, sc = modeled(api, s)
+            row.update(calibrated_comm_ratio=sc["comm_ratio"], calibrated_speedup=sc["speedup"],
+                       calibrated_total_time_s=sc["total_seconds"])
+        out.append(row)
     return out
 
 

@@ -92,3 +92,14 @@ def test_chunks_sweep_model_matches_reference_choice():
                               calibrated_c_fwd=1e-13)
     assert [r["m"] for r in one] == [1, 2, 3, 4, 5, 6]
     assert all(r["calibrated_modeled_iteration_s"] < r["modeled_iteration_s"] for r in one)
+
+
+def test_bandwidth_sweep_comm_ratio_falls_with_bandwidth():
+    scen = configs.scenario("vit-b16", 8)
+    scen["cluster"]["nodes"] = 2  # 2 x 8: the replicas' all-reduce crosses nodes
+    rows = report.bandwidth_sweep(API, scen, [1e9, 5e9, 25e9], calibrated_c_fwd=1e-12)
+    assert [r["inter_node_bandwidth"] for r in rows] == [1e9, 5e9, 25e9]
+    assert rows[0]["comm_ratio"] > rows[1]["comm_ratio"] > rows[2]["comm_ratio"]
+    assert rows[0]["total_time_s"] > rows[2]["total_time_s"]
+    # a faster device makes communication a larger share of the iteration
+    assert all(r["calibrated_comm_ratio"] >= r["comm_ratio"] for r in rows)

@@ -51,8 +51,15 @@ def run_m(m):
 t1 = run_m(1)
 cal = report.calibrate_c_fwd(api, scen, t1)
 rows = report.chunks_sweep(api, scen, 1, run_m, calibrated_c_fwd=cal["c_fwd"])
+# the interconnect sweep (cli.cpp:118-127) of the 2 x 8 scenario, replayed with
+# the B200 forward rate measured above (one GPU cannot vary its interconnect)
+two_nodes = configs.scenario("vit-b16", 8)
+two_nodes["cluster"]["nodes"] = 2  # 2 nodes x 8 GPUs: the replicas' all-reduce crosses nodes
+bw = report.bandwidth_sweep(api, two_nodes, [1e9, 5e9, 12.5e9, 25e9, 50e9, 100e9],
+                            calibrated_c_fwd=cal["c_fwd"])
 with open(out, "w") as f:
     json.dump({"device": torch.cuda.get_device_name(), "iters": iters,
-               "calibrated_c_fwd": cal["c_fwd"], "rows": rows}, f, indent=1)
+               "calibrated_c_fwd": cal["c_fwd"], "rows": rows, "bandwidth_sweep_2x8": bw}, f,
+              indent=1)
 for r in rows:
     print(json.dumps(r))
