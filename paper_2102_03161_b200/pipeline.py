@@ -292,13 +292,17 @@ class StageRunner:
         return [self.tp.group(plan.dp_group_ranks(s)) for s in range(plan.K)]
 
     def set_plan(self, plan: StagePlan):
-        """Adopt an epoch plan; on a K / span change migrate parameters and
-        momentum from their previous owners (pipeline 0's stages) to all
-        ranks, then rebuild the per-stage data-parallel groups."""
+        """Adopt an epoch plan; on a K / ownership change migrate parameters
+        and momentum from their previous owners (pipeline 0's stages) to all
+        ranks, then (re)select the per-stage data-parallel groups."""
         if plan.K * plan.R != self.world:
             raise ValueError(f"plan needs {plan.K * plan.R} ranks, world has {self.world}")
         old = self.plan
-        if old is not None and (old.K, old.spans) != (plan.K, plan.spans):
+        # Parameters move only when ownership moves: with the same K and the
+        # same owner spans (a freeze-boundary move inside stage 0's span),
+        # every rank already holds -- and its DP replicas hold identical --
+        # values for everything it owns next epoch.
+        if old is not None and (old.K != plan.K or old.owner_spans() != plan.owner_spans()):
             self.migrate(old)
         self.plan = plan
         self.pipe, self.stage = plan.role(self.rank)
