@@ -303,7 +303,7 @@ class StageRunner:
         # every rank already holds -- and its DP replicas hold identical --
         # values for everything it owns next epoch.
         if old is not None and (old.K != plan.K or old.owner_spans() != plan.owner_spans()):
-            self.migrate(old)
+            self.migrate(old, plan)
         self.plan = plan
         self.pipe, self.stage = plan.role(self.rank)
         self.g0, self.g1 = plan.spans[self.stage]
@@ -326,17 +326,48 @@ class StageRunner:
                 hi, acc = g, 0
         return out
 
-    def migrate(self, old: StagePlan):
-        """Every parameter (and its momentum) is broadcast from the rank that
-        owned and updated it under `old` (stage s of pipeline 0 == rank s);
+    @staticmethod
+    def moved_runs(old: StagePlan, new: StagePlan) -> List[Tuple[int, int, int]]:
+        """Sublayer runs [g0, g1) whose parameters some rank must receive:
+        a rank whose new stage owns g but whose old stage did not.  Each run
+        is served by its old owner, stage s of pipeline 0 = rank s."""
+        def owner(plan, g):
+            for st, (a, b) in enumerate(plan.owner_spans()):
+                if a <= g < b:
+                    return st
+            raise ValueError(g)
+
+        world = new.K * new.R
+        runs: List[Tuple[int, int, int]] = []
+        for g in range(2 * new.layers):
+            os_, ns = owner(old, g), owner(new, g)
+            need = any(new.role(r)[1] == ns and old.role(r)[1] != os_ for r in range(world))
+            if not need:
+                continue
+            if runs and runs[-1][1] == g and runs[-1][2] == os_:
+                runs[-1] = (runs[-1][0], g + 1, os_)
+            else:
+                runs.append((g, g + 1, os_))
+        return runs
+
+    def gather_model(self):
+        """Every rank receives every parameter from its current owner (e.g. to
+        checkpoint or compare the whole model)."""
+        p = self.plan
+        everyone = StagePlan(1, self.world, 1, p.l_frozen, p.layers, ((0, 2 * p.layers),))
+        self.migrate(p, everyone)
+
+    def migrate(self, old: StagePlan, new: StagePlan):
+        """Parameters (and momentum) of every sublayer some rank newly owns are
+        broadcast from the rank that owned and updated them under `old`;
         the bf16 working copy is re-derived."""
         if self.world == 1:
             return  # a single rank owns everything already
-        for s, (g0, g1) in enumerate(old.owner_spans()):
+        for g0, g1, src in self.moved_runs(old, new):
             a, b = self.ex.param_range(g0, g1)
             if b > a:
-                self.tp.broadcast(self.ex.p32[a:b], s)
-                self.tp.broadcast(self.ex.mom[a:b], s)
+                self.tp.broadcast(self.ex.p32[a:b], src)
+                self.tp.broadcast(self.ex.mom[a:b], src)
         self.ex.p16.copy_(self.ex.p32)
 
     # -- one iteration -------------------------------------------------------------------

@@ -80,7 +80,7 @@ def _worker(rank, world, port, name, out_dir):
             run.step(lr=0.05)
             losses.append((float(loss), norms.tolist(), stage == p.K - 1))
         # gather the model: every parameter from its current owner
-        run.migrate(run.plan)
+        run.gather_model()
         torch.save({"p32": ex.p32, "mom": ex.mom, "losses": losses},
                    os.path.join(out_dir, f"{name}_{rank}.pt"))
     finally:
@@ -159,3 +159,18 @@ def test_plan_from_planner_decision():
         assert sp.K * sp.R == 8
         assert sp.spans[0][0] == 2 * sp.l_frozen and sp.spans[-1][1] == 24
         assert all(a[1] == b[0] for a, b in zip(sp.spans, sp.spans[1:]))
+
+
+def test_moved_runs_only_ownership_changes():
+    """Plan transitions broadcast exactly the sublayers some rank newly owns,
+    each from its old owner (stage s of pipeline 0 = rank s)."""
+    from paper_2102_03161_b200.pipeline import StagePlan, StageRunner
+    n = 12
+    a = StagePlan(2, 1, 7, 0, n, ((0, 12), (12, 24)))
+    b = StagePlan(2, 1, 5, 6, n, ((12, 18), (18, 24)))  # AutoPipe re-balance at K = 2
+    c = StagePlan(1, 2, 1, 9, n, ((18, 24),))           # K 2 -> 1 with a replica fork
+    d = StagePlan(1, 2, 1, 10, n, ((20, 24),))          # boundary move, same ownership
+    assert StageRunner.moved_runs(a, a) == []
+    assert StageRunner.moved_runs(a, b) == [(12, 18, 1)]
+    assert StageRunner.moved_runs(b, c) == [(0, 18, 0), (18, 24, 1)]
+    assert StageRunner.moved_runs(c, d) == []
