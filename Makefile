@@ -9,6 +9,10 @@ PKG       := paper_2102_03161_b200
 NLOHMANN  ?= $(firstword $(wildcard \
     /opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann \
     /usr/include/nlohmann /usr/local/include/nlohmann))
+ifeq ($(strip $(NLOHMANN)),)
+  $(error nlohmann/json.hpp not found: pass NLOHMANN=<dir containing json.hpp> \
+      (scenario.cpp / runner.cpp need it, SURVEY.md 8(c)))
+endif
 ARCH      := -gencode arch=compute_100a,code=sm_100a
 CXXFLAGS  := -std=c++20 -O2 -fPIC -Wall -Wextra -Iinclude -I$(NLOHMANN)
 NVFLAGS   := -std=c++20 -O3 $(ARCH) -lineinfo -Xcompiler -fPIC -Iinclude -I$(NLOHMANN) \
@@ -21,7 +25,7 @@ CONTROL_OBJ := $(patsubst %.cpp,$(OBJDIR)/%.o,$(CONTROL_SRC))
 KERNEL_OBJ  := $(patsubst %.cu,$(OBJDIR)/%.o,$(KERNEL_SRC))
 LIB         := $(PKG)/libeps_b200.so
 
-.PHONY: all lib oracle clean
+.PHONY: all lib oracle conformance clean
 all: lib oracle
 lib: $(LIB)
 
@@ -54,6 +58,27 @@ oracle/_ref/obj/capi_ref.o: $(PKG)/csrc/capi_control.cpp include/eps_capi.h
 
 oracle/_ref/libeps_ref.so: $(REF_OBJ) oracle/_ref/obj/capi_ref.o
 	$(CXX) -shared -o $@ $^
+
+# ---- conformance: the reference's own unit suites against the product -------
+# proj/tests/test_*.cpp compiled unchanged against include/eps/*.hpp with the
+# doctest shim (tests/conformance/doctest.h) and linked to libeps_b200.so.
+# test_cli needs CLI11 (absent); everything else is built.
+CONF_SUITES := test_model test_freeze test_autopipe test_autodp test_autocache test_engine \
+               test_scenario
+CONF_BINS   := $(patsubst %,oracle/_ref/conformance/%,$(CONF_SUITES))
+conformance: $(CONF_BINS) oracle/_ref/conformance/test_autodp_chain
+
+oracle/_ref/conformance/test_autodp_chain: tests/conformance/test_autodp_chain.cpp $(LIB) \
+    tests/conformance/doctest.h
+	@mkdir -p $(dir $@)
+	$(CXX) -std=c++20 -O1 -Itests/conformance -Iinclude $< -L$(PKG) -leps_b200 \
+	    -Wl,-rpath,$(abspath $(PKG)) -o $@
+
+oracle/_ref/conformance/%: $(REF)/tests/%.cpp $(LIB) tests/conformance/doctest.h
+	@mkdir -p $(dir $@)
+	$(CXX) -std=c++20 -O1 -Itests/conformance -Iinclude -I$(REF)/tests -I$(NLOHMANN) \
+	    -DEPS_CONFIG_DIR=\"$(REF)/configs\" $< -L$(PKG) -leps_b200 \
+	    -Wl,-rpath,$(abspath $(PKG)) -o $@
 
 clean:
 	rm -rf build $(LIB) oracle/_ref

@@ -1,17 +1,7 @@
-"""BERT train step on the sm_100a executor vs the fp32 CPU oracle
-(BASELINE configs 4 and 5 and test-size variants), plus a 2-stage pipeline.
-
-Tolerance: loss within rtol 1e-2 (north_star); gradient tensors and
-per-layer norms within 8e-2 relative L2.  The SQuAD head sends a gradient
-into every one of the T=384 token rows and every post-norm sublayer ends in
-a LayerNorm whose backward re-rounds dS to bf16, so gradient matrices sit
-at 1-6 % of their fp32 value (measured).  1-D bias / LayerNorm gradients are
-sums over B*T rows that cancel heavily: for layer 11's FC2 bias at
-bert-base-384 |sum| is ~16x below the row noise floor, and rounding the fp32
-oracle's own dS rows to bf16 before summing already moves it by 8 %
-(tests/test_bert_gpu.py docstring experiment) -- those are checked at 30 %.
-The per-layer norms the freeze decision consumes are checked at 5e-2.
-"""
+"""BERT executor properties on the sm_100a path: AdamW, a 2-stage pipeline
+(host-staged and peer-memory cuts) and the full-size BASELINE configs 4 / 5
+(micro-batch invariance, loss additivity).  Per-tensor numerics parity vs
+the CPU oracles lives in test_numerics_gpu.py."""
 import os
 import socket
 
@@ -20,17 +10,12 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from oracle import bert_fp32
 from paper_2102_03161_b200.bert import BertExecutor, init_params
 from paper_2102_03161_b200.configs import GEOMETRIES
 from paper_2102_03161_b200.pipeline import StagePlan, StageRunner, Transport
 
 pytestmark = pytest.mark.gpu
 
-LOSS_RTOL = 1e-2
-GRAD_REL = 8e-2
-VEC_REL = 0.3
-NORM_REL = 5e-2
 
 
 def _rel(a, b):
@@ -48,47 +33,6 @@ def _data(g, batch, seed):
     else:
         lab = torch.randint(0, g.classes, (batch,), generator=gen)
     return tok, seg, lab
-
-
-@pytest.mark.parametrize("cfg,batch,l_frozen,micro", [
-    ("tiny-bert-qa", 4, 0, 1),
-    ("tiny-bert-qa", 5, 1, 2),
-    ("tiny-bert-cls", 6, 0, 3),
-    ("tiny-bert-cls", 4, 1, 1),
-    ("bert-base-384", 2, 0, 1),
-    ("bert-large-128", 3, 20, 2),
-])
-def test_bert_train_step_matches_oracle(cuda, cfg, batch, l_frozen, micro):
-    g = GEOMETRIES[cfg]
-    params = init_params(g, seed=11)
-    tok, seg, lab = _data(g, batch, seed=3)
-    ex = BertExecutor(g, max_batch=batch, params=params)
-    inputs = torch.stack([tok, seg]).cuda()
-    loss_sum = ex.train_step(inputs, lab.reshape(-1).cuda(), micro_batches=micro,
-                             l_frozen=l_frozen)
-    torch.cuda.synchronize()
-    loss = loss_sum.item() / batch
-    ref_loss, ref_grads = bert_fp32.train_step(params, tok, seg, lab, g, l_frozen)
-    assert abs(loss - ref_loss.item()) <= LOSS_RTOL * abs(ref_loss.item()), (loss, ref_loss)
-    grads = ex.grads()
-    errs = {}
-    for name, ref in ref_grads.items():
-        if not bert_fp32.trainable(name, l_frozen):
-            assert grads[name].abs().max().item() == 0.0, name
-            continue
-        if ref.norm() < 1e-6:
-            continue
-        errs[name] = _rel(grads[name], ref)
-    bad = {k: round(v, 4) for k, v in errs.items()
-           if v >= (GRAD_REL if ref_grads[k].dim() > 1 else VEC_REL)}
-    assert not bad, (bad, {k: round(v, 4) for k, v in errs.items()})
-    norms = ex.layer_norms(l_frozen)
-    ref_norms = bert_fp32.layer_norms(ref_grads, g, l_frozen)
-    for l in range(g.layers):
-        if l < l_frozen:
-            assert norms[l] == 0.0
-        else:
-            assert abs(norms[l] - ref_norms[l]) <= NORM_REL * ref_norms[l], l
 
 
 def test_bert_adamw_step(cuda):
