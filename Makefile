@@ -14,11 +14,12 @@ ifeq ($(strip $(NLOHMANN)),)
       (scenario.cpp / runner.cpp need it, SURVEY.md 8(c)))
 endif
 ARCH      := -gencode arch=compute_100a,code=sm_100a
-CXXFLAGS  := -std=c++20 -O2 -fPIC -Wall -Wextra -Iinclude -I$(NLOHMANN)
+CXXFLAGS  := -std=c++20 -O2 -fPIC -Wall -Wextra -Iinclude -I$(NLOHMANN) -I/usr/local/cuda/include
 NVFLAGS   := -std=c++20 -O3 $(ARCH) -lineinfo -Xcompiler -fPIC -Iinclude -I$(NLOHMANN) \
              --expt-relaxed-constexpr -Xptxas -v
 
-CONTROL_SRC := $(wildcard $(PKG)/csrc/control/*.cpp) $(PKG)/csrc/capi_control.cpp
+CONTROL_SRC := $(wildcard $(PKG)/csrc/control/*.cpp) $(PKG)/csrc/capi_control.cpp \
+               $(PKG)/csrc/runtime/comm.cpp
 KERNEL_SRC  := $(wildcard $(PKG)/csrc/kernels/*.cu) $(wildcard $(PKG)/csrc/runtime/*.cu)
 OBJDIR      := build/obj
 CONTROL_OBJ := $(patsubst %.cpp,$(OBJDIR)/%.o,$(CONTROL_SRC))
@@ -38,7 +39,7 @@ $(OBJDIR)/%.o: %.cu $(wildcard $(PKG)/csrc/kernels/*.cuh) include/eps_capi.h $(w
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $@.ptxas.log || (cat $@.ptxas.log; false)
 
 $(LIB): $(CONTROL_OBJ) $(KERNEL_OBJ)
-	$(NVCC) $(ARCH) -shared -Xcompiler -fPIC -o $@ $^ -cudart static
+	$(NVCC) $(ARCH) -shared -Xcompiler -fPIC -o $@ $^ -cudart static -ldl
 
 # ---- oracle: the reference compiled from its own sources -------------------
 REF       ?= /root/reference/proj

@@ -459,6 +459,15 @@ int eps_cache_gather_bg(const void* store, const int64_t* ids, int n, int64_t ro
                         void* dst, int ctas, void* stream);
 int eps_cache_scatter(void* store, const int64_t* ids, int n, int64_t row_bytes,
                       const void* src, void* stream);
+/* Store sharded over the GPUs of a node (autodp.cpp:113-151:
+ * redistribute moves samples between replicas every epoch): `shards` is a
+ * device array of n base pointers (local or CUDA-IPC-mapped peer HBM), shard
+ * r holding sample rows [r * rows_per_shard, (r + 1) * rows_per_shard).  The
+ * gather reads (the scatter writes) the owning GPU's HBM over NVLink. */
+int eps_cache_gather_sharded(const uint64_t* shards, int64_t rows_per_shard, const int64_t* ids,
+                             int n, int64_t row_bytes, void* dst, void* stream);
+int eps_cache_scatter_sharded(const uint64_t* shards, int64_t rows_per_shard, const int64_t* ids,
+                              int n, int64_t row_bytes, const void* src, void* stream);
 
 /* Fused SGD-momentum over an fp32 master copy + bf16 working copy:
  * v = mu*v + g (+wd*p); p -= lr*v; p_bf16 = bf16(p); g = 0. */
@@ -508,6 +517,45 @@ int eps_peer_signal(void* flag, uint32_t value, void* stream);
 int eps_peer_wait(const void* flag, uint32_t value, void* stream);
 /* Stream-ordered device copy (peer addresses allowed, UVA). */
 int eps_copy_async(void* dst, const void* src, int64_t bytes, void* stream);
+/* Page-lock / release an existing host range (cudaHostRegister, portable +
+ * mapped): the node-wide shared-memory host tier of the AutoCache store. */
+int eps_host_register(void* ptr, int64_t bytes);
+int eps_host_unregister(void* ptr);
+
+/* ---- communicator plane (csrc/runtime/comm.cpp; NCCL) ----
+ * The reference's message group (every rank) and training group (active
+ * pipeline heads), autodp.hpp:17-21 / autodp.cpp:31-37, as NCCL
+ * communicators: a world communicator from a 128-byte unique id (rank 0
+ * creates it, the host exchanges it out of band), per-stage data-parallel
+ * communicators split from it (color = stage, key = pipeline; color < 0 =
+ * not a member, *out = NULL), rebuilt when freezing changes K.  Every
+ * operation is stream-ordered on `stream` (cudaStream_t) and never
+ * synchronises the host.  NCCL is loaded at run time; without it every entry
+ * returns EPS_ENCCL (eps_last_error names the cause). */
+typedef struct eps_comm eps_comm_t;
+enum { EPS_DT_F32 = 0, EPS_DT_F64 = 1, EPS_DT_BF16 = 2, EPS_DT_U8 = 3, EPS_DT_I64 = 4 };
+enum { EPS_OP_SUM = 0, EPS_OP_AVG = 1, EPS_OP_MAX = 2 };
+int eps_comm_version(int* version);
+int eps_comm_unique_id(void* id /* 128 bytes */);
+int eps_comm_world_init(const void* id, int nranks, int rank, eps_comm_t** out);
+int eps_comm_split(eps_comm_t* parent, int color, int key, eps_comm_t** out);
+int eps_comm_free(eps_comm_t* comm);
+int eps_comm_rank(const eps_comm_t* comm, int* rank, int* size);
+/* In-place all-reduce of `count` elements of `dtype` with `op`. */
+int eps_allreduce(eps_comm_t* comm, void* buf, int64_t count, int dtype, int op, void* stream);
+/* One DDP gradient bucket (schedule.cpp:137-178): fp32 in place, average =
+ * ncclAvg (the 1/R mean inside the collective, no extra scaling pass). */
+int eps_allreduce_bucket(eps_comm_t* comm, float* grads, int64_t count, int average,
+                         void* stream);
+/* Byte broadcast from comm rank `root` (parameter / momentum migration on a
+ * transition, autodp.cpp:81-111). */
+int eps_broadcast(eps_comm_t* comm, void* buf, int64_t bytes, int root, void* stream);
+/* Stage-to-stage cut activations / gradients (schedule.cpp:60-68, 97-105);
+ * pair sends and receives inside eps_comm_group_start / _end. */
+int eps_p2p_send(eps_comm_t* comm, const void* buf, int64_t bytes, int peer, void* stream);
+int eps_p2p_recv(eps_comm_t* comm, void* buf, int64_t bytes, int peer, void* stream);
+int eps_comm_group_start(void);
+int eps_comm_group_end(void);
 
 /* Kernels launched by this library in this process (launch accounting). */
 unsigned long long eps_launch_count(void);
@@ -537,7 +585,14 @@ void* eps_vit_activation(eps_vit_t* h, int which, int layer);
  * g0 >= 2*l_frozen (PartitionPlan spans shifted by 2*l_frozen).  The host
  * drives the GPipe order of schedule.cpp:54-117 and moves the cut
  * activations (eps_vit_cut) between stages.
- * front = 1 on pipeline stage 0: frozen prefix / AutoCache / embedding first. */
+ * front = 1 on pipeline stage 0: frozen prefix / AutoCache / embedding first.
+ * cache_mode (AutoCache, autocache.cpp:45-67 / runner.cpp:180-213):
+ *   0 recompute the frozen prefix [0, l_frozen);
+ *   1 gather X[l_frozen] from store rows `ids` (prefix skipped);
+ *   2 boundary move cache_old -> l_frozen: gather X[cache_old] (cache_old > 0)
+ *     or embed, forward [cache_old, l_frozen), scatter X[l_frozen];
+ *   3 trailing boundary: gather X[cache_old] (0 < cache_old < l_frozen),
+ *     forward [cache_old, l_frozen), write nothing. */
 int eps_vit_stage_forward(eps_vit_t* h, const float* images, int b0, int b, int g0, int g1,
                           int l_frozen, int front, int cache_mode, int cache_old, void* store,
                           const int64_t* ids, void* stream);
@@ -562,6 +617,10 @@ void* eps_vit_cut(eps_vit_t* h, int g, int grad);
  * out_ptr (the next stage's cut buffer, IPC-mapped) and the gradient at the
  * input cut `dx_g` into dx_ptr (the previous stage's dX buffer) directly from
  * the producing kernel.  NULL pointers restore local writes. */
+/* AutoCache store sharded over the node (see eps_cache_gather_sharded):
+ * `table` = device uint64[n] of shard bases, `rows_per_shard` rows each; the
+ * stage calls' store argument is then only a non-null marker.  null reverts. */
+int eps_vit_set_cache_shards(eps_vit_t* h, const uint64_t* table, int64_t rows_per_shard);
 int eps_vit_set_redirect(eps_vit_t* h, int out_g, void* out_ptr, int dx_g, void* dx_ptr);
 /* Parameter elements [begin, end) of global sublayers [g0, g1) (embedding in
  * sublayer 0, final LN + head in sublayer 2L-1); contiguous by layout. */
@@ -631,6 +690,10 @@ int eps_bert_stage_backward(eps_bert_t* h, int b0, int b, int g0, int g1, int l_
 int eps_bert_stage_backward_part(eps_bert_t* h, int b0, int b, int g0, int g1, int stage_g0,
                                  int l_frozen, int cut_out, void* stream);
 void* eps_bert_cut(eps_bert_t* h, int g, int grad);
+/* AutoCache store sharded over the node (see eps_cache_gather_sharded):
+ * `table` = device uint64[n] of shard bases, `rows_per_shard` rows each; the
+ * stage calls' store argument is then only a non-null marker.  null reverts. */
+int eps_bert_set_cache_shards(eps_bert_t* h, const uint64_t* table, int64_t rows_per_shard);
 int eps_bert_set_redirect(eps_bert_t* h, int out_g, void* out_ptr, int dx_g, void* dx_ptr);
 int eps_bert_param_range(eps_bert_t* h, int g0, int g1, int64_t* begin, int64_t* end);
 int eps_bert_sgd_range(eps_bert_t* h, int64_t begin, int64_t end, float lr, float momentum,

@@ -212,6 +212,13 @@ void copy_out(const std::string& s, char* buf, size_t cap, size_t* len) {
 
 }  // namespace
 
+#ifndef EPS_REFERENCE_BUILD
+// Error text for the entry points implemented outside this file (comm.cpp).
+namespace eps_detail {
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+}  // namespace eps_detail
+#endif
+
 extern "C" {
 
 const char* EPS_FN(last_error)(void) { return g_last_error.c_str(); }

@@ -233,6 +233,28 @@ __global__ void cache_copy_kernel(const uint8_t* __restrict__ src, uint8_t* __re
     d[i] = s[i];
 }
 
+// AutoCache store sharded over the ranks of a node (one shard per GPU, rows
+// [r * rows_per_shard, (r + 1) * rows_per_shard) on rank r, every shard
+// mapped into every rank over CUDA IPC): sample `key` lives at row
+// key % rows_per_shard of shard key / rows_per_shard, so a gather reads a
+// peer GPU's HBM over NVLink (and a scatter writes it) inside this one
+// kernel -- no store replication, broadcast or all-reduce.
+__global__ void cache_copy_sharded_kernel(const uint64_t* __restrict__ shards,
+                                          int64_t rows_per_shard, uint8_t* __restrict__ local,
+                                          const int64_t* __restrict__ ids, int64_t row_bytes,
+                                          bool gather) {
+  const int r = blockIdx.y;
+  const int64_t key = ids[r];
+  uint8_t* remote = reinterpret_cast<uint8_t*>(shards[key / rows_per_shard]) +
+                    (key % rows_per_shard) * row_bytes;
+  const uint4* s = reinterpret_cast<const uint4*>(gather ? remote : local + r * row_bytes);
+  uint4* d = reinterpret_cast<uint4*>(gather ? local + r * row_bytes : remote);
+  const int64_t n16 = row_bytes / 16;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n16;
+       i += int64_t(gridDim.x) * blockDim.x)
+    d[i] = s[i];
+}
+
 // Background gather for the host tier's prefetch window: a few CTAs walk all
 // (row, 16-byte) pairs with four independent 16-byte loads in flight per
 // thread (enough outstanding host-link reads for full PCIe rate from ~8 SMs),
@@ -510,6 +532,32 @@ extern "C" int eps_cache_gather(const void* store, const int64_t* ids, int n, in
   count_launch(); cache_copy_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
       static_cast<const uint8_t*>(store), static_cast<uint8_t*>(dst), ids, row_bytes, true);
   return ok_or_cuda();
+}
+
+// shards: device array of n_shards base pointers (uint64), shard r holding
+// sample rows [r * rows_per_shard, (r + 1) * rows_per_shard).
+static int cache_sharded(const uint64_t* shards, int64_t rows_per_shard, const int64_t* ids,
+                         int n, int64_t row_bytes, void* local, bool gather, void* stream) {
+  if (n <= 0) return EPS_OK;
+  if (row_bytes % 16 || shards == nullptr || rows_per_shard <= 0) return EPS_EINVAL;
+  dim3 grid(unsigned(std::min<int64_t>((row_bytes / 16 + 255) / 256, 64)), unsigned(n));
+  count_launch();
+  cache_copy_sharded_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      shards, rows_per_shard, static_cast<uint8_t*>(local), ids, row_bytes, gather);
+  return ok_or_cuda();
+}
+
+extern "C" int eps_cache_gather_sharded(const uint64_t* shards, int64_t rows_per_shard,
+                                        const int64_t* ids, int n, int64_t row_bytes, void* dst,
+                                        void* stream) {
+  return cache_sharded(shards, rows_per_shard, ids, n, row_bytes, dst, true, stream);
+}
+
+extern "C" int eps_cache_scatter_sharded(const uint64_t* shards, int64_t rows_per_shard,
+                                         const int64_t* ids, int n, int64_t row_bytes,
+                                         const void* src, void* stream) {
+  return cache_sharded(shards, rows_per_shard, ids, n, row_bytes, const_cast<void*>(src), false,
+                       stream);
 }
 
 extern "C" int eps_cache_gather_bg(const void* store, const int64_t* ids, int n,

@@ -179,6 +179,10 @@ struct eps_bert {
   float* loss_sum = nullptr;
   // Stage hand-off over peer memory (see the ViT executor).
   int out_g = -1, dx_g = -1;
+  // AutoCache store sharded over the node's GPUs (eps_cache_gather_sharded):
+  // device table of shard base pointers; null = one local / host store.
+  const uint64_t* shard_table = nullptr;
+  int64_t rows_per_shard = 0;
   uint16_t* out_to = nullptr;
   uint16_t* dx_to = nullptr;
   uint16_t* out_buf(int gs, uint16_t* local) const {
@@ -449,6 +453,11 @@ struct eps_bert {
     const int64_t rb = int64_t(g.tokens) * g.d * 2;
     auto cache_io = [&](bool gather, uint16_t* x) {
       run(EPS_TC_CACHE, 0.0, 2.0 * b * double(rb), st, [&] {
+        if (shard_table != nullptr)
+          return gather ? eps_cache_gather_sharded(shard_table, rows_per_shard, ids + b0, b, rb,
+                                                   x + xoff, st)
+                        : eps_cache_scatter_sharded(shard_table, rows_per_shard, ids + b0, b, rb,
+                                                    x + xoff, st);
         return gather ? eps_cache_gather(store, ids + b0, b, rb, x + xoff, st)
                       : eps_cache_scatter(store, ids + b0, b, rb, x + xoff, st);
       });
@@ -462,7 +471,7 @@ struct eps_bert {
       if (cache_mode == 1) {
         cache_io(true, act.X[l_frozen]);
         start = l_frozen;
-      } else if (cache_mode == 2 && cache_old > 0) {
+      } else if ((cache_mode == 2 || cache_mode == 3) && cache_old > 0) {
         cache_io(true, act.X[cache_old]);
         start = cache_old;
       }
@@ -611,6 +620,8 @@ int eps_bert_stage_forward(eps_bert* h, const int64_t* inputs, int batch_rows, i
       throw int(EPS_EINVAL);
     if (cache_mode != 0 && (!front || store == nullptr || ids == nullptr || l_frozen == 0))
       throw int(EPS_EINVAL);
+    if (cache_mode == 3 && (cache_old < 1 || cache_old >= l_frozen))
+      throw int(EPS_EINVAL);
     h->stage_fwd(inputs, batch_rows, b0, b, g0, g1, l_frozen, front != 0, cache_mode, cache_old,
                  store, ids, static_cast<cudaStream_t>(stream));
   });
@@ -647,6 +658,18 @@ int eps_bert_stage_backward(eps_bert* h, int b0, int b, int g0, int g1, int l_fr
     h->check_rows(b0, b);
     h->check_span(g0, g1, l_frozen);
     h->stage_bwd(b0, b, g0, g1, l_frozen, static_cast<cudaStream_t>(stream));
+  });
+}
+
+// AutoCache store layout for cache_mode != 0: `table` (device uint64[n]) of
+// shard base pointers with `rows_per_shard` sample rows each -- the store
+// argument of the stage calls is then ignored except as a non-null marker;
+// table = null reverts to a single store.
+int eps_bert_set_cache_shards(eps_bert* h, const uint64_t* table, int64_t rows_per_shard) {
+  return guard([&] {
+    if (h == nullptr || (table != nullptr && rows_per_shard <= 0)) throw int(EPS_EINVAL);
+    h->shard_table = table;
+    h->rows_per_shard = table != nullptr ? rows_per_shard : 0;
   });
 }
 

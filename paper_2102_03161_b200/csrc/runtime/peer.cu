@@ -105,6 +105,22 @@ int eps_copy_async(void* dst, const void* src, int64_t bytes, void* stream) {
              : EPS_ECUDA;
 }
 
+// Page-lock an existing host range (e.g. a node-wide shared-memory AutoCache
+// host tier that every rank of the node maps) so the gather / scatter
+// kernels can address it over the host link (UVA).
+int eps_host_register(void* ptr, int64_t bytes) {
+  if (ptr == nullptr || bytes <= 0) return EPS_EINVAL;
+  return cudaHostRegister(ptr, size_t(bytes), cudaHostRegisterPortable | cudaHostRegisterMapped) ==
+                 cudaSuccess
+             ? EPS_OK
+             : EPS_ECUDA;
+}
+
+int eps_host_unregister(void* ptr) {
+  if (ptr == nullptr) return EPS_EINVAL;
+  return cudaHostUnregister(ptr) == cudaSuccess ? EPS_OK : EPS_ECUDA;
+}
+
 int eps_peer_wait(const void* flag, uint32_t value, void* stream) {
   StreamWaitValue32Fn wait = stream_wait();
   if (flag == nullptr || wait == nullptr) return EPS_EINVAL;

@@ -178,6 +178,10 @@ struct eps_vit {
   // `out_to` (the next stage's buffer) and the gradient at the input cut
   // `dx_g` to `dx_to` (the previous stage's dX), both [max_batch*T, d].
   int out_g = -1, dx_g = -1;
+  // AutoCache store sharded over the node's GPUs (eps_cache_gather_sharded):
+  // device table of shard base pointers; null = one local / host store.
+  const uint64_t* shard_table = nullptr;
+  int64_t rows_per_shard = 0;
   uint16_t* out_to = nullptr;
   uint16_t* dx_to = nullptr;
   uint16_t* out_buf(int gs, uint16_t* local) const {
@@ -452,7 +456,11 @@ struct eps_vit {
   //   cache_mode 1: X[L_f] gathered from the store rows `ids` (prefix skipped);
   //   cache_mode 2: boundary move old -> L_f: X[old] gathered (old > 0) or
   //                 computed from the images, [old, L_f) forwarded once, X[L_f]
-  //                 scattered into the store (autocache.cpp:45-67).
+  //                 scattered into the store (autocache.cpp:45-67);
+  //   cache_mode 3: the boundary trails L_f (the cache stays on at its old
+  //                 boundary when the policy no longer wants a move,
+  //                 runner.cpp:186-213): X[old] gathered, [old, L_f)
+  //                 forwarded, nothing written.
   void stage_fwd(const float* images, int b0, int b, int g0, int g1, int l_frozen, bool front,
                  int cache_mode, int cache_old, void* store, const int64_t* ids,
                  cudaStream_t st) {
@@ -460,6 +468,11 @@ struct eps_vit {
     const int64_t rb = row_bytes();
     auto cache_io = [&](bool gather, uint16_t* x) {
       run(EPS_TC_CACHE, 0.0, 2.0 * b * double(rb), st, [&] {
+        if (shard_table != nullptr)
+          return gather ? eps_cache_gather_sharded(shard_table, rows_per_shard, ids + b0, b, rb,
+                                                   x + xoff, st)
+                        : eps_cache_scatter_sharded(shard_table, rows_per_shard, ids + b0, b, rb,
+                                                    x + xoff, st);
         return gather ? eps_cache_gather(store, ids + b0, b, rb, x + xoff, st)
                       : eps_cache_scatter(store, ids + b0, b, rb, x + xoff, st);
       });
@@ -469,7 +482,7 @@ struct eps_vit {
       if (cache_mode == 1) {
         cache_io(true, act.X[l_frozen]);
         start = l_frozen;
-      } else if (cache_mode == 2 && cache_old > 0) {
+      } else if ((cache_mode == 2 || cache_mode == 3) && cache_old > 0) {
         cache_io(true, act.X[cache_old]);
         start = cache_old;
       }
@@ -627,6 +640,7 @@ int eps_vit_train_step(eps_vit* h, const float* images, const int64_t* labels, i
       throw int(EPS_EINVAL);
     if (cache_mode != 0 && (store == nullptr || ids == nullptr || l_frozen == 0))
       throw int(EPS_EINVAL);
+    if (cache_mode == 3 && (cache_old < 1 || cache_old >= l_frozen)) throw int(EPS_EINVAL);
     auto st = static_cast<cudaStream_t>(stream);
     h->loss_sum = loss_sum;
     const int g0 = 2 * l_frozen, g1 = 2 * h->g.layers;
@@ -659,6 +673,7 @@ int eps_vit_stage_forward(eps_vit* h, const float* images, int b0, int b, int g0
     if (cache_mode != 0 &&
         (!front || store == nullptr || ids == nullptr || l_frozen == 0 || g0 < 2 * l_frozen))
       throw int(EPS_EINVAL);
+    if (cache_mode == 3 && (cache_old < 1 || cache_old >= l_frozen)) throw int(EPS_EINVAL);
     h->stage_fwd(images, b0, b, g0, g1, l_frozen, front != 0, cache_mode, cache_old, store, ids,
                  static_cast<cudaStream_t>(stream));
   });
@@ -693,6 +708,18 @@ int eps_vit_stage_backward_part(eps_vit* h, int b0, int b, int g0, int g1, int s
     h->check_span(stage_g0, g1, l_frozen);
     h->stage_bwd(b0, b, g0, g1, stage_g0, l_frozen, cut_out != 0,
                  static_cast<cudaStream_t>(stream));
+  });
+}
+
+// AutoCache store layout for cache_mode != 0: `table` (device uint64[n]) of
+// shard base pointers with `rows_per_shard` sample rows each -- the store
+// argument of the stage calls is then ignored except as a non-null marker;
+// table = null reverts to a single store.
+int eps_vit_set_cache_shards(eps_vit* h, const uint64_t* table, int64_t rows_per_shard) {
+  return guard([&] {
+    if (h == nullptr || (table != nullptr && rows_per_shard <= 0)) throw int(EPS_EINVAL);
+    h->shard_table = table;
+    h->rows_per_shard = table != nullptr ? rows_per_shard : 0;
   });
 }
 

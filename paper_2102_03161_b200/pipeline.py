@@ -126,15 +126,21 @@ class Transport:
         else:
             dist.recv(t, src)
 
-    def all_reduce(self, t: torch.Tensor, group, op=dist.ReduceOp.SUM, async_op: bool = False):
+    def all_reduce(self, t: torch.Tensor, group, op=dist.ReduceOp.SUM, async_op: bool = False,
+                   avg: bool = False):
         """Returns a work handle for an asynchronous NCCL all-reduce (the
         collective runs on NCCL's stream, ordered after the kernels already
-        queued on the current stream), else None."""
+        queued on the current stream), else None.  avg: mean over the group
+        (ncclAvg: the 1/R scaling happens inside the collective)."""
         if self.host_staged:
             buf = t.detach().cpu()
             dist.all_reduce(buf, op=op, group=group)
+            if avg:
+                buf /= dist.get_world_size(group)
             t.copy_(buf)
             return None
+        if avg:
+            op = dist.ReduceOp.AVG
         return dist.all_reduce(t, op=op, group=group, async_op=async_op)
 
     def broadcast(self, t: torch.Tensor, src: int):
@@ -144,6 +150,88 @@ class Transport:
             t.copy_(buf)
         else:
             dist.broadcast(t, src)
+
+
+class _StreamWork:
+    """Completion handle of a collective issued on the comm stream: wait()
+    orders the caller's current stream after it (no host block)."""
+
+    def __init__(self, event):
+        self.event = event
+
+    def wait(self):
+        torch.cuda.current_stream().wait_event(self.event)
+
+
+class EpsTransport(Transport):
+    """The same moves through the library's communicator plane (NCCL behind
+    the C ABI, paper_2102_03161_b200.comm): a world communicator, per-group
+    communicators split from it (ncclCommSplit, cached per membership),
+    ncclAvg bucket all-reduces on a dedicated comm stream that overlap the
+    drain, ncclSend / ncclRecv for the cut hand-off, ncclBroadcast for
+    migration.  torch.distributed only carries the unique id."""
+
+    def __init__(self, rank: int, world: int):
+        super().__init__(host_staged=False)
+        from .comm import Comm
+        self.rank, self.world = rank, world
+        self.comm = Comm.world(rank, world)
+        self._splits: Dict[Tuple[int, ...], object] = {}
+        self.stream = torch.cuda.Stream()
+
+    def group(self, ranks: Sequence[int]):
+        key = tuple(ranks)
+        if key not in self._splits:
+            # collective over the world communicator: every rank splits, in
+            # the same order; non-members pass no color
+            member = self.rank in key
+            sub = self.comm.split(0 if member else -1, key.index(self.rank) if member else 0)
+            self._splits[key] = sub
+        return self._splits[key]
+
+    def send(self, t: torch.Tensor, dst: int):
+        self.comm.send(t.contiguous(), dst)
+
+    def recv(self, t: torch.Tensor, src: int):
+        if t.is_contiguous():
+            self.comm.recv(t, src)
+        else:
+            buf = torch.empty_like(t, memory_format=torch.contiguous_format)
+            self.comm.recv(buf, src)
+            t.copy_(buf)
+
+    def all_reduce(self, t: torch.Tensor, group, op=dist.ReduceOp.SUM, async_op: bool = False,
+                   avg: bool = False):
+        from .comm import OP_AVG, OP_MAX, OP_SUM
+        c = self.comm if group is None else group
+        if c is None:  # single-member group
+            return None
+        code = OP_AVG if avg else {dist.ReduceOp.SUM: OP_SUM, dist.ReduceOp.MAX: OP_MAX,
+                                   dist.ReduceOp.AVG: OP_AVG}[op]
+        if not async_op:
+            c.all_reduce(t, code)
+            return None
+        ready = torch.cuda.Event()
+        ready.record()
+        self.stream.wait_event(ready)
+        c.all_reduce(t, code, stream=self.stream)
+        done = torch.cuda.Event()
+        done.record(self.stream)
+        return _StreamWork(done)
+
+    def broadcast(self, t: torch.Tensor, src: int):
+        self.comm.broadcast(t, src)
+
+    def comm_version(self) -> int:
+        from .comm import nccl_version
+        return nccl_version()
+
+    def close(self):
+        for c in self._splits.values():
+            if c is not None:
+                c.free()
+        self._splits = {}
+        self.comm.free()
 
 
 # ---- one rank's stage ------------------------------------------------------------------
@@ -205,7 +293,7 @@ class PeerLink:
         self.opened = []
         self.ex.set_redirect(-1, None, -1, None)
 
-    def setup(self, plan: StagePlan, stage: int, g0: int, g1: int):
+    def setup(self, plan: StagePlan, stage: int, g0: int, g1: int, idle: bool = False):
         """Collective over the world: exchange handles, map the neighbours."""
         self.close()
         self.flags.zero_()
@@ -221,6 +309,10 @@ class PeerLink:
         out_g, out_ptr, dx_g, dx_ptr = -1, None, -1, None
         self.next_flags = self.prev_flags = None
         self.copy_out = None
+        if idle:
+            self.ex.set_redirect(-1, None, -1, None)
+            self.fwd = self.bwd = self.iters = 0
+            return
         if stage < K - 1:
             nxt = allh[rank + 1]
             peer_cut = self._open(nxt["cut"])
@@ -285,6 +377,9 @@ class StageRunner:
         self.buckets: List[Tuple[int, int]] = []
         self.pending: List[Tuple[object, int, int]] = []
         self.trace: Optional[list] = None  # [] records the next iteration's blocks
+        self.front_events: Optional[list] = None  # [] records stage 0's front per micro-batch
+        self.t_ar_first = self.t_bwd_end = self.t_sync_end = None
+        self.idle = False
 
     # -- plan changes ------------------------------------------------------------
     def _dp_groups(self, plan: StagePlan):
@@ -295,7 +390,7 @@ class StageRunner:
         """Adopt an epoch plan; on a K / ownership change migrate parameters
         and momentum from their previous owners (pipeline 0's stages) to all
         ranks, then (re)select the per-stage data-parallel groups."""
-        if plan.K * plan.R != self.world:
+        if plan.K * plan.R > self.world:
             raise ValueError(f"plan needs {plan.K * plan.R} ranks, world has {self.world}")
         old = self.plan
         # Parameters move only when ownership moves: with the same K and the
@@ -305,14 +400,18 @@ class StageRunner:
         if old is not None and (old.K != plan.K or old.owner_spans() != plan.owner_spans()):
             self.migrate(old, plan)
         self.plan = plan
-        self.pipe, self.stage = plan.role(self.rank)
+        # AutoPipe without AutoDP packs the pipeline into fewer GPUs but keeps
+        # R (runner.cpp:445): ranks >= K*R sit idle for the epoch, joining only
+        # the world collectives (migration broadcasts, norms, timing)
+        self.idle = self.rank >= plan.K * plan.R
+        self.pipe, self.stage = plan.role(min(self.rank, plan.K * plan.R - 1))
         self.g0, self.g1 = plan.spans[self.stage]
         self.a0 = plan.first_active(self.stage)  # trainable sublayers: [a0, g1)
         self.groups = self._dp_groups(plan)
         self.range = self.ex.param_range(*plan.owner_spans()[self.stage])
         self.buckets = self._plan_buckets() if plan.R > 1 else []
         if self.peer is not None and self.world > 1:
-            self.peer.setup(plan, self.stage, self.g0, self.g1)
+            self.peer.setup(plan, self.stage, self.g0, self.g1, idle=self.idle)
 
     def _plan_buckets(self) -> List[Tuple[int, int]]:
         """Sublayer pieces [g_lo, g_hi) of this stage, top first, each closed
@@ -337,11 +436,13 @@ class StageRunner:
                     return st
             raise ValueError(g)
 
-        world = new.K * new.R
+        world = new.K * new.R  # active ranks of the new plan
         runs: List[Tuple[int, int, int]] = []
         for g in range(2 * new.layers):
             os_, ns = owner(old, g), owner(new, g)
-            need = any(new.role(r)[1] == ns and old.role(r)[1] != os_ for r in range(world))
+            # a rank idle under `old` (r >= K*R, AutoDP off) owns nothing
+            need = any(new.role(r)[1] == ns and (r >= old.K * old.R or old.role(r)[1] != os_)
+                       for r in range(world))
             if not need:
                 continue
             if runs and runs[-1][1] == g and runs[-1][2] == os_:
@@ -372,18 +473,25 @@ class StageRunner:
 
     # -- one iteration -------------------------------------------------------------------
     def iteration(self, images, labels, batch: int, cache_mode: int = 0, cache_old: int = 0,
-                  store=None, ids=None):
+                  store=None, ids=None, micro: Optional[int] = None):
         """Forward + backward of one per-pipeline batch on this rank's stage.
-        images / labels / ids are only read on the first / last stage."""
+        images / labels / ids are only read on the first / last stage.
+        `micro` overrides the plan's M (a ragged last batch of an epoch with
+        fewer samples than M).  With `front_events` a list, stage 0 appends
+        (start, end) CUDA events around each micro-batch's frozen-prefix /
+        AutoCache work (the cache-transition measurement)."""
         p, s, K = self.plan, self.stage, self.plan.K
         ex, lf = self.ex, p.l_frozen
-        mbs = microbatch_offsets(batch, p.M)
+        if self.idle:
+            return ex.loss_sum.zero_()
+        mbs = microbatch_offsets(batch, min(p.M, batch) if micro is None else micro)
         prev, nxt = self.rank - 1, self.rank + 1
         pl = self.peer if (self.peer is not None and K > 1) else None
         ex.loss_sum.zero_()
         tr = self.trace
         if tr is not None:
             tr.clear()
+            self.t_ar_first = self.t_bwd_end = self.t_sync_end = None
             t_iter = self._mark()
         if pl is not None and s < K - 1 and pl.iters > 0:
             pl.wait(PeerLink.FREE, pl.iters)  # receiver done with last iteration's rows
@@ -394,10 +502,19 @@ class StageRunner:
             elif s > 0:
                 self.tp.recv(ex.cut_rows(self.g0, b0, b), prev)
             t0 = self._mark() if tr is not None else None
-            ex.stage_forward(images if s == 0 else None, b0, b, self.g0, self.g1, lf,
-                             front=(s == 0), cache_mode=cache_mode if s == 0 else 0,
-                             cache_old=cache_old, store=store if s == 0 else None,
-                             ids=ids if s == 0 else None)
+            if s == 0 and self.front_events is not None:
+                # stage 0's front (frozen prefix / AutoCache) as its own call,
+                # bracketed by events; then the span
+                fa = self._mark()
+                ex.stage_forward(images, b0, b, self.g0, self.g0, lf, front=True,
+                                 cache_mode=cache_mode, cache_old=cache_old, store=store, ids=ids)
+                self.front_events.append((fa, self._mark()))
+                ex.stage_forward(None, b0, b, self.g0, self.g1, lf, front=False)
+            else:
+                ex.stage_forward(images if s == 0 else None, b0, b, self.g0, self.g1, lf,
+                                 front=(s == 0), cache_mode=cache_mode if s == 0 else 0,
+                                 cache_old=cache_old, store=store if s == 0 else None,
+                                 ids=ids if s == 0 else None)
             if tr is not None:
                 tr.append(("F", f"mb{len(tr)}", t0, self._mark()))
             if s < K - 1:
@@ -428,7 +545,10 @@ class StageRunner:
                         ex.stage_backward_part(b0, b, lo, hi, self.g0, lf,
                                                cut_out=(s < K - 1 and j == 0))
                         a, e = ex.param_range(lo, hi)
-                        work = self.tp.all_reduce(ex.g32[a:e], self.groups[s], async_op=True)
+                        if tr is not None and j == 0:
+                            self.t_ar_first = self._mark()
+                        work = self.tp.all_reduce(ex.g32[a:e], self.groups[s], async_op=True,
+                                                  avg=True)
                         self.pending.append((work, a, e))
                 else:
                     ex.stage_backward(b0, b, self.g0, self.g1, lf, cut_out=s < K - 1)
@@ -447,6 +567,7 @@ class StageRunner:
                 pl.signal(pl.prev_flags, PeerLink.FREE, pl.iters)
         if tr is not None:
             tr.insert(0, ("iteration", "", t_iter, None))
+            self.t_bwd_end = self._mark()
         return ex.loss_sum
 
     # -- measured timeline (report bundle) -------------------------
@@ -470,18 +591,47 @@ class StageRunner:
                 for k, tag, a, b in self.trace[1:]]
 
     def sync_grads(self):
-        """Finish the bucket all-reduces of this iteration and average this
-        stage's active gradients over its replicas."""
+        """Finish the bucket all-reduces of this iteration: the buckets were
+        reduced with an average (NCCL's ncclAvg on the device path), so the
+        stage's active gradients are the replica mean when this returns."""
         p = self.plan
-        if p.R > 1 and p.trainable(self.stage):
+        if p.R > 1 and p.trainable(self.stage) and not self.idle:
             for work, a, e in self.pending:
                 if work is not None:
                     work.wait()
-                self.ex.g32[a:e].mul_(1.0 / p.R)
             self.pending = []
+        if self.trace is not None:
+            self.t_sync_end = self._mark()
+
+    def comm_times(self):
+        """(comm, exposed) seconds of the last traced iteration: first bucket
+        launch -> last bucket done, and end of the drain -> last bucket done
+        (as the compute stream sees them; schedule.cpp:137-178 semantics)."""
+        if self.t_sync_end is None or self.t_bwd_end is None:
+            return 0.0, 0.0
+        torch.cuda.synchronize()
+        exposed = max(0.0, self.t_bwd_end.elapsed_time(self.t_sync_end) / 1e3)
+        comm = (self.t_ar_first.elapsed_time(self.t_sync_end) / 1e3
+                if self.t_ar_first is not None else 0.0)
+        return comm, exposed
+
+    def bubble_time(self) -> float:
+        """Idle time of this stage inside the last traced iteration: span from
+        the iteration start to its last block minus the busy F / B blocks
+        (schedule.cpp:126-131 bubble_per_device)."""
+        if not self.trace:
+            return 0.0
+        torch.cuda.synchronize()
+        t0 = self.trace[0][2]
+        blocks = self.trace[1:]
+        if not blocks:
+            return 0.0
+        span = max(t0.elapsed_time(b) for _, _, _, b in blocks) / 1e3
+        busy = sum(a.elapsed_time(b) for _, _, a, b in blocks) / 1e3
+        return max(0.0, span - busy)
 
     def step(self, lr: float, momentum: float = 0.9, weight_decay: float = 0.0):
-        if self.plan.trainable(self.stage):
+        if self.plan.trainable(self.stage) and not self.idle:
             a, b = self.ex.param_range(self.a0, self.g1)
             self.ex.sgd_range(a, b, lr, momentum, weight_decay)
 
@@ -493,7 +643,7 @@ class StageRunner:
         p = self.plan
         L = len(segments) - 1
         out = torch.zeros(L, dtype=torch.float64, device=self.ex.g32.device)
-        if p.trainable(self.stage):
+        if p.trainable(self.stage) and not self.idle:
             a, b = self.ex.param_range(self.a0, self.g1)
             cuts = sorted({a, b} | {x for x in segments if a < x < b})
             part = torch.zeros(len(cuts) - 1, dtype=torch.float64, device=out.device)

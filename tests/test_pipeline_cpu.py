@@ -58,7 +58,17 @@ def scenario_transition():
     return [(a, [31]), (b, [32, 33]), (b, [34, 35])]
 
 
-SCENARIOS = {"pipeline": scenario_pipeline, "dp": scenario_dp, "transition": scenario_transition}
+def scenario_idle():
+    # AutoPipe on, AutoDP off: K 2 -> 1 keeps R = 1, so rank 1 idles
+    # (runner.cpp:445) yet joins the migration broadcast and the norm
+    # all-reduce
+    a = plan(2, 1, 2, 0, [(0, 2), (2, 6)])
+    b = plan(1, 1, 2, 1, [(2, 6)])
+    return [(a, [41]), (b, [42]), (b, [43])]
+
+
+SCENARIOS = {"pipeline": scenario_pipeline, "dp": scenario_dp, "transition": scenario_transition,
+             "idle": scenario_idle}
 BATCH = 7
 
 
@@ -73,7 +83,7 @@ def _worker(rank, world, port, name, out_dir):
         for p, seeds in SCENARIOS[name]():
             run.set_plan(p)
             pipe, stage = p.role(rank)
-            x, y = _data(seeds[pipe], BATCH, ex)
+            x, y = _data(seeds[min(pipe, len(seeds) - 1)], BATCH, ex)
             loss = run.iteration(x, y, BATCH)
             run.sync_grads()
             norms = run.layer_sqnorms(ex.segments())

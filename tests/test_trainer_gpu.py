@@ -85,41 +85,108 @@ def _port():
     return p
 
 
-def _worker(rank, world, port, out, tier="hbm", peer=False):
+def _worker(rank, world, port, out, tier="hbm", peer=False, autodp=True):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         torch.cuda.set_device(0)
         scen = _elastic_scenario()
-        tr = Trainer(scen, configs.GEOMETRIES["tiny-vit"], iterations_per_epoch=2, rank=rank,
+        scen["features"]["autodp"] = autodp
+        tr = Trainer(scen, configs.GEOMETRIES["tiny-vit"], iterations_per_epoch=3, rank=rank,
                      world=world, device="cuda:0", host_staged=True, device_norms=False,
                      cache_tier=tier, peer=peer)
-        rows = tr.run()
-        torch.save([(r.l_frozen, r.k, r.r, r.m, r.cache_enabled, r.mean_loss) for r in rows],
+        rows = []
+        for e in range(5):
+            rows.append(tr.run_epoch(e))
+            if e == 1:
+                store_bytes = tr.store.shard_bytes()
+        tr.close()
+        torch.save({"rows": [(r.l_frozen, r.k, r.r, r.m, r.cache_enabled, r.mean_loss,
+                              r.samples) for r in rows],
+                    "csv": Trainer.report_csv(rows), "store_bytes": store_bytes,
+                    "dataset": tr.dataset},
                    os.path.join(out, f"tr_{rank}.pt"))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("tier,peer", [("hbm", False), ("host", False), ("hbm", True)])
-def test_two_rank_elastic_run(cuda, tmp_path, tier, peer):
-    mp.spawn(_worker, args=(2, _port(), str(tmp_path), tier, peer), nprocs=2, join=True)
-    a, b = (torch.load(tmp_path / f"tr_{r}.pt") for r in range(2))
+@pytest.mark.parametrize("tier,peer,autodp", [("hbm", False, True), ("host", False, True),
+                                              ("hbm", True, True), ("hbm", False, False)])
+def test_two_rank_elastic_run(cuda, tmp_path, tier, peer, autodp):
+    """Two ranks run the elastic schedule: K 2 -> 1 with a replica fork (or,
+    AutoDP off, with the freed GPU idle -- runner.cpp:445), cache writes into
+    the node-sharded store (HBM: each rank holds half the rows, peers'
+    rows over IPC) or the shared host segment, measured CSV columns."""
+    mp.spawn(_worker, args=(2, _port(), str(tmp_path), tier, peer, autodp), nprocs=2, join=True)
+    ra, rb = (torch.load(tmp_path / f"tr_{r}.pt") for r in range(2))
+    a, b = ra["rows"], rb["rows"]
     assert [x[:5] for x in a] == [x[:5] for x in b]
     ks = [x[1] for x in a]
-    assert ks == [2, 2, 1, 1, 1] and [x[2] for x in a] == [1, 1, 2, 2, 2]
+    assert ks == [2, 2, 1, 1, 1]
+    assert [x[2] for x in a] == ([1, 1, 2, 2, 2] if autodp else [1, 1, 1, 1, 1])
     assert [x[4] for x in a] == [False, True, True, True, True]
+    assert all(x[6] == ra["dataset"] for x in a)  # every sample trained every epoch
     # the planner packs 2 stages into 1 and forks a second replica at some epoch
     from paper_2102_03161_b200 import LIB_PATH
     from paper_2102_03161_b200.capi import EpsApi
     from paper_2102_03161_b200.planner import Planner
-    pl = Planner(EpsApi(LIB_PATH, "eps_"), _elastic_scenario())
+    sc = _elastic_scenario()
+    sc["features"]["autodp"] = autodp
+    pl = Planner(EpsApi(LIB_PATH, "eps_"), sc)
     want = [pl.begin_epoch(e) for e in range(5)]
     assert ks == [d.pipeline_length for d in want]
     assert [x[0] for x in a] == [d.l_frozen for d in want]
     for x in a + b:
         if x[5] == x[5]:  # last-stage ranks report a loss
             assert 0 < x[5] < 20
+    g = configs.GEOMETRIES["tiny-vit"]
+    row = g.tokens * g.hidden * 2
+    if tier == "hbm":  # per-GPU store bytes ~ dataset / world
+        assert ra["store_bytes"] == rb["store_bytes"] == -(-ra["dataset"] // 2) * row
+    else:  # one node-wide segment
+        assert ra["store_bytes"] == ra["dataset"] * row
+    lines = ra["csv"].splitlines()
+    assert len(lines) == 6 and all(len(ln.split(",")) == 15 for ln in lines)
+
+
+def _shard_worker(rank, world, port, out):
+    """Each rank scatters the rows it 'processed' into the node-sharded store
+    (half of them land on the peer's HBM over IPC), then gathers every row."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import ctypes as C
+        from paper_2102_03161_b200 import ops
+        from paper_2102_03161_b200.trainer import CacheStore
+        torch.cuda.set_device(0)
+        n, elems = 13, 96
+        st = CacheStore("hbm", n, elems, rank, world, torch.device("cuda:0"), collective=True)
+        mine = torch.arange(rank, n, world, device="cuda:0")
+        src = (mine.to(torch.float32)[:, None] * 1000 +
+               torch.arange(elems, device="cuda:0")[None, :]).to(torch.bfloat16)
+        s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        ops.call("eps_cache_scatter_sharded", st.table, C.c_int64(st.rows_per_shard), mine,
+                 mine.numel(), C.c_int64(elems * 2), src, s)
+        torch.cuda.synchronize()
+        dist.barrier()
+        got = st.rows(torch.arange(n, device="cuda:0"))
+        torch.cuda.synchronize()
+        torch.save({"got": got.cpu(), "local_rows": st.local.shape[0]},
+                   os.path.join(out, f"sh_{rank}.pt"))
+        dist.barrier()
+        st.close()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_store_peer_gather(cuda, tmp_path):
+    mp.spawn(_shard_worker, args=(2, _port(), str(tmp_path)), nprocs=2, join=True)
+    want = (torch.arange(13, dtype=torch.float32)[:, None] * 1000 +
+            torch.arange(96)[None, :]).to(torch.bfloat16)
+    for r in range(2):
+        o = torch.load(tmp_path / f"sh_{r}.pt")
+        assert o["local_rows"] == 7  # ceil(13 / 2) rows per GPU
+        assert torch.equal(o["got"], want)
 
 
 def test_measured_timeline_blocks(cuda):
@@ -145,6 +212,19 @@ def test_host_tier_prefetch_window_matches_hbm_tier(cuda):
     scen["training"]["alpha"] = 0.5
     scen["cache"]["policy"] = "always_on"
     g = configs.GEOMETRIES["tiny-vit"]
+    # the window stages exactly the store's rows (bitwise)
+    tr = Trainer(scen, g, iterations_per_epoch=3, device_norms=False, cache_tier="host",
+                 cache_prefetch=True)
+    rows = [tr.run_epoch(e) for e in range(5)]
+    last = rows[-1]
+    assert last.cache_enabled and not last.cache_moved
+    _, shards = tr.api.redistribute(tr.dataset, tr.cluster, last.k, last.epoch, tr.seed)
+    ids = torch.tensor(shards[0], dtype=torch.int64, device="cuda")
+    n_its = len(shards[0]) // tr.batch
+    ids_last = ids[(n_its - 1) * tr.batch:n_its * tr.batch]
+    torch.cuda.synchronize()
+    assert torch.equal(tr._win_buf[(n_its - 1) % 2], tr.store.rows(ids_last))
+    tr.close()
     runs = {}
     for name, kw in {"hbm": dict(cache_tier="hbm"),
                      "host": dict(cache_tier="host", cache_prefetch=False),
@@ -157,6 +237,7 @@ def test_host_tier_prefetch_window_matches_hbm_tier(cuda):
         for a, b in zip(runs[name], runs["hbm"]):
             assert a[:3] == b[:3]
             # bias-gradient reductions use float atomics (run-to-run order), so
-            # equal inputs agree to rounding, not bit for bit
+            # equal inputs agree to rounding, not bit for bit (the staged rows
+            # themselves are checked bitwise above)
             assert abs(a[3] - b[3]) <= 1e-3 * abs(b[3])
             assert all(abs(x - y) <= 1e-2 * max(abs(y), 1e-6) for x, y in zip(a[4], b[4]))

@@ -55,6 +55,19 @@ def test_cache_paths_equivalent(cuda):
     assert abs(cached - base) <= 1e-5 * abs(base)
     assert _rel(g_moved, g_base) < 1e-5
     assert _rel(ex.g32, g_base) < 1e-5
+    # trailing boundary (runner.cpp:186-213): the store stays at X[2] while
+    # L_f = 3 -- gather X[2], forward layer 2, write nothing
+    before = store.clone()
+    ex.g32.zero_()
+    trail = ex.train_step(images, labels, l_frozen=3, cache_mode=3, cache_old=2, store=store,
+                          ids=ids).item()
+    g_trail = ex.g32.clone()
+    ex.g32.zero_()
+    ref3 = ex.train_step(images, labels, l_frozen=3).item()
+    torch.cuda.synchronize()
+    assert torch.equal(store, before)
+    assert abs(trail - ref3) <= 1e-5 * abs(ref3)
+    assert _rel(g_trail, ex.g32) < 1e-5
     # boundary move 2 -> 3 reads the old boundary from the store
     ex.g32.zero_()
     ex.train_step(images, labels, l_frozen=3, cache_mode=2, cache_old=2, store=store, ids=ids)

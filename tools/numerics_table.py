@@ -22,7 +22,7 @@ CASES = [("tiny-vit", 16, 0, 1), ("tiny-vit", 16, 2, 3), ("vit-b16", 8, 0, 1),
          ("vit-b16", 8, 6, 2), ("vit-b16-cifar100", 4, 4, 1), ("tiny-bert-qa", 4, 0, 1),
          ("tiny-bert-cls", 6, 1, 3), ("bert-base-384", 4, 0, 1), ("bert-base-384", 4, 6, 2),
          ("bert-large-128", 8, 0, 1), ("bert-large-128", 8, 12, 2)]
-TRAJ = [("vit-b16", 8, 0, 1e-3), ("vit-b16", 8, 6, 1e-3), ("bert-base-384", 4, 0, 5e-4),
+TRAJ = [("vit-b16", 8, 0, 5e-4), ("vit-b16", 8, 6, 1e-3), ("bert-base-384", 4, 0, 5e-4),
         ("bert-large-128", 8, 0, 1e-3)]
 
 
