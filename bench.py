@@ -471,7 +471,7 @@ def main_ours(args, world, rank, local):
     try:
         with open(os.path.join(ROOT, "profiles", "gemm_traffic.json")) as f:
             tr = json.load(f)
-        t = tr.get("configs", {}).get(cfg, tr)
+        t = tr["configs"][cfg]
         roofline["traffic"] = round(t["mean_dram_bytes_per_launch"])
         if "mean_algorithmic_bytes_per_launch" in t:
             roofline["traffic_algorithmic"] = round(t["mean_algorithmic_bytes_per_launch"])
