@@ -19,6 +19,7 @@ import os
 import re
 import subprocess
 
+import filelock
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -42,18 +43,21 @@ KNOWN_FAILURES = {"test_engine": ["test_engine.cpp:260: CHECK(profile.chosen < 2
 def built():
     if not os.path.isdir(REF):
         pytest.skip("reference sources not present (GPU box)")
-    r = subprocess.run(["make", "-s", "conformance"], cwd=ROOT, capture_output=True, text=True,
-                       timeout=600)
+    os.makedirs(os.path.join(ROOT, "build"), exist_ok=True)
+    # one build at a time when pytest-xdist runs several workers
+    with filelock.FileLock(os.path.join(ROOT, "build", ".conformance.lock")):
+        r = subprocess.run(["make", "-s", "conformance"], cwd=ROOT, capture_output=True,
+                           text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     return BIN
 
 
 @pytest.mark.parametrize("suite", sorted(SUITES))
-def test_reference_suite_against_product(built, suite):
+def test_reference_suite_against_product(built, suite, tmp_path):
     bad_expected, skip = SUITES[suite]
     env = dict(os.environ, DOCTEST_SKIP="|".join(skip))
     r = subprocess.run([os.path.join(built, suite)], capture_output=True, text=True, timeout=120,
-                       env=env, cwd=ROOT)
+                       env=env, cwd=tmp_path)
     m = re.search(r"test cases: (\d+) passed, (\d+) failed, (\d+) skipped \| checks: (\d+) "
                   r"passed, (\d+) failed", r.stdout)
     assert m, (r.stdout[-2000:], r.stderr[-2000:])
