@@ -16,7 +16,7 @@ the final LayerNorm bias under a span head: sum over tokens of softmax - one
 -hot = 0) have no relative error; they are held to an absolute bound instead
 (`zero_tensors`).
 
-Why `kernel` is not the gate (measured, profiles/r02_numerics.md): a bf16-
+Why `kernel` is not the gate (measured, profiles/r02/numerics.md): a bf16-
 storage computation is chaotic at the rounding level.  Perturbing the input
 images by 1e-6 (relative) moves BF16_STORAGE's own gradients by 0.9-1.4 %
 relative L2 at ViT-B/16 -- as much as its distance from FP32 -- while FP32

@@ -13,7 +13,7 @@ under both numerics policies (oracle/numerics.py; harness tests/parity_lib.py):
   1e-2 vs FP32 is not attainable by any bf16-storage design at these depths
   (the emulation itself sits at 1.0-1.5 % for ViT-B/16 and 2-4 % for BERT;
   measured table and the rounding-chaos experiment in
-  profiles/r02_numerics.md);
+  profiles/r02/numerics.md);
 * mathematically-zero gradients (QA span head: classifier bias, final LN
   bias): no larger than the emulation's rounding noise (x 3);
 * frozen tensors: exactly zero;

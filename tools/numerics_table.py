@@ -37,8 +37,8 @@ def tensor_class(name: str) -> str:
 def main():
     out = sys.argv[1] if len(sys.argv) > 1 else "gpurun_out/numerics"
     torch.set_num_threads(os.cpu_count() or 8)
-    rows, md = [], ["| case | loss dev / fp32 (rel) | class | kernel | vs fp32 | intrinsic |",
-                    "|---|---|---|---|---|---|"]
+    rows, md = [], ["| case | loss dev / fp32 (rel) | class | kernel | vs fp32 (worst tensor) | "
+                    "intrinsic | self noise |", "|---|---|---|---|---|---|---|"]
     for cfg, b, lf, m in CASES:
         t = time.time()
         c = run_case(cfg, b, lf, m, self_noise=True)
