@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 
 #include <cfloat>
+#include <cstdlib>
 #include <unordered_map>
 
 #include "eps_capi.h"
@@ -1073,6 +1074,14 @@ size_t bwd_fused_smem(int T) {
 // time.)  A single TMA warp loads head i into buffer i & 1.
 constexpr int kFwdThreads = 12 * 32;  // TMA, MMA0, MMA1, (alloc), WG0 (4-7), WG1 (8-11)
 
+// POLY of the 16 exp pairs of a full 32-key chunk run as poly_exp2_x2 on the
+// FMA / ALU pipes, the rest on the SFU (evenly interleaved).
+template <int POLY>
+__device__ __forceinline__ constexpr bool fwd_poly_pair(int j) {
+  return (j * POLY) / 16 != ((j + 1) * POLY) / 16;
+}
+
+template <int POLY>
 __global__ void __launch_bounds__(kFwdThreads, 1)
     attn_fwd_persistent_tc_kernel(const __grid_constant__ CUtensorMap map_qkv, const Params p,
                                   int n_heads) {
@@ -1202,13 +1211,17 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         float ms = 0.f;
         const float2 sl2x2 = make_float2(sl2, sl2);
         float2 sum2 = make_float2(0.f, 0.f);  // two interleaved partial sums (packed FADD2)
-        for (int ch = 0; ch * 32 < Tn; ++ch) {
+        const int nch = (Tn + 31) / 32;
+        uint32_t ra[32];
+        auto issue = [&](int ch, uint32_t(&r)[32]) {
+          if (p.T - ch * 32 <= 16)
+            tmem_ld_32x32_x16(tS + uint32_t(ch * 32), reinterpret_cast<uint32_t(&)[16]>(r));
+          else
+            tmem_ld_32x32(tS + uint32_t(ch * 32), r);
+        };
+        auto process = [&](int ch, uint32_t(&r)[32]) {
           uint32_t pk[16];
           const int rem = p.T - ch * 32;  // valid keys in this chunk (>= 1)
-          uint32_t r[32];
-          if (rem <= 16) tmem_ld_32x32_x16(tS + uint32_t(ch * 32), reinterpret_cast<uint32_t(&)[16]>(r));
-          else tmem_ld_32x32(tS + uint32_t(ch * 32), r);
-          tmem_ld_wait();
           // the chunk max is needed up front only for chunk 0; later chunks
           // compute exps and max side by side and redo the exps on a rescale
           auto chunk_max = [&]() {
@@ -1230,12 +1243,13 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           auto chunk_exp = [&](float msr) {
             const float2 nms2 = make_float2(-msr, -msr);
             float2 cs = make_float2(0.f, 0.f);
-            if (rem >= 32) {  // full chunk: no key mask
+            if (rem >= 32) {  // full chunk: no key mask; POLY of the 16 pairs on the FMA pipe
 #pragma unroll
               for (int j = 0; j < 16; ++j) {
                 const float2 a = __ffma2_rn(
                     make_float2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1])), sl2x2, nms2);
-                const float2 e = make_float2(fast_exp2(a.x), fast_exp2(a.y));
+                const float2 e = fwd_poly_pair<POLY>(j) ? poly_exp2_x2(a)
+                                                        : make_float2(fast_exp2(a.x), fast_exp2(a.y));
                 cs = __fadd2_rn(cs, e);
                 pk[j] = pack_bf16(e.x, e.y);
               }
@@ -1289,6 +1303,13 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           }
           sum2 = __fadd2_rn(sum2, cs);
           tmem_st_32x32_x16(tS + uint32_t(ch * 16), pk);
+        };
+        // (a register double-buffered variant -- the load of chunk ch + 1 in
+        // flight while chunk ch is exponentiated -- measured 10 % slower)
+        for (int ch = 0; ch < nch; ++ch) {
+          issue(ch, ra);
+          tmem_ld_wait_regs(ra);
+          process(ch, ra);
         }
         const float sum = sum2.x + sum2.y;
         tmem_st_wait();
@@ -1355,6 +1376,18 @@ bool attn_tc_supported(int T, int head_dim) { return head_dim == 64 && T >= 1 &&
 
 static int g_trace_on = 0;
 
+// Pairs of exps per 32-key chunk computed on the FMA pipe in the forward
+// (attn_fwd_persistent_tc_kernel<POLY>): 4 of 16 measured best (0.173 ->
+// 0.168 ms at ViT-B/16 b400; 6: 0.171, 8: 0.176, 10: 0.182).  EPS_ATTN_POLY=0
+// selects the all-SFU variant for A/B runs.
+static int fwd_poly_mode() {
+  static const int mode = [] {
+    const char* e = std::getenv("EPS_ATTN_POLY");
+    return e == nullptr ? 4 : std::atoi(e);
+  }();
+  return mode;
+}
+
 int attn_fwd_tc(const void* qkv, void* out, float* lse, int B, int T, int H, float scale,
                 cudaStream_t st) {
   using namespace attn_tc;
@@ -1375,12 +1408,13 @@ int attn_fwd_tc(const void* qkv, void* out, float* lse, int B, int T, int H, flo
   p.trace = g_trace_on;
   if (T <= 2 * kTile) {
     const size_t sp = fwd_persistent_smem(T);
-    if (!ensure_smem(attn_fwd_persistent_tc_kernel, sp)) return EPS_ECUDA;
+    auto kern = fwd_poly_mode() == 0 ? attn_fwd_persistent_tc_kernel<0>
+                                      : attn_fwd_persistent_tc_kernel<4>;
+    if (!ensure_smem(kern, sp)) return EPS_ECUDA;
     const int heads = B * H;
     const int grid = heads < sm_count() ? heads : sm_count();
     count_launch();
-    if (launch_k(attn_fwd_persistent_tc_kernel, dim3(grid), dim3(kFwdThreads), sp, st, 1, m, p,
-                 heads) != cudaSuccess)
+    if (launch_k(kern, dim3(grid), dim3(kFwdThreads), sp, st, 1, m, p, heads) != cudaSuccess)
       return EPS_ECUDA;
     return cudaGetLastError() == cudaSuccess ? EPS_OK : EPS_ECUDA;
   }

@@ -381,6 +381,44 @@ __device__ __forceinline__ float fast_exp2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+
+// 2^x for a pair on the FMA / ALU pipes instead of the SFU (which retires 16
+// lane-ops per SM clock): x = n + f with n = round(x), f in [-1/2, 1/2];
+// 2^f by a degree-4 minimax polynomial (max relative error 2.7e-6 in fp32;
+// degree 3, 7.5e-5, measurably moved the tiniest gradient tensors), 2^n added to the exponent field with one shift-add (the
+// rounding constant 1.5 * 2^23 leaves n in the low mantissa bits of t, and its
+// own bits above bit 8 shift out).  x is clamped at -125 so the result stays
+// a normal number (2^-125 is zero for every softmax sum it can enter).
+__device__ __forceinline__ float2 poly_exp2_x2(float2 x) {
+  constexpr float kRound = 12582912.0f;  // 1.5 * 2^23
+  x.x = fmaxf(x.x, -125.0f);
+  x.y = fmaxf(x.y, -125.0f);
+  const float2 t = __fadd2_rn(x, make_float2(kRound, kRound));
+  const float2 n = __fadd2_rn(t, make_float2(-kRound, -kRound));
+  const float2 f = __fadd2_rn(x, make_float2(-n.x, -n.y));
+  float2 p = __ffma2_rn(make_float2(0.009570087306f, 0.009570087306f), f,
+                        make_float2(0.05591785535f, 0.05591785535f));
+  p = __ffma2_rn(p, f, make_float2(0.24024744332f, 0.24024744332f));
+  p = __ffma2_rn(p, f, make_float2(0.69312179089f, 0.69312179089f));
+  p = __ffma2_rn(p, f, make_float2(0.99999928474f, 0.99999928474f));
+  return make_float2(__uint_as_float((__float_as_uint(t.x) << 23) + __float_as_uint(p.x)),
+                     __uint_as_float((__float_as_uint(t.y) << 23) + __float_as_uint(p.y)));
+}
+
+// tcgen05.wait::ld that also orders the compiler: the loaded registers are
+// operands, so no use of them can be scheduled above the wait (a prefetched
+// TMEM chunk is consumed one loop step after its load was issued).
+__device__ __forceinline__ void tmem_ld_wait_regs(uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.wait::ld.sync.aligned;"
+      : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]),
+        "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]),
+        "+r"(r[14]), "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]),
+        "+r"(r[20]), "+r"(r[21]), "+r"(r[22]), "+r"(r[23]), "+r"(r[24]), "+r"(r[25]),
+        "+r"(r[26]), "+r"(r[27]), "+r"(r[28]), "+r"(r[29]), "+r"(r[30]), "+r"(r[31])
+      :
+      : "memory");
+}
 }  // namespace eps_k
 
 // ---- warp-synchronous tcgen05 issue -----------------------------------------

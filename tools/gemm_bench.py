@@ -35,6 +35,27 @@ SHAPES = {  # name: (M, N, K, a_mn, b_mn, epi, split)
     "mb17_dgrad_fc2": (17 * 197, 3072, 768, False, True, ops.EPI_MUL_BF16, 1),
     "mb17_dgrad_qkv": (17 * 197, 768, 2304, False, True, ops.EPI_STORE_BF16, 1),
 }
+# one ViT-B/16 layer's 12 GEMMs at a K = 8 pipeline micro-batch (18 samples,
+# the planner's 1 x 8 epoch-0 plan: M = 23 micro-batches of 400 samples)
+R18 = 18 * 197
+LAYER18 = {
+    "b18_fwd_qkv": (R18, 2304, 768, False, False, ops.EPI_BIAS_BF16, 1),
+    "b18_fwd_proj": (R18, 768, 768, False, False, ops.EPI_BIAS_RESID_BF16, 1),
+    "b18_fwd_fc1": (R18, 3072, 768, False, False, ops.EPI_BIAS_GELU2_BF16, 1),
+    "b18_fwd_fc2": (R18, 768, 3072, False, False, ops.EPI_BIAS_RESID_BF16, 1),
+    "b18_wgrad_fc2": (768, 3072, R18, True, True, ops.EPI_ACCUM_F32, 0),
+    "b18_dgrad_fc2": (R18, 3072, 768, False, True, ops.EPI_MUL_BF16, 1),
+    "b18_wgrad_fc1": (3072, 768, R18, True, True, ops.EPI_ACCUM_F32, 0),
+    "b18_dgrad_fc1": (R18, 768, 3072, False, True, ops.EPI_STORE_BF16, 1),
+    "b18_wgrad_proj": (768, 768, R18, True, True, ops.EPI_ACCUM_F32, 0),
+    "b18_dgrad_proj": (R18, 768, 768, False, True, ops.EPI_ROWDOT_BF16, 1),
+    "b18_wgrad_qkv": (2304, 768, R18, True, True, ops.EPI_ACCUM_F32, 0),
+    "b18_dgrad_qkv": (R18, 768, 2304, False, True, ops.EPI_STORE_BF16, 1),
+}
+SHAPES.update(LAYER18)
+SHAPES.update({k.replace("b18", "b400"): (400 * 197 if v[0] == R18 else v[0], v[1],
+                                           400 * 197 if v[2] == R18 else v[2]) + v[3:]
+               for k, v in LAYER18.items()})
 
 
 def run(name, M, N, K, a_mn, b_mn, epi, split, iters=20):
@@ -53,9 +74,16 @@ def run(name, M, N, K, a_mn, b_mn, epi, split, iters=20):
         ops.gemm(a, b, out, **kw)
     torch.cuda.synchronize()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # device time: `iters` launches captured in one CUDA graph (a Python loop
+    # of ctypes calls is host-bound for the small micro-batch shapes)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        for _ in range(iters):
+            ops.gemm(a, b, out, **kw)
+    graph.replay()
+    torch.cuda.synchronize()
     s.record()
-    for _ in range(iters):
-        ops.gemm(a, b, out, **kw)
+    graph.replay()
     e.record()
     torch.cuda.synchronize()
     ms = s.elapsed_time(e) / iters
@@ -63,6 +91,9 @@ def run(name, M, N, K, a_mn, b_mn, epi, split, iters=20):
     # torch reference speed for context
     A = a.t() if a_mn else a
     B = b.t() if b_mn else b
+    for _ in range(3):
+        torch.matmul(A, B.t())
+    torch.cuda.synchronize()
     s.record()
     for _ in range(iters):
         torch.matmul(A, B.t())
@@ -75,5 +106,20 @@ def run(name, M, N, K, a_mn, b_mn, epi, split, iters=20):
 
 if __name__ == "__main__":
     names = sys.argv[1:] or list(SHAPES)
-    for n in names:
-        print(json.dumps(run(n, *SHAPES[n])), flush=True)
+    if names == ["layer18"] or names == ["layer400"]:
+        tag = names[0][5:]
+        names = [k for k in SHAPES if k.startswith(f"b{tag}_")]
+        tot, tot_t, fl = 0.0, 0.0, 0.0
+        for n in names:
+            r = run(n, *SHAPES[n])
+            tot += r["ms"]
+            tot_t += r["torch_ms"]
+            M, N, K = SHAPES[n][:3]
+            fl += 2.0 * M * N * K
+            print(json.dumps(r), flush=True)
+        print(json.dumps({"layer": f"b{tag}", "ms": round(tot, 4), "tflops": round(fl / tot / 1e9, 1),
+                          "torch_ms": round(tot_t, 4),
+                          "torch_tflops": round(fl / tot_t / 1e9, 1)}), flush=True)
+    else:
+        for n in names:
+            print(json.dumps(run(n, *SHAPES[n])), flush=True)
