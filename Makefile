@@ -19,7 +19,7 @@ NVFLAGS   := -std=c++20 -O3 $(ARCH) -lineinfo -Xcompiler -fPIC -Iinclude -I$(NLO
              --expt-relaxed-constexpr -Xptxas -v
 
 CONTROL_SRC := $(wildcard $(PKG)/csrc/control/*.cpp) $(PKG)/csrc/capi_control.cpp \
-               $(PKG)/csrc/runtime/comm.cpp
+               $(PKG)/csrc/runtime/comm.cpp $(PKG)/csrc/runtime/disk_tier.cpp
 KERNEL_SRC  := $(wildcard $(PKG)/csrc/kernels/*.cu) $(wildcard $(PKG)/csrc/runtime/*.cu)
 OBJDIR      := build/obj
 CONTROL_OBJ := $(patsubst %.cpp,$(OBJDIR)/%.o,$(CONTROL_SRC))

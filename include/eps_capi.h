@@ -282,6 +282,13 @@ int EPS_FN(cache_transition)(int enabled, int boundary_layer, const eps_cache_ti
                              const eps_cost_model_t* cm, double* read_s, double* compute_s,
                              double* write_s);
 
+/* One epoch of the modeled disk -> host window (CacheTierSim,
+ * autocache.cpp:69-150) as runner.cpp:258-265 charges it: batches consumed in
+ * order, each taking iteration_seconds plus its stall.  out: [total stall s,
+ * max resident bytes, prefetches, evictions, sliding (0/1)]. */
+int EPS_FN(cache_tier_epoch)(const eps_cache_tiers_t* tiers, double bytes_per_batch,
+                             int total_batches, double iteration_seconds, double* out);
+
 /* ---- scenario.hpp / runner.hpp ---------------------------------------- */
 int EPS_FN(scenario_load)(const char* path, eps_scenario_t** out);
 int EPS_FN(scenario_parse)(const char* json_text, eps_scenario_t** out);
@@ -517,10 +524,56 @@ int eps_peer_signal(void* flag, uint32_t value, void* stream);
 int eps_peer_wait(const void* flag, uint32_t value, void* stream);
 /* Stream-ordered device copy (peer addresses allowed, UVA). */
 int eps_copy_async(void* dst, const void* src, int64_t bytes, void* stream);
+/* Stream-ordered 2D copy (UVA, any direction): `height` rows of `width`
+ * bytes with row pitches dpitch / spitch (disk-tier window -> HBM staging). */
+int eps_copy2d_async(void* dst, int64_t dpitch, const void* src, int64_t spitch, int64_t width,
+                     int64_t height, void* stream);
 /* Page-lock / release an existing host range (cudaHostRegister, portable +
  * mapped): the node-wide shared-memory host tier of the AutoCache store. */
 int eps_host_register(void* ptr, int64_t bytes);
 int eps_host_unregister(void* ptr);
+
+/* ---- AutoCache disk tier (csrc/runtime/disk_tier.cpp) ---------------------
+ * Replaces the reference's modeled disk -> host sliding window,
+ * CacheTierSim (autocache.cpp:69-150; CacheTierParams autocache.hpp:11-20:
+ * window_batches, block_batches), with real I/O: a backing file of `rows`
+ * cached samples (row_bytes each, padded to 4 KiB, O_DIRECT when the
+ * filesystem allows) and a page-locked host window of
+ * window_batches / block_batches block slots filled by `threads` I/O threads
+ * in the epoch's consumption order.  Host memory only, no CUDA calls on the
+ * data path; the window is cudaHostRegister'ed when a device is present.
+ *   open: create != 0 makes / truncates the file (one node-wide file; ranks
+ *         open it after the creator);
+ *   write: rows `ids` from host rows `src` (src_stride bytes apart);
+ *   begin_epoch: the epoch's sample order; batches of batch_rows rows (last
+ *         ragged) or, with batch_offsets (n_batches + 1 entries, each batch <=
+ *         batch_rows), explicit ones; stages the leading window
+ *         (CacheTierSim constructor);
+ *   acquire: blocks until batch `batch` (batch_rows rows of the order) is
+ *         resident; *rows = its first row (rows `stride` bytes apart,
+ *         eps_disk_tier_info), *stall_s = the wait (WindowStep::stall_seconds);
+ *         EPS_ELOGIC if the batch lies beyond the window (release earlier
+ *         batches first, batches are consumed in order as in
+ *         CacheTierSim::advance);
+ *   release: the batch is consumed; fully consumed blocks are evicted and
+ *         their slots refilled with the next blocks (issue_prefetches);
+ *   stats: [bytes read, I/O-thread read seconds, stall seconds, max resident
+ *         window bytes, prefetches, evictions, bytes written, O_DIRECT]. */
+typedef struct eps_disk_tier eps_disk_tier_t;
+int eps_disk_tier_open(const char* path, int64_t rows, int64_t row_bytes, int64_t batch_rows,
+                       int block_batches, int window_batches, int threads, int create,
+                       eps_disk_tier_t** out);
+int eps_disk_tier_close(eps_disk_tier_t* h);
+int eps_disk_tier_info(eps_disk_tier_t* h, int64_t* stride, int* direct, int* window_blocks,
+                       void** window);
+int eps_disk_tier_write(eps_disk_tier_t* h, const int64_t* ids, int64_t n, const void* src,
+                        int64_t src_stride);
+int eps_disk_tier_begin_epoch(eps_disk_tier_t* h, const int64_t* order, int64_t n,
+                              const int64_t* batch_offsets, int64_t n_batches);
+int eps_disk_tier_acquire(eps_disk_tier_t* h, int64_t batch, const void** rows,
+                          int64_t* n_rows, double* stall_s);
+int eps_disk_tier_release(eps_disk_tier_t* h, int64_t batch);
+int eps_disk_tier_stats(eps_disk_tier_t* h, double* out);
 
 /* ---- communicator plane (csrc/runtime/comm.cpp; NCCL) ----
  * The reference's message group (every rank) and training group (active

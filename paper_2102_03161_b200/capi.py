@@ -504,6 +504,16 @@ class EpsApi:
                   C.byref(c), C.byref(w))
         return r.value, c.value, w.value
 
+    def cache_tier_epoch(self, tiers, bytes_per_batch, total_batches, iteration_seconds):
+        """The modeled disk -> host window over one epoch (CacheTierSim as
+        runner.cpp:258-265 drives it): dict of total stall seconds, max resident
+        bytes, prefetches, evictions, sliding."""
+        out = (C.c_double * 5)()
+        self.call("cache_tier_epoch", C.byref(self._tiers(tiers)), C.c_double(bytes_per_batch),
+                  int(total_batches), C.c_double(iteration_seconds), out)
+        return {"stall_s": out[0], "max_resident_bytes": out[1], "prefetches": int(out[2]),
+                "evictions": int(out[3]), "sliding": bool(out[4])}
+
     # -- scenario.hpp / runner.hpp --
     def scenario(self, source) -> "Scenario":
         return Scenario(self, source)

@@ -524,6 +524,29 @@ int EPS_FN(cache_transition)(int enabled, int boundary_layer, const eps_cache_ti
   });
 }
 
+int EPS_FN(cache_tier_epoch)(const eps_cache_tiers_t* tiers, double bytes_per_batch,
+                             int total_batches, double iteration_seconds, double* out) {
+  return guarded([&] {
+    need_ptr(out, "out");
+    eps::CacheTierSim sim(to_tiers(tiers), bytes_per_batch, total_batches);
+    double now = 0.0;
+    int prefetches = 0, evictions = 0;
+    for (int b = 0; b < total_batches; ++b) {
+      const eps::WindowStep step = sim.advance(b, now);
+      now += iteration_seconds + step.stall_seconds;
+      for (const eps::TierAction& a : step.actions) {
+        if (a.kind == eps::TierAction::Kind::kPrefetch) ++prefetches;
+        if (a.kind == eps::TierAction::Kind::kEvict) ++evictions;
+      }
+    }
+    out[0] = sim.total_stall();
+    out[1] = sim.max_resident_bytes();
+    out[2] = prefetches;
+    out[3] = evictions;
+    out[4] = sim.sliding() ? 1.0 : 0.0;
+  });
+}
+
 int EPS_FN(scenario_load)(const char* path, eps_scenario_t** out) {
   return guarded([&] {
     need_ptr(path, "path");

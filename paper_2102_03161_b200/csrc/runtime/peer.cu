@@ -105,6 +105,23 @@ int eps_copy_async(void* dst, const void* src, int64_t bytes, void* stream) {
              : EPS_ECUDA;
 }
 
+// Stream-ordered 2D copy between any two UVA addresses (host <-> device):
+// `height` rows of `width` bytes, row pitches dpitch / spitch.  The AutoCache
+// disk tier moves a batch from its padded host window rows into HBM staging
+// with one call.
+int eps_copy2d_async(void* dst, int64_t dpitch, const void* src, int64_t spitch, int64_t width,
+                     int64_t height, void* stream) {
+  if (dst == nullptr || src == nullptr || width < 0 || height < 0 || dpitch < width ||
+      spitch < width)
+    return EPS_EINVAL;
+  if (width == 0 || height == 0) return EPS_OK;
+  return cudaMemcpy2DAsync(dst, size_t(dpitch), src, size_t(spitch), size_t(width),
+                           size_t(height), cudaMemcpyDefault,
+                           static_cast<cudaStream_t>(stream)) == cudaSuccess
+             ? EPS_OK
+             : EPS_ECUDA;
+}
+
 // Page-lock an existing host range (e.g. a node-wide shared-memory AutoCache
 // host tier that every rank of the node maps) so the gather / scatter
 // kernels can address it over the host link (UVA).

@@ -25,7 +25,11 @@ same norm vectors) and then *runs* the epoch:
     bytes ~ dataset / world, no replication or exchange.  Host tier: one
     node-wide pinned shared-memory segment every rank maps
     (autocache.cpp:69-150's host tier), read through a sliding prefetch
-    window on a copy stream.  Boundary-move epochs run the cache-write path
+    window on a copy stream.  Disk tier: a node-wide backing file behind a
+    page-locked host window refilled block by block by native I/O threads
+    (the reference's modeled disk -> host CacheTierSim, run for real:
+    disk_tier.py), copied batch by batch into HBM staging on a copy stream.
+    Boundary-move epochs run the cache-write path
     (autocache.cpp:45-67), trailing-boundary epochs gather the old boundary
     and forward the rest of the frozen prefix (runner.cpp:186-213), steady
     epochs gather and skip the frozen forward entirely.
@@ -65,7 +69,8 @@ class EpochResult:
     = the epoch's DP all-reduce time / the part not hidden behind the drain;
     transition = set_plan (migration + regroup); cache_transition = extra
     time of a boundary-move epoch's prefix work over a steady gather; stall
-    = compute-stream waits on the host tier's prefetch window."""
+    = compute-stream waits on the host tier's prefetch window, plus (disk
+    tier) host waits for blocks still being read from disk."""
     epoch: int
     l_frozen: int
     k: int
@@ -101,7 +106,9 @@ def _lib():
                     "eps_ipc_open": [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p],
                     "eps_ipc_close": [C.c_void_p],
                     "eps_host_register": [C.c_void_p, C.c_int64],
-                    "eps_host_unregister": [C.c_void_p]}.items():
+                    "eps_host_unregister": [C.c_void_p],
+                    "eps_copy2d_async": [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
+                                         C.c_int64, C.c_int64, C.c_void_p]}.items():
         getattr(lib, n).argtypes = args
         getattr(lib, n).restype = C.c_int
     return lib
@@ -116,10 +123,15 @@ class CacheStore:
     executor is switched to the sharded gather / scatter kernels.
     tier "host": one pinned host segment of dataset rows: private pinned
     memory at world 1, a POSIX shared-memory segment registered by every rank
-    (cudaHostRegister, mapped) when several ranks share the node."""
+    (cudaHostRegister, mapped) when several ranks share the node.
+    tier "disk": one node-wide file of dataset rows (rank 0 creates it under
+    `cache_dir`), each rank with its own DiskTier window of the scenario's
+    window_batches / block_batches (CacheTierParams) and I/O threads, plus a
+    pinned batch buffer for the write path."""
 
     def __init__(self, tier: str, dataset: int, row_elems: int, rank: int, world: int, device,
-                 collective: bool):
+                 collective: bool, batch: int = 0, tiers: Optional[dict] = None,
+                 cache_dir: Optional[str] = None):
         self.tier, self.dataset, self.row_elems = tier, dataset, row_elems
         self.rank, self.world, self.device = rank, world, device
         self.row_bytes = row_elems * 2
@@ -128,7 +140,11 @@ class CacheStore:
         self.shm = None
         self.registered = None
         self.table = None
-        if tier == "hbm":
+        self.disk = None
+        self.path = None
+        if tier == "disk":
+            self._open_disk(batch, tiers or {}, cache_dir, collective)
+        elif tier == "hbm":
             self.rows_per_shard = -(-dataset // world)
             self.local = torch.zeros(self.rows_per_shard, row_elems, dtype=torch.bfloat16,
                                      device=device)
@@ -185,6 +201,31 @@ class CacheStore:
         self.registered = self.local.data_ptr()
         dist.barrier()
 
+    # -- disk tier ------------------------------------------------------------------
+    def _open_disk(self, batch: int, tiers: dict, cache_dir: Optional[str], collective: bool):
+        import tempfile
+        from .disk_tier import DiskTier
+        d = cache_dir or os.environ.get("EPS_CACHE_DIR") or tempfile.gettempdir()
+        name = [f"eps_cache_{uuid.uuid4().hex[:16]}.bin" if self.rank == 0 else None]
+        if collective and self.world > 1:
+            dist.broadcast_object_list(name, src=0)
+        self.path = os.path.join(d, name[0])
+        wb = int(tiers.get("window_batches", 64))
+        bb = int(tiers.get("block_batches", 8))
+        # host capacity caps the window like CacheTierSim's constructor
+        cap = float(tiers.get("host_capacity_bytes", 64e9))
+        wb = max(bb, min(wb, int(cap // max(1, batch * self.row_bytes)) // bb * bb))
+        create = self.rank == 0 or not collective
+        if not create:
+            dist.barrier()  # the creator has sized the file
+        self.disk = DiskTier(self.path, self.dataset, self.row_bytes, batch, block_batches=bb,
+                             window_batches=wb, threads=8, create=create)
+        if create and collective and self.world > 1:
+            dist.barrier()
+        self.rows_per_shard = self.dataset
+        self.local = None
+        self.wbuf = torch.empty(batch, self.row_elems, dtype=torch.bfloat16).pin_memory()
+
     # -- use ------------------------------------------------------------------------
     def attach(self, ex):
         """Point the executor's cache_mode gathers / scatters at this store."""
@@ -194,12 +235,25 @@ class CacheStore:
             ex._call(ex.PREFIX + "set_cache_shards", C.c_void_p(0), C.c_int64(0))
 
     def store_arg(self):
-        """What the stage calls receive as `store`."""
+        """What the stage calls receive as `store` (disk tier: none -- the
+        trainer passes its HBM staging window)."""
         return self.local
 
     def rows(self, ids: torch.Tensor) -> torch.Tensor:
         """Rows of sample ids (test / report helper; gathers on the device)."""
         out = torch.empty(ids.numel(), self.row_elems, dtype=torch.bfloat16, device=self.device)
+        if self.disk is not None:  # read straight from the backing file
+            order = ids.cpu()
+            self.disk.begin_epoch(order)
+            o = 0
+            for b in range(-(-ids.numel() // self.disk.batch_rows)):
+                view, _ = self.disk.batch_view(b)
+                n = view.shape[0]
+                out[o:o + n].view(torch.uint8).view(n, self.row_bytes).copy_(
+                    view[:, :self.row_bytes])
+                self.disk.release(b)
+                o += n
+            return out
         if self.table is not None:
             ops.call("eps_cache_gather_sharded", self.table, C.c_int64(self.rows_per_shard),
                      ids, ids.numel(), C.c_int64(self.row_bytes), out,
@@ -211,10 +265,18 @@ class CacheStore:
         return out
 
     def shard_bytes(self) -> int:
-        """Bytes of the store this rank holds (HBM shard or its host segment)."""
+        """Bytes of the store this rank holds (HBM shard, its host segment, or
+        the disk tier's file)."""
+        if self.disk is not None:
+            return self.dataset * self.row_bytes
         return self.local.numel() * 2
 
     def close(self):
+        if self.disk is not None:
+            self.disk.close()
+            self.disk = None
+            if self.rank == 0 and self.path and os.path.exists(self.path):
+                os.unlink(self.path)
         for b in self.opened:
             self.lib.eps_ipc_close(C.c_void_p(b))
         self.opened = []
@@ -248,7 +310,8 @@ class Trainer:
                  seed: int = 17, lr: float = 1e-3, momentum: float = 0.9,
                  rank: int = 0, world: int = 1, device=None, host_staged: bool = False,
                  device_norms: bool = True, cache_tier: str = "hbm", peer: bool = False,
-                 cache_prefetch: bool = True, comm: str = "torch"):
+                 cache_prefetch: bool = True, comm: str = "torch",
+                 cache_dir: Optional[str] = None):
         self.g = geometry
         self.api = EpsApi(LIB_PATH, "eps_")
         self.planner = Planner(self.api, scenario)
@@ -283,9 +346,11 @@ class Trainer:
                                   device=self.device, generator=gen)
         self.labels = torch.randint(0, g.classes, (self.dataset,), device=self.device,
                                     generator=gen)
-        if cache_tier not in ("hbm", "host"):
-            raise ValueError("cache_tier must be 'hbm' or 'host'")
+        if cache_tier not in ("hbm", "host", "disk"):
+            raise ValueError("cache_tier must be 'hbm', 'host' or 'disk'")
         self.cache_tier = cache_tier
+        self.cache_dir = cache_dir
+        self.disk_stats: List[dict] = []
         self.cache_prefetch = cache_prefetch
         self.cache_prefetch_ctas = 8  # SMs the background gather borrows
         self._win_buf = None
@@ -350,7 +415,8 @@ class Trainer:
         if d.cache_enabled and self.store is None:
             self.store = CacheStore(self.cache_tier, self.dataset, self.g.tokens * self.g.hidden,
                                     self.rank, self.world, self.device,
-                                    collective=self.world > 1)
+                                    collective=self.world > 1, batch=self.batch,
+                                    tiers=self.scenario.get("cache"), cache_dir=self.cache_dir)
             self.store.attach(self.ex)
         if not d.cache_enabled:
             cache_mode, cache_old = 0, 0
@@ -378,6 +444,38 @@ class Trainer:
         window = (self.cache_tier == "host" and cache_mode == 1 and stage == 0 and not idle
                   and self.cache_prefetch)
         stream = torch.cuda.current_stream(self.device)
+        # Disk tier (stage 0 of a cache epoch): the executor always sees the
+        # HBM staging window with identity ids.  Batches that read the store
+        # (gather, trailing boundary, a boundary move from an old boundary)
+        # come from the disk tier's host window -- acquire (host wait = the
+        # disk stall), one 2D copy per batch on the copy stream one iteration
+        # ahead, release once copied; boundary moves write the new boundary
+        # rows back: staging -> pinned buffer -> file by sample id.
+        disk = self.cache_tier == "disk" and cache_mode in (1, 2, 3) and stage == 0 and not idle
+        disk_reads = disk and (cache_mode != 2 or cache_old > 0)
+        disk_stall = 0.0
+        if disk:
+            self._window_setup(self.batch)
+            self.ex._call(self.ex.PREFIX + "set_cache_shards", C.c_void_p(0), C.c_int64(0))
+            dt = self.store.disk
+            rb = self.store.row_bytes
+            if disk_reads:
+                dt.begin_epoch(shard.cpu(), its)
+
+            def dfetch(i):
+                nonlocal disk_stall
+                slot = i % 2
+                addr, n, st = dt.acquire(i)
+                disk_stall += st
+                self._win_copy.wait_event(self._win_free[slot])
+                if self.store.lib.eps_copy2d_async(
+                        C.c_void_p(self._win_buf[slot].data_ptr()), rb, C.c_void_p(addr),
+                        dt.stride, rb, n, C.c_void_p(self._win_copy.cuda_stream)) != 0:
+                    raise RuntimeError("eps_copy2d_async failed (disk tier)")
+                self._win_ready[slot].record(self._win_copy)
+
+            if disk_reads:
+                dfetch(0)
         if window:
             self._window_setup(self.batch)
             self.ex._call(self.ex.PREFIX + "set_cache_shards", C.c_void_p(0), C.c_int64(0))
@@ -406,6 +504,19 @@ class Trainer:
                  else None)
             y = self.labels.index_select(0, ids) if not idle else None
             store, sids = (self.store.store_arg() if self.store is not None else None), ids
+            if disk:
+                if disk_reads and it + 1 < len(its):
+                    self._win_ready[it % 2].synchronize()  # batch it copied out of the window
+                    dt.release(it)
+                    dfetch(it + 1)
+                if disk_reads:
+                    w0 = torch.cuda.Event(enable_timing=True)
+                    w1 = torch.cuda.Event(enable_timing=True)
+                    w0.record(stream)
+                    stream.wait_event(self._win_ready[it % 2])
+                    w1.record(stream)
+                    stalls.append((w0, w1))
+                store, sids = self._win_buf[it % 2], self._win_ids[:n]
             if window:
                 if it + 1 < len(its):
                     fetch(it + 1)
@@ -418,7 +529,12 @@ class Trainer:
                 store, sids = self._win_buf[it % 2], self._win_ids[:n]
             loss = self.runner.iteration(x, y, n, cache_mode=cache_mode, cache_old=cache_old,
                                          store=store, ids=sids)
-            if window:
+            if disk and cache_mode == 2:  # the new boundary rows go to the file
+                wb = self.store.wbuf[:n]
+                wb.copy_(self._win_buf[it % 2][:n], non_blocking=True)
+                torch.cuda.current_stream(self.device).synchronize()
+                dt.write(ids.cpu(), wb)
+            if window or disk:
                 self._win_free[it % 2].record(stream)
             self.runner.sync_grads()
             if last:
@@ -427,7 +543,12 @@ class Trainer:
             if stage == plan.K - 1 and not idle:
                 losses.append((loss.clone(), n))
         stop.record()
-        if window:
+        if disk_reads:
+            self._win_ready[(len(its) - 1) % 2].synchronize()
+            dt.release(len(its) - 1)
+        if disk:
+            self.disk_stats.append(dict(dt.stats(), epoch=epoch, mode=cache_mode))
+        if window or disk:
             self.store.attach(self.ex)
         self.runner.front_events = None
         # a boundary move wrote rows into other GPUs' shards: every write is
@@ -446,12 +567,15 @@ class Trainer:
         comm, exposed = self.runner.comm_times() if plan.R > 1 else (0.0, 0.0)
         comm = self._max_over_ranks(comm) * len(its)
         exposed = self._max_over_ranks(exposed) * len(its)
-        stall = self._max_over_ranks(sum(a.elapsed_time(b) for a, b in stalls) / 1e3)
+        stall = self._max_over_ranks(sum(a.elapsed_time(b) for a, b in stalls) / 1e3 + disk_stall)
         cache_tr = 0.0
         if cache_mode == 2 and front:
             torch.cuda.synchronize()
             prefix = sum(a.elapsed_time(b) for a, b in front) / 1e3
-            steady = sum(self._time_gather(shard[o:o + n]) for o, n in its)
+            # disk tier: the whole prefix work is charged (its steady gather
+            # reads the HBM staging window, timed in the iteration itself)
+            steady = (0.0 if disk else
+                      sum(self._time_gather(shard[o:o + n]) for o, n in its))
             cache_tr = max(0.0, prefix - steady)
         cache_tr = self._max_over_ranks(cache_tr)
         return EpochResult(epoch, d.l_frozen, plan.K, plan.R, plan.M,

@@ -244,6 +244,23 @@ def test_autocache_random(prod, ref):
             ref.cache_transition(True, old, t, old, new, model, cm)
 
 
+def test_cache_tier_epoch_random(prod, ref):
+    """The modeled disk -> host window (CacheTierSim, the model the disk tier's
+    measured stalls are reported beside) equals the reference call for call."""
+    r = _rng(4)
+    for _ in range(200):
+        bb = r.choice([1, 2, 8])
+        t = CacheTierParams(disk_bandwidth=r.choice([6e9, 2e9, 5e10]),
+                            host_capacity_bytes=r.choice([64e9, 2e9, 5e8]),
+                            window_batches=bb * r.randrange(1, 9), block_batches=bb)
+        bpb = r.choice([1.2e8, 3.0e7, 1e6])
+        if t.host_capacity_bytes < bb * bpb:
+            continue
+        n = r.randrange(1, 200)
+        it = r.choice([0.0074, 0.045, 1e-4])
+        assert prod.cache_tier_epoch(t, bpb, n, it) == ref.cache_tier_epoch(t, bpb, n, it)
+
+
 def test_model_profiles(prod, ref):
     """Explicit specs built from geometry equal the reference presets."""
     vit = configs.model_spec(configs.GEOMETRIES["vit-b16"])

@@ -111,7 +111,8 @@ def _worker(rank, world, port, out, tier="hbm", peer=False, autodp=True):
 
 
 @pytest.mark.parametrize("tier,peer,autodp", [("hbm", False, True), ("host", False, True),
-                                              ("hbm", True, True), ("hbm", False, False)])
+                                              ("hbm", True, True), ("hbm", False, False),
+                                              ("disk", False, True)])
 def test_two_rank_elastic_run(cuda, tmp_path, tier, peer, autodp):
     """Two ranks run the elastic schedule: K 2 -> 1 with a replica fork (or,
     AutoDP off, with the freed GPU idle -- runner.cpp:445), cache writes into
@@ -143,7 +144,7 @@ def test_two_rank_elastic_run(cuda, tmp_path, tier, peer, autodp):
     row = g.tokens * g.hidden * 2
     if tier == "hbm":  # per-GPU store bytes ~ dataset / world
         assert ra["store_bytes"] == rb["store_bytes"] == -(-ra["dataset"] // 2) * row
-    else:  # one node-wide segment
+    else:  # one node-wide segment / file
         assert ra["store_bytes"] == ra["dataset"] * row
     lines = ra["csv"].splitlines()
     assert len(lines) == 6 and all(len(ln.split(",")) == 15 for ln in lines)
@@ -241,3 +242,43 @@ def test_host_tier_prefetch_window_matches_hbm_tier(cuda):
             # themselves are checked bitwise above)
             assert abs(a[3] - b[3]) <= 1e-3 * abs(b[3])
             assert all(abs(x - y) <= 1e-2 * max(abs(y), 1e-6) for x, y in zip(a[4], b[4]))
+
+
+def test_disk_tier_matches_hbm_tier(cuda, tmp_path):
+    """SURVEY.md 8(f) row 1, the disk level: the cached boundary activations
+    live in a file behind the DiskTier host window (CacheTierSim's disk ->
+    host prefetch, autocache.cpp:69-150, executed).  The staged rows equal the
+    file's rows bitwise, and every epoch's decisions, loss and norms equal the
+    HBM tier's (to the float-atomic rounding of the bias gradients)."""
+    scen = _tiny_scenario(epochs=5)
+    scen["training"]["alpha"] = 0.5
+    scen["cache"]["policy"] = "always_on"
+    scen["cache"]["window_batches"] = 2  # a sliding window: 3 batches per epoch
+    scen["cache"]["block_batches"] = 1
+    g = configs.GEOMETRIES["tiny-vit"]
+    tr = Trainer(scen, g, iterations_per_epoch=3, device_norms=False, cache_tier="disk",
+                 cache_dir=str(tmp_path))
+    rows = [tr.run_epoch(e) for e in range(5)]
+    last = rows[-1]
+    assert last.cache_enabled and not last.cache_moved
+    _, shards = tr.api.redistribute(tr.dataset, tr.cluster, last.k, last.epoch, tr.seed)
+    ids = torch.tensor(shards[0], dtype=torch.int64, device="cuda")
+    n_its = len(shards[0]) // tr.batch
+    ids_last = ids[(n_its - 1) * tr.batch:n_its * tr.batch]
+    torch.cuda.synchronize()
+    staged = tr._win_buf[(n_its - 1) % 2].clone()
+    assert torch.equal(staged, tr.store.rows(ids_last))
+    st = [s for s in tr.disk_stats if s["mode"] == 1]
+    assert st and st[-1]["bytes_read"] > 0 and st[-1]["evictions"] >= 3
+    assert st[-1]["max_resident_bytes"] <= 2 * tr.batch * tr.store.disk.stride
+    assert any(s["bytes_written"] > 0 for s in tr.disk_stats)
+    path = tr.store.path
+    tr.close()
+    assert not os.path.exists(path)
+    hbm = Trainer(scen, g, iterations_per_epoch=3, device_norms=False, cache_tier="hbm")
+    ref = hbm.run()
+    for a, b in zip(rows, ref):
+        assert (a.l_frozen, a.cache_enabled, a.cache_moved) == (b.l_frozen, b.cache_enabled,
+                                                                b.cache_moved)
+        assert abs(a.mean_loss - b.mean_loss) <= 1e-3 * abs(b.mean_loss)
+        assert all(abs(x - y) <= 1e-2 * max(abs(y), 1e-6) for x, y in zip(a.norms, b.norms))
