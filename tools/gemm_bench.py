@@ -53,6 +53,10 @@ LAYER18 = {
     "b18_dgrad_qkv": (R18, 768, 2304, False, True, ops.EPI_STORE_BF16, 1),
 }
 SHAPES.update(LAYER18)
+# fixed-cost probe: one b18 N = 768 tile wave at growing K (time = a + b K)
+for _k in (64, 256, 768, 1536, 3072):
+    SHAPES[f"probe18_k{_k}"] = (R18, 768, _k, False, False, ops.EPI_STORE_BF16, 1)
+    SHAPES[f"probe18r_k{_k}"] = (R18, 768, _k, False, False, ops.EPI_BIAS_RESID_BF16, 1)
 SHAPES.update({k.replace("b18", "b400"): (400 * 197 if v[0] == R18 else v[0], v[1],
                                            400 * 197 if v[2] == R18 else v[2]) + v[3:]
                for k, v in LAYER18.items()})
