@@ -230,7 +230,12 @@ __global__ void __launch_bounds__(kThreads, 2)
 }
 
 // ---------------------------------------------------------------------------
-// dQ (and D = rowsum(dO * O)): one CTA per (128-query tile, b, h).
+// dQ (and D = rowsum(dO * O)): one CTA per (128-query tile, b, h).  K and V
+// stream through a kBwdRing-deep ring of 64-key chunks (a slot is refilled
+// once the dQ MMA that last reads its K chunk completes), so a CTA holds
+// 32 KB + kBwdRing x 16 KB of smem and two CTAs share an SM: one's loads and
+// exp work overlap the other's MMAs (T = 384, BERT-base).
+constexpr int kBwdRing = 3;
 __global__ void __launch_bounds__(kThreads, 2)
     attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap map_qkv,
                           const __grid_constant__ CUtensorMap map_do, const Params p) {
@@ -238,11 +243,15 @@ __global__ void __launch_bounds__(kThreads, 2)
   uint8_t* smem = align1024(smem_raw);
   const int Tp = p.Tp;
   uint8_t* sQ = smem;
-  uint8_t* sO = sQ + kTile * kRowBytes;  // dO tile
-  uint8_t* sK = sO + kTile * kRowBytes;
-  uint8_t* sV = sK + Tp * kRowBytes;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sV + Tp * kRowBytes);  // load, s, p, acc, done
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 5);
+  uint8_t* sO = sQ + kTile * kRowBytes;      // dO tile
+  uint8_t* sR = sO + kTile * kRowBytes;      // ring: stage s = K chunk | V chunk
+  constexpr int kStage = 2 * kChunk * kRowBytes;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sR + kBwdRing * kStage);
+  // 0 tile loaded, 1 S/dP ready, 2 dS written, 3 dQ MMA done, 4 all done,
+  // 5.. full[kBwdRing], empty[kBwdRing]
+  uint64_t* full = bar + 5;
+  uint64_t* empty = full + kBwdRing;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(empty + kBwdRing);
   const int bh = blockIdx.y, b = bh / p.H, h = bh % p.H;
   const int q0 = blockIdx.x * kTile;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -257,6 +266,10 @@ __global__ void __launch_bounds__(kThreads, 2)
     mbar_init(&bar[2], 4);
     mbar_init(&bar[3], 1);
     mbar_init(&bar[4], 1);
+    for (int i = 0; i < kBwdRing; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
     mbar_fence_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, 256);
@@ -268,27 +281,35 @@ __global__ void __launch_bounds__(kThreads, 2)
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_expect_tx(&bar[0], uint32_t(2 * kTile + 2 * Tp) * kRowBytes);
+      mbar_expect_tx(&bar[0], uint32_t(2 * kTile) * kRowBytes);
       load_rows(sQ, &map_qkv, &bar[0], h * kD, q0, kTile, b);
       load_rows(sO, &map_do, &bar[0], h * kD, q0, kTile, b);
-      load_rows(sK, &map_qkv, &bar[0], HD + h * kD, 0, Tp, b);
-      load_rows(sV, &map_qkv, &bar[0], 2 * HD + h * kD, 0, Tp, b);
+      for (int c = 0; c < n_chunks; ++c) {
+        const int st = c % kBwdRing;
+        mbar_wait(&empty[st], ((c / kBwdRing) & 1) ^ 1);
+        uint8_t* slot = sR + st * kStage;
+        mbar_expect_tx(&full[st], uint32_t(kStage));
+        tma_load_3d(slot, &map_qkv, &full[st], HD + h * kD, c * kChunk, b);
+        tma_load_3d(slot + kChunk * kRowBytes, &map_qkv, &full[st], 2 * HD + h * kD, c * kChunk, b);
+      }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       mbar_wait(&bar[0], 0);
       tc_fence_after();
-      const uint32_t q_s = smem_addr(sQ), o_s = smem_addr(sO), k_s = smem_addr(sK),
-                     v_s = smem_addr(sV);
+      const uint32_t q_s = smem_addr(sQ), o_s = smem_addr(sO);
       const uint32_t idesc_kk = umma_idesc_bf16(128, kChunk, false, false);
       const uint32_t idesc_km = umma_idesc_bf16(128, kD, false, true);
       for (int c = 0; c < n_chunks; ++c) {
+        const int st = c % kBwdRing;
         if (c > 0) {
           mbar_wait(&bar[3], (c - 1) & 1);
           tc_fence_after();
         }
-        const uint32_t kc = k_s + uint32_t(c * kChunk) * kRowBytes;
-        const uint32_t vc = v_s + uint32_t(c * kChunk) * kRowBytes;
+        mbar_wait(&full[st], (c / kBwdRing) & 1);
+        tc_fence_after();
+        const uint32_t kc = smem_addr(sR + st * kStage);
+        const uint32_t vc = kc + uint32_t(kChunk * kRowBytes);
 #pragma unroll
         for (int kk = 0; kk < kD / 16; ++kk)
           tc_mma_bf16(tS, kdesc(q_s, kk), kdesc(kc, kk), idesc_kk, kk > 0 ? 1u : 0u);
@@ -303,6 +324,7 @@ __global__ void __launch_bounds__(kThreads, 2)
           tc_mma_bf16_ts(tdQ, tdP + uint32_t(kk * 8), mndesc(kc + uint32_t(kk * 16) * kRowBytes),
                          idesc_km, (c > 0 || kk > 0) ? 1u : 0u);
         tc_commit(&bar[3]);
+        tc_commit(&empty[st]);  // K_c / V_c read by every MMA of this chunk
       }
       tc_commit(&bar[4]);
     }
@@ -390,12 +412,14 @@ __global__ void __launch_bounds__(kThreads, 2)
   const int Tp = p.Tp;
   uint8_t* sK = smem;
   uint8_t* sV = sK + kTile * kRowBytes;
-  uint8_t* sQ = sV + kTile * kRowBytes;
-  uint8_t* sO = sQ + Tp * kRowBytes;  // dO, all queries
-  float* sL = reinterpret_cast<float*>(sO + Tp * kRowBytes);
+  uint8_t* sR = sV + kTile * kRowBytes;  // ring: stage s = Q chunk | dO chunk
+  constexpr int kStage = 2 * kChunk * kRowBytes;
+  float* sL = reinterpret_cast<float*>(sR + kBwdRing * kStage);
   float* sD = sL + Tp;
   uint64_t* bar = reinterpret_cast<uint64_t*>(sD + Tp);  // load, s, p, acc, done
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 5);
+  uint64_t* full = bar + 5;
+  uint64_t* empty = full + kBwdRing;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(empty + kBwdRing);
   const int bh = blockIdx.y, b = bh / p.H, h = bh % p.H;
   const int k0 = blockIdx.x * kTile;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -410,6 +434,10 @@ __global__ void __launch_bounds__(kThreads, 2)
     mbar_init(&bar[2], 4);
     mbar_init(&bar[3], 1);
     mbar_init(&bar[4], 1);
+    for (int i = 0; i < kBwdRing; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
     mbar_fence_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, 256);
@@ -421,27 +449,35 @@ __global__ void __launch_bounds__(kThreads, 2)
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_expect_tx(&bar[0], uint32_t(2 * kTile + 2 * Tp) * kRowBytes);
+      mbar_expect_tx(&bar[0], uint32_t(2 * kTile) * kRowBytes);
       load_rows(sK, &map_qkv, &bar[0], HD + h * kD, k0, kTile, b);
       load_rows(sV, &map_qkv, &bar[0], 2 * HD + h * kD, k0, kTile, b);
-      load_rows(sQ, &map_qkv, &bar[0], h * kD, 0, Tp, b);
-      load_rows(sO, &map_do, &bar[0], h * kD, 0, Tp, b);
+      for (int c = 0; c < n_chunks; ++c) {
+        const int st = c % kBwdRing;
+        mbar_wait(&empty[st], ((c / kBwdRing) & 1) ^ 1);
+        uint8_t* slot = sR + st * kStage;
+        mbar_expect_tx(&full[st], uint32_t(kStage));
+        tma_load_3d(slot, &map_qkv, &full[st], h * kD, c * kChunk, b);
+        tma_load_3d(slot + kChunk * kRowBytes, &map_do, &full[st], h * kD, c * kChunk, b);
+      }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       mbar_wait(&bar[0], 0);
       tc_fence_after();
-      const uint32_t k_s = smem_addr(sK), v_s = smem_addr(sV), q_s = smem_addr(sQ),
-                     o_s = smem_addr(sO);
+      const uint32_t k_s = smem_addr(sK), v_s = smem_addr(sV);
       const uint32_t idesc_kk = umma_idesc_bf16(128, kChunk, false, false);
       const uint32_t idesc_km = umma_idesc_bf16(128, kD, false, true);
       for (int c = 0; c < n_chunks; ++c) {
+        const int st = c % kBwdRing;
         if (c > 0) {
           mbar_wait(&bar[3], (c - 1) & 1);
           tc_fence_after();
         }
-        const uint32_t qc = q_s + uint32_t(c * kChunk) * kRowBytes;
-        const uint32_t oc = o_s + uint32_t(c * kChunk) * kRowBytes;
+        mbar_wait(&full[st], (c / kBwdRing) & 1);
+        tc_fence_after();
+        const uint32_t qc = smem_addr(sR + st * kStage);
+        const uint32_t oc = qc + uint32_t(kChunk * kRowBytes);
 #pragma unroll
         for (int kk = 0; kk < kD / 16; ++kk)
           tc_mma_bf16(tS, kdesc(k_s, kk), kdesc(qc, kk), idesc_kk, kk > 0 ? 1u : 0u);
@@ -460,6 +496,7 @@ __global__ void __launch_bounds__(kThreads, 2)
                          idesc_km, acc);
         }
         tc_commit(&bar[3]);
+        tc_commit(&empty[st]);  // Q_c / dO_c read by every MMA of this chunk
       }
       tc_commit(&bar[4]);
     }
@@ -1350,9 +1387,11 @@ size_t fwd_persistent_smem(int T) {
 }
 
 size_t fwd_smem(int Tp) { return size_t(kTile + 2 * Tp) * kRowBytes + 1024 + 64; }
-size_t bwd_dq_smem(int Tp) { return size_t(2 * kTile + 2 * Tp) * kRowBytes + 1024 + 64; }
+size_t bwd_dq_smem(int) {
+  return size_t(2 * kTile + 2 * kBwdRing * kChunk) * kRowBytes + 1024 + 128;
+}
 size_t bwd_dkdv_smem(int Tp) {
-  return size_t(2 * kTile + 2 * Tp) * kRowBytes + size_t(2 * Tp) * 4 + 1024 + 64;
+  return size_t(2 * kTile + 2 * kBwdRing * kChunk) * kRowBytes + size_t(2 * Tp) * 4 + 1024 + 128;
 }
 
 template <typename K>
