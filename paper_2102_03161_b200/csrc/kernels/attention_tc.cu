@@ -111,109 +111,183 @@ __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
 }
 
 // ---------------------------------------------------------------------------
+// Forward for 256 < T <= 384 (BERT-base-384): one CTA per (128-query tile,
+// b, h), keys in blocks of 192 (three 64-key chunks) so a CTA needs only 256
+// TMEM columns (S block [0, 192), O [192, 256)) and K / V stream through a
+// kFwdRing-deep ring of 64-key chunks (80 KB of smem): two CTAs share an SM
+// and overlap each other's loads, exps and MMAs.
+//   MMA warp: per block, S = Q K_c^T for its chunks (N = 64 each) -> SF;
+//             after the softmax, O += P V_c (TS form, P packed in TMEM) -> OB,
+//             and the block's ring slots are released; the next block's S
+//             waits for OB (it overwrites the P columns).
+//   softmax warps: one row per thread, one pass per 32 keys; exponent
+//             reference = max of the first 32 keys; a later 32-key group that
+//             leads it by > 2^32 rescales this block's P chunks, the row sum,
+//             and (from the second block on) O -- complete, since the block's
+//             S was issued after the previous PV finished (rare path).
+constexpr int kFwdRing = 4;
+constexpr int kFwdBlock = 3;  // 64-key chunks per key block
 __global__ void __launch_bounds__(kThreads, 2)
     attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap map_qkv, const Params p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   const int Tp = p.Tp;
+  const int n_chunks = Tp / kChunk;
+  const int n_blocks = (n_chunks + kFwdBlock - 1) / kFwdBlock;
+  constexpr int kStage = 2 * kChunk * kRowBytes;  // K chunk | V chunk
   uint8_t* sQ = smem;
-  uint8_t* sK = sQ + kTile * kRowBytes;
-  uint8_t* sV = sK + Tp * kRowBytes;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sV + Tp * kRowBytes);  // load, s, p, o
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 4);
+  uint8_t* sR = sQ + kTile * kRowBytes;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sR + kFwdRing * kStage);
+  enum { BQ = 0, SF, PF, OB, DONE, FULL0 };
+  uint64_t* full = bar + FULL0;
+  uint64_t* empty = full + kFwdRing;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(empty + kFwdRing);
   const int bh = blockIdx.y, b = bh / p.H, h = bh % p.H;
   const int q0 = blockIdx.x * kTile;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t ncols = tmem_cols_for(max(Tp, Tp / 2 + kD));
+  constexpr uint32_t kO = uint32_t(kFwdBlock * kChunk);  // 192
 
   if (threadIdx.x == 0) {
     tma_prefetch(&map_qkv);
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-    mbar_init(&bar[2], 4);
-    mbar_init(&bar[3], 1);
+    for (int i = 0; i < FULL0; ++i) mbar_init(&bar[i], i == PF ? 4 : 1);
+    for (int i = 0; i < kFwdRing; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
     mbar_fence_init();
   }
-  if (warp == 1) tmem_alloc(tmem_slot, ncols);
+  if (warp == 1) tmem_alloc(tmem_slot, 256);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tmem_o = tmem + uint32_t(Tp / 2);
 
   if (warp == 0) {
     if (lane == 0) {
       const int HD = p.H * kD;
-      mbar_expect_tx(&bar[0], uint32_t(kTile + 2 * Tp) * kRowBytes);
-      load_rows(sQ, &map_qkv, &bar[0], h * kD, q0, kTile, b);
-      load_rows(sK, &map_qkv, &bar[0], HD + h * kD, 0, Tp, b);
-      load_rows(sV, &map_qkv, &bar[0], 2 * HD + h * kD, 0, Tp, b);
+      mbar_expect_tx(&bar[BQ], uint32_t(kTile * kRowBytes));
+      load_rows(sQ, &map_qkv, &bar[BQ], h * kD, q0, kTile, b);
+      for (int c = 0; c < n_chunks; ++c) {
+        const int st = c % kFwdRing;
+        mbar_wait(&empty[st], ((c / kFwdRing) & 1) ^ 1);
+        uint8_t* slot = sR + st * kStage;
+        mbar_expect_tx(&full[st], uint32_t(kStage));
+        tma_load_3d(slot, &map_qkv, &full[st], HD + h * kD, c * kChunk, b);
+        tma_load_3d(slot + kChunk * kRowBytes, &map_qkv, &full[st], 2 * HD + h * kD, c * kChunk, b);
+      }
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      mbar_wait(&bar[0], 0);
+      mbar_wait(&bar[BQ], 0);
       tc_fence_after();
-      const uint32_t q_s = smem_addr(sQ), k_s = smem_addr(sK), v_s = smem_addr(sV);
-      const int nc = Tp / p.n_split;
-      const uint32_t idesc_s = umma_idesc_bf16(128, nc, false, false);
-      for (int c = 0; c < p.n_split; ++c)
-#pragma unroll
-        for (int kk = 0; kk < kD / 16; ++kk)
-          tc_mma_bf16(tmem + uint32_t(c * nc), kdesc(q_s, kk),
-                      kdesc(k_s + uint32_t(c * nc) * kRowBytes, kk), idesc_s, kk > 0 ? 1u : 0u);
-      tc_commit(&bar[1]);
-      mbar_wait(&bar[2], 0);
-      tc_fence_after();
+      const uint32_t q_s = smem_addr(sQ);
+      const uint32_t idesc_s = umma_idesc_bf16(128, kChunk, false, false);
       const uint32_t idesc_o = umma_idesc_bf16(128, kD, false, true);
-      for (int kk = 0; kk < Tp / 16; ++kk)
-        tc_mma_bf16_ts(tmem_o, tmem + uint32_t(kk * 8), mndesc(v_s + uint32_t(kk * 16) * kRowBytes),
-                       idesc_o, kk > 0 ? 1u : 0u);
-      tc_commit(&bar[3]);
+      for (int kb = 0; kb < n_blocks; ++kb) {
+        const int c0 = kb * kFwdBlock, c1 = min(c0 + kFwdBlock, n_chunks);
+        if (kb > 0) {  // the previous PV has read the P columns S overwrites
+          mbar_wait(&bar[OB], (kb - 1) & 1);
+          tc_fence_after();
+        }
+        for (int c = c0; c < c1; ++c) {
+          const int st = c % kFwdRing;
+          mbar_wait(&full[st], (c / kFwdRing) & 1);
+          tc_fence_after();
+          const uint32_t kc = smem_addr(sR + st * kStage);
+#pragma unroll
+          for (int kk = 0; kk < kD / 16; ++kk)
+            tc_mma_bf16(tmem + uint32_t((c - c0) * kChunk), kdesc(q_s, kk), kdesc(kc, kk), idesc_s,
+                        kk > 0 ? 1u : 0u);
+        }
+        tc_commit(&bar[SF]);
+        mbar_wait(&bar[PF], kb & 1);
+        tc_fence_after();
+        for (int c = c0; c < c1; ++c) {
+          const uint32_t vc = smem_addr(sR + (c % kFwdRing) * kStage) + uint32_t(kChunk * kRowBytes);
+#pragma unroll
+          for (int kk = 0; kk < kChunk / 16; ++kk)
+            tc_mma_bf16_ts(tmem + kO, tmem + uint32_t((c - c0) * 32 + kk * 8),
+                           mndesc(vc + uint32_t(kk * 16) * kRowBytes), idesc_o,
+                           (kb > 0 || c > c0 || kk > 0) ? 1u : 0u);
+          tc_commit(&empty[c % kFwdRing]);
+        }
+        tc_commit(&bar[OB]);
+      }
+      tc_commit(&bar[DONE]);
     }
   } else {
     const int quarter = warp & 3;
     const int row = quarter * 32 + lane;
     const int q = q0 + row;
     const uint32_t lane_off = uint32_t(quarter * 32) << 16;
-    mbar_wait(&bar[1], 0);
-    tc_fence_after();
-    float m = -FLT_MAX;
-    for (int c = 0; c < Tp / 32; ++c) {
-      uint32_t r[32];
-      tmem_ld_32x32(tmem + lane_off + uint32_t(c * 32), r);
-      tmem_ld_wait();
+    const uint32_t tS = tmem + lane_off;
+    const float sl2 = p.scale_log2;
+    float ms = 0.f, sum = 0.f;
+    for (int kb = 0; kb < n_blocks; ++kb) {
+      const int k0 = kb * kFwdBlock * kChunk;
+      const int ncol = min(kFwdBlock, n_chunks - kb * kFwdBlock) * kChunk;
+      mbar_wait(&bar[SF], kb & 1);
+      tc_fence_after();
+      for (int g = 0; g < ncol / 32; ++g) {
+        uint32_t r[32];
+        tmem_ld_32x32(tS + uint32_t(g * 32), r);
+        tmem_ld_wait();
+        const int kbase = k0 + g * 32;  // keys >= T are masked (zero-filled K rows)
+        float cm = -FLT_MAX;
 #pragma unroll
-      for (int j = 0; j < 32; ++j)
-        if (c * 32 + j < p.T) m = fmaxf(m, __uint_as_float(r[j]));
-    }
-    const float ms = m * p.scale_log2;
-    float sum = 0.f;
-    for (int c = 0; c < Tp / 32; ++c) {
-      uint32_t r[32];
-      tmem_ld_32x32(tmem + lane_off + uint32_t(c * 32), r);
-      tmem_ld_wait();
-      uint32_t pk[16];
+        for (int j = 0; j < 32; ++j)
+          if (kbase + j < p.T) cm = fmaxf(cm, __uint_as_float(r[j]));
+        cm *= sl2;
+        if (kb == 0 && g == 0) {
+          ms = cm;
+        } else if (__any_sync(0xffffffffu, cm > ms + 32.f)) {
+          const float ms_new = cm > ms + 32.f ? cm : ms;
+          const float f = fast_exp2(ms - ms_new);  // 1 on lanes without overflow
+          sum *= f;
+          tmem_st_wait();
+          for (int pc = 0; pc < g; ++pc) {  // this block's P
+            uint32_t q16[16];
+            tmem_ld_32x32_x16(tS + uint32_t(pc * 16), q16);
+            tmem_ld_wait();
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int k = c * 32 + 2 * j;
-        const float e0 = k < p.T ? fast_exp2(fmaf(__uint_as_float(r[2 * j]), p.scale_log2, -ms)) : 0.f;
-        const float e1 =
-            k + 1 < p.T ? fast_exp2(fmaf(__uint_as_float(r[2 * j + 1]), p.scale_log2, -ms)) : 0.f;
-        sum += e0 + e1;
-        pk[j] = pack_bf16(e0, e1);
+            for (int j = 0; j < 16; ++j) q16[j] = pack_bf16(bf16_lo(q16[j]) * f, bf16_hi(q16[j]) * f);
+            tmem_st_32x32_x16(tS + uint32_t(pc * 16), q16);
+          }
+          if (kb > 0) {  // O of the earlier blocks (their PV finished before this S)
+            uint32_t o32[32];
+#pragma unroll
+            for (int hlf = 0; hlf < 2; ++hlf) {
+              tmem_ld_32x32(tS + kO + uint32_t(hlf * 32), o32);
+              tmem_ld_wait();
+#pragma unroll
+              for (int j = 0; j < 32; ++j) o32[j] = __float_as_uint(__uint_as_float(o32[j]) * f);
+              tmem_st_32x32_x32(tS + kO + uint32_t(hlf * 32), o32);
+            }
+          }
+          ms = ms_new;
+        }
+        uint32_t pk[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int k = kbase + 2 * j;
+          const float e0 = k < p.T ? fast_exp2(fmaf(__uint_as_float(r[2 * j]), sl2, -ms)) : 0.f;
+          const float e1 = k + 1 < p.T ? fast_exp2(fmaf(__uint_as_float(r[2 * j + 1]), sl2, -ms)) : 0.f;
+          sum += e0 + e1;
+          pk[j] = pack_bf16(e0, e1);
+        }
+        // P overwrites S columns [16g, 16g+16) -- already consumed (16g+16 <= 32g+32)
+        tmem_st_32x32_x16(tS + uint32_t(g * 16), pk);
       }
-      // P overwrites S columns [16c, 16c+16) -- already consumed (16c+16 <= 32c+32)
-      tmem_st_32x32_x16(tmem + lane_off + uint32_t(c * 16), pk);
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bar[PF]);
     }
-    tmem_st_wait();
-    tc_fence_before();
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&bar[2]);
     if (q < p.T) p.lse[int64_t(bh) * p.T + q] = (ms + __log2f(sum)) * kLn2;
-    mbar_wait(&bar[3], 0);
+    mbar_wait(&bar[DONE], 0);
     tc_fence_after();
     float o[64];
-    load_tmem_row64(tmem_o + lane_off, o);
+    load_tmem_row64(tS + kO, o);
     if (q < p.T) {
       const float inv = 1.f / sum;
 #pragma unroll
@@ -225,7 +299,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    tmem_dealloc(tmem, ncols);
+    tmem_dealloc(tmem, 256);
   }
 }
 
@@ -1386,7 +1460,9 @@ size_t fwd_persistent_smem(int T) {
   return 2 * size_t(3 * Tr) * kRowBytes + 1024 + 256;
 }
 
-size_t fwd_smem(int Tp) { return size_t(kTile + 2 * Tp) * kRowBytes + 1024 + 64; }
+size_t fwd_smem(int) {
+  return size_t(kTile + 2 * kFwdRing * kChunk) * kRowBytes + 1024 + 128;
+}
 size_t bwd_dq_smem(int) {
   return size_t(2 * kTile + 2 * kBwdRing * kChunk) * kRowBytes + 1024 + 128;
 }

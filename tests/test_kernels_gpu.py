@@ -110,7 +110,8 @@ def test_attention_fwd_bwd(cuda, B, T, H, dh):
         assert _rel(dbias2, dbias) < 1e-2
 
 
-@pytest.mark.parametrize("T,spike", [(197, 40), (197, 196), (128, 100), (256, 255)])
+@pytest.mark.parametrize("T,spike", [(197, 40), (197, 196), (128, 100), (256, 255), (384, 100),
+                                     (384, 250), (384, 383), (300, 299)])
 def test_attention_fwd_score_spike(cuda, T, spike):
     """Keys whose score exceeds every score of the first 32 keys by far more than
     2^32 (in exp2 units): the forward's one-pass softmax must rescale the P
