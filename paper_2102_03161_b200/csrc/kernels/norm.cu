@@ -7,6 +7,8 @@
 // stream ("backward dataflow").
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "eps_capi.h"
 #include "ptx.cuh"
 #include "tma_host.cuh"
@@ -438,6 +440,18 @@ __global__ void __launch_bounds__(LnWide<D>::THREADS, 3)
   }
 }
 
+// CTAs per SM of the wide-row kernels (A/B: EPS_LN_FWD_GRID / EPS_LN_BWD_GRID)
+static int ln_grid_mult(int which, int dflt) {
+  static const int m[2] = {[] {
+    const char* e = std::getenv("EPS_LN_FWD_GRID");
+    return e ? std::atoi(e) : 0;
+  }(), [] {
+    const char* e = std::getenv("EPS_LN_BWD_GRID");
+    return e ? std::atoi(e) : 0;
+  }()};
+  return m[which] > 0 ? m[which] : dflt;
+}
+
 template <int D>
 int ln_fwd_wide_launch(const void* x, const float* gamma, const float* beta, void* y, float* mean,
                        float* rstd, int64_t rows, float eps, cudaStream_t st) {
@@ -450,9 +464,9 @@ int ln_fwd_wide_launch(const void* x, const float* gamma, const float* beta, voi
       return EPS_ECUDA;
     configured = true;
   }
-  const int sms = sm_count();
+  const int sms = sm_count() * ln_grid_mult(0, 3);
   const int64_t need = (rows + 7) / 8;
-  const int grid = int(need < 3 * sms ? need : 3 * sms);
+  const int grid = int(need < sms ? need : sms);
   count_launch();
   if (launch_k(ln_fwd_wide_kernel<D>, dim3(grid), dim3(L::THREADS), smem, st, 1,
                static_cast<const uint16_t*>(x), gamma, beta, static_cast<uint16_t*>(y), mean, rstd,
@@ -473,9 +487,9 @@ int ln_bwd_wide_launch(const void* dy, const void* x, const float* gamma, const 
       return EPS_ECUDA;
     configured = true;
   }
-  const int sms = sm_count();
+  const int sms = sm_count() * ln_grid_mult(1, 2);
   const int64_t need = (rows + 7) / 8;  // >= 8 rows per CTA
-  const int grid = int(need < 2 * sms ? need : 2 * sms);
+  const int grid = int(need < sms ? need : sms);
   count_launch();
   if (launch_k(ln_bwd_wide_kernel<D>, dim3(grid), dim3(L::THREADS), L::SMEM, st, 1,
                static_cast<const uint16_t*>(dy), static_cast<const uint16_t*>(x), gamma, mean, rstd,

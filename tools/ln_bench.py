@@ -8,7 +8,8 @@ import torch
 sys.path.insert(0, ".")
 from paper_2102_03161_b200 import ops  # noqa: E402
 
-R, d = 400 * 197, int(sys.argv[1]) if len(sys.argv) > 1 else 768
+d = int(sys.argv[1]) if len(sys.argv) > 1 else 768
+R = int(sys.argv[2]) if len(sys.argv) > 2 else 400 * 197
 dev = torch.device("cuda")
 x = torch.randn(R, d, device=dev).bfloat16()
 y = torch.empty_like(x)
@@ -24,10 +25,12 @@ s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
 def fwd():
+    s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
     ops.call("eps_layernorm_fwd", x, gam, bet, y, mean, rstd, R, d, C.c_float(1e-6), s)
 
 
 def bwd():
+    s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
     ops.call("eps_layernorm_bwd", dy, x, gam, mean, rstd, dres, dx, dg, db, cs, R, d, None, s)
 
 
@@ -36,10 +39,17 @@ for tag, fn, nbytes in (("fwd", fwd, 4 * R * d), ("bwd", bwd, 8 * R * d)):
     for _ in range(3):
         fn()
     torch.cuda.synchronize()
+    # device time of 20 launches captured in one CUDA graph (a ctypes loop is
+    # host-bound for the small row counts)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        for _ in range(20):
+            fn()
+    graph.replay()
+    torch.cuda.synchronize()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
-    for _ in range(20):
-        fn()
+    graph.replay()
     b.record()
     torch.cuda.synchronize()
     ms = a.elapsed_time(b) / 20
