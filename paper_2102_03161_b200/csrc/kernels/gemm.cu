@@ -31,12 +31,10 @@ namespace eps_k {
 
 constexpr int kBM = 128;
 constexpr int kBK = 64;  // one 128B swizzle atom of bf16 along K
-constexpr int kEpiWarps = 8;
-constexpr int kThreads = 64 + 32 * kEpiWarps;
-// Warp roles: epilogue warps 0..7, then the TMA producer and the MMA issuer on
-// the two highest warp ids -- the SMSP arbiter favours higher warp ids, so the
-// single-warp roles are not starved of issue slots by the busy epilogue warps.
-constexpr int kTmaWarp = kEpiWarps, kMmaWarp = kEpiWarps + 1;
+// Warp roles: EW epilogue warps (8 by default), then the TMA producer and the
+// MMA issuer on the two highest warp ids -- the SMSP arbiter favours higher
+// warp ids, so the single-warp roles are not starved of issue slots by the
+// busy epilogue warps.
 constexpr int kMnChunk = 64;  // MN extent of one swizzle atom (MN-major operands)
 
 struct GemmArgs {
@@ -61,7 +59,7 @@ struct GemmArgs {
 // MMAs (M = 256): each CTA stages its 128 rows of A and BN/2 rows of B, so a
 // stage is 16 KB + BN*64 B per CTA instead of 16 KB + BN*128 B, and the even
 // CTA issues the MMAs for both.
-template <int BN, int STAGES, bool A_MN, bool B_MN, int EPIB, bool PAIR = false>
+template <int BN, int STAGES, bool A_MN, bool B_MN, int EPIB, bool PAIR = false, int EW = 8>
 struct GemmCfg {
   static constexpr int kBRows = PAIR ? BN / 2 : BN;  // B rows staged by this CTA
   static constexpr int kABytes = kBM * kBK * 2;
@@ -69,7 +67,7 @@ struct GemmCfg {
   static constexpr int kStageBytes = kABytes + kBBytes;
   // double-buffered accumulator (2 x BN columns), allocation rounded to a power of two
   static constexpr int kTmemCols = 2 * BN <= 256 ? 256 : 512;
-  static constexpr size_t kSmem = size_t(STAGES) * kStageBytes + 8 * size_t(EPIB) /*epilogue*/ +
+  static constexpr size_t kSmem = size_t(STAGES) * kStageBytes + EW * size_t(EPIB) /*epilogue*/ +
                                   1024 /*align*/ + 1024 /*barriers*/;
   static constexpr uint32_t kIdesc = umma_idesc_bf16(PAIR ? 2 * kBM : kBM, BN, A_MN, B_MN);
 };
@@ -231,13 +229,18 @@ constexpr int kAuxDepthMax = 7;  // barrier slots per epilogue warp
 
 std::atomic<int>& gemm_pair_mode();
 
-template <int BN, int STAGES, bool A_MN, bool B_MN, int EPIB, bool PAIR>
-__global__ void __launch_bounds__(kThreads, 1)
+// EW: epilogue warps (a multiple of 4: EW / 4 warps per TMEM lane quarter,
+// taking every (EW / 4)-th 32-column chunk of a tile).
+template <int BN, int STAGES, bool A_MN, bool B_MN, int EPIB, bool PAIR, int EW>
+__global__ void __launch_bounds__(64 + 32 * EW, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap map_a,
                    const __grid_constant__ CUtensorMap map_b,
                    const __grid_constant__ CUtensorMap map_c,
                    const __grid_constant__ CUtensorMap map_x, const GemmArgs args) {
-  using Cfg = GemmCfg<BN, STAGES, A_MN, B_MN, EPIB, PAIR>;
+  using Cfg = GemmCfg<BN, STAGES, A_MN, B_MN, EPIB, PAIR, EW>;
+  constexpr int kEpiWarps = EW, kTmaWarp = EW, kMmaWarp = EW + 1;
+  constexpr int kParts = EW / 4;  // epilogue warps per TMEM lane quarter
+  static_assert(EW % 4 == 0 && kAuxDepthMax * EW * 8 + 256 <= 1024, "epilogue warps");
   // aux TMA ring depth: the per-warp epilogue area minus one 2 KB out slot
   constexpr int kAuxDepth = EPIB >= 8192 ? (EPIB - 2048) / 2048 : 1;
   static_assert(kAuxDepth <= kAuxDepthMax, "aux ring");
@@ -379,7 +382,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else {
     const int ew = warp;             // 0..7
     const int quarter = warp & 3;    // TMEM lane quarter this warp may access
-    const int part = ew >> 2;        // this warp takes chunks part, part+2, ...
+    const int part = ew >> 2;        // this warp takes chunks part, part+kParts, ...
     uint8_t* my_area = epi_area + ew * EPIB;
     const uint32_t area_s = smem_addr(my_area);
     const int epi = args.epi;
@@ -394,7 +397,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint16_t* auxp = static_cast<const uint16_t*>(args.aux);
     uint64_t* my_aux_bar = aux_full + kAuxDepthMax * ew;
     const uint32_t aux_s = area_s + kChunkBf16;
-    // TMA prefetch cursor over this warp's (tile, chunk) stream: c = part, part+2, ...
+    // TMA prefetch cursor over this warp's (tile, chunk) stream: c = part, part+kParts, ...
     // Tile coordinates are decoded once per tile (integer division is a
     // ~20-instruction sequence and lane 0 runs this once per chunk).
     int pf_u = cta0, pf_c = part, pf_row = 0, pf_col = 0, pf_chunks = -1;
@@ -421,7 +424,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_load_2d(my_area + kChunkBf16 * (1 + slot), &map_x, &my_aux_bar[slot],
                     pf_col + pf_c * 32, pf_row);
         ++pf_n;
-        pf_c += 2;
+        pf_c += kParts;
       }
     };
     if (aux_tma && lane == 0) tma_prefetch_until(kAuxDepth);
@@ -435,7 +438,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int prow = (tt / args.tiles_n) * kTileM + rank * kBM + quarter * 32 + lane;
       if (prow >= args.M) return;
       const int pch = min(BN / 32, (args.N - pn0 + 31) / 32);
-      for (int c = part; c < pch; c += 2) prefetch_l2(auxp + int64_t(prow) * args.ldc + pn0 + c * 32);
+      for (int c = part; c < pch; c += kParts) prefetch_l2(auxp + int64_t(prow) * args.ldc + pn0 + c * 32);
     };
     prefetch_aux(cta0);
 
@@ -460,14 +463,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_after();
       const uint32_t taddr = tmem_base + (uint32_t(quarter * 32) << 16) + uint32_t(acc * BN);
 #pragma unroll 1
-      for (int c = part; c < chunks; c += 2) {
+      for (int c = part; c < chunks; c += kParts) {
         const int col0 = n0 + c * 32;
         const int valid = min(32, args.N - col0);
         uint32_t raw[32];
         tmem_ld_32x32(taddr + uint32_t(c * 32), raw);
         uint4 xn[4];
-        if (aux_in && !aux_tma && c + 2 < chunks)
-          load_aux_row(auxp, args.ldc, my_row, args.M, col0 + 64, args.N, xn);
+        if (aux_in && !aux_tma && c + kParts < chunks)
+          load_aux_row(auxp, args.ldc, my_row, args.M, col0 + 32 * kParts, args.N, xn);
         tmem_ld_wait();
         float v[32];
 #pragma unroll
@@ -631,11 +634,12 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 // ---- host side -------------------------------------------------------------
 
-template <int BN, int STAGES, bool A_MN, bool B_MN, int EPIB = 4096, bool PAIR = false>
+template <int BN, int STAGES, bool A_MN, bool B_MN, int EPIB = 4096, bool PAIR = false,
+          int EW = 8>
 int launch(const void* A, const void* B, int64_t lda, int64_t ldb, GemmArgs args,
            cudaStream_t stream) {
-  using Cfg = GemmCfg<BN, STAGES, A_MN, B_MN, EPIB, PAIR>;
-  auto kern = gemm_tc_kernel<BN, STAGES, A_MN, B_MN, EPIB, PAIR>;
+  using Cfg = GemmCfg<BN, STAGES, A_MN, B_MN, EPIB, PAIR, EW>;
+  auto kern = gemm_tc_kernel<BN, STAGES, A_MN, B_MN, EPIB, PAIR, EW>;
   static bool configured = false;
   if (!configured) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -662,7 +666,7 @@ int launch(const void* A, const void* B, int64_t lda, int64_t ldb, GemmArgs args
   const int workers = PAIR ? sm_count() / 2 : sm_count();
   const int grid = (units < workers ? units : workers) * (PAIR ? 2 : 1);
   count_launch();
-  if (launch_k(kern, dim3(grid), dim3(kThreads), Cfg::kSmem, stream, PAIR ? 2 : 1, ma, mb, mc, mx,
+  if (launch_k(kern, dim3(grid), dim3(64 + 32 * EW), Cfg::kSmem, stream, PAIR ? 2 : 1, ma, mb, mc, mx,
                args) != cudaSuccess)
     return EPS_ECUDA;
   return cudaGetLastError() == cudaSuccess ? EPS_OK : EPS_ECUDA;
@@ -675,6 +679,16 @@ int launch(const void* A, const void* B, int64_t lda, int64_t ldb, GemmArgs args
 std::atomic<unsigned long long*>& gemm_prof_buf() {
   static std::atomic<unsigned long long*> buf{nullptr};
   return buf;
+}
+
+// Epilogue warps of the pair-tile aux / two-output GEMMs forced by
+// EPS_GEMM_EW (8 or 12; 0 = per-epilogue default).
+int gemm_epi_warps() {
+  static const int ew = [] {
+    const char* e = std::getenv("EPS_GEMM_EW");
+    return e == nullptr ? 0 : std::atoi(e);
+  }();
+  return ew;
 }
 
 std::atomic<int>& gemm_pair_mode() {
@@ -779,6 +793,23 @@ extern "C" int eps_gemm_bf16(int a_mn_major, int b_mn_major, int epilogue, const
     // beside the 4 KB-per-warp epilogue staging, or 5 beside the 8 KB aux ring.
     args.tiles_n = int(N / 256);
     if (aux_or_two) {
+      // The GELU + GELU' (FC1 forward) and gelu'-product + column-sum (FC2
+      // dgrad) epilogues are issue-latency bound: 12 epilogue warps (3 per
+      // TMEM lane quarter) with 4 operand stages beat 8 warps with 5 stages
+      // (ViT-B b400: 0.381 -> 0.363 ms, 0.352 -> 0.340 ms); the residual /
+      // row-dot epilogues and K = 3072 mainloops prefer the fifth stage
+      // (+2..7 % with 12 warps).  EPS_GEMM_EW = 8 / 12 forces either.
+      const int ew = gemm_epi_warps() != 0 ? gemm_epi_warps()
+                     : (epilogue == EPS_EPI_BIAS_GELU2_BF16 || epilogue == EPS_EPI_MUL_BF16) ? 12
+                                                                                             : 8;
+      if (ew == 12) {
+        switch (key) {
+          case 0: return launch<256, 4, false, false, 8192, true, 12>(A, B, lda, ldb, args, st);
+          case 1: return launch<256, 4, false, true, 8192, true, 12>(A, B, lda, ldb, args, st);
+          case 2: return launch<256, 4, true, false, 8192, true, 12>(A, B, lda, ldb, args, st);
+          default: return launch<256, 4, true, true, 8192, true, 12>(A, B, lda, ldb, args, st);
+        }
+      }
       switch (key) {
         case 0: return launch<256, 5, false, false, 8192, true>(A, B, lda, ldb, args, st);
         case 1: return launch<256, 5, false, true, 8192, true>(A, B, lda, ldb, args, st);
