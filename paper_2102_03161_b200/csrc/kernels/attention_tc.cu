@@ -95,6 +95,7 @@ __device__ __forceinline__ void load_tmem_row64(uint32_t taddr, float (&v)[64]) 
 
 struct Params {
   int trace;  // record phase stamps of CTA 0 (eps_attn_trace_*)
+  int dbg;    // EPS_ATTN_DBG bit 0: every head loads head (0, 0) (L2-resident; experiments)
   int T, H, Tp, n_split;
   float scale, scale_log2;
   const uint16_t* out;  // forward output (bwd: for D = rowsum(dO * O))
@@ -1192,7 +1193,11 @@ __device__ __forceinline__ constexpr bool fwd_poly_pair(int j) {
   return (j * POLY) / 16 != ((j + 1) * POLY) / 16;
 }
 
-template <int POLY>
+// V2 (round 2): the overflow test of chunks after the first reads their exp
+// sum instead of a 32-key max (as in attn_fwd_ring_tc_kernel), the first
+// chunk's max is an FMNMX3 tree, and warps whose rows are all >= T skip the
+// softmax and the O read-out.
+template <int POLY, bool V2>
 __global__ void __launch_bounds__(kFwdThreads, 1)
     attn_fwd_persistent_tc_kernel(const __grid_constant__ CUtensorMap map_qkv, const Params p,
                                   int n_heads) {
@@ -1238,7 +1243,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
       int i = 0;
       for (int bh = blockIdx.x; bh < n_heads; bh += gridDim.x, ++i) {
         if ((i & 1) != c) continue;
-        const int b = bh / p.H, h = bh % p.H;
+        const int b = (p.dbg & 1) ? 0 : bh / p.H, h = (p.dbg & 1) ? 0 : bh % p.H;
         const uint32_t par = ((i >> 1) & 1) ^ 1;
         for (int t = 0; t < nt; ++t) {
           mbar_wait(&pb[EQ0 + t], par);
@@ -1337,7 +1342,17 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           // compute exps and max side by side and redo the exps on a rescale
           auto chunk_max = [&]() {
             float cm = -FLT_MAX;
-            if (rem >= 32) {
+            if (V2 && rem >= 32) {
+              float m1 = -FLT_MAX, m2 = -FLT_MAX, m3 = -FLT_MAX;
+#pragma unroll
+              for (int j = 0; j < 32; j += 8) {
+                cm = fmax3f(cm, __uint_as_float(r[j]), __uint_as_float(r[j + 1]));
+                m1 = fmax3f(m1, __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+                m2 = fmax3f(m2, __uint_as_float(r[j + 4]), __uint_as_float(r[j + 5]));
+                m3 = fmax3f(m3, __uint_as_float(r[j + 6]), __uint_as_float(r[j + 7]));
+              }
+              cm = fmaxf(fmaxf(cm, m1), fmaxf(m2, m3));
+            } else if (rem >= 32) {
 #pragma unroll
               for (int j = 0; j < 32; ++j) cm = fmaxf(cm, __uint_as_float(r[j]));
             } else if (rem <= 16) {
@@ -1359,7 +1374,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
               for (int j = 0; j < 16; ++j) {
                 const float2 a = __ffma2_rn(
                     make_float2(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1])), sl2x2, nms2);
-                const float2 e = fwd_poly_pair<POLY>(j) ? poly_exp2_x2(a)
+                const float2 e = fwd_poly_pair<POLY>(j) ? poly_exp2_x2<V2>(a)
                                                         : make_float2(fast_exp2(a.x), fast_exp2(a.y));
                 cs = __fadd2_rn(cs, e);
                 pk[j] = pack_bf16(e.x, e.y);
@@ -1392,10 +1407,11 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
           if (ch == 0) ms = chunk_max();
           float2 cs = chunk_exp(ms);
           if (ch > 0) {
-            const float cms = chunk_max();
-            const bool up = cms > ms + 32.f;
+            // V2: an exp sum above 2^32 (or inf) means a key leads ms by > 2^27
+            const float cms = V2 ? 0.f : chunk_max();
+            const bool up = V2 ? cs.x + cs.y > 4294967296.0f : cms > ms + 32.f;
             if (__any_sync(0xffffffffu, up)) {
-              const float ms_new = up ? cms : ms;
+              const float ms_new = up ? (V2 ? fmaxf(ms, chunk_max()) : cms) : ms;
               const float f = fast_exp2(ms - ms_new);  // 1 on lanes without overflow
               sum2 = __fmul2_rn(sum2, make_float2(f, f));
               tmem_st_wait();
@@ -1417,10 +1433,13 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         };
         // (a register double-buffered variant -- the load of chunk ch + 1 in
         // flight while chunk ch is exponentiated -- measured 10 % slower)
-        for (int ch = 0; ch < nch; ++ch) {
-          issue(ch, ra);
-          tmem_ld_wait_regs(ra);
-          process(ch, ra);
+        const bool live = !V2 || t * kTile + quarter * 32 < p.T;  // warp-uniform
+        if (live) {
+          for (int ch = 0; ch < nch; ++ch) {
+            issue(ch, ra);
+            tmem_ld_wait_regs(ra);
+            process(ch, ra);
+          }
         }
         const float sum = sum2.x + sum2.y;
         tmem_st_wait();
@@ -1433,7 +1452,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         tc_fence_after();
         EPS_TRACE(c == 0 && k < 32 && warp == 4 && lane == 0, 832 + k * 5 + 3);
         float o[64];
-        load_tmem_row64(tS + 128, o);
+        if (live) load_tmem_row64(tS + 128, o);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&pb[TF]);
@@ -1458,6 +1477,358 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 size_t fwd_persistent_smem(int T) {
   const int Tr = (T + kTile - 1) / kTile * kTile;
   return 2 * size_t(3 * Tr) * kRowBytes + 1024 + 256;
+}
+
+// ---------------------------------------------------------------------------
+// Ring forward for T <= 256 (the default since round 2).  Same roles and
+// Q / K / V smem buffers as attn_fwd_persistent_tc_kernel (one TMA warp, one
+// MMA warp and one softmax warpgroup per pipeline c, heads alternating
+// between the two pipelines), but the softmax warpgroups never wait for a
+// tile's O: the persistent kernel's per-tile chain
+//   S (all keys) -> softmax -> PV -> O read-out -> next S
+// kept a warpgroup busy ~5.0 k of ~7.9 k cycles per tile (CTA-0 clock trace,
+// ViT-B/16).  Here keys go in blocks of 64 through a ring of three 64-column
+// S slots per pipeline; O owns the pipeline's first 64 TMEM columns:
+//   pipeline c: O [256c, 256c + 64), slot s [256c + 64 + 64s, +64)
+//   MMA warp:  S(g) = Q_t K_j^T into slot g % 3 up to two blocks ahead of
+//              the block it feeds to PV (in-order tensor pipe: S(g + 3) is
+//              issued after PV(g), which read slot g % 3 as P);
+//              PV(g): O (+)= P_g V_j (TS form, P packed bf16 in the slot)
+//   softmax:   block by block, one row per thread; P written back packed
+//              into the slot's first 32 columns; after block 0 of tile k it
+//              reads O(k-1) (complete: OF) and only then releases P(k, 0),
+//              so PV(k, 0) (accumulate = 0) cannot overwrite an unread O.
+//              O(k-1) / rowsum goes out through a per-warp 32-row smem stage
+//              and a TMA store (rows >= T clipped by the tensor map).
+// Softmax per row: the exponent reference is the max of the first 32 keys
+// (FMNMX3 tree); later chunks test their exp sum instead of a max: a sum
+// above 2^32 (or inf) means some key leads the reference by > 2^27, and the
+// chunk is redone after rescaling the row sum, the block's earlier P chunk
+// and -- when earlier blocks already went to PV -- O (rare, warp-collective).
+// Warps whose 32 rows are all >= T (the last query tile's padding) skip the
+// softmax and only arrive.
+constexpr int kRingSlots = 3;
+constexpr int kStageBytes = 32 * kRowBytes;  // one warp's 32 O rows
+template <int POLY, bool PIPE>
+__global__ void __launch_bounds__(kFwdThreads, 1)
+    attn_fwd_ring_tc_kernel(const __grid_constant__ CUtensorMap map_qkv,
+                            const __grid_constant__ CUtensorMap map_out, const Params p,
+                            int n_heads) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  const int nt = (p.T + kTile - 1) / kTile;
+  const int Tr = nt * kTile;
+  const int Tn = (p.T + 15) / 16 * 16;
+  const int nb = (Tn + 63) / 64;  // 64-key blocks per query tile
+  const size_t buf_bytes = size_t(3 * Tr) * kRowBytes;
+  uint8_t* stage_base = smem + 2 * buf_bytes;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(stage_base + 8 * kStageBytes);
+  // per pipeline: operand regions full / empty; per slot SF (S ready), PF (P
+  // written), PD (PV done); OF (a tile's O complete)
+  // Q tiles, K / V 64-row blocks: full / empty each, so the next head's
+  // block j loads as soon as this head's last S / PV of block j is done
+  enum { FQ = 0, EQ = 2, FK = 4, EK = 8, FV = 12, EV = 16, SF = 20, PF = SF + kRingSlots,
+         PD = PF + kRingSlots, OF = PD + kRingSlots, NB };
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 2 * NB);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int HD = p.H * kD;
+
+  if (threadIdx.x == 0) {
+    tma_prefetch(&map_qkv);
+    tma_prefetch(&map_out);
+    for (int c = 0; c < 2; ++c)
+      for (int i = 0; i < NB; ++i) mbar_init(&bar[c * NB + i], (i >= PF && i < PD) ? 4 : 1);
+    mbar_fence_init();
+  }
+  if (warp == 3) tmem_alloc(tmem_slot, 512);
+  pdl_launch_dependents();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_wait();
+
+  if (warp == 0 || warp == 3) {
+    const int c = warp == 0 ? 0 : 1;
+    uint64_t* pb = bar + c * NB;
+    uint8_t* base = smem + c * buf_bytes;
+    if (lane == 0) {
+      int i = 0;
+      for (int bh = blockIdx.x; bh < n_heads; bh += gridDim.x, ++i) {
+        if ((i & 1) != c) continue;
+        const int b = (p.dbg & 1) ? 0 : bh / p.H, h = (p.dbg & 1) ? 0 : bh % p.H;
+        const uint32_t par = ((i >> 1) & 1) ^ 1;
+        // in release order: Q_0, K blocks, Q_1, V blocks
+        for (int t = 0; t < nt; ++t) {
+          mbar_wait(&pb[EQ + t], par);
+          mbar_expect_tx(&pb[FQ + t], uint32_t(kTile * kRowBytes));
+          load_rows(base + t * kTile * kRowBytes, &map_qkv, &pb[FQ + t], h * kD, t * kTile,
+                    kTile, b);
+          if (t == 0) {
+            for (int j = 0; j < nb; ++j) {
+              mbar_wait(&pb[EK + j], par);
+              mbar_expect_tx(&pb[FK + j], uint32_t(kChunk * kRowBytes));
+              tma_load_3d(base + (Tr + j * kChunk) * kRowBytes, &map_qkv, &pb[FK + j],
+                          HD + h * kD, j * kChunk, b);
+            }
+          }
+        }
+        for (int j = 0; j < nb; ++j) {
+          mbar_wait(&pb[EV + j], par);
+          mbar_expect_tx(&pb[FV + j], uint32_t(kChunk * kRowBytes));
+          tma_load_3d(base + (2 * Tr + j * kChunk) * kRowBytes, &map_qkv, &pb[FV + j],
+                      2 * HD + h * kD, j * kChunk, b);
+        }
+      }
+    }
+  } else if (warp == 1 || warp == 2) {
+    const int c = warp - 1;
+    uint64_t* pb = bar + c * NB;
+    const uint32_t tO = tmem + uint32_t(256 * c);
+    const uint32_t idesc_o = umma_idesc_bf16(128, kD, false, true);
+    // this pipeline's heads: bh = blockIdx.x + (2m + c) gridDim.x
+    const int first = int(blockIdx.x) + c * int(gridDim.x);
+    const int n_my = first < n_heads ? (n_heads - first + 2 * int(gridDim.x) - 1) /
+                                           (2 * int(gridDim.x))
+                                     : 0;
+    const int per_head = nt * nb;
+    const int G = n_my * per_head;
+    const uint64_t q0 = umma_sdesc(smem_addr(smem + c * buf_bytes), 16, 1024);
+    const uint64_t k0 = q0 + uint64_t((Tr * kRowBytes) >> 4);
+    const uint64_t v0 = umma_sdesc(smem_addr(smem + c * buf_bytes + 2 * Tr * kRowBytes),
+                                   64 * 128, 1024);
+    int gs = 0;  // next block whose S is issued
+    for (int g = 0; g < G; ++g) {
+      const int m = g / per_head;
+      // S ahead: at most two blocks past g, and not into head m + 2 (its Q /
+      // K load waits for V(m + 1), i.e. for PV(m))
+      while (gs < G && gs <= g + kRingSlots - 1 && gs / per_head <= m + 1) {
+        const int ms_ = gs / per_head, ts = (gs / nb) % nt, js = gs % nb;
+        const int w = min(64, Tn - 64 * js);
+        if (js == 0) mbar_wait(&pb[FQ + ts], ms_ & 1);
+        if (ts == 0) mbar_wait(&pb[FK + js], ms_ & 1);
+        if (!PIPE && gs >= kRingSlots)
+          mbar_wait(&pb[PD + gs % kRingSlots], ((gs - kRingSlots) / kRingSlots) & 1);
+        tc_fence_after();
+        const uint64_t qt = q0 + uint64_t((ts * kTile * kRowBytes) >> 4);
+        const uint64_t kj = k0 + uint64_t((js * 64 * kRowBytes) >> 4);
+        const uint32_t idesc_s = umma_idesc_bf16(128, w, false, false);
+        const uint32_t tS = tO + 64u + uint32_t(64 * (gs % kRingSlots));
+#pragma unroll
+        for (int kk = 0; kk < kD / 16; ++kk)
+          tc_mma_ss_ws(tS, qt + uint64_t(2 * kk), kj + uint64_t(2 * kk), idesc_s, kk > 0 ? 1u : 0u);
+        tc_commit_ws(&pb[SF + gs % kRingSlots]);
+        EPS_TRACE(c == 0 && gs < 60 && lane == 0, 832 + gs * 3 + 2);
+        if (js == nb - 1) tc_commit_ws(&pb[EQ + ts]);   // Q_t read
+        if (ts == nt - 1) tc_commit_ws(&pb[EK + js]);  // K block js read
+        ++gs;
+      }
+      const int t = (g / nb) % nt, j = g % nb;
+      const int w = min(64, Tn - 64 * j);
+      mbar_wait(&pb[PF + g % kRingSlots], (g / kRingSlots) & 1);
+      if (t == 0) mbar_wait(&pb[FV + j], m & 1);
+      tc_fence_after();
+      const uint32_t tP = tO + 64u + uint32_t(64 * (g % kRingSlots));
+      for (int kk = 0; kk < w / 16; ++kk)
+        tc_mma_ts_ws(tO, tP + uint32_t(kk * 8), v0 + uint64_t((4 * j + kk) * 128), idesc_o,
+                     (j > 0 || kk > 0) ? 1u : 0u);
+      tc_commit_ws(&pb[PD + g % kRingSlots]);
+      if (t == nt - 1) tc_commit_ws(&pb[EV + j]);  // V block j read by the head's last PV
+      if (j == nb - 1) tc_commit_ws(&pb[OF]);
+    }
+  } else if (warp >= 4) {
+    const int c = (warp - 4) >> 2;
+    uint64_t* pb = bar + c * NB;
+    const int quarter = warp & 3;
+    const uint32_t tO = tmem + uint32_t(256 * c) + (uint32_t(quarter * 32) << 16);
+    uint8_t* stage = stage_base + (c * 4 + quarter) * kStageBytes;
+    const uint32_t stage_s = smem_addr(stage);
+    const float sl2 = p.scale_log2;
+    const float2 sl2x2 = make_float2(sl2, sl2);
+    // previous tile of this pipeline: live warp, 1 / rowsum, TMA coordinates
+    bool prev_live = false;
+    float prev_inv = 0.f;
+    int prev_row = 0, prev_b = 0, prev_col = 0;
+    auto emit_o = [&]() {  // O(prev) from TMEM -> smem stage -> TMA store
+      uint32_t oa[32], ob[32];
+      tmem_ld_32x32(tO, oa);
+      tmem_ld_32x32(tO + 32, ob);
+      tmem_ld_wait_regs(oa);
+      tmem_ld_wait_regs(ob);
+      if (lane == 0) bulk_wait_read<0>();  // the stage's previous store has read it
+      __syncwarp();
+#pragma unroll
+      for (int v = 0; v < 8; ++v) {
+        const uint32_t* s = v < 4 ? &oa[8 * v] : &ob[8 * (v - 4)];
+        float f[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(s[e]) * prev_inv;
+        st_shared_v4(stage_s + uint32_t(lane * kRowBytes + ((v ^ (lane & 7)) << 4)),
+                     pack_bf16(f[0], f[1]), pack_bf16(f[2], f[3]), pack_bf16(f[4], f[5]),
+                     pack_bf16(f[6], f[7]));
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        tma_store_3d(&map_out, stage, prev_col, prev_row, prev_b);
+        bulk_commit();
+      }
+    };
+    int g = 0, k = 0;
+    for (int bh = blockIdx.x, i = 0; bh < n_heads; bh += gridDim.x, ++i) {
+      if ((i & 1) != c) continue;
+      const int b = bh / p.H, h = bh % p.H;
+      for (int t = 0; t < nt; ++t, ++k) {
+        const int row0 = t * kTile + quarter * 32;
+        const int q = row0 + lane;
+        const bool live = row0 < p.T;  // warp-uniform
+        float ms = 0.f;
+        float2 sum2 = make_float2(0.f, 0.f);
+        for (int j = 0; j < nb; ++j, ++g) {
+          const int w = min(64, Tn - 64 * j);
+          const uint32_t tS = tO + 64u + uint32_t(64 * (g % kRingSlots));
+          mbar_wait(&pb[SF + g % kRingSlots], (g / kRingSlots) & 1);
+          tc_fence_after();
+          EPS_TRACE(c == 0 && g < 60 && warp == 4 && lane == 0, 832 + g * 3);
+          if (live) {
+            for (int ch = 0; ch < (w + 31) / 32; ++ch) {
+              const int rem = p.T - 64 * j - 32 * ch;  // valid keys in the chunk (>= 1)
+              uint32_t ra[32];
+              if (rem <= 16)
+                tmem_ld_32x32_x16(tS + uint32_t(32 * ch), reinterpret_cast<uint32_t(&)[16]>(ra));
+              else
+                tmem_ld_32x32(tS + uint32_t(32 * ch), ra);
+              tmem_ld_wait_regs(ra);
+              uint32_t pk[16];
+              auto chunk_exp = [&](float msr) {
+                const float2 nms2 = make_float2(-msr, -msr);
+                float2 cs = make_float2(0.f, 0.f);
+                if (rem >= 32) {
+#pragma unroll
+                  for (int e = 0; e < 16; ++e) {
+                    const float2 a = __ffma2_rn(make_float2(__uint_as_float(ra[2 * e]),
+                                                            __uint_as_float(ra[2 * e + 1])),
+                                                sl2x2, nms2);
+                    const float2 x = fwd_poly_pair<POLY>(e)
+                                         ? poly_exp2_x2<true>(a)
+                                         : make_float2(fast_exp2(a.x), fast_exp2(a.y));
+                    cs = __fadd2_rn(cs, x);
+                    pk[e] = pack_bf16(x.x, x.y);
+                  }
+                } else {
+#pragma unroll
+                  for (int e = 0; e < 16; ++e) {
+                    if (2 * e >= rem) {  // (also the unloaded half of an x16 chunk)
+                      pk[e] = 0u;
+                      continue;
+                    }
+                    const float2 a = __ffma2_rn(make_float2(__uint_as_float(ra[2 * e]),
+                                                            __uint_as_float(ra[2 * e + 1])),
+                                                sl2x2, nms2);
+                    const float2 x = make_float2(2 * e < rem ? fast_exp2(a.x) : 0.f,
+                                                 2 * e + 1 < rem ? fast_exp2(a.y) : 0.f);
+                    cs = __fadd2_rn(cs, x);
+                    pk[e] = pack_bf16(x.x, x.y);
+                  }
+                }
+                return cs;
+              };
+              auto chunk_max = [&]() {
+                float m0 = -FLT_MAX, m1 = -FLT_MAX, m2 = -FLT_MAX, m3 = -FLT_MAX;
+                if (rem >= 32) {
+#pragma unroll
+                  for (int e = 0; e < 32; e += 8) {
+                    m0 = fmax3f(m0, __uint_as_float(ra[e]), __uint_as_float(ra[e + 1]));
+                    m1 = fmax3f(m1, __uint_as_float(ra[e + 2]), __uint_as_float(ra[e + 3]));
+                    m2 = fmax3f(m2, __uint_as_float(ra[e + 4]), __uint_as_float(ra[e + 5]));
+                    m3 = fmax3f(m3, __uint_as_float(ra[e + 6]), __uint_as_float(ra[e + 7]));
+                  }
+                } else {
+#pragma unroll
+                  for (int e = 0; e < 32; ++e)
+                    if (e < rem) m0 = fmaxf(m0, __uint_as_float(ra[e]));
+                }
+                return fmaxf(fmaxf(m0, m1), fmaxf(m2, m3)) * sl2;
+              };
+              const bool first_chunk = j == 0 && ch == 0;
+              if (first_chunk) ms = chunk_max();
+              float2 cs = chunk_exp(ms);
+              if (!first_chunk) {
+                const bool up = cs.x + cs.y > 4294967296.0f;
+                if (__any_sync(0xffffffffu, up)) {  // rare: rescale, redo the chunk
+                  const float ms_new = up ? fmaxf(ms, chunk_max()) : ms;
+                  const float f = fast_exp2(ms - ms_new);  // 1 on lanes without overflow
+                  sum2 = __fmul2_rn(sum2, make_float2(f, f));
+                  tmem_st_wait();
+                  if (ch == 1) {  // this block's first P chunk
+                    uint32_t q16[16];
+                    tmem_ld_32x32_x16(tS, q16);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int e = 0; e < 16; ++e)
+                      q16[e] = pack_bf16(bf16_lo(q16[e]) * f, bf16_hi(q16[e]) * f);
+                    tmem_st_32x32_x16(tS, q16);
+                  }
+                  if (j > 0) {  // O = P V of this tile's earlier blocks, once complete
+                    const int gp = g - 1;
+                    mbar_wait(&pb[PD + gp % kRingSlots], (gp / kRingSlots) & 1);
+                    tc_fence_after();
+                    for (int hf = 0; hf < 2; ++hf) {
+                      uint32_t o32[32];
+                      tmem_ld_32x32(tO + uint32_t(hf * 32), o32);
+                      tmem_ld_wait_regs(o32);
+#pragma unroll
+                      for (int e = 0; e < 32; ++e)
+                        o32[e] = __float_as_uint(__uint_as_float(o32[e]) * f);
+                      tmem_st_32x32_x32(tO + uint32_t(hf * 32), o32);
+                    }
+                  }
+                  ms = ms_new;
+                  cs = chunk_exp(ms);
+                }
+              }
+              sum2 = __fadd2_rn(sum2, cs);
+              tmem_st_32x32_x16(tS + uint32_t(16 * ch), pk);
+            }
+          }
+          if (j == 0 && k > 0) {  // O(k-1): read out before PV(k, 0) may overwrite it
+            mbar_wait(&pb[OF], (k - 1) & 1);
+            tc_fence_after();
+            if (prev_live) emit_o();
+          }
+          if (live) tmem_st_wait();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&pb[PF + g % kRingSlots]);
+          EPS_TRACE(c == 0 && g < 60 && warp == 4 && lane == 0, 832 + g * 3 + 1);
+        }
+        const float sum = sum2.x + sum2.y;
+        if (live && q < p.T) p.lse[int64_t(bh) * p.T + q] = (ms + __log2f(sum)) * kLn2;
+        prev_live = live;
+        prev_inv = 1.f / sum;
+        prev_row = row0;
+        prev_b = b;
+        prev_col = h * kD;
+      }
+    }
+    if (k > 0) {  // the last tile's O
+      mbar_wait(&pb[OF], (k - 1) & 1);
+      tc_fence_after();
+      if (prev_live) emit_o();
+    }
+    if (lane == 0) bulk_wait<0>();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 3) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+size_t fwd_ring_smem(int T) {
+  const int Tr = (T + kTile - 1) / kTile * kTile;
+  return 2 * size_t(3 * Tr) * kRowBytes + 8 * size_t(kStageBytes) + 1024 + 1024;
 }
 
 size_t fwd_smem(int) {
@@ -1503,6 +1874,18 @@ static int fwd_poly_mode() {
   return mode;
 }
 
+// Forward kernel for T <= 256 (EPS_ATTN_FWD, for A/B runs; unset = by T):
+// 0 = the round-1 attn_fwd_persistent_tc_kernel, 1 = attn_fwd_ring_tc_kernel,
+// 2 = the ring kernel without the in-order tensor-pipe assumption, 3 = the
+// persistent kernel's V2 softmax.
+static int fwd_kernel_mode() {
+  static const int mode = [] {
+    const char* e = std::getenv("EPS_ATTN_FWD");
+    return e == nullptr ? -1 : std::atoi(e);
+  }();
+  return mode;
+}
+
 int attn_fwd_tc(const void* qkv, void* out, float* lse, int B, int T, int H, float scale,
                 cudaStream_t st) {
   using namespace attn_tc;
@@ -1521,15 +1904,42 @@ int attn_fwd_tc(const void* qkv, void* out, float* lse, int B, int T, int H, flo
   p.out_w = static_cast<uint16_t*>(out);
   p.lse = lse;
   p.trace = g_trace_on;
+  p.dbg = [] {
+    const char* e = std::getenv("EPS_ATTN_DBG");
+    return e == nullptr ? 0 : std::atoi(e);
+  }();
   if (T <= 2 * kTile) {
-    const size_t sp = fwd_persistent_smem(T);
-    auto kern = fwd_poly_mode() == 0 ? attn_fwd_persistent_tc_kernel<0>
-                                      : attn_fwd_persistent_tc_kernel<4>;
-    if (!ensure_smem(kern, sp)) return EPS_ECUDA;
+    const bool poly = fwd_poly_mode() != 0;
     const int heads = B * H;
     const int grid = heads < sm_count() ? heads : sm_count();
+    // default: the ring kernel for T <= 128 (one query tile), the persistent
+    // V2 kernel above (measured: ring 0.0162 vs 0.0177 ms at BERT-large-128,
+    // persistent V2 faster at ViT-B/16 T = 197)
+    const int mode = fwd_kernel_mode() >= 0 ? fwd_kernel_mode() : (T <= kTile ? 1 : 3);
+    if (mode == 0 || mode == 3) {
+      const size_t sp = fwd_persistent_smem(T);
+      auto kern = mode == 0 ? (poly ? attn_fwd_persistent_tc_kernel<4, false>
+                                    : attn_fwd_persistent_tc_kernel<0, false>)
+                            : (poly ? attn_fwd_persistent_tc_kernel<4, true>
+                                    : attn_fwd_persistent_tc_kernel<0, true>);
+      if (!ensure_smem(kern, sp)) return EPS_ECUDA;
+      count_launch();
+      if (launch_k(kern, dim3(grid), dim3(kFwdThreads), sp, st, 1, m, p, heads) != cudaSuccess)
+        return EPS_ECUDA;
+      return cudaGetLastError() == cudaSuccess ? EPS_OK : EPS_ECUDA;
+    }
+    // O rows leave through per-warp 32-row TMA stores (rows >= T clipped)
+    CUtensorMap mo;
+    if (!make_map_3d(&mo, out, int64_t(H) * kD, T, B, int64_t(H) * kD, int64_t(T) * H * kD, kD,
+                     32, CU_TENSOR_MAP_SWIZZLE_128B))
+      return EPS_ECUDA;
+    const size_t sp = fwd_ring_smem(T);
+    auto kern = mode == 2
+                    ? (poly ? attn_fwd_ring_tc_kernel<4, false> : attn_fwd_ring_tc_kernel<0, false>)
+                    : (poly ? attn_fwd_ring_tc_kernel<4, true> : attn_fwd_ring_tc_kernel<0, true>);
+    if (!ensure_smem(kern, sp)) return EPS_ECUDA;
     count_launch();
-    if (launch_k(kern, dim3(grid), dim3(kFwdThreads), sp, st, 1, m, p, heads) != cudaSuccess)
+    if (launch_k(kern, dim3(grid), dim3(kFwdThreads), sp, st, 1, m, mo, p, heads) != cudaSuccess)
       return EPS_ECUDA;
     return cudaGetLastError() == cudaSuccess ? EPS_OK : EPS_ECUDA;
   }

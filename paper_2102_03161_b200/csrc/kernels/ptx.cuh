@@ -392,6 +392,12 @@ __device__ __forceinline__ float fast_exp2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// Three-input max (sm_100: one FMNMX3).
+__device__ __forceinline__ float fmax3f(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
 
 // 2^x for a pair on the FMA / ALU pipes instead of the SFU (which retires 16
 // lane-ops per SM clock): x = n + f with n = round(x), f in [-1/2, 1/2];
@@ -400,10 +406,17 @@ __device__ __forceinline__ float fast_exp2(float x) {
 // rounding constant 1.5 * 2^23 leaves n in the low mantissa bits of t, and its
 // own bits above bit 8 shift out).  x is clamped at -125 so the result stays
 // a normal number (2^-125 is zero for every softmax sum it can enter).
+// HI: also clamp from above at 2^126 (a caller that detects overflow from the
+// exps themselves needs a huge result, not the wrapped exponent field).
+template <bool HI = false>
 __device__ __forceinline__ float2 poly_exp2_x2(float2 x) {
   constexpr float kRound = 12582912.0f;  // 1.5 * 2^23
   x.x = fmaxf(x.x, -125.0f);
   x.y = fmaxf(x.y, -125.0f);
+  if (HI) {
+    x.x = fminf(x.x, 126.0f);
+    x.y = fminf(x.y, 126.0f);
+  }
   const float2 t = __fadd2_rn(x, make_float2(kRound, kRound));
   const float2 n = __fadd2_rn(t, make_float2(-kRound, -kRound));
   const float2 f = __fadd2_rn(x, make_float2(-n.x, -n.y));

@@ -26,9 +26,15 @@ torch.cuda.synchronize()
 L.eps_attn_trace_enable(0)
 buf = (C.c_longlong * 1024)()
 L.eps_attn_trace_read(buf, 1024)
-t = list(buf)[832:832 + 160]
+t = list(buf)[832:832 + 192]
 t0 = min(x for x in t if x > 0)
-print("tile S_iss SF_wg PF_arr OF_wg TF_arr")
-for k in range(20):
-    e = [(t[k * 5 + i] - t0) if t[k * 5 + i] > 0 else -1 for i in range(5)]
-    print(k, *e)
+import os
+if os.environ.get("EPS_ATTN_FWD", "1") == "0":
+    print("tile S_iss SF_wg PF_arr OF_wg TF_arr")
+    for k in range(20):
+        print(k, *[(t[k * 5 + i] - t0) if t[k * 5 + i] > 0 else -1 for i in range(5)])
+else:  # attn_fwd_ring_tc_kernel: per 64-key block g: SF seen, PF arrived, S issued
+    print("block S_iss SF_wg PF_arr (cycles from first stamp; d = PF - SF)")
+    for g in range(60):
+        sf, pf, si = (t[g * 3 + i] - t0 if t[g * 3 + i] > 0 else -1 for i in range(3))
+        print(g, si, sf, pf, pf - sf)
