@@ -344,7 +344,11 @@ __global__ void __launch_bounds__(LnWide<D>::THREADS, 2)
 // y with 16-byte vector stores.
 constexpr int kLnFwdStages = 32;
 
-template <int D>
+// ONEPASS: mean and variance from one reduction of (sum d, sum d^2), d = x -
+// x[row][0] (the row's first element, read from the ring by every thread: the
+// shift keeps E[d^2] - E[d]^2 free of cancellation for rows whose mean is
+// large against their spread), so a row needs one named barrier, not two.
+template <int D, bool ONEPASS>
 __global__ void __launch_bounds__(LnWide<D>::THREADS, 3)
     ln_fwd_wide_kernel(const uint16_t* __restrict__ x, const float* __restrict__ gamma,
                        const float* __restrict__ beta, uint16_t* __restrict__ y,
@@ -357,6 +361,7 @@ __global__ void __launch_bounds__(LnWide<D>::THREADS, 3)
   uint64_t* full = reinterpret_cast<uint64_t*>(ring + size_t(kLnFwdStages) * ROW);
   uint64_t* empty = full + kLnFwdStages;
   __shared__ float red[GROUPS][2][WPR];
+  __shared__ float red1[GROUPS][2][2][WPR];  // ONEPASS: [row parity][sum d, sum d^2]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t n_mine = rows > blockIdx.x ? (rows - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   if (threadIdx.x == 0) {
@@ -400,10 +405,52 @@ __global__ void __launch_bounds__(LnWide<D>::THREADS, 3)
     const int64_t r = blockIdx.x + k * gridDim.x;
     mbar_wait(&full[st], uint32_t((k / kLnFwdStages) & 1));
     const uint4 xx = ld_shared_v4(smem_addr(ring + size_t(st) * ROW) + uint32_t(col * 2));
+    const float x0 = ONEPASS ? bf16_lo(*reinterpret_cast<const uint32_t*>(ring + size_t(st) * ROW))
+                             : 0.f;
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
     float v[8];
     load_vec<8>(reinterpret_cast<const uint16_t*>(&xx), v);
+    if constexpr (ONEPASS) {
+      float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float d = v[i] - x0;
+        s1 += d;
+        s2 = fmaf(d, d, s2);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+        s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+      }
+      const int par = int((k / GROUPS) & 1);
+      if (lane == 0) {
+        red1[grp][par][0][wig] = s1;
+        red1[grp][par][1][wig] = s2;
+      }
+      asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(TPR) : "memory");
+      s1 = 0.f;
+      s2 = 0.f;
+#pragma unroll
+      for (int w = 0; w < WPR; ++w) {
+        s1 += red1[grp][par][0][w];
+        s2 += red1[grp][par][1][w];
+      }
+      const float md = s1 * (1.0f / D);
+      const float var = fmaxf(s2 * (1.0f / D) - md * md, 0.f);
+      const float mu = x0 + md;
+      const float rs = rsqrtf(var + eps);
+      float o[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) o[i] = (v[i] - mu) * rs * gam[i] + bet[i];
+      store_vec<8>(y + r * D + col, o);
+      if (t == 0) {
+        mean_out[r] = mu;
+        rstd_out[r] = rs;
+      }
+      continue;
+    }
     float s = 0.f;
 #pragma unroll
     for (int i = 0; i < 8; ++i) s += v[i];
@@ -457,10 +504,17 @@ int ln_fwd_wide_launch(const void* x, const float* gamma, const float* beta, voi
                        float* rstd, int64_t rows, float eps, cudaStream_t st) {
   using L = LnWide<D>;
   constexpr size_t smem = size_t(kLnFwdStages) * L::ROW + 2 * kLnFwdStages * 8 + 16;
+  static const bool onepass = [] {
+    const char* e = std::getenv("EPS_LN_ONEPASS");
+    return e == nullptr || std::atoi(e) != 0;
+  }();
+  auto kern = onepass ? ln_fwd_wide_kernel<D, true> : ln_fwd_wide_kernel<D, false>;
   static bool configured = false;
   if (!configured) {
-    if (cudaFuncSetAttribute(ln_fwd_wide_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             int(smem)) != cudaSuccess)
+    if (cudaFuncSetAttribute(ln_fwd_wide_kernel<D, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess ||
+        cudaFuncSetAttribute(ln_fwd_wide_kernel<D, false>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess)
       return EPS_ECUDA;
     configured = true;
   }
@@ -468,7 +522,7 @@ int ln_fwd_wide_launch(const void* x, const float* gamma, const float* beta, voi
   const int64_t need = (rows + 7) / 8;
   const int grid = int(need < sms ? need : sms);
   count_launch();
-  if (launch_k(ln_fwd_wide_kernel<D>, dim3(grid), dim3(L::THREADS), smem, st, 1,
+  if (launch_k(kern, dim3(grid), dim3(L::THREADS), smem, st, 1,
                static_cast<const uint16_t*>(x), gamma, beta, static_cast<uint16_t*>(y), mean, rstd,
                rows, eps) != cudaSuccess)
     return EPS_ECUDA;

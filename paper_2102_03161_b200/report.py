@@ -158,7 +158,14 @@ def chunks_sweep(api: EpsApi, scenario: dict, k: int, run_m: Callable[[int], flo
     cost = CostModel(cm_d["c_fwd"], cm_d["backward_ratio"], cm_d["c_update"],
                      cm_d["per_microbatch_overhead"], cm_d["allreduce_bucket_bytes"],
                      cm_d["comm_latency"])
-    model = api.model_preset(scenario["model"]["preset"])
+    md = scenario["model"]
+    if "preset" in md:
+        model = api.model_preset(md["preset"])
+    else:  # explicit arrays (configs.scenario for the tiny ViT / BERT / CIFAR configs)
+        from .capi import ModelSpec
+        model = ModelSpec(list(md["attention_params"]), list(md["mlp_params"]),
+                          list(md["activation_bytes"]), int(md.get("bytes_per_param", 4)),
+                          md.get("name", "custom"))
     seq = api.m_partition(model, 0)
     crit = 1 if scenario.get("balance_criterion") == "paper-variance" else 0  # scenario.cpp:219-225
     plan = api.load_balance(seq, k, scenario["training"]["lambda_frozen"], crit)

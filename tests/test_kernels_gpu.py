@@ -51,6 +51,37 @@ def test_layernorm_fwd_bwd(cuda, d):
     assert _rel(cs, want.sum(0)) < 1e-2  # fp32 column sums of the produced dx
 
 
+@pytest.mark.parametrize("d", [768, 1024])
+def test_layernorm_fwd_offset_rows(cuda, d):
+    """Rows whose mean is large against their spread (offsets up to 300 sigma,
+    a constant row, one outlier column): the one-pass (shifted) statistics of
+    ln_fwd_wide_kernel must match fp32 LayerNorm; mean / rstd are checked too."""
+    g = torch.Generator(device=cuda).manual_seed(7)
+    R = 1000
+    off = torch.linspace(-300, 300, R, device=cuda).unsqueeze(1)
+    x = torch.randn(R, d, device=cuda, generator=g) * 0.5 + off
+    x[5] = 3.0                   # zero variance
+    x[6, 17] += 1e4              # one outlier column
+    x[7, 0] = x[7, 1:].mean() + 50.0  # the shift element itself is the outlier
+    x = x.bfloat16()
+    gamma = torch.randn(d, device=cuda, generator=g)
+    beta = torch.randn(d, device=cuda, generator=g)
+    y = torch.empty_like(x)
+    mean = torch.empty(R, device=cuda)
+    rstd = torch.empty(R, device=cuda)
+    ops.call("eps_layernorm_fwd", x, gamma, beta, y, mean, rstd, R, d, C.c_float(1e-6), _s())
+    xf = x.float()
+    ref = F.layer_norm(xf, (d,), gamma, beta, eps=1e-6)
+    torch.cuda.synchronize()
+    assert torch.isfinite(y.float()).all()
+    assert _rel(y, ref) < 1e-2
+    per_row = (y.float() - ref).norm(dim=1) / ref.norm(dim=1).clamp_min(1e-6)
+    assert per_row.max().item() < 2e-2
+    assert ((mean - xf.mean(1)).abs() / xf.std(1).clamp_min(1e-3)).max().item() < 1e-3
+    want_rstd = torch.rsqrt(xf.var(1, unbiased=False) + 1e-6)
+    assert ((rstd - want_rstd).abs() / want_rstd).max().item() < 1e-3
+
+
 def _attn_ref(qkv, B, T, H, dh):
     D = H * dh
     q, k, v = qkv.float().reshape(B, T, 3 * D).split(D, dim=-1)

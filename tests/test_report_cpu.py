@@ -94,6 +94,18 @@ def test_chunks_sweep_model_matches_reference_choice():
     assert all(r["calibrated_modeled_iteration_s"] < r["modeled_iteration_s"] for r in one)
 
 
+def test_chunks_sweep_custom_model_spec():
+    """Scenarios with explicit model arrays (tiny ViT, BERT, CIFAR ViT: no
+    preset) go through the same sweep (tools/multi_gpu_sweeps.py uses them)."""
+    for cfg in ("tiny-vit", "bert-large-128"):
+        scen = configs.scenario(cfg, 2)
+        assert "preset" not in scen["model"]
+        rows = report.chunks_sweep(API, scen, 2, lambda m: 0.01 + 0.001 * m)
+        assert [r["m"] for r in rows] == list(range(2, 13))
+        assert sum(r["is_optimal"] for r in rows) == 1
+        assert all(r["modeled_iteration_s"] > 0 for r in rows)
+
+
 def test_bandwidth_sweep_comm_ratio_falls_with_bandwidth():
     scen = configs.scenario("vit-b16", 8)
     scen["cluster"]["nodes"] = 2  # 2 x 8: the replicas' all-reduce crosses nodes
