@@ -19,16 +19,24 @@ NVFLAGS   := -std=c++20 -O3 $(ARCH) -lineinfo -Xcompiler -fPIC -Iinclude -I$(NLO
              --expt-relaxed-constexpr -Xptxas -v
 
 CONTROL_SRC := $(wildcard $(PKG)/csrc/control/*.cpp) $(PKG)/csrc/capi_control.cpp \
-               $(PKG)/csrc/runtime/comm.cpp $(PKG)/csrc/runtime/disk_tier.cpp
+               $(PKG)/csrc/runtime/comm.cpp $(PKG)/csrc/runtime/disk_tier.cpp \
+               $(PKG)/csrc/runtime/trainer.cpp
 KERNEL_SRC  := $(wildcard $(PKG)/csrc/kernels/*.cu) $(wildcard $(PKG)/csrc/runtime/*.cu)
 OBJDIR      := build/obj
 CONTROL_OBJ := $(patsubst %.cpp,$(OBJDIR)/%.o,$(CONTROL_SRC))
 KERNEL_OBJ  := $(patsubst %.cu,$(OBJDIR)/%.o,$(KERNEL_SRC))
 LIB         := $(PKG)/libeps_b200.so
 
-.PHONY: all lib oracle conformance clean
+.PHONY: all lib oracle conformance train clean
 all: lib oracle
 lib: $(LIB)
+
+# native CLI over the library (examples/eps_train.cpp): the reference CLI's
+# `run --scenario`, executed on the GPU
+train: build/eps_train
+build/eps_train: examples/eps_train.cpp include/eps_capi.h $(LIB)
+	@mkdir -p build
+	$(CXX) -std=c++20 -O2 -Wall -Iinclude $< -L$(PKG) -leps_b200 -Wl,-rpath,'$$ORIGIN/../$(PKG)' -o $@
 
 $(OBJDIR)/%.o: %.cpp $(wildcard include/eps/*.hpp) include/eps_capi.h
 	@mkdir -p $(dir $@)

@@ -632,6 +632,32 @@ int eps_vit_forward_logits(eps_vit_t* h, const float* images, int batch, void* l
                            void* stream);
 void* eps_vit_activation(eps_vit_t* h, int which, int layer);
 
+/* ---- native single-GPU training loop (csrc/runtime/trainer.cpp) --------
+ * The reference's epoch loop (runner.cpp:139-298 decision order through
+ * EpochPlanner, redistribute, AutoCache modes, ragged last iteration) run on
+ * one GPU by the ViT executor with device gradient norms feeding the freeze
+ * decision -- the C++ host path of trainer.py:Trainer for a 1 x 1 cluster.
+ * init_params_host: fp32 [param_total] in eps_vit_layout order (NULL: seeded
+ * trunc-normal init); images_dev / labels_dev: the dataset (fp32 [N, C, H, W],
+ * int64 [N], N = iterations x per_pipeline_batch) or NULL for seeded synthetic
+ * data.  EPS_EINVAL for clusters other than 1 x 1. */
+typedef struct eps_trainer eps_trainer_t;
+typedef struct {
+  int epoch, l_frozen, pipeline_length, replica_width, micro_batches;
+  int cache_enabled, cache_moved, cache_mode; /* cache_mode: 0 off, 1 gather, 2 move, 3 trailing */
+  int iterations;
+  double epoch_time_s, iteration_time_s, throughput_sps, samples, mean_loss;
+  double cache_transition_time_s;
+} eps_train_epoch_t;
+int eps_trainer_create(const eps_scenario_t* scenario, const int* geom, int iterations_per_epoch,
+                       uint64_t seed, float lr, float momentum, int device_norms,
+                       const float* init_params_host, const float* images_dev,
+                       const int64_t* labels_dev, eps_trainer_t** out);
+/* One epoch; norms_out (host double[L], may be NULL) receives the per-layer
+ * gradient L2 norms the next epoch's freeze test reads. */
+int eps_trainer_run_epoch(eps_trainer_t* t, int epoch, eps_train_epoch_t* out, double* norms_out);
+void eps_trainer_destroy(eps_trainer_t* t);
+
 /* Pipeline-stage operations (AutoPipe executor).  Global sublayer g in
  * [0, 2L): layer g/2, ATT if even, MLP if odd (SublayerSeq order,
  * model.hpp:56-74); a stage owns global sublayers [g0, g1) with

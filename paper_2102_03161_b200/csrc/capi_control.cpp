@@ -38,6 +38,17 @@ namespace {
 
 thread_local std::string g_last_error;
 
+}  // namespace
+
+#ifndef EPS_REFERENCE_BUILD
+namespace eps {
+// error text for the runtime's C entry points (trainer.cpp)
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+}  // namespace eps
+#endif
+
+namespace {
+
 template <typename F>
 int guarded(F&& body) {
   try {
