@@ -563,6 +563,11 @@ def main_ours(args, world, rank, local):
         trainer = trainer_run(cfg, g, world, rank, dev, args.trainer_iters,
                               "eps" if use_eps else "torch")
 
+    # the same loop with the host side in C++ (csrc/runtime/trainer.cpp, one GPU)
+    trainer_native = None
+    if not args.no_trainer and g.kind == "vit" and world == 1:
+        trainer_native = trainer_run_native(cfg, g, args.trainer_iters)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cpu = cpu_baseline(cfg, args.cpu_seconds)
@@ -590,6 +595,7 @@ def main_ours(args, world, rank, local):
                "clocks": clock_rec,
                "freeze_schedule": sched,
                "trainer_run": trainer,
+               "trainer_run_native": trainer_native,
                "stage_emulation": emu,
                "nccl": nccl,
                "cpu_baseline": cpu}
@@ -672,6 +678,30 @@ def trainer_run(cfg, g, world, rank, dev, iters, comm="torch"):
     out["iterations_per_epoch"] = iters
     out["note"] = ("Trainer epochs with device gradient norms feeding the reference planner; "
                    "totals include set_plan transitions and cache boundary moves")
+    return out
+
+
+def trainer_run_native(cfg, g, iters):
+    """trainer_run with the epoch loop in C++ (eps_trainer_*: planner, shards,
+    AutoCache modes, device norms; csrc/runtime/trainer.cpp) on one GPU."""
+    from paper_2102_03161_b200 import configs
+    from paper_2102_03161_b200.native_trainer import NativeTrainer
+    out = {}
+    for name, sc in (("freeze", configs.scenario(cfg, 1)),
+                     ("no_freeze", configs.no_freeze(configs.scenario(cfg, 1)))):
+        tr = NativeTrainer(sc, g, iterations_per_epoch=iters)
+        rows = tr.run(int(sc["training"]["epochs"]))
+        tr.close()
+        out[name] = {"total_s": round(sum(r.epoch_time_s for r in rows), 4),
+                     "epochs": [{"epoch": r.epoch, "l_frozen": r.l_frozen, "cache": r.cache_enabled,
+                                 "moved": r.cache_moved, "epoch_s": round(r.epoch_time_s, 4),
+                                 "loss": round(r.mean_loss, 4),
+                                 "samples_per_s": round(r.throughput_sps, 1)} for r in rows]}
+        torch.cuda.empty_cache()
+    out["speedup_vs_no_freeze"] = round(out["no_freeze"]["total_s"] / out["freeze"]["total_s"], 4)
+    out["iterations_per_epoch"] = iters
+    out["note"] = ("native C++ epoch loop (eps_trainer_run_epoch), device gradient norms feeding "
+                   "the reference planner; seeded synthetic data and init inside the library")
     return out
 
 

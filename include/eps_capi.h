@@ -508,6 +508,10 @@ int eps_gather_rows(const void* src, int64_t src_stride_rows, void* dst, int row
 int eps_scatter_rows(const void* src, void* dst, int64_t dst_stride_rows, int rows, int64_t d,
                      int64_t offset_rows, void* stream);
 int eps_colsum_bf16(const void* x, float* out, int64_t rows, int64_t cols, void* stream);
+/* Seeded synthetic data: dst[i] ~ N(0, 1) / uniform in [0, classes), a pure
+ * function of (seed, i) (SplitMix64 finaliser + Box-Muller). */
+int eps_fill_normal(float* dst, int64_t n, uint64_t seed, void* stream);
+int eps_fill_labels(int64_t* dst, int64_t n, int64_t classes, uint64_t seed, void* stream);
 
 /* ---- peer memory (csrc/runtime/peer.cu) ---------------------------------- */
 /* CUDA IPC export of the allocation holding dev_ptr: 64-byte handle + byte

@@ -610,5 +610,49 @@ extern "C" int eps_colsum_bf16(const void* x, float* out, int64_t rows, int64_t 
   return ok_or_cuda();
 }
 
+// Seeded synthetic data (the native trainer's dataset): element i of a
+// stream is a function of (seed, i) only -- SplitMix64 finalisers of the
+// counter, Box-Muller for N(0, 1) -- so any grid shape gives the same data.
+namespace eps_k {
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__global__ void fill_normal_kernel(float* __restrict__ dst, int64_t n, uint64_t seed) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x) {
+    const uint64_t a = mix64(seed + 0x9E3779B97F4A7C15ull * uint64_t(2 * i + 1));
+    const uint64_t b = mix64(seed + 0x9E3779B97F4A7C15ull * uint64_t(2 * i + 2));
+    const float u1 = (float(a >> 40) + 0.5f) * (1.0f / 16777216.0f);  // (0, 1)
+    const float u2 = float(b >> 40) * (1.0f / 16777216.0f);
+    dst[i] = sqrtf(-2.0f * logf(u1)) * cospif(2.0f * u2);
+  }
+}
+__global__ void fill_labels_kernel(int64_t* __restrict__ dst, int64_t n, int64_t classes,
+                                   uint64_t seed) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += int64_t(gridDim.x) * blockDim.x)
+    dst[i] = int64_t(mix64(seed + 0x9E3779B97F4A7C15ull * uint64_t(i + 1)) % uint64_t(classes));
+}
+}  // namespace eps_k
+
+extern "C" int eps_fill_normal(float* dst, int64_t n, uint64_t seed, void* stream) {
+  if (n <= 0) return EPS_OK;
+  count_launch();
+  eps_k::fill_normal_kernel<<<num_sms() * 8, 256, 0, static_cast<cudaStream_t>(stream)>>>(dst, n,
+                                                                                          seed);
+  return ok_or_cuda();
+}
+
+extern "C" int eps_fill_labels(int64_t* dst, int64_t n, int64_t classes, uint64_t seed,
+                               void* stream) {
+  if (n <= 0 || classes < 1) return n <= 0 ? EPS_OK : EPS_EINVAL;
+  count_launch();
+  eps_k::fill_labels_kernel<<<num_sms() * 2, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      dst, n, classes, seed);
+  return ok_or_cuda();
+}
+
 // Number of kernels this library has launched in the process so far.
 extern "C" unsigned long long eps_launch_count(void) { return eps_k::launch_counter().load(); }

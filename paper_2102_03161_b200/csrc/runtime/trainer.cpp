@@ -260,17 +260,19 @@ int eps_trainer_create(const eps_scenario_t* scenario, const int* geom, int iter
       cuda_check(cudaMemcpy(t->labels_host.data(), labels_dev, t->labels_host.size() * 8,
                             cudaMemcpyDeviceToHost),
                  "labels D2H");
-    } else {
-      SplitMix rng{seed ^ 0xD1B54A32D192ED03ull};
-      std::vector<float> img(size_t(t->image_elems) * 64);
-      for (int64_t s0 = 0; s0 < t->dataset; s0 += 64) {
-        const int64_t n = std::min<int64_t>(64, t->dataset - s0);
-        for (int64_t e = 0; e < n * t->image_elems; ++e) img[size_t(e)] = float(rng.normal());
-        cuda_check(cudaMemcpy(t->images.p + s0 * t->image_elems, img.data(),
-                              size_t(n * t->image_elems) * 4, cudaMemcpyHostToDevice),
-                   "images H2D");
-      }
-      for (auto& l : t->labels_host) l = int64_t(rng.next() % uint64_t(geom[5]));
+    } else {  // seeded synthetic data, generated on the device
+      DevBuf<int64_t> lab;
+      lab.alloc(t->labels_host.size());
+      eps_check(eps_fill_normal(t->images.p, int64_t(t->images.n), seed ^ 0xD1B54A32D192ED03ull,
+                                t->st),
+                "eps_fill_normal");
+      eps_check(eps_fill_labels(lab.p, int64_t(lab.n), geom[5], seed ^ 0x8CB92BA72F3D8DD7ull,
+                                t->st),
+                "eps_fill_labels");
+      cuda_check(cudaMemcpyAsync(t->labels_host.data(), lab.p, lab.n * 8, cudaMemcpyDeviceToHost,
+                                 t->st),
+                 "labels D2H");
+      cuda_check(cudaStreamSynchronize(t->st), "synthetic data");
     }
     t->xb.alloc(size_t(t->batch * t->image_elems));
     t->yb.alloc(size_t(t->batch) * size_t(t->iters));
