@@ -211,17 +211,39 @@ __device__ __forceinline__ void gelu_and_grad_f(float x, float& g, float& gp) {
 }
 
 // Two columns at once on the packed fp32 pipe (FFMA2 / FMUL2: one issue slot
-// for two IEEE fp32 operations); same function as gelu_and_grad_f.
+// for two IEEE fp32 operations); same function as gelu_and_grad_f, with erfc by
+// Abramowitz & Stegun 7.1.25 when EPS_GELU_AS3 (three terms, p = 0.47047,
+// |erf error| <= 2.5e-5, i.e. <= 1.3e-5 in Phi: two orders under the bf16
+// rounding of the stored gelu / gelu') -- two packed FMAs fewer per pair in the
+// issue-bound FC1 epilogue.  (Tried: the reciprocal on the FMA pipe, linear
+// start + three Newton steps, instead of MUFU.RCP: FC1 forward 0.375 -> 0.403
+// ms -- the epilogue is issue-bound, not SFU-bound.)
+#ifndef EPS_GELU_AS3
+#define EPS_GELU_AS3 1
+#endif
+constexpr float kGeluP3 = 0.47047f * 0.70710678118654752f;
+constexpr float kGeluB1 = 0.5f * 0.3480242f;
+constexpr float kGeluB2 = 0.5f * -0.0958798f;
+constexpr float kGeluB3 = 0.5f * 0.7478556f;
 __device__ __forceinline__ void gelu_and_grad_f2(float2 x, float2& g, float2& gp) {
   const float2 ax = make_float2(fabsf(x.x), fabsf(x.y));
+#if EPS_GELU_AS3
+  const float2 den = __ffma2_rn(make_float2(kGeluP3, kGeluP3), ax, make_float2(1.f, 1.f));
+#else
   const float2 den = __ffma2_rn(make_float2(kGeluP, kGeluP), ax, make_float2(1.f, 1.f));
+#endif
   const float2 t = make_float2(rcp_approx(den.x), rcp_approx(den.y));
   const float2 arg = __fmul2_rn(x, __fmul2_rn(make_float2(kGeluE, kGeluE), x));
   const float2 e = make_float2(ex2_approx(arg.x), ex2_approx(arg.y));
+#if EPS_GELU_AS3
+  float2 p = __ffma2_rn(make_float2(kGeluB3, kGeluB3), t, make_float2(kGeluB2, kGeluB2));
+  p = __ffma2_rn(p, t, make_float2(kGeluB1, kGeluB1));
+#else
   float2 p = __ffma2_rn(make_float2(kGeluA5, kGeluA5), t, make_float2(kGeluA4, kGeluA4));
   p = __ffma2_rn(p, t, make_float2(kGeluA3, kGeluA3));
   p = __ffma2_rn(p, t, make_float2(kGeluA2, kGeluA2));
   p = __ffma2_rn(p, t, make_float2(kGeluA1, kGeluA1));
+#endif
   const float2 h = __fmul2_rn(__fmul2_rn(p, t), e);
   const float2 c = make_float2(x.x >= 0.0f ? 1.0f - h.x : h.x, x.y >= 0.0f ? 1.0f - h.y : h.y);
   g = __fmul2_rn(x, c);

@@ -87,6 +87,20 @@ __global__ void __launch_bounds__(384, 1) mma_rate(int iters, int n, int ts, int
 
 // cta_group::2 (cluster of 2): M = 256 (128 rows per CTA), N, K = 16; and
 // cta_group::1 M = 64 for comparison.
+__device__ __forceinline__ void tc_mma_pair_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc,
+                                               uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// mode: 0 SS K-major, 1 TS (A from TMEM, B MN-major SW128), 2 SS A MN-major + B MN-major
+template <int mode>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
     mma_rate_pair(int iters, int n, long long* out) {
   extern __shared__ uint8_t smem_raw[];
@@ -107,12 +121,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1)
   if (warp == 1 && rank == 0) {
     const uint64_t a = umma_sdesc(smem_addr(smem), 16, 1024);
     const uint64_t b = umma_sdesc(smem_addr(smem + 32768), 16, 1024);
-    const uint32_t idesc = umma_idesc_bf16(256, n, false, false);
+    const uint64_t amn = umma_sdesc(smem_addr(smem), 64 * 128, 1024);
+    const uint64_t bmn = umma_sdesc(smem_addr(smem + 32768), 64 * 128, 1024);
+    const uint32_t idesc = umma_idesc_bf16(256, n, mode == 2, mode >= 1);
     long long t0 = clock64();
     for (int i = 0; i < iters; i += 8) {
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        if (lane == 0) tc_mma_pair(tmem + 256, a + uint64_t(2 * (u & 3)), b + uint64_t(2 * (u & 3)), idesc, 1u);
+        if (lane == 0) {
+          if constexpr (mode == 0)
+            tc_mma_pair(tmem + 256, a + uint64_t(2 * (u & 3)), b + uint64_t(2 * (u & 3)), idesc, 1u);
+          else if constexpr (mode == 1)
+            tc_mma_pair_ts(tmem + 256, tmem + uint32_t(u * 8), bmn + uint64_t(128 * (u & 3)), idesc, 1u);
+          else
+            tc_mma_pair(tmem + 256, amn + uint64_t(128 * (u & 3)), bmn + uint64_t(128 * (u & 3)), idesc, 1u);
+        }
         __syncwarp();
       }
     }
@@ -196,15 +219,21 @@ int main() {
                ts ? "TS" : "SS", n, nd, loaders, double(h[0]) / iters, double(h[1]) / iters);
       }
     }
-  cudaFuncSetAttribute(mma_rate_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  cudaFuncSetAttribute(mma_rate_pair<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  cudaFuncSetAttribute(mma_rate_pair<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+  cudaFuncSetAttribute(mma_rate_pair<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
   cudaFuncSetAttribute(mma_rate_m64, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
-  for (int n : {32, 64, 128, 256}) {
-    mma_rate_pair<<<2, 128, 100 * 1024>>>(iters, n, d);
-    long long h[2];
-    cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
-    printf("PAIR M=256 N=%3d: issue %.1f, complete %.1f cycles/MMA (%s)\n", n, double(h[0]) / iters,
-           double(h[1]) / iters, cudaGetErrorString(cudaGetLastError()));
-  }
+  for (int mode = 0; mode < 3; ++mode)
+    for (int n : {32, 64, 128, 256}) {
+      if (mode == 0) mma_rate_pair<0><<<2, 128, 100 * 1024>>>(iters, n, d);
+      if (mode == 1) mma_rate_pair<1><<<2, 128, 100 * 1024>>>(iters, n, d);
+      if (mode == 2) mma_rate_pair<2><<<2, 128, 100 * 1024>>>(iters, n, d);
+      long long h[2];
+      cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
+      printf("PAIR %s M=256 N=%3d: issue %.1f, complete %.1f cycles/MMA (%s)\n",
+             mode == 0 ? "SS" : mode == 1 ? "TS" : "SS-MN", n, double(h[0]) / iters,
+             double(h[1]) / iters, cudaGetErrorString(cudaGetLastError()));
+    }
   for (int n : {32, 64, 128, 256}) {
     mma_rate_m64<<<1, 128, 100 * 1024>>>(iters, n, d);
     long long h[2];
