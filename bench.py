@@ -565,7 +565,7 @@ def main_ours(args, world, rank, local):
 
     # the same loop with the host side in C++ (csrc/runtime/trainer.cpp, one GPU)
     trainer_native = None
-    if not args.no_trainer and g.kind == "vit" and world == 1:
+    if not args.no_trainer and world == 1:
         trainer_native = trainer_run_native(cfg, g, args.trainer_iters)
 
     cpu = None

@@ -8,8 +8,9 @@
 //   build/eps_train --scenario s.json --geometry tiny-vit --iterations 3 [--epochs 10]
 //                   [--seed 17] [--lr 1e-3] [--momentum 0.9] [--csv out.csv]
 //
-// Synthetic data (seeded N(0,1) images, uniform labels) and a seeded
-// trunc-normal initialisation; a 1 x 1 cluster (other clusters: trainer.py).
+// Synthetic data (seeded N(0,1) images or uniform token ids with half-and-half
+// segment ids, uniform labels) and a seeded trunc-normal initialisation; a
+// 1 x 1 cluster (other clusters: trainer.py).
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -22,18 +23,25 @@ namespace {
 
 struct Geo {
   const char* name;
-  int v[10];  // layers, d, mlp, heads, tokens, classes, image, stored image, patch, channels
+  int kind;   // EPS_MODEL_VIT / EPS_MODEL_BERT
+  int v[10];  // ViT: layers, d, mlp, heads, tokens, classes, image, stored image, patch, channels
+              // BERT: layers, d, mlp, heads, tokens, classes, vocab, positions, head (1 SQuAD), pooler
 };
-// configs.py GEOMETRIES (the ViT family)
+// configs.py GEOMETRIES
 const Geo kGeos[] = {
-    {"tiny-vit", {4, 128, 512, 4, 65, 100, 32, 32, 4, 3}},
-    {"vit-b16", {12, 768, 3072, 12, 197, 1000, 224, 224, 16, 3}},
-    {"vit-b16-cifar100", {12, 768, 3072, 12, 197, 100, 224, 32, 16, 3}},
+    {"tiny-vit", EPS_MODEL_VIT, {4, 128, 512, 4, 65, 100, 32, 32, 4, 3}},
+    {"vit-b16", EPS_MODEL_VIT, {12, 768, 3072, 12, 197, 1000, 224, 224, 16, 3}},
+    {"vit-b16-cifar100", EPS_MODEL_VIT, {12, 768, 3072, 12, 197, 100, 224, 32, 16, 3}},
+    {"bert-base-384", EPS_MODEL_BERT, {12, 768, 3072, 12, 384, 2, 30522, 512, 1, 1}},
+    {"bert-large-128", EPS_MODEL_BERT, {24, 1024, 4096, 16, 128, 2, 30522, 512, 0, 1}},
+    {"tiny-bert-qa", EPS_MODEL_BERT, {2, 128, 512, 2, 64, 2, 1000, 128, 1, 1}},
+    {"tiny-bert-cls", EPS_MODEL_BERT, {2, 256, 1024, 4, 48, 3, 500, 64, 0, 1}},
 };
 
 int usage(const char* argv0) {
   std::fprintf(stderr,
-               "usage: %s --scenario FILE --geometry {tiny-vit|vit-b16|vit-b16-cifar100} "
+               "usage: %s --scenario FILE --geometry {tiny-vit|vit-b16|vit-b16-cifar100|bert-base-384|"
+               "bert-large-128|tiny-bert-qa|tiny-bert-cls} "
                "--iterations N [--epochs E] [--seed S] [--lr X] [--momentum X] [--csv OUT]\n",
                argv0);
   return 2;
@@ -85,8 +93,8 @@ int main(int argc, char** argv) {
   geom[10] = batch;
 
   eps_trainer_t* t = nullptr;
-  rc = eps_trainer_create(sc, geom, iterations, seed, lr, momentum, 1, nullptr, nullptr, nullptr,
-                          &t);
+  rc = eps_trainer_create(sc, geo->kind, geom, iterations, seed, lr, momentum, 1, nullptr, nullptr,
+                          nullptr, &t);
   if (rc != EPS_OK) return fail("eps_trainer_create", rc);
   FILE* out = csv.empty() ? stdout : std::fopen(csv.c_str(), "w");
   if (out == nullptr) {

@@ -641,11 +641,15 @@ void* eps_vit_activation(eps_vit_t* h, int which, int layer);
  * EpochPlanner, redistribute, AutoCache modes, ragged last iteration) run on
  * one GPU by the ViT executor with device gradient norms feeding the freeze
  * decision -- the C++ host path of trainer.py:Trainer for a 1 x 1 cluster.
- * init_params_host: fp32 [param_total] in eps_vit_layout order (NULL: seeded
- * trunc-normal init); images_dev / labels_dev: the dataset (fp32 [N, C, H, W],
- * int64 [N], N = iterations x per_pipeline_batch) or NULL for seeded synthetic
- * data.  EPS_EINVAL for clusters other than 1 x 1. */
+ * kind: EPS_MODEL_VIT (geom as eps_vit_layout) or EPS_MODEL_BERT (geom as
+ * eps_bert_layout).  init_params_host: fp32 [param_total] in the executor's
+ * layout (NULL: seeded trunc-normal init); inputs_dev / labels_dev: the dataset
+ * (N = iterations x per_pipeline_batch samples; ViT fp32 images [N, C, H, W],
+ * BERT int64 [2, N, T] token then segment ids; labels int64 [N], SQuAD head
+ * [2, N] start then end) or NULL for seeded synthetic data.  EPS_EINVAL for
+ * clusters other than 1 x 1. */
 typedef struct eps_trainer eps_trainer_t;
+enum { EPS_MODEL_VIT = 0, EPS_MODEL_BERT = 1 };
 typedef struct {
   int epoch, l_frozen, pipeline_length, replica_width, micro_batches;
   int cache_enabled, cache_moved, cache_mode; /* cache_mode: 0 off, 1 gather, 2 move, 3 trailing */
@@ -653,9 +657,9 @@ typedef struct {
   double epoch_time_s, iteration_time_s, throughput_sps, samples, mean_loss;
   double cache_transition_time_s;
 } eps_train_epoch_t;
-int eps_trainer_create(const eps_scenario_t* scenario, const int* geom, int iterations_per_epoch,
-                       uint64_t seed, float lr, float momentum, int device_norms,
-                       const float* init_params_host, const float* images_dev,
+int eps_trainer_create(const eps_scenario_t* scenario, int kind, const int* geom,
+                       int iterations_per_epoch, uint64_t seed, float lr, float momentum,
+                       int device_norms, const float* init_params_host, const void* inputs_dev,
                        const int64_t* labels_dev, eps_trainer_t** out);
 /* One epoch; norms_out (host double[L], may be NULL) receives the per-layer
  * gradient L2 norms the next epoch's freeze test reads. */

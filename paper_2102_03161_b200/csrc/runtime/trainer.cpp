@@ -1,6 +1,6 @@
 // Native single-GPU training loop: the reference's epoch loop
 // (runner.cpp:simulate_run, decision order of EpochPlanner) executed on the
-// device by the ViT stage executor, with no Python on the path.
+// device by the ViT or BERT stage executor, with no Python on the path.
 //
 // Per epoch (runner.cpp:139-298, trainer.py:run_epoch for K = R = 1):
 //   decision = EpochPlanner::begin_epoch(epoch, norms of the previous epoch)
@@ -96,9 +96,11 @@ struct DevBuf {
 
 struct eps_trainer {
   eps::ScenarioConfig cfg;
+  int kind = 0;  // EPS_MODEL_VIT / EPS_MODEL_BERT
   int geom[kGeom];
   int layers = 0, tokens = 0, hidden = 0, batch = 0, iters = 0;
-  int64_t image_elems = 0;  // fp32 per sample
+  int64_t image_elems = 0;  // ViT: fp32 per sample
+  bool qa = false;          // BERT SQuAD span head: labels are (start, end) pairs
   uint64_t seed = 0;
   float lr = 0.f, momentum = 0.f;
   int64_t dataset = 0;
@@ -112,17 +114,53 @@ struct eps_trainer {
   DevBuf<float> p32, g32, mom;
   DevBuf<uint16_t> p16;
   DevBuf<uint8_t> ws;
-  DevBuf<float> images, xb, loss;
+  DevBuf<float> images, xb, loss;   // ViT dataset / batch
+  DevBuf<int64_t> tok, segs, tb;  // BERT dataset [N][T] x 2, batch [2][b][T]
   DevBuf<int64_t> yb, shard;
-  std::vector<int64_t> labels_host;  // per-batch labels are assembled on the host
+  std::vector<int64_t> labels_host;  // [N] (class) or [N][2] (start, end), host side
   DevBuf<double> sq;
   DevBuf<uint16_t> store;  // AutoCache store: dataset x (tokens * hidden) bf16
   eps_vit_t* ex = nullptr;
+  eps_bert_t* bx = nullptr;
   cudaStream_t st = nullptr;
 
   ~eps_trainer() {
     if (ex) eps_vit_destroy(ex);
+    if (bx) eps_bert_destroy(bx);
     if (st) cudaStreamDestroy(st);
+  }
+  bool bert() const { return kind == EPS_MODEL_BERT; }
+  // executor calls shared by both families
+  void set_cache_shards() {
+    eps_check(bert() ? eps_bert_set_cache_shards(bx, nullptr, 0)
+                     : eps_vit_set_cache_shards(ex, nullptr, 0),
+              "set_cache_shards");
+  }
+  void head(const int64_t* y, int b0, int b, int gb) {
+    eps_check(bert() ? eps_bert_stage_head(bx, y, b0, b, gb, loss.p, st)
+                     : eps_vit_stage_head(ex, y, b0, b, gb, loss.p, st),
+              "stage head");
+  }
+  void backward(int b0, int b, int g0, int g1, int lf) {
+    eps_check(bert() ? eps_bert_stage_backward(bx, b0, b, g0, g1, lf, 0, st)
+                     : eps_vit_stage_backward(ex, b0, b, g0, g1, lf, 0, st),
+              "stage backward");
+  }
+  void sqnorms(int lf) {  // per-layer sum of squares of layers [lf, L) into sq; frozen zero
+    cuda_check(cudaMemsetAsync(sq.p, 0, sq.n * 8, st), "sq");
+    eps_check(bert() ? eps_bert_sqnorm_ranges(bx, segments.data() + lf, layers - lf, sq.p + lf, st)
+                     : eps_vit_sqnorm_ranges(ex, segments.data() + lf, layers - lf, sq.p + lf, st),
+              "sqnorm ranges");
+  }
+  void sgd(int lf) {  // SGD-momentum over the trainable tail [sublayer 2 lf, end)
+    int64_t a = 0, e = 0;
+    eps_check(bert() ? eps_bert_param_range(bx, 2 * lf, 2 * layers, &a, &e)
+                     : eps_vit_param_range(ex, 2 * lf, 2 * layers, &a, &e),
+              "param range");
+    e = param_total;  // the tail (head / pooler / classifier) trains too
+    eps_check(bert() ? eps_bert_sgd_range(bx, a, e, lr, momentum, 0.f, st)
+                     : eps_vit_sgd_range(ex, a, e, lr, momentum, 0.f, st),
+              "sgd");
   }
 };
 
@@ -146,28 +184,40 @@ int guarded_rt(F&& body) {
 }
 
 // Seeded initialisation in the executor's flat layout: trunc-normal(0.02,
-// +-0.04) weights, zero biases, unit LayerNorm gains (vit.py:init_params);
-// the head's padded class rows stay zero.
-void init_params(eps_trainer* t, const int64_t* tens, std::vector<float>& host) {
+// +-0.04) matrices / embeddings, zero biases, unit LayerNorm gains
+// (vit.py / bert.py init_params); the head's padded class rows stay zero.
+// tensor kinds in eps_*_layout order: 0 weight, 1 bias, 2 LayerNorm gain.
+void init_params(eps_trainer* t, const int64_t* tens, int n_tensors, std::vector<float>& host) {
   host.assign(size_t(t->param_total), 0.f);
   SplitMix rng{t->seed * 0x2545F4914F6CDD1Dull + 1};
   const int L = t->layers;
-  const int n_tensors = 4 + 12 * L + 4;
   const int classes = t->geom[5], d = t->hidden;
   for (int i = 0; i < n_tensors; ++i) {
     const int64_t off = tens[2 * i], n = tens[2 * i + 1];
-    // kind: 0 weight (trunc-normal), 1 bias (zero), 2 LayerNorm gain (one)
     int kind = 0;
     int64_t valid = n;
-    if (i < 4) {
-      kind = i == 1 ? 1 : 0;
-    } else if (i < 4 + 12 * L) {
-      const int j = (i - 4) % 12;
-      kind = (j == 0 || j == 6) ? 2 : (j % 2 == 1) ? 1 : 0;
-    } else {
-      const int j = i - 4 - 12 * L;  // norm.w, norm.b, head.w, head.b
-      kind = j == 0 ? 2 : (j == 1 || j == 3) ? 1 : 0;
-      if (j == 2) valid = int64_t(classes) * d;
+    if (!t->bert()) {  // patch W, patch b, cls, pos | 12 per block | norm w, b, head W, b
+      if (i < 4) {
+        kind = i == 1 ? 1 : 0;
+      } else if (i < 4 + 12 * L) {
+        const int j = (i - 4) % 12;
+        kind = (j == 0 || j == 6) ? 2 : (j % 2 == 1) ? 1 : 0;
+      } else {
+        const int j = i - 4 - 12 * L;
+        kind = j == 0 ? 2 : (j == 1 || j == 3) ? 1 : 0;
+        if (j == 2) valid = int64_t(classes) * d;
+      }
+    } else {  // word, pos, type, LN w, LN b | 12 per layer | [pooler W, b] classifier W, b
+      if (i < 5) {
+        kind = i == 3 ? 2 : i == 4 ? 1 : 0;
+      } else if (i < 5 + 12 * L) {
+        const int j = (i - 5) % 12;
+        kind = (j == 4 || j == 10) ? 2 : (j % 2 == 1) ? 1 : 0;
+      } else {
+        const int j = i - 5 - 12 * L;  // 0, 1: pooler (if any); last two: classifier
+        kind = (j % 2 == 1) ? 1 : 0;
+        if (i == n_tensors - 2) valid = int64_t(classes) * d;
+      }
     }
     for (int64_t e = 0; e < valid; ++e) {
       float v = 0.f;
@@ -188,15 +238,17 @@ void init_params(eps_trainer* t, const int64_t* tens, std::vector<float>& host) 
 
 extern "C" {
 
-int eps_trainer_create(const eps_scenario_t* scenario, const int* geom, int iterations_per_epoch,
-                       uint64_t seed, float lr, float momentum, int device_norms,
-                       const float* init_params_host, const float* images_dev,
+int eps_trainer_create(const eps_scenario_t* scenario, int kind, const int* geom,
+                       int iterations_per_epoch, uint64_t seed, float lr, float momentum,
+                       int device_norms, const float* init_params_host, const void* inputs_dev,
                        const int64_t* labels_dev, eps_trainer_t** out) {
   return guarded_rt([&] {
-    if (scenario == nullptr || geom == nullptr || out == nullptr || iterations_per_epoch < 1)
-      throw std::invalid_argument("eps_trainer_create: null argument or iterations < 1");
+    if (scenario == nullptr || geom == nullptr || out == nullptr || iterations_per_epoch < 1 ||
+        (kind != EPS_MODEL_VIT && kind != EPS_MODEL_BERT))
+      throw std::invalid_argument("eps_trainer_create: null argument, iterations < 1 or bad kind");
     auto t = std::make_unique<eps_trainer>();
     t->cfg = scenario->cfg;
+    t->kind = kind;
     const int world = t->cfg.cluster.node_count * t->cfg.cluster.gpus_per_node;
     if (world != 1 || t->cfg.pipeline_length_at_start() != 1)
       throw std::invalid_argument(
@@ -205,6 +257,7 @@ int eps_trainer_create(const eps_scenario_t* scenario, const int* geom, int iter
     t->layers = geom[0];
     t->hidden = geom[1];
     t->tokens = geom[4];
+    t->qa = t->bert() && geom[8] == 1;
     t->batch = int(t->cfg.training.per_pipeline_batch);
     if (t->batch < 1 || t->batch > geom[10])
       throw std::invalid_argument("per_pipeline_batch must be in [1, geometry max_batch]");
@@ -215,7 +268,7 @@ int eps_trainer_create(const eps_scenario_t* scenario, const int* geom, int iter
     t->lr = lr;
     t->momentum = momentum;
     t->device_norms = device_norms != 0;
-    t->image_elems = int64_t(geom[9]) * geom[7] * geom[7];
+    if (!t->bert()) t->image_elems = int64_t(geom[9]) * geom[7] * geom[7];
     // dataset = iterations x batch x initial replica count (runner.cpp:103-104)
     t->dataset = int64_t(t->iters) * t->batch;
     t->planner = std::make_unique<eps::EpochPlanner>(t->cfg);
@@ -224,14 +277,19 @@ int eps_trainer_create(const eps_scenario_t* scenario, const int* geom, int iter
 
     int64_t ws_bytes = 0;
     t->segments.resize(size_t(t->layers) + 1);
-    std::vector<int64_t> tens(2 * size_t(4 + 12 * t->layers + 4));
-    eps_check(eps_vit_layout(geom, &t->param_total, &ws_bytes, t->segments.data(), tens.data()),
-              "eps_vit_layout");
+    const int n_tensors = t->bert() ? 5 + 12 * t->layers + (geom[9] ? 2 : 0) + 2
+                                    : 4 + 12 * t->layers + 4;
+    std::vector<int64_t> tens(2 * size_t(n_tensors));
+    eps_check(t->bert() ? eps_bert_layout(geom, &t->param_total, &ws_bytes, t->segments.data(),
+                                          tens.data())
+                        : eps_vit_layout(geom, &t->param_total, &ws_bytes, t->segments.data(),
+                                         tens.data()),
+              "layout");
     cuda_check(cudaStreamCreateWithFlags(&t->st, cudaStreamNonBlocking), "stream");
     t->p32.alloc(size_t(t->param_total));
     t->p16.alloc(size_t(t->param_total));
     t->g32.alloc(size_t(t->param_total));
-    t->mom.alloc(size_t(t->param_total));
+    t->mom.alloc(size_t(t->param_total) * (t->bert() ? 2 : 1));  // BERT: room for AdamW m | v
     t->ws.alloc(size_t(ws_bytes));
     t->loss.alloc(1);
     t->sq.alloc(size_t(t->layers));
@@ -239,7 +297,7 @@ int eps_trainer_create(const eps_scenario_t* scenario, const int* geom, int iter
     cuda_check(cudaMemset(t->mom.p, 0, t->mom.n * 4), "memset");
     std::vector<float> host;
     if (init_params_host == nullptr) {
-      init_params(t.get(), tens.data(), host);
+      init_params(t.get(), tens.data(), n_tensors, host);
       init_params_host = host.data();
     }
     cuda_check(cudaMemcpy(t->p32.p, init_params_host, size_t(t->param_total) * 4,
@@ -249,33 +307,65 @@ int eps_trainer_create(const eps_scenario_t* scenario, const int* geom, int iter
     eps_check(eps_sgd_momentum(t->p32.p, t->p16.p, t->g32.p, t->mom.p, t->param_total, 0.f, 0.f,
                                0.f, t->st),
               "bf16 params");
-    eps_check(eps_vit_create(geom, t->p32.p, t->p16.p, t->g32.p, t->mom.p, t->ws.p, &t->ex),
-              "eps_vit_create");
-    // synthetic dataset (or the caller's device tensors)
-    t->images.alloc(size_t(t->dataset * t->image_elems));
-    t->labels_host.resize(size_t(t->dataset));
-    if (images_dev != nullptr && labels_dev != nullptr) {
-      cuda_check(cudaMemcpy(t->images.p, images_dev, t->images.n * 4, cudaMemcpyDeviceToDevice),
-                 "images D2D");
-      cuda_check(cudaMemcpy(t->labels_host.data(), labels_dev, t->labels_host.size() * 8,
+    eps_check(t->bert() ? eps_bert_create(geom, t->p32.p, t->p16.p, t->g32.p, t->mom.p, t->ws.p,
+                                          &t->bx)
+                        : eps_vit_create(geom, t->p32.p, t->p16.p, t->g32.p, t->mom.p, t->ws.p,
+                                         &t->ex),
+              "executor create");
+    // dataset: the caller's device tensors, or seeded synthetic data (device)
+    const int64_t N = t->dataset, T = t->tokens;
+    const int64_t n_lab = t->qa ? 2 * N : N;
+    t->labels_host.resize(size_t(n_lab));
+    if (!t->bert()) {
+      t->images.alloc(size_t(N * t->image_elems));
+      t->xb.alloc(size_t(t->batch * t->image_elems));
+    } else {
+      t->tok.alloc(size_t(N * T));
+      t->segs.alloc(size_t(N * T));
+      t->tb.alloc(size_t(2 * t->batch * T));
+    }
+    if (inputs_dev != nullptr && labels_dev != nullptr) {
+      if (!t->bert()) {
+        cuda_check(cudaMemcpy(t->images.p, inputs_dev, t->images.n * 4, cudaMemcpyDeviceToDevice),
+                   "images D2D");
+      } else {  // int64 [2][N][T]: token ids, then segment ids
+        const int64_t* in = static_cast<const int64_t*>(inputs_dev);
+        cuda_check(cudaMemcpy(t->tok.p, in, size_t(N * T) * 8, cudaMemcpyDeviceToDevice), "D2D");
+        cuda_check(cudaMemcpy(t->segs.p, in + N * T, size_t(N * T) * 8, cudaMemcpyDeviceToDevice),
+                   "D2D");
+      }
+      cuda_check(cudaMemcpy(t->labels_host.data(), labels_dev, size_t(n_lab) * 8,
                             cudaMemcpyDeviceToHost),
                  "labels D2H");
-    } else {  // seeded synthetic data, generated on the device
+    } else {
       DevBuf<int64_t> lab;
-      lab.alloc(t->labels_host.size());
-      eps_check(eps_fill_normal(t->images.p, int64_t(t->images.n), seed ^ 0xD1B54A32D192ED03ull,
-                                t->st),
-                "eps_fill_normal");
-      eps_check(eps_fill_labels(lab.p, int64_t(lab.n), geom[5], seed ^ 0x8CB92BA72F3D8DD7ull,
-                                t->st),
-                "eps_fill_labels");
+      lab.alloc(size_t(n_lab));
+      if (!t->bert()) {
+        eps_check(eps_fill_normal(t->images.p, int64_t(t->images.n), seed ^ 0xD1B54A32D192ED03ull,
+                                  t->st),
+                  "eps_fill_normal");
+        eps_check(eps_fill_labels(lab.p, N, geom[5], seed ^ 0x8CB92BA72F3D8DD7ull, t->st),
+                  "eps_fill_labels");
+      } else {  // token ids U[0, vocab), segment ids 0 | 1 by half (bench.py synthetic_inputs)
+        eps_check(eps_fill_labels(t->tok.p, N * T, geom[6], seed ^ 0xD1B54A32D192ED03ull,
+                                  t->st),
+                  "eps_fill_labels");
+        std::vector<int64_t> sg(size_t(N * T));
+        for (int64_t i = 0; i < N * T; ++i) sg[size_t(i)] = (i % T) >= T / 2 ? 1 : 0;
+        cuda_check(cudaMemcpyAsync(t->segs.p, sg.data(), sg.size() * 8, cudaMemcpyHostToDevice,
+                                   t->st),
+                   "segments H2D");
+        eps_check(eps_fill_labels(lab.p, n_lab, t->qa ? T : geom[5], seed ^ 0x8CB92BA72F3D8DD7ull,
+                                  t->st),
+                  "eps_fill_labels");
+        cuda_check(cudaStreamSynchronize(t->st), "segments");
+      }
       cuda_check(cudaMemcpyAsync(t->labels_host.data(), lab.p, lab.n * 8, cudaMemcpyDeviceToHost,
                                  t->st),
                  "labels D2H");
       cuda_check(cudaStreamSynchronize(t->st), "synthetic data");
     }
-    t->xb.alloc(size_t(t->batch * t->image_elems));
-    t->yb.alloc(size_t(t->batch) * size_t(t->iters));
+    t->yb.alloc(size_t(n_lab));
     t->shard.alloc(size_t(t->dataset));
     cuda_check(cudaStreamSynchronize(t->st), "init");
     *out = t.release();
@@ -320,7 +410,7 @@ int eps_trainer_run_epoch(eps_trainer_t* t, int epoch, eps_train_epoch_t* out, d
     if (cache_mode != 0 && t->store.p == nullptr) {
       t->store.alloc(size_t(t->dataset * row_elems));
       cuda_check(cudaMemsetAsync(t->store.p, 0, t->store.n * 2, t->st), "store");
-      eps_check(eps_vit_set_cache_shards(t->ex, nullptr, 0), "set_cache_shards");
+      t->set_cache_shards();
     }
     // this epoch's sample order (one replica: the whole dataset)
     const eps::Topology topo(t->cfg.cluster, 1);
@@ -334,9 +424,21 @@ int eps_trainer_run_epoch(eps_trainer_t* t, int epoch, eps_train_epoch_t* out, d
     for (int64_t o = 0; o + t->batch <= n; o += t->batch) its.emplace_back(o, t->batch);
     if (n % t->batch) its.emplace_back(n - n % t->batch, int(n % t->batch));
     // the epoch's labels in sample order (one upload; iteration it reads [o, o + b))
-    std::vector<int64_t> ylab(static_cast<size_t>(n));
-    for (int64_t i = 0; i < n; ++i) ylab[size_t(i)] = t->labels_host[size_t(ids[size_t(i)])];
-    cuda_check(cudaMemcpyAsync(t->yb.p, ylab.data(), size_t(n) * 8, cudaMemcpyHostToDevice, t->st),
+    // (SQuAD head: per iteration the b start positions, then the b end positions)
+    const int64_t per = t->qa ? 2 : 1;
+    std::vector<int64_t> ylab(static_cast<size_t>(per * n));
+    for (const auto& itv : its)
+      for (int i = 0; i < itv.second; ++i) {
+        const int64_t sid = ids[size_t(itv.first + i)];
+        if (t->qa) {
+          ylab[size_t(2 * itv.first + i)] = t->labels_host[size_t(sid)];
+          ylab[size_t(2 * itv.first + itv.second + i)] = t->labels_host[size_t(t->dataset + sid)];
+        } else {
+          ylab[size_t(itv.first + i)] = t->labels_host[size_t(sid)];
+        }
+      }
+    cuda_check(cudaMemcpyAsync(t->yb.p, ylab.data(), ylab.size() * 8, cudaMemcpyHostToDevice,
+                               t->st),
                "labels H2D");
     const int g0 = 2 * lf, g1 = 2 * L;
     const bool split_front = cache_mode != 0;  // front work timed on its own (cache transition)
@@ -355,10 +457,19 @@ int eps_trainer_run_epoch(eps_trainer_t* t, int epoch, eps_train_epoch_t* out, d
       const int64_t o = its[it].first;
       const int b = its[it].second;
       const int64_t* bid = t->shard.p + o;
-      if (cache_mode != 1)
-        eps_check(eps_cache_gather(t->images.p, bid, b, t->image_elems * 4, t->xb.p, t->st),
-                  "image gather");
-      const int64_t* yl = t->yb.p + o;
+      if (cache_mode != 1) {
+        if (!t->bert()) {
+          eps_check(eps_cache_gather(t->images.p, bid, b, t->image_elems * 4, t->xb.p, t->st),
+                    "image gather");
+        } else {  // [2][b][T]: token ids, then segment ids
+          eps_check(eps_cache_gather(t->tok.p, bid, b, int64_t(t->tokens) * 8, t->tb.p, t->st),
+                    "token gather");
+          eps_check(eps_cache_gather(t->segs.p, bid, b, int64_t(t->tokens) * 8,
+                                     t->tb.p + int64_t(b) * t->tokens, t->st),
+                    "segment gather");
+        }
+      }
+      const int64_t* yl = t->yb.p + per * o;
       const int M = std::max(1, std::min(d.micro_batches, b));
       std::vector<int> b0s, bs;
       for (int m = 0, at = 0; m < M; ++m) {
@@ -368,30 +479,31 @@ int eps_trainer_run_epoch(eps_trainer_t* t, int epoch, eps_train_epoch_t* out, d
         at += nb;
       }
       const float* xi = cache_mode != 1 ? t->xb.p : nullptr;
+      const int64_t* ti = cache_mode != 1 ? t->tb.p : nullptr;
+      auto fwd = [&](bool with_input, int b0, int nb, int ga, int gb, int front, int cm, int co,
+                     void* store, const int64_t* sids) {
+        eps_check(t->bert() ? eps_bert_stage_forward(t->bx, with_input ? ti : nullptr, b, b0, nb,
+                                                     ga, gb, lf, front, cm, co, store, sids, t->st)
+                            : eps_vit_stage_forward(t->ex, with_input ? xi : nullptr, b0, nb, ga,
+                                                    gb, lf, front, cm, co, store, sids, t->st),
+                  "stage forward");
+      };
       for (int m = 0; m < M; ++m) {
         if (split_front) {
           const cudaEvent_t fa = mark();
-          eps_check(eps_vit_stage_forward(t->ex, xi, b0s[m], bs[m], g0, g0, lf, 1, cache_mode,
-                                          cache_old, t->store.p, bid, t->st),
-                    "stage front");
+          fwd(true, b0s[m], bs[m], g0, g0, 1, cache_mode, cache_old, t->store.p, bid);
           front.emplace_back(fa, mark());
-          eps_check(eps_vit_stage_forward(t->ex, nullptr, b0s[m], bs[m], g0, g1, lf, 0, 0, 0,
-                                          nullptr, nullptr, t->st),
-                    "stage forward");
+          fwd(false, b0s[m], bs[m], g0, g1, 0, 0, 0, nullptr, nullptr);
         } else {
-          eps_check(eps_vit_stage_forward(t->ex, xi, b0s[m], bs[m], g0, g1, lf, 1, 0, 0, nullptr,
-                                          nullptr, t->st),
-                    "stage forward");
+          fwd(true, b0s[m], bs[m], g0, g1, 1, 0, 0, nullptr, nullptr);
         }
-        eps_check(eps_vit_stage_head(t->ex, yl, b0s[m], bs[m], b, t->loss.p, t->st),
-                  "stage head");
+        t->head(yl, b0s[m], bs[m], b);
       }
       for (int m = M - 1; m >= 0; --m)
-        eps_check(eps_vit_stage_backward(t->ex, b0s[m], bs[m], g0, g1, lf, 0, t->st),
-                  "stage backward");
+        t->backward(b0s[m], bs[m], g0, g1, lf);
       if (it + 1 == its.size())
-        eps_check(eps_vit_layer_sqnorms(t->ex, lf, t->sq.p, t->st), "layer sqnorms");
-      eps_check(eps_vit_sgd(t->ex, lf, t->lr, t->momentum, 0.f, t->st), "sgd");
+        t->sqnorms(lf);
+      t->sgd(lf);
     }
     const cudaEvent_t stop = mark();
     cuda_check(cudaEventSynchronize(stop), "epoch");

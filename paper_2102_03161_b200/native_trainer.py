@@ -18,7 +18,8 @@ from . import LIB_PATH, ops
 from .capi import EpsApi, Scenario
 from .configs import Geometry
 from .trainer import EpochResult
-from .vit import geom_array
+from . import bert as _bert
+from .vit import geom_array as _vit_geom
 
 
 class CTrainEpoch(C.Structure):
@@ -32,18 +33,19 @@ class CTrainEpoch(C.Structure):
 
 
 class NativeTrainer:
-    """One-GPU PipeTransformer run with the epoch loop in C++.
+    """One-GPU PipeTransformer run with the epoch loop in C++ (ViT or BERT).
 
     init_params: fp32 flat parameters in the executor layout (CPU or CUDA
     tensor; None = the library's seeded init); images / labels: CUDA dataset
-    tensors (None = the library's seeded synthetic data)."""
+    tensors (ViT fp32 [N, C, H, W] / BERT int64 [2, N, T] token + segment ids;
+    labels int64 [N], SQuAD head [2, N]) or None for the library's seeded
+    synthetic data."""
 
     def __init__(self, scenario: dict, geometry: Geometry, *, iterations_per_epoch: int,
                  seed: int = 17, lr: float = 1e-3, momentum: float = 0.9,
                  device_norms: bool = True, init_params: Optional[torch.Tensor] = None,
                  images: Optional[torch.Tensor] = None, labels: Optional[torch.Tensor] = None):
-        if geometry.kind != "vit":
-            raise ValueError("the native trainer drives the ViT executor")
+        kind = 0 if geometry.kind == "vit" else 1
         self.api = EpsApi(LIB_PATH, "eps_")
         self.scenario = Scenario(self.api, scenario)
         self.g = geometry
@@ -51,8 +53,8 @@ class NativeTrainer:
         lib = ops.api().lib
         for n, res, args in [
                 ("eps_trainer_create", C.c_int,
-                 [C.c_void_p, C.c_void_p, C.c_int, C.c_uint64, C.c_float, C.c_float, C.c_int,
-                  C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+                 [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_uint64, C.c_float, C.c_float,
+                  C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
                 ("eps_trainer_run_epoch", C.c_int,
                  [C.c_void_p, C.c_int, C.POINTER(CTrainEpoch), C.c_void_p]),
                 ("eps_trainer_destroy", None, [C.c_void_p])]:
@@ -68,7 +70,8 @@ class NativeTrainer:
             if t is not None and not t.is_cuda:
                 raise TypeError("images / labels must be CUDA tensors")
         h = C.c_void_p()
-        rc = lib.eps_trainer_create(self.scenario.h, geom_array(geometry, batch),
+        geom = (_vit_geom if kind == 0 else _bert.geom_array)(geometry, batch)
+        rc = lib.eps_trainer_create(self.scenario.h, kind, geom,
                                     iterations_per_epoch, seed, lr, momentum, int(device_norms),
                                     hp, C.c_void_p(images.data_ptr()) if images is not None else None,
                                     C.c_void_p(labels.data_ptr()) if labels is not None else None,

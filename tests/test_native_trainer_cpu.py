@@ -20,11 +20,11 @@ def test_trainer_refuses_multi_gpu_cluster():
     lib = ops.api().lib
     f = lib.eps_trainer_create
     f.restype = C.c_int
-    f.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_uint64, C.c_float, C.c_float, C.c_int,
-                  C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+    f.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_uint64, C.c_float, C.c_float,
+                  C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
     sc = Scenario(api, configs.scenario("tiny-vit", 8))
     h = C.c_void_p()
-    rc = f(sc.h, geom_array(configs.GEOMETRIES["tiny-vit"], 64), 2, 17, 1e-3, 0.9, 1, None,
+    rc = f(sc.h, 0, geom_array(configs.GEOMETRIES["tiny-vit"], 64), 2, 17, 1e-3, 0.9, 1, None,
            None, None, C.byref(h))
     assert rc == 1 and not h.value  # EPS_EINVAL
     lib.eps_last_error.restype = C.c_char_p

@@ -87,3 +87,59 @@ def test_cli_runs_scenario_file(cuda, tmp_path):
     assert [int(x[0]) for x in rows] == [0, 1, 2, 3]
     assert all(float(x[7]) > 0 for x in rows)  # throughput
     assert "loss" in r.stderr
+
+
+# ---- BERT (configs 4 / 5 family) through the same native loop ----------------------
+def _bert_scenario(geo_name, batch=16, epochs=5, alpha=0.5):
+    g = configs.GEOMETRIES[geo_name]
+    s = configs.scenario("bert-large-128", 1)
+    s["model"] = dict(name=geo_name, bytes_per_param=4, **configs.model_spec(g))
+    s["training"]["per_pipeline_batch"] = batch
+    s["training"]["epochs"] = epochs
+    s["training"]["alpha"] = alpha
+    return s, g
+
+
+@pytest.mark.parametrize("geo_name", ["tiny-bert-qa", "tiny-bert-cls"])
+def test_native_bert_first_iteration_matches_executor(cuda, geo_name):
+    """One iteration per epoch: the native loop's epoch-0 loss is the BERT
+    executor's train_step loss on the same batch (the epoch's first shard ids:
+    token / segment gathers and the SQuAD start | end label layout line up)."""
+    from paper_2102_03161_b200 import bert
+    from paper_2102_03161_b200.capi import ClusterSpec, EpsApi
+    from paper_2102_03161_b200 import LIB_PATH
+    scen, g = _bert_scenario(geo_name, batch=16)
+    N, T = 16, g.tokens
+    gen = torch.Generator(device=cuda).manual_seed(5)
+    tok = torch.randint(0, g.vocab, (N, T), device=cuda, generator=gen)
+    seg = torch.zeros(N, T, dtype=torch.int64, device=cuda)
+    seg[:, T // 2:] = 1
+    lab = (torch.randint(0, T, (2, N), device=cuda, generator=gen) if g.head == "qa" else
+           torch.randint(0, g.classes, (N,), device=cuda, generator=gen))
+    ex = bert.BertExecutor(g, max_batch=N, seed=11)
+    p0 = ex.p32.detach().clone()
+    nat = NativeTrainer(scen, g, iterations_per_epoch=1, lr=0.05, seed=17, init_params=p0,
+                        images=torch.stack([tok, seg]).contiguous(), labels=lab.contiguous())
+    r0 = nat.run_epoch(0)
+    nat.close()
+    api = EpsApi(LIB_PATH, "eps_")
+    _, shards = api.redistribute(N, ClusterSpec(1, 1), 1, 0, 17)
+    ids = torch.tensor(shards[0], device=cuda)
+    x = torch.stack([tok[ids], seg[ids]]).contiguous()
+    y = (torch.cat([lab[0][ids], lab[1][ids]]) if g.head == "qa" else lab[ids]).contiguous()
+    loss = ex.train_step(x, y).item() / N
+    assert abs(loss - r0.mean_loss) <= 2e-3 * abs(loss), (loss, r0.mean_loss)
+
+
+@pytest.mark.parametrize("geo_name", ["tiny-bert-qa", "tiny-bert-cls"])
+def test_native_bert_device_norm_decisions(cuda, geo_name):
+    scen, g = _bert_scenario(geo_name, batch=16, epochs=5)
+    nat = NativeTrainer(scen, g, iterations_per_epoch=3, lr=0.05)
+    rows = nat.run(5)
+    nat.close()
+    st = O.FreezeState(scen["training"]["alpha"])
+    for e in range(len(rows)):
+        assert rows[e].mean_loss == rows[e].mean_loss and rows[e].throughput_sps > 0
+        assert len(rows[e].norms) == g.layers and all(n >= 0 for n in rows[e].norms)
+        if e > 0:
+            assert O.next_frozen_count(st, rows[e - 1].norms, g.layers) == rows[e].l_frozen
