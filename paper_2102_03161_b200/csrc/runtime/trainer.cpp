@@ -442,7 +442,13 @@ int eps_trainer_run_epoch(eps_trainer_t* t, int epoch, eps_train_epoch_t* out, d
                "labels H2D");
     const int g0 = 2 * lf, g1 = 2 * L;
     const bool split_front = cache_mode != 0;  // front work timed on its own (cache transition)
-    std::vector<cudaEvent_t> ev;
+    struct Events {  // destroyed on every exit path
+      std::vector<cudaEvent_t> v;
+      ~Events() {
+        for (auto e : v) cudaEventDestroy(e);
+      }
+    } events;
+    std::vector<cudaEvent_t>& ev = events.v;
     auto mark = [&]() {
       cudaEvent_t e;
       cuda_check(cudaEventCreate(&e), "event");
@@ -541,7 +547,6 @@ int eps_trainer_run_epoch(eps_trainer_t* t, int epoch, eps_train_epoch_t* out, d
       }
       cache_tr = std::max(0.0, prefix - steady);
     }
-    for (auto e : ev) cudaEventDestroy(e);
     const double epoch_s = ms / 1e3;
     out->epoch = epoch;
     out->l_frozen = lf;
