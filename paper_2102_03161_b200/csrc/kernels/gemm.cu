@@ -763,16 +763,18 @@ extern "C" int eps_gemm_bf16(int a_mn_major, int b_mn_major, int epilogue, const
   const int64_t tile_m = pair ? 2 * kBM : kBM;
   if (auto_split) {
     // wgrad: few output tiles, long contraction over token rows.  Pick the
-    // split s minimising waves(s) * (k-blocks per split + 1): one k-block of
-    // MMA is about the cost of a unit's fp32 tile reduce-add.  Each split
-    // keeps >= 4 k-blocks.
+    // split s minimising waves(s) * (k-blocks per split + 7): a unit's fixed
+    // cost (fill, drain, fp32 tile reduce-add) is ~7 k-blocks of MMA (fit of
+    // BERT-large-128 FC weight gradients, 64 pair tiles x 128 k-blocks, split
+    // 1..8: 0.0519 / 0.053 / 0.0572 / 0.0604 ms; the former "+ 1" picked 8).
+    // Each split keeps >= 4 k-blocks.
     const int64_t tiles = ((M + tile_m - 1) / tile_m) * ((N + 255) / 256);
     const int64_t sms = pair ? sm_count() / 2 : sm_count();  // concurrent tile workers
     const int cap = std::max(1, std::min(16, kblocks / 4));
     double best = 1e30;
     for (int sk = 1; sk <= cap; ++sk) {
       const double waves = double((tiles * sk + sms - 1) / sms);
-      const double cost = waves * (double(kblocks) / sk + 1.0);
+      const double cost = waves * (double(kblocks) / sk + 7.0);
       if (cost < best - 1e-12) {
         best = cost;
         split_k = sk;

@@ -53,6 +53,26 @@ LAYER18 = {
     "b18_dgrad_qkv": (R18, 768, 2304, False, True, ops.EPI_STORE_BF16, 1),
 }
 SHAPES.update(LAYER18)
+# one BERT-large-128 layer at b64 (M = 8192 token rows, d = 1024, f = 4096)
+RBL = 64 * 128
+LAYER_BL = {
+    "bbl_fwd_qkv": (RBL, 3072, 1024, False, False, ops.EPI_BIAS_BF16, 1),
+    "bbl_fwd_proj": (RBL, 1024, 1024, False, False, ops.EPI_BIAS_RESID_BF16, 1),
+    "bbl_fwd_fc1": (RBL, 4096, 1024, False, False, ops.EPI_BIAS_GELU2_BF16, 1),
+    "bbl_fwd_fc2": (RBL, 1024, 4096, False, False, ops.EPI_BIAS_RESID_BF16, 1),
+    "bbl_wgrad_fc2": (1024, 4096, RBL, True, True, ops.EPI_ACCUM_F32, 0),
+    "bbl_dgrad_fc2": (RBL, 4096, 1024, False, True, ops.EPI_MUL_BF16, 1),
+    "bbl_wgrad_fc1": (4096, 1024, RBL, True, True, ops.EPI_ACCUM_F32, 0),
+    "bbl_dgrad_fc1": (RBL, 1024, 4096, False, True, ops.EPI_STORE_BF16, 1),
+    "bbl_wgrad_proj": (1024, 1024, RBL, True, True, ops.EPI_ACCUM_F32, 0),
+    "bbl_dgrad_proj": (RBL, 1024, 1024, False, True, ops.EPI_ROWDOT_BF16, 1),
+    "bbl_wgrad_qkv": (3072, 1024, RBL, True, True, ops.EPI_ACCUM_F32, 0),
+    "bbl_dgrad_qkv": (RBL, 1024, 3072, False, True, ops.EPI_STORE_BF16, 1),
+}
+SHAPES.update(LAYER_BL)
+for _s in (1, 2, 3, 4, 6, 8):  # explicit split-K of the BERT-large FC weight gradients
+    SHAPES[f"bl_wgrad_fc2_s{_s}"] = (1024, 4096, RBL, True, True, ops.EPI_ACCUM_F32, _s)
+    SHAPES[f"bl_wgrad_fc1_s{_s}"] = (4096, 1024, RBL, True, True, ops.EPI_ACCUM_F32, _s)
 # fixed-cost probe: one b18 N = 768 tile wave at growing K (time = a + b K)
 for _k in (64, 256, 768, 1536, 3072):
     SHAPES[f"probe18_k{_k}"] = (R18, 768, _k, False, False, ops.EPI_STORE_BF16, 1)
@@ -110,7 +130,7 @@ def run(name, M, N, K, a_mn, b_mn, epi, split, iters=20):
 
 if __name__ == "__main__":
     names = sys.argv[1:] or list(SHAPES)
-    if names == ["layer18"] or names == ["layer400"]:
+    if names in (["layer18"], ["layer400"], ["layerbl"]):
         tag = names[0][5:]
         names = [k for k in SHAPES if k.startswith(f"b{tag}_")]
         tot, tot_t, fl = 0.0, 0.0, 0.0
