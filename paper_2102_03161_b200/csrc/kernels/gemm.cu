@@ -691,6 +691,16 @@ int gemm_epi_warps() {
   return ew;
 }
 
+// Utilisation-based tile width for M < 4096 (1, default; EPS_GEMM_SMALL=0
+// keeps the fixed choice, for A/B runs).
+bool gemm_small_tiles() {
+  static const bool on = [] {
+    const char* e = std::getenv("EPS_GEMM_SMALL");
+    return e == nullptr || std::atoi(e) != 0;
+  }();
+  return on;
+}
+
 std::atomic<int>& gemm_pair_mode() {
   static std::atomic<int> mode{[] {
     const char* e = std::getenv("EPS_GEMM_PAIR");
@@ -831,10 +841,49 @@ extern "C" int eps_gemm_bf16(int a_mn_major, int b_mn_major, int epilogue, const
   const bool aux_epi = epilogue == EPS_EPI_BIAS_RESID_BF16 || epilogue == EPS_EPI_DGELU_BF16 ||
                        epilogue == EPS_EPI_RESID_BF16 || epilogue == EPS_EPI_ROWDOT_BF16 ||
                        epilogue == EPS_EPI_MUL_BF16;
+  const bool ring_epi = aux_epi || epilogue == EPS_EPI_BIAS_GELU2_BF16;
+  // Few tiles (M < 4096 rows: a K = 8 pipeline micro-batch of <= 20 ViT
+  // samples; single-CTA tiles): pick the tile width that keeps the most SMs
+  // busy over whole waves -- e.g. M = 3546, N = 768: 256-wide tiles give 84
+  // tiles (57 % of the SMs), 192-wide 112 (76 %): FC1 / QKV dgrad at b18
+  // 0.0211 -> 0.0195 ms, 0.0173 -> 0.0161 ms.
+  int bn_small = 0;
+  if (split_k == 1 && M < 4096 && gemm_small_tiles()) {
+    const int64_t tm = (M + kBM - 1) / kBM;
+    const int64_t sms = sm_count();
+    double best = -1.0;
+    for (int bn : {256, 192, 128}) {
+      if (ring_epi && bn == 256) continue;  // the aux ring needs the 192 / 128 smem layout
+      if (N < bn && bn != 128) continue;
+      const int64_t tiles = tm * ((N + bn - 1) / bn);
+      const int64_t waves = (tiles + sms - 1) / sms;
+      // useful columns per wave slot (the last tile column may be partial),
+      // times the MMA efficiency of the width: a single-CTA M = 128, K = 16
+      // MMA never takes fewer than ~89 cycles (tools/mma_rate.cu), i.e. 72 %
+      // of the math rate at N = 128 (measured: 128-wide GELU2 / MUL tiles at
+      // b18 lose to 192-wide despite 91 % vs 76 % wave utilisation)
+      const double eff = std::min(1.0, (bn / 2.0) / 89.0);
+      const double util =
+          eff * double(M) * double(N) / (double(waves * sms) * double(kBM) * bn);
+      if (util > best + 0.02) {
+        best = util;
+        bn_small = bn;
+      }
+    }
+  }
+  if (bn_small == 128 && ring_epi) {
+    args.tiles_n = int((N + 127) / 128);
+    switch (key) {
+      case 0: return launch<128, 4, false, false, 8192>(A, B, lda, ldb, args, st);
+      case 1: return launch<128, 4, false, true, 8192>(A, B, lda, ldb, args, st);
+      case 2: return launch<128, 4, true, false, 8192>(A, B, lda, ldb, args, st);
+      default: return launch<128, 4, true, true, 8192>(A, B, lda, ldb, args, st);
+    }
+  }
   // Two-output GELU forward: BN = 192 leaves 8 KB per epilogue warp, i.e. two
   // 4 KB (gelu, gelu') staging slots, so a chunk's stores drain while the
   // next chunk is computed.
-  if ((aux_epi || epilogue == EPS_EPI_BIAS_GELU2_BF16) && N >= 192) {
+  if ((ring_epi && N >= 192) || bn_small == 192) {
     args.tiles_n = int((N + 191) / 192);
     switch (key) {
       case 0: return launch<192, 4, false, false, 8192>(A, B, lda, ldb, args, st);
@@ -844,7 +893,7 @@ extern "C" int eps_gemm_bf16(int a_mn_major, int b_mn_major, int epilogue, const
     }
   }
   // BN = 256 when N fills it; 128 otherwise (fewer wasted MMA columns).
-  const bool wide = N % 256 == 0 || N >= 1024;
+  const bool wide = bn_small != 0 ? bn_small == 256 : (N % 256 == 0 || N >= 1024);
   const int bn = wide ? 256 : 128;
   args.tiles_n = int((N + bn - 1) / bn);
   if (wide) {
