@@ -734,6 +734,9 @@ enum {
   EPS_TC_SQNORM = 6,
   EPS_TC_COUNT = 7
 };
+/* Weight-gradient GEMMs on a side stream beside the input-gradient chain
+ * (default on; EPS_SIDE_STREAM=0 disables the stream at creation). */
+int eps_vit_set_side_stream(eps_vit_t* h, int on);
 int eps_vit_timing_enable(eps_vit_t* h, int on);
 int eps_vit_timing_read(eps_vit_t* h, double* ms, double* flops, double* bytes, int64_t* count);
 /* ---- BERT front end / heads (csrc/kernels/bert_ops.cu) ------------------ */

@@ -19,6 +19,8 @@
 // segments and the optimizer walks one contiguous tail [layer L_f, end).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include <cmath>
 #include <cstring>
 #include <new>
@@ -190,9 +192,49 @@ struct eps_vit {
   uint16_t* dx_buf(int gs) const { return (gs == dx_g && dx_to != nullptr) ? dx_to : act.dX; }
   eps_vit(const Geometry& geom, float* p, uint16_t* pb, float* gr, float* m, uint8_t* ws)
       : g(geom), lay(geom), act(geom, lay.total, ws), p32(p), p16(pb), g32(gr), mom(m),
-        loss_sum(nullptr) {}
+        loss_sum(nullptr) {
+    if (side_stream_on()) {
+      cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking);
+      cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&join_ev, cudaEventDisableTiming);
+    }
+  }
   ~eps_vit() {
     for (cudaEvent_t e : ev_pool) cudaEventDestroy(e);
+    if (side) {
+      cudaStreamSynchronize(side);
+      cudaStreamDestroy(side);
+      cudaEventDestroy(fork_ev);
+      cudaEventDestroy(join_ev);
+    }
+  }
+
+  // ---- weight gradients on a side stream ----------------------------------------
+  // A weight-gradient GEMM only reads its inputs and accumulates into g32, so
+  // it can run beside the input-gradient chain: fork() makes the side stream
+  // wait for the main stream's work so far, join() makes the main stream wait
+  // for the side stream.  Small micro-batches (K = 8 pipeline stages) leave
+  // most SMs idle during each GEMM; the side stream fills them.
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+  static bool side_stream_on() {
+    static const bool on = [] {
+      const char* e = std::getenv("EPS_SIDE_STREAM");
+      return e == nullptr || std::atoi(e) != 0;
+    }();
+    return on;
+  }
+  bool side_on = true;  // eps_vit_set_side_stream
+  cudaStream_t fork(cudaStream_t st) {
+    if (!side || !side_on) return st;
+    cudaEventRecord(fork_ev, st);
+    cudaStreamWaitEvent(side, fork_ev, 0);
+    return side;
+  }
+  void join(cudaStream_t st) {
+    if (!side || !side_on) return;
+    cudaEventRecord(join_ev, side);
+    cudaStreamWaitEvent(st, join_ev, 0);
   }
 
   // ---- per-class launch timing (eps_vit_timing_*) ----------------------------
@@ -382,12 +424,14 @@ struct eps_vit {
     // du overwrites G (its last reader was the dW2 GEMM above)
     mm(0, 1, EPS_EPI_MUL_BF16, dX, W(s.w2), Gm, nullptr, act.U[l] + r0 * f, Gr(s.b1), R, f, d,
        d, f, f, 1, st);
+    // dW1 (reads du, H2) beside dH = du W1 and the LayerNorm backward
     mm(1, 1, EPS_EPI_ACCUM_F32, Gm, act.H2[l] + r0 * d, Gr(s.w1), nullptr, nullptr, nullptr, f,
-       d, R, f, d, d, split, st);
+       d, R, f, d, d, split, fork(st));
     mm(0, 1, EPS_EPI_STORE_BF16, Gm, W(s.w1), act.dH + r0 * d, nullptr, nullptr, nullptr, R, d,
        f, f, d, d, 1, st);
     layernorm_bwd(act.dH + r0 * d, act.X1[l] + r0 * d, s.ln2g, s.ln2b, act.mean2[l] + r0,
                   act.rstd2[l] + r0, dX, dx_buf(2 * l + 1) + r0 * d, colsum_prev, R, st);
+    join(st);  // du (G) is overwritten by the next layer's backward
   }
 
   // need_dx: write dL/dX[l] (false for the lowest trainable layer when the
@@ -397,8 +441,9 @@ struct eps_vit {
     const int64_t d = g.d, r0 = int64_t(b0) * g.tokens, R = int64_t(b) * g.tokens;
     uint16_t* dX = act.dX + r0 * d;
     const int split = 0;  // auto split-K (eps_gemm_bf16)
+    // dW_o (reads dX, A) beside dA and the attention backward
     mm(1, 1, EPS_EPI_ACCUM_F32, dX, act.A[l] + r0 * d, Gr(s.wp), nullptr, nullptr, nullptr, d, d,
-       R, d, d, d, split, st);
+       R, d, d, d, split, fork(st));
     // dA = dX1 W_o; for the fused attention backward its epilogue also forms
     // D = rowsum(dA * A) per (row, head) (EPS_EPI_ROWDOT_BF16)
     const bool rowdot = eps_attn_bwd_uses_rowdot(g.tokens, g.head_dim()) != 0;
@@ -415,10 +460,12 @@ struct eps_vit {
                                  act.dsum + int64_t(b0) * g.heads * g.tokens, b, g.tokens,
                                  g.heads, g.head_dim(), scale(), st);
     });
+    // dW_qkv (reads dQKV, H1) beside dH = dQKV W_qkv
     mm(1, 1, EPS_EPI_ACCUM_F32, act.dQKV + r0 * 3 * d, act.H1[l] + r0 * d, Gr(s.wqkv), nullptr,
-       nullptr, nullptr, 3 * d, d, R, 3 * d, d, d, split, st);
+       nullptr, nullptr, 3 * d, d, R, 3 * d, d, d, split, fork(st));
     mm(0, 1, EPS_EPI_STORE_BF16, act.dQKV + r0 * 3 * d, W(s.wqkv), act.dH + r0 * d, nullptr,
        nullptr, nullptr, R, d, 3 * d, 3 * d, d, d, 1, st);
+    join(st);  // dW_o read dX, which the LayerNorm backward rewrites in place
     layernorm_bwd(act.dH + r0 * d, act.X[l] + r0 * d, s.ln1g, s.ln1b, act.mean1[l] + r0,
                   act.rstd1[l] + r0, dX, need_dx ? dx_buf(2 * l) + r0 * d : nullptr,
                   need_dx ? colsum_prev : nullptr, R, st);
@@ -813,6 +860,12 @@ void* eps_vit_activation(eps_vit* h, int which, int layer) {
   if (which == 0 && layer >= 0 && layer <= h->g.layers) return h->act.X[layer];
   if (which == 1) return h->act.dX;
   return nullptr;
+}
+
+int eps_vit_set_side_stream(eps_vit* h, int on) {
+  if (h == nullptr) return EPS_EINVAL;
+  h->side_on = on != 0;
+  return EPS_OK;
 }
 
 int eps_vit_timing_enable(eps_vit* h, int on) {
