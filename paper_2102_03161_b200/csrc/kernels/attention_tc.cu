@@ -680,7 +680,9 @@ __device__ long long g_attn_trace[1024];
 constexpr int kDsChunk = kTile * kRowBytes;  // [128 keys][64 queries] bf16 = 16 KB
 constexpr int kBwdExpWarps = 8, kBwdEpiWarps = 4;
 // dK MMAs read dS^T from the smem staging tile (SS) instead of TMEM (TS)
-constexpr bool kBwdDkSS = false;  // measured neutral-to-slower (0.295 -> 0.297 ms, ViT-B)
+constexpr bool kBwdDkSS = false;
+// Issue the S^T / dP^T MMAs of iteration it + 2 ahead of dQ(it) (see the post issuer)
+constexpr bool kBwdSFirst = false;  // measured 0.2937 -> 0.297 ms (ViT-B), off  // measured neutral-to-slower (0.295 -> 0.297 ms, ViT-B)
 // queries of a 64-query chunk per exp warp (4 warps per TMEM lane quarter)
 constexpr int kBwdQPW = kChunk / (kBwdExpWarps / 4);
 constexpr int kBwdPasses = kBwdQPW / 16;  // 16-query passes per warp
@@ -744,7 +746,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   // tiles are reloaded as soon as their last reader is done: KV_j = rows of
   // key tile j of K and V; QO_t = rows of query tile t of Q and dO.
   //   region r: 0 = KV0, 1 = KV1, 2 = QO0, 3 = QO1   (FR + r, ER + r)
+  // SI0 / SI1: S^T / dP^T of an iteration issued (plain arrive by the S issuer)
   enum { FR = 0, ER = 4, SF0 = 8, SF1, PF0, PF1, AC0, AC1, KVF, KVE, DQF, DQE, LF0, LF1, LE0, LE1,
+         SI0, SI1,
          NBAR };
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + NBAR);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -896,6 +900,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           for (int kk = 0; kk < kD / 16; ++kk)
             tc_mma_ss_ws(tdP, vj + uint64_t(2 * kk), oc + uint64_t(2 * kk), idesc_kk, kk > 0 ? 1u : 0u);
           tc_commit_ws(&bar[SF0 + bsel]);
+          if (kBwdSFirst) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&bar[SI0 + bsel]);
+          }
           EPS_TRACE(it < 64 && lane == 0, it * 8 + 0);
         }
       }
@@ -939,6 +947,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           if (c == NC - 1) tc_commit_ws(&bar[KVF]);
           if (c & 1) {  // both halves of 128-query tile c/2 staged: dQ_t += dS_t K_j
             const int t = c >> 1;
+            // S^T / dP^T of iteration it + 2 (the next user of the TMEM buffer
+            // just released) go into the tensor pipe before these dQ MMAs,
+            // so the exp warps find them complete (same head only: the next
+            // head's first S may wait for K regions these dQ MMAs release)
+            if (kBwdSFirst && k + 2 < NIT) mbar_wait(&bar[SI0 + bsel], ((it + 2) >> 1) & 1);
             if (j == 0 && t == 0 && hi > 0) {
               mbar_wait(&bar[DQE], (hi - 1) & 1);
               tc_fence_after();
