@@ -25,6 +25,7 @@
 
 #include <cfloat>
 #include <cstdlib>
+#include <string>
 #include <unordered_map>
 
 #include "eps_capi.h"
@@ -721,56 +722,76 @@ __device__ __forceinline__ void zero32(uint32_t (&pk)[32]) {
 }
 
 
-template <int NT>
+// UNIT (256 < T <= 384, NT = 3): a work unit is one (head, key tile): the
+// unit's K / V tile plus the head's whole Q / dO sit in smem (a head's four
+// 384-row operands do not fit), dV / dK of the tile accumulate as above, and
+// each 128-query tile's dQ partial (dS_t K_j over this key tile) is read out
+// as soon as its two chunks are done -- two TMEM dQ buffers in turn -- and
+// stored in bf16 into slice j of a partial buffer (map_dqp, [NT*B][T][HD]);
+// attn_dq_reduce_kernel sums the slices into dQ and its bias column sums.
+template <int NT, bool UNIT = false>
 __global__ void __launch_bounds__(kBwdThreads, 1)
     attn_bwd_fused_tc_kernel(const __grid_constant__ CUtensorMap map_qkv,
                              const __grid_constant__ CUtensorMap map_do,
-                             const __grid_constant__ CUtensorMap map_dq, const Params p,
+                             const __grid_constant__ CUtensorMap map_dq,
+                             const __grid_constant__ CUtensorMap map_dqp, const Params p,
                              int n_heads) {
-  constexpr int Tr = NT * kTile;   // rows loaded per operand (zero-filled past T)
-  constexpr int NC = Tr / kChunk;  // 64-query chunks per key tile (2 or 4)
-  constexpr int LNC = NC == 2 ? 1 : 2;
-  constexpr int NIT = NT * NC;     // iterations per head (2 or 8, even)
+  constexpr int Tr = NT * kTile;   // Q / dO rows loaded (zero-filled past T)
+  constexpr int NK = UNIT ? 1 : NT;  // key tiles per work unit
+  constexpr int KR = NK * kTile;   // K / V rows loaded
+  constexpr int NC = Tr / kChunk;  // 64-query chunks per key tile (2, 4 or 6)
+  constexpr int NIT = NK * NC;     // iterations per unit (2, 8 or 6, even)
+  constexpr int NU = UNIT ? NT : 1;  // units per head
+  constexpr int NR = NK + NT;      // operand regions
+  static_assert(NR <= 4 && NIT % 2 == 0, "regions / iterations");
+  const int n_units = n_heads * NU;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   uint8_t* sQ = smem;
   uint8_t* sO = sQ + Tr * kRowBytes;  // dO
   uint8_t* sK = sO + Tr * kRowBytes;
-  uint8_t* sV = sK + Tr * kRowBytes;
-  uint8_t* sS = sV + Tr * kRowBytes;  // dS staging: 2 buffers x 2 chunks x 16 KB
+  uint8_t* sV = sK + KR * kRowBytes;
+  uint8_t* sS = sV + KR * kRowBytes;  // dS staging: 2 buffers x 2 chunks x 16 KB
   uint8_t* sStage = sS + 4 * kDsChunk;  // epilogue: one 128x64 bf16 output tile
   float2* sLD = reinterpret_cast<float2*>(sStage + kDsChunk);  // [2][Tr] (-lse2, D)
   float* sRed = reinterpret_cast<float*>(sLD + 2 * Tr);  // [64] bias column sums of a head
   uint64_t* bar = reinterpret_cast<uint64_t*>(sRed + 64);
-  // Operand regions, each with its own full / empty barrier pair so a head's
+  // Operand regions, each with its own full / empty barrier pair so a unit's
   // tiles are reloaded as soon as their last reader is done: KV_j = rows of
   // key tile j of K and V; QO_t = rows of query tile t of Q and dO.
-  //   region r: 0 = KV0, 1 = KV1, 2 = QO0, 3 = QO1   (FR + r, ER + r)
-  // SI0 / SI1: S^T / dP^T of an iteration issued (plain arrive by the S issuer)
+  //   whole head: 0 = KV0, 1 = KV1, 2 = QO0, 3 = QO1;  UNIT: 0 = KV, 1 + t = QO_t
+  // SI0 / SI1: S^T / dP^T of an iteration issued (plain arrive by the S issuer);
+  // UNIT: DQF / DQE (buffer 0) and DQF1 / DQE1 (buffer 1) per dQ tile
   enum { FR = 0, ER = 4, SF0 = 8, SF1, PF0, PF1, AC0, AC1, KVF, KVE, DQF, DQE, LF0, LF1, LE0, LE1,
-         SI0, SI1,
+         SI0, SI1, DQF1, DQE1,
          NBAR };
+  auto kv_region = [](int j) { return j; };
+  auto qo_region = [](int t) { return UNIT ? 1 + t : 2 + t; };
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + NBAR);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int HD = p.H * kD;
-  // last iteration of a head that reads region r: KV_j is read by S (key
+  // last iteration of a unit that reads region r: KV_j is read by S (key
   // tile j) and by the dQ MMAs of its odd chunks; QO_t by the S and post MMAs
-  // of chunks 2t, 2t+1 of the last key tile
+  // of chunks 2t, 2t+1 of the last key tile; -1: region unused
   auto last_use = [](int r) {
-    return r < 2 ? r * NC + NC - 1 : (NT - 1) * NC + 2 * (r - 2) + 1;
+    if (UNIT) return r == 0 ? NC - 1 : r <= NT ? 2 * (r - 1) + 1 : -1;
+    if (r < 2) return r < NT ? r * NC + NC - 1 : -1;
+    return r - 2 < NT ? (NT - 1) * NC + 2 * (r - 2) + 1 : -1;
   };
 
   if (threadIdx.x == 0) {
     tma_prefetch(&map_qkv);
     tma_prefetch(&map_do);
     tma_prefetch(&map_dq);
+    if (UNIT) tma_prefetch(&map_dqp);
     for (int i = 0; i < NBAR; ++i) {
       uint32_t cnt = 1;
       if (i == PF0 || i == PF1) cnt = kBwdExpWarps;
-      if (i == KVE || i == DQE) cnt = kBwdEpiWarps;
+      if (i == KVE || i == DQE || i == DQE1) cnt = kBwdEpiWarps;
       if (i == LF0 || i == LF1) cnt = 32 * kBwdEpiWarps;
       if (i == LE0 || i == LE1) cnt = 32 * kBwdExpWarps;
-      if (i == ER + 2 || i == ER + 3) cnt = 2;  // post issuer's commit + the TMA warp's dO sums
+      for (int t = 0; t < NT; ++t)
+        if (i == ER + qo_region(t)) cnt = 2;  // post issuer's commit + the TMA warp's dO sums
       mbar_init(&bar[i], cnt);
     }
     mbar_fence_init();
@@ -787,21 +808,28 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 
   if (warp == 0) {
     int hi = 0;
-    for (int bh = blockIdx.x; bh < n_heads; bh += gridDim.x, ++hi) {
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++hi) {
+      const int bh = u / NU, jb = u % NU;  // head, key-tile block of the unit
       const int b = bh / p.H, h = bh % p.H;
-      // regions in the order the previous head releases them: KV0, QO0, KV1, QO1
-      const int order[4] = {0, 2, 1, 3};
-      for (int oi = 0; oi < 2 * NT; ++oi) {
-        const int r = order[oi];  // NT == 1: KV0, QO0
-        const int t = r & 1;  // key tile (KV) or query tile (QO)
+      // regions in the order the previous unit releases them (whole head:
+      // KV0, QO0, KV1, QO1; UNIT: QO0, QO1, KV, QO2)
+      int order[4] = {0, 0, 0, 0}, n_ord = 0;
+      for (int lu = 0; lu < NIT; ++lu)
+        for (int r = 0; r < 4; ++r)
+          if (last_use(r) == lu) order[n_ord++] = r;
+      for (int oi = 0; oi < n_ord; ++oi) {
+        const int r = order[oi];
+        const bool kv = UNIT ? r == 0 : r < 2;
+        const int t = kv ? r : r - qo_region(0);  // key tile (KV) or query tile (QO)
         mbar_wait(&bar[ER + r], (hi & 1) ^ 1);
         if (lane == 0) {
           mbar_expect_tx(&bar[FR + r], uint32_t(2 * kTile * kRowBytes));
-          if (r < 2) {
-            load_rows(sK + t * kTile * kRowBytes, &map_qkv, &bar[FR + r], HD + h * kD, t * kTile,
+          if (kv) {
+            const int kr = (jb * NK + t) * kTile;  // global key row
+            load_rows(sK + t * kTile * kRowBytes, &map_qkv, &bar[FR + r], HD + h * kD, kr,
                       kTile, b);
-            load_rows(sV + t * kTile * kRowBytes, &map_qkv, &bar[FR + r], 2 * HD + h * kD,
-                      t * kTile, kTile, b);
+            load_rows(sV + t * kTile * kRowBytes, &map_qkv, &bar[FR + r], 2 * HD + h * kD, kr,
+                      kTile, b);
           } else {
             load_rows(sQ + t * kTile * kRowBytes, &map_qkv, &bar[FR + r], h * kD, t * kTile,
                       kTile, b);
@@ -810,7 +838,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           }
         }
       }
-      if (lane == 0) {
+      if (lane == 0 && !UNIT) {
         // warm L2 with the next head's tiles
         const int nb = bh + gridDim.x;
         if (nb < n_heads) {
@@ -832,9 +860,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       // query), so no K column sums are formed.
       float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
       const int g = lane & 7, rs = lane >> 3;  // 16-byte column group, row set
+      // (UNIT: the head's first key-tile unit forms the sums)
+      const bool vsum = p.dbias != nullptr && (!UNIT || jb == 0);
       for (int t = 0; t < NT; ++t) {
-        mbar_wait(&bar[FR + 2 + t], hi & 1);
-        if (p.dbias != nullptr) {
+        mbar_wait(&bar[FR + qo_region(t)], hi & 1);
+        if (vsum) {
           const uint32_t o_s = smem_addr(sO);
 #pragma unroll 4
           for (int r = t * kTile + rs * 32; r < t * kTile + rs * 32 + 32; ++r) {
@@ -845,9 +875,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           }
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&bar[ER + 2 + t]);
+        if (lane == 0) mbar_arrive(&bar[ER + qo_region(t)]);
       }
-      if (p.dbias != nullptr) {
+      if (vsum) {
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], 8);
@@ -879,12 +909,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const uint64_t dK0 = umma_sdesc(smem_addr(sK), 16, 1024);
       const uint64_t dV0 = umma_sdesc(smem_addr(sV), 16, 1024);
       int hi = 0;
-      for (int bh = blockIdx.x; bh < n_heads; bh += gridDim.x, ++hi) {
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++hi) {
         const int it0 = hi * NIT;
         for (int k = 0; k < NIT; ++k) {
-          const int it = it0 + k, bsel = k & 1, j = k >> LNC, c = k & (NC - 1);
-          mbar_wait(&bar[FR + j], hi & 1);             // K_j, V_j of this head
-          mbar_wait(&bar[FR + 2 + (c >> 1)], hi & 1);  // Q, dO rows of chunk c
+          const int it = it0 + k, bsel = k & 1, j = k / NC, c = k % NC;
+          mbar_wait(&bar[FR + kv_region(j)], hi & 1);       // K_j, V_j of this unit
+          mbar_wait(&bar[FR + qo_region(c >> 1)], hi & 1);  // Q, dO rows of chunk c
           if (k == 0) EPS_TRACE(hi < 16 && lane == 0, 640 + hi * 4 + 2);
           if (it >= 2) {  // post(it - 2) finished reading this S^T / dP^T buffer
             mbar_wait(&bar[AC0 + bsel], ((it >> 1) - 1) & 1);
@@ -913,9 +943,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const uint64_t mK0 = umma_sdesc(smem_addr(sK), 64 * 128, 1024);
       const uint64_t mS0 = umma_sdesc(smem_addr(sS), kDsChunk, 1024);
       int kt = 0, hi = 0;
-      for (int bh = blockIdx.x; bh < n_heads; bh += gridDim.x, ++hi) {
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++hi) {
         for (int k = 0; k < NIT; ++k) {
-          const int it = hi * NIT + k, bsel = k & 1, j = k >> LNC, c = k & (NC - 1);
+          const int it = hi * NIT + k, bsel = k & 1, j = k / NC, c = k % NC;
           mbar_wait(&bar[PF0 + bsel], (it >> 1) & 1);
           tc_fence_after();
           EPS_TRACE(it < 64 && lane == 0, it * 8 + 1);
@@ -952,25 +982,33 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             // so the exp warps find them complete (same head only: the next
             // head's first S may wait for K regions these dQ MMAs release)
             if (kBwdSFirst && k + 2 < NIT) mbar_wait(&bar[SI0 + bsel], ((it + 2) >> 1) & 1);
-            if (j == 0 && t == 0 && hi > 0) {
+            const int g = hi * NT + t;  // UNIT: dQ tile counter -> buffer g & 1
+            if (UNIT) {
+              if (g >= 2) {  // the epilogue read out buffer g & 1's previous tile
+                mbar_wait(&bar[(g & 1) ? DQE1 : DQE], ((g >> 1) - 1) & 1);
+                tc_fence_after();
+              }
+            } else if (j == 0 && t == 0 && hi > 0) {
               mbar_wait(&bar[DQE], (hi - 1) & 1);
               tc_fence_after();
             }
             const uint64_t stg = mS0 + uint64_t(((it >> 1) & 1) * 2 * (kDsChunk >> 4));
             const uint64_t kj = mK0 + uint64_t(j * kTile * 8);
+            const uint32_t tq = tdQ + uint32_t((UNIT ? (g & 1) : t) * kD);
 #pragma unroll
             for (int kk = 0; kk < kTile / 16; ++kk)
-              tc_mma_ss_ws(tdQ + uint32_t(t * kD), stg + uint64_t(kk * 128), kj + uint64_t(kk * 128),
-                           idesc_mm, (j > 0 || kk > 0) ? 1u : 0u);
+              tc_mma_ss_ws(tq, stg + uint64_t(kk * 128), kj + uint64_t(kk * 128), idesc_mm,
+                           ((!UNIT && j > 0) || kk > 0) ? 1u : 0u);
+            if (UNIT) tc_commit_ws(&bar[(g & 1) ? DQF1 : DQF]);
           }
           EPS_TRACE(it < 64 && lane == 0, it * 8 + 2);
           if (c == NC - 1) ++kt;
           // operand regions whose last reader this was (tracks the dQ MMAs too)
 #pragma unroll
           for (int r = 0; r < 4; ++r)
-            if ((r & 1) < NT && last_use(r) == k) tc_commit_ws(&bar[ER + r]);
+            if (last_use(r) == k) tc_commit_ws(&bar[ER + r]);
         }
-        tc_commit_ws(&bar[DQF]);
+        if (!UNIT) tc_commit_ws(&bar[DQF]);
       }
     }
   } else if (warp < 2 + kBwdExpWarps) {
@@ -985,15 +1023,16 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const int row = quarter * 32 + lane;
     const float sl2 = p.scale_log2;
     int hi = 0;
-    for (int bh = blockIdx.x; bh < n_heads; bh += gridDim.x, ++hi) {
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++hi) {
+      const int jb = u % NU;
       const int lb = hi & 1;
       mbar_wait(&bar[LF0 + lb], (hi >> 1) & 1);
       EPS_TRACE(hi < 16 && warp == 2 && lane == 0, 640 + hi * 4 + 3);
       const uint32_t ld = smem_addr(sLD + lb * Tr);
 #pragma unroll 1
       for (int k = 0; k < NIT; ++k) {
-        const int it = hi * NIT + k, bsel = k & 1, j = k >> LNC, c = k & (NC - 1);
-        const int kbase = j * kTile + quarter * 32;  // this warp's 32 keys
+        const int it = hi * NIT + k, bsel = k & 1, j = k / NC, c = k % NC;
+        const int kbase = (jb * NK + j) * kTile + quarter * 32;  // this warp's 32 keys
         const int q0 = c * kChunk + sub * kBwdQPW;
         mbar_wait(&bar[SF0 + bsel], (it >> 1) & 1);
         tc_fence_after();
@@ -1101,7 +1140,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     // (coalesced, asynchronous); `te == 0` owns the bulk groups.
     const uint32_t stage_s = smem_addr(sStage);
     auto epi_sync = [] { asm volatile("bar.sync 1, 128;" ::: "memory"); };
-    auto store_tile = [&](const uint32_t (&pk)[32], int col, int row0, int b) {
+    auto store_tile_to = [&](const CUtensorMap* map, const uint32_t (&pk)[32], int col, int row0,
+                             int z) {
       if (te == 0) bulk_wait_read<0>();  // previous tile read out of the staging buffer
       epi_sync();
 #pragma unroll
@@ -1110,15 +1150,46 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       fence_proxy_async_smem();
       epi_sync();
       if (te == 0) {
-        tma_store_3d(&map_dq, sStage, col, row0, b);
-        tma_store_3d(&map_dq, sStage + 64 * kRowBytes, col, row0 + 64, b);
+        tma_store_3d(map, sStage, col, row0, z);
+        tma_store_3d(map, sStage + 64 * kRowBytes, col, row0 + 64, z);
         bulk_commit();
       }
     };
+    auto store_tile = [&](const uint32_t (&pk)[32], int col, int row0, int b) {
+      store_tile_to(&map_dq, pk, col, row0, b);
+    };
     int hi = 0, kt = 0;
-    if (int(blockIdx.x) < n_heads) fill_table(blockIdx.x, 0);
-    for (int bh = blockIdx.x; bh < n_heads; bh += gridDim.x, ++hi) {
+    if (int(blockIdx.x) < n_units) fill_table(int(blockIdx.x) / NU, 0);
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++hi) {
+      const int bh = u / NU, jb = u % NU;
       const int b = bh / p.H, h = bh % p.H;
+      if constexpr (UNIT) {
+        // dQ partials of the unit's key tile, one 128-query tile at a time
+        for (int t = 0; t < NT; ++t) {
+          const int g = hi * NT + t;
+          mbar_wait(&bar[(g & 1) ? DQF1 : DQF], (g >> 1) & 1);
+          tc_fence_after();
+          uint32_t pq[32];
+          load_tmem_packed64(tdQ + uint32_t((g & 1) * kD) + lane_off, p.scale, pq);
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&bar[(g & 1) ? DQE1 : DQE]);
+          store_tile_to(&map_dqp, pq, h * kD, t * kTile, jb * (n_heads / p.H) + b);
+          if (t == 0 && u + int(gridDim.x) < n_units) fill_table((u + int(gridDim.x)) / NU, hi + 1);
+        }
+        mbar_wait(&bar[KVF], kt & 1);
+        tc_fence_after();
+        uint32_t pv[32], pk[32];
+        load_tmem_packed64(tdV + lane_off, 1.f, pv);
+        load_tmem_packed64(tdK + lane_off, p.scale, pk);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bar[KVE]);
+        store_tile(pv, 2 * HD + h * kD, jb * kTile, b);
+        store_tile(pk, HD + h * kD, jb * kTile, b);
+        ++kt;
+        continue;
+      }
       // TMEM is read out and released first (the MMA warp is waiting for
       // it); stores work from the packed registers.
       for (int j = 0; j < NT; ++j, ++kt) {
@@ -1137,20 +1208,20 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         EPS_TRACE(hi < 16 && j == 0 && warp == 2 + kBwdExpWarps && lane == 0, 760 + hi * 4 + 2);
         // the next head's table, off the key-tile hand-off path (its exp work
         // starts only after this head's remaining iterations)
-        if (j == 0 && bh + int(gridDim.x) < n_heads) fill_table(bh + gridDim.x, hi + 1);
+        if (j == 0 && u + int(gridDim.x) < n_units) fill_table(u + int(gridDim.x), hi + 1);
       }
       mbar_wait(&bar[DQF], hi & 1);
       tc_fence_after();
       EPS_TRACE(hi < 16 && warp == 2 + kBwdExpWarps && lane == 0, 640 + hi * 4);
-      uint32_t pq[NT][32];
+      uint32_t pq[UNIT ? 1 : NT][32];
 #pragma unroll
-      for (int t = 0; t < NT; ++t) load_tmem_packed64(tdQ + uint32_t(t * kD) + lane_off, p.scale, pq[t]);
+      for (int t = 0; t < (UNIT ? 1 : NT); ++t) load_tmem_packed64(tdQ + uint32_t(t * kD) + lane_off, p.scale, pq[t]);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bar[DQE]);
       EPS_TRACE(hi < 16 && warp == 2 + kBwdExpWarps && lane == 0, 640 + hi * 4 + 1);
 #pragma unroll
-      for (int t = 0; t < NT; ++t) {
+      for (int t = 0; t < (UNIT ? 1 : NT); ++t) {
         if (t * kTile + row >= p.T) zero32(pq[t]);
         store_tile(pq[t], h * kD, t * kTile, b);
       }
@@ -1161,7 +1232,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           u[2 * d] = bf16_lo(pq[0][d]);
           u[2 * d + 1] = bf16_hi(pq[0][d]);
 #pragma unroll
-          for (int t = 1; t < NT; ++t) u[2 * d] += bf16_lo(pq[t][d]), u[2 * d + 1] += bf16_hi(pq[t][d]);
+          for (int t = 1; t < (UNIT ? 1 : NT); ++t) u[2 * d] += bf16_lo(pq[t][d]), u[2 * d + 1] += bf16_hi(pq[t][d]);
         }
 #pragma unroll
         for (int half = 0; half < 2; ++half) {
@@ -1191,7 +1262,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 
 size_t bwd_fused_smem(int T) {
   const int Tr = (T + kTile - 1) / kTile * kTile;
-  return size_t(4 * Tr) * kRowBytes + 5 * size_t(kDsChunk) + size_t(2 * Tr) * 8 + 256 + 1024 + 256;
+  const int KR = Tr > 2 * kTile ? kTile : Tr;  // UNIT (T > 256): one key tile per unit
+  return size_t(2 * Tr + 2 * KR) * kRowBytes + 5 * size_t(kDsChunk) + size_t(2 * Tr) * 8 + 256 +
+         1024 + 256;
 }
 
 // ---------------------------------------------------------------------------
@@ -2003,8 +2076,70 @@ __global__ void attn_rowdot_kernel(const uint16_t* __restrict__ out,
 }
 
 
+// dQ = sum over the key-tile slices of the UNIT kernel's bf16 partials,
+// rounded to bf16 into dqkv's Q columns, plus the Q bias column sums (of the
+// rounded values).  A thread owns one 8-column vector of a row; the block
+// (192 threads = 2 rows of 96 vectors at HD = 768) strides over rows, so each
+// thread's column sums stay in registers until one block reduction.
+__global__ void attn_dq_reduce_kernel(const uint16_t* __restrict__ part, int64_t slice, int nslices,
+                                      uint16_t* __restrict__ dq, int64_t ld_out, int64_t rows,
+                                      int HD, float* __restrict__ dbias) {
+  extern __shared__ float red[];  // [blockDim.x / nv][HD]
+  const int nv = HD / 8;
+  const int v = threadIdx.x % nv, rsub = threadIdx.x / nv, rper = blockDim.x / nv;
+  float cs[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+  for (int64_t r = int64_t(blockIdx.x) * rper + rsub; r < rows; r += int64_t(gridDim.x) * rper) {
+    float a[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int s = 0; s < nslices; ++s) {
+      const uint4 w = __ldg(reinterpret_cast<const uint4*>(part + s * slice + r * HD) + v);
+      a[0] += bf16_lo(w.x), a[1] += bf16_hi(w.x), a[2] += bf16_lo(w.y), a[3] += bf16_hi(w.y);
+      a[4] += bf16_lo(w.z), a[5] += bf16_hi(w.z), a[6] += bf16_lo(w.w), a[7] += bf16_hi(w.w);
+    }
+    const uint4 o = make_uint4(pack_bf16(a[0], a[1]), pack_bf16(a[2], a[3]), pack_bf16(a[4], a[5]),
+                               pack_bf16(a[6], a[7]));
+    *(reinterpret_cast<uint4*>(dq + r * ld_out) + v) = o;
+    cs[0] += bf16_lo(o.x), cs[1] += bf16_hi(o.x), cs[2] += bf16_lo(o.y), cs[3] += bf16_hi(o.y);
+    cs[4] += bf16_lo(o.z), cs[5] += bf16_hi(o.z), cs[6] += bf16_lo(o.w), cs[7] += bf16_hi(o.w);
+  }
+  if (dbias == nullptr) return;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) red[rsub * HD + v * 8 + i] = cs[i];
+  __syncthreads();
+  for (int c = threadIdx.x; c < HD; c += blockDim.x) {
+    float t = 0.f;
+    for (int q = 0; q < rper; ++q) t += red[q * HD + c];
+    atomicAdd(dbias + c, t);
+  }
+}
+
+// grow-only device scratch for the UNIT kernel's dQ partials
+static void* dq_partial_scratch(size_t bytes) {
+  static void* buf = nullptr;
+  static size_t have = 0;
+  if (bytes > have) {
+    if (buf != nullptr) cudaFree(buf);
+    buf = nullptr;
+    have = 0;
+    if (cudaMalloc(&buf, bytes) != cudaSuccess) return nullptr;
+    have = bytes;
+  }
+  return buf;
+}
+
+// The fused backward (one kernel; D = rowsum(dO * O) precomputed) covers
+// T <= 384: whole heads for T <= 256, (head, key tile) units above.
+// EPS_ATTN_BWD=split selects the round-1 two-kernel path for 256 < T <= 384.
+static bool bwd_unit_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("EPS_ATTN_BWD");
+    return e == nullptr || std::string(e) != "split";
+  }();
+  return on;
+}
+
 bool attn_bwd_fused_supported(int T, int head_dim) {
-  return head_dim == 64 && T >= 1 && T <= 2 * attn_tc::kTile;
+  return head_dim == 64 && T >= 1 &&
+         T <= (bwd_unit_on() ? 3 * attn_tc::kTile : 2 * attn_tc::kTile);
 }
 
 // drow: precomputed D [B*T, H] (fused path) or nullptr (computed here into
@@ -2031,7 +2166,7 @@ int attn_bwd_tc(const void* qkv, const void* out, const void* dout, const float*
   p.dsum = dsum;
   p.dqkv = static_cast<uint16_t*>(dqkv);
   p.dbias = dbias;
-  if (T <= 2 * kTile) {
+  if (attn_bwd_fused_supported(T, kD)) {
     if (drow == nullptr) {
       const int64_t rows = int64_t(B) * T;
       count_launch();
@@ -2046,11 +2181,33 @@ int attn_bwd_tc(const void* qkv, const void* out, const void* dout, const float*
       return EPS_ECUDA;
     const size_t sf = bwd_fused_smem(T);
     const int heads = B * H;
+    if (T > 2 * kTile) {  // (head, key tile) units + the dQ slice reduction
+      const int64_t R = int64_t(B) * T;
+      uint16_t* part = static_cast<uint16_t*>(dq_partial_scratch(size_t(3 * R * WO) * 2));
+      if (part == nullptr) return EPS_ECUDA;
+      CUtensorMap mdqp;
+      if (!make_map_3d(&mdqp, part, WO, T, 3 * B, WO, int64_t(T) * WO, kD, kChunk,
+                       CU_TENSOR_MAP_SWIZZLE_128B))
+        return EPS_ECUDA;
+      auto kern = attn_bwd_fused_tc_kernel<3, true>;
+      if (!ensure_smem(kern, sf)) return EPS_ECUDA;
+      const int units = 3 * heads;
+      const int grid = units < sm_count() ? units : sm_count();
+      count_launch();
+      if (launch_k(kern, dim3(grid), dim3(kBwdThreads), sf, st, 1, mq, mo, mdq, mdqp, p, heads) !=
+          cudaSuccess)
+        return EPS_ECUDA;
+      const int threads = int(2 * (WO / 8));  // two rows per block iteration
+      count_launch();
+      attn_dq_reduce_kernel<<<sm_count() * 2, threads, size_t(2 * WO) * 4, st>>>(
+          part, R * WO, 3, static_cast<uint16_t*>(dqkv), W, R, int(WO), dbias);
+      return cudaGetLastError() == cudaSuccess ? EPS_OK : EPS_ECUDA;
+    }
     const int grid = heads < sm_count() ? heads : sm_count();
     auto kern = T <= kTile ? attn_bwd_fused_tc_kernel<1> : attn_bwd_fused_tc_kernel<2>;
     if (!ensure_smem(kern, sf)) return EPS_ECUDA;
     count_launch();
-    if (launch_k(kern, dim3(grid), dim3(kBwdThreads), sf, st, 1, mq, mo, mdq, p, heads) !=
+    if (launch_k(kern, dim3(grid), dim3(kBwdThreads), sf, st, 1, mq, mo, mdq, mdq, p, heads) !=
         cudaSuccess)
       return EPS_ECUDA;
     return cudaGetLastError() == cudaSuccess ? EPS_OK : EPS_ECUDA;

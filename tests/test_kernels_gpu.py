@@ -100,7 +100,10 @@ def _attn_ref(qkv, B, T, H, dh):
                                       (1, 384, 12, 64), (2, 50, 2, 64), (30, 197, 12, 64),
                                       (64, 128, 16, 64), (3, 256, 4, 64), (7, 129, 3, 64),
                                       (5, 1, 2, 64), (1, 255, 1, 64), (300, 197, 1, 64),
-                                      (40, 64, 8, 64)])
+                                      (40, 64, 8, 64),
+                                      # 256 < T <= 384: (head, key tile) units, several per
+                                      # CTA, ragged last key / query tile, dQ slice reduce
+                                      (8, 384, 12, 64), (3, 300, 4, 64), (2, 257, 3, 64)])
 def test_attention_fwd_bwd(cuda, B, T, H, dh):
     g = torch.Generator(device=cuda).manual_seed(T * H)
     D = H * dh
