@@ -729,7 +729,11 @@ __device__ __forceinline__ void zero32(uint32_t (&pk)[32]) {
 // as soon as its two chunks are done -- two TMEM dQ buffers in turn -- and
 // stored in bf16 into slice j of a partial buffer (map_dqp, [NT*B][T][HD]);
 // attn_dq_reduce_kernel sums the slices into dQ and its bias column sums.
-template <int NT, bool UNIT = false>
+// PH (T <= 128, NT = 2): a work unit is a PAIR of heads laid out as one
+// 256-row problem: key tile j and query tile t are heads 2u + j / 2u + t, and
+// only the diagonal (j = t) iterations run -- four per unit instead of two per
+// head, so the per-unit fill / drain is paid half as often.
+template <int NT, bool UNIT = false, bool PH = false>
 __global__ void __launch_bounds__(kBwdThreads, 1)
     attn_bwd_fused_tc_kernel(const __grid_constant__ CUtensorMap map_qkv,
                              const __grid_constant__ CUtensorMap map_do,
@@ -740,11 +744,24 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   constexpr int NK = UNIT ? 1 : NT;  // key tiles per work unit
   constexpr int KR = NK * kTile;   // K / V rows loaded
   constexpr int NC = Tr / kChunk;  // 64-query chunks per key tile (2, 4 or 6)
-  constexpr int NIT = NK * NC;     // iterations per unit (2, 8 or 6, even)
+  constexpr int NIT = PH ? NC : NK * NC;  // iterations per unit (2, 8, 6; PH: 4)
   constexpr int NU = UNIT ? NT : 1;  // units per head
   constexpr int NR = NK + NT;      // operand regions
   static_assert(NR <= 4 && NIT % 2 == 0, "regions / iterations");
-  const int n_units = n_heads * NU;
+  const int n_units = PH ? n_heads / 2 : n_heads * NU;
+  static_assert(!PH || (NT == 2 && !UNIT), "paired heads: NT = 2 layout");
+  // iteration k of a unit -> (key tile j, query chunk c); PH: diagonal only
+  auto jc = [](int k, int& j, int& c) {
+    if (PH) {
+      j = k >> 1;
+      c = 2 * j + (k & 1);
+    } else {
+      j = k / NC;
+      c = k % NC;
+    }
+  };
+  // PH: global (b, h) of tile x of unit u (head 2u + x); else of the unit's head
+  auto head_of = [&](int u, int x) { return PH ? 2 * u + x : u / NU; };
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   uint8_t* sQ = smem;
@@ -774,6 +791,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   // tile j) and by the dQ MMAs of its odd chunks; QO_t by the S and post MMAs
   // of chunks 2t, 2t+1 of the last key tile; -1: region unused
   auto last_use = [](int r) {
+    if (PH) return r < 2 ? 2 * r + 1 : 2 * (r - 2) + 1;
     if (UNIT) return r == 0 ? NC - 1 : r <= NT ? 2 * (r - 1) + 1 : -1;
     if (r < 2) return r < NT ? r * NC + NC - 1 : -1;
     return r - 2 < NT ? (NT - 1) * NC + 2 * (r - 2) + 1 : -1;
@@ -809,7 +827,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   if (warp == 0) {
     int hi = 0;
     for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++hi) {
-      const int bh = u / NU, jb = u % NU;  // head, key-tile block of the unit
+      const int bh = head_of(u, 0), jb = u % NU;  // head, key-tile block of the unit
       const int b = bh / p.H, h = bh % p.H;
       // regions in the order the previous unit releases them (whole head:
       // KV0, QO0, KV1, QO1; UNIT: QO0, QO1, KV, QO2)
@@ -824,21 +842,23 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         mbar_wait(&bar[ER + r], (hi & 1) ^ 1);
         if (lane == 0) {
           mbar_expect_tx(&bar[FR + r], uint32_t(2 * kTile * kRowBytes));
+          // PH: tile t is head 2u + t, rows 0..127 of that head
+          const int bt = PH ? head_of(u, t) / p.H : b, ht = PH ? head_of(u, t) % p.H : h;
           if (kv) {
-            const int kr = (jb * NK + t) * kTile;  // global key row
-            load_rows(sK + t * kTile * kRowBytes, &map_qkv, &bar[FR + r], HD + h * kD, kr,
-                      kTile, b);
-            load_rows(sV + t * kTile * kRowBytes, &map_qkv, &bar[FR + r], 2 * HD + h * kD, kr,
-                      kTile, b);
+            const int kr = PH ? 0 : (jb * NK + t) * kTile;  // global key row
+            load_rows(sK + t * kTile * kRowBytes, &map_qkv, &bar[FR + r], HD + ht * kD, kr,
+                      kTile, bt);
+            load_rows(sV + t * kTile * kRowBytes, &map_qkv, &bar[FR + r], 2 * HD + ht * kD, kr,
+                      kTile, bt);
           } else {
-            load_rows(sQ + t * kTile * kRowBytes, &map_qkv, &bar[FR + r], h * kD, t * kTile,
-                      kTile, b);
-            load_rows(sO + t * kTile * kRowBytes, &map_do, &bar[FR + r], h * kD, t * kTile, kTile,
-                      b);
+            load_rows(sQ + t * kTile * kRowBytes, &map_qkv, &bar[FR + r], ht * kD,
+                      PH ? 0 : t * kTile, kTile, bt);
+            load_rows(sO + t * kTile * kRowBytes, &map_do, &bar[FR + r], ht * kD,
+                      PH ? 0 : t * kTile, kTile, bt);
           }
         }
       }
-      if (lane == 0 && !UNIT) {
+      if (lane == 0 && !UNIT && !PH) {
         // warm L2 with the next head's tiles
         const int nb = bh + gridDim.x;
         if (nb < n_heads) {
@@ -876,8 +896,22 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&bar[ER + qo_region(t)]);
+        if (PH && vsum) {  // each query tile is its own head
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], 8);
+            acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], 16);
+          }
+          if (lane < 8) {
+            float* dst = p.dbias + 2 * HD + (head_of(u, t) % p.H) * kD + g * 8;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) atomicAdd(dst + i, acc[i]);
+          }
+#pragma unroll
+          for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+        }
       }
-      if (vsum) {
+      if (vsum && !PH) {
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           acc[i] += __shfl_xor_sync(0xffffffffu, acc[i], 8);
@@ -912,7 +946,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++hi) {
         const int it0 = hi * NIT;
         for (int k = 0; k < NIT; ++k) {
-          const int it = it0 + k, bsel = k & 1, j = k / NC, c = k % NC;
+          const int it = it0 + k, bsel = k & 1;
+          int j, c;
+          jc(k, j, c);
           mbar_wait(&bar[FR + kv_region(j)], hi & 1);       // K_j, V_j of this unit
           mbar_wait(&bar[FR + qo_region(c >> 1)], hi & 1);  // Q, dO rows of chunk c
           if (k == 0) EPS_TRACE(hi < 16 && lane == 0, 640 + hi * 4 + 2);
@@ -945,11 +981,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       int kt = 0, hi = 0;
       for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++hi) {
         for (int k = 0; k < NIT; ++k) {
-          const int it = hi * NIT + k, bsel = k & 1, j = k / NC, c = k % NC;
+          const int it = hi * NIT + k, bsel = k & 1;
+          int j, c;
+          jc(k, j, c);
           mbar_wait(&bar[PF0 + bsel], (it >> 1) & 1);
           tc_fence_after();
           EPS_TRACE(it < 64 && lane == 0, it * 8 + 1);
-          if (c == 0 && kt > 0) {  // dK / dV of the previous key tile read out
+          if ((PH ? (c & 1) == 0 : c == 0) && kt > 0) {  // dK / dV of the previous key tile read out
             mbar_wait(&bar[KVE], (kt - 1) & 1);
             tc_fence_after();
           }
@@ -963,7 +1001,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
                                           16, 1024);
 #pragma unroll
           for (int kk = 0; kk < kChunk / 16; ++kk) {
-            const uint32_t acc = (c > 0 || kk > 0) ? 1u : 0u;
+            // dV / dK of key tile j start at its first chunk (PH: chunk 2j)
+            const uint32_t acc = ((PH ? (c & 1) : c) > 0 || kk > 0) ? 1u : 0u;
             const uint32_t pcol = uint32_t(pk_col(kk));  // see the exp loop
             tc_mma_ts_ws(tdV, tS + pcol, oc + uint64_t(kk * 128), idesc_km, acc);
             if (kBwdDkSS)
@@ -974,7 +1013,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           // P^T / dS^T in this TMEM buffer are consumed: release it to the S
           // issuer before the dQ MMAs (they read dS from the smem staging)
           tc_commit_ws(&bar[AC0 + bsel]);
-          if (c == NC - 1) tc_commit_ws(&bar[KVF]);
+          const bool tile_end = PH ? (c & 1) == 1 : c == NC - 1;  // last chunk of key tile j
+          if (tile_end) tc_commit_ws(&bar[KVF]);
           if (c & 1) {  // both halves of 128-query tile c/2 staged: dQ_t += dS_t K_j
             const int t = c >> 1;
             // S^T / dP^T of iteration it + 2 (the next user of the TMEM buffer
@@ -998,11 +1038,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 #pragma unroll
             for (int kk = 0; kk < kTile / 16; ++kk)
               tc_mma_ss_ws(tq, stg + uint64_t(kk * 128), kj + uint64_t(kk * 128), idesc_mm,
-                           ((!UNIT && j > 0) || kk > 0) ? 1u : 0u);
+                           ((!UNIT && !PH && j > 0) || kk > 0) ? 1u : 0u);
             if (UNIT) tc_commit_ws(&bar[(g & 1) ? DQF1 : DQF]);
           }
           EPS_TRACE(it < 64 && lane == 0, it * 8 + 2);
-          if (c == NC - 1) ++kt;
+          if (tile_end) ++kt;
           // operand regions whose last reader this was (tracks the dQ MMAs too)
 #pragma unroll
           for (int r = 0; r < 4; ++r)
@@ -1031,8 +1071,11 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const uint32_t ld = smem_addr(sLD + lb * Tr);
 #pragma unroll 1
       for (int k = 0; k < NIT; ++k) {
-        const int it = hi * NIT + k, bsel = k & 1, j = k / NC, c = k % NC;
-        const int kbase = (jb * NK + j) * kTile + quarter * 32;  // this warp's 32 keys
+        const int it = hi * NIT + k, bsel = k & 1;
+        int j, c;
+        jc(k, j, c);
+        // this warp's 32 keys (index within the key tile's head for PH)
+        const int kbase = PH ? quarter * 32 : (jb * NK + j) * kTile + quarter * 32;
         const int q0 = c * kChunk + sub * kBwdQPW;
         mbar_wait(&bar[SF0 + bsel], (it >> 1) & 1);
         tc_fence_after();
@@ -1071,7 +1114,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           for (int hh = 0; hh < kBwdPasses; ++hh) {
             const uint32_t l4 = ld + uint32_t(q0 + hh * 16) * 8u;
             uint32_t pp[8], pd[8];
-            if (q0 + hh * 16 >= p.T) {
+            if (((q0 + hh * 16) & (PH ? kTile - 1 : 0x7fffffff)) >= p.T) {
               // 16 query columns wholly past T (up to 23 % of a ViT head's
               // columns): their dO rows are zero, so P^T = dS^T = 0 is exact
               // and the exps are skipped
@@ -1119,18 +1162,21 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     const int te = threadIdx.x - (64 + 32 * kBwdExpWarps);  // 0..127
     // (-lse * log2e, D = rowsum(dO * O)) of every query of head `bh` into
     // table hi & 1, once the exp warps released it (head hi - 2).
+    // bh: the unit's (first) head; PH: rows 128 r .. of the table are head bh + r
     auto fill_table = [&](int bh, int hi) {
-      const int lb = hi & 1, b = bh / p.H, h = bh % p.H;
+      const int lb = hi & 1;
       if (hi >= 2) mbar_wait(&bar[LE0 + lb], ((hi >> 1) - 1) & 1);
       EPS_TRACE(hi < 16 && warp == 2 + kBwdExpWarps && lane == 0, 704 + hi * 2);
 #pragma unroll
       for (int r = 0; r < Tr / 128; ++r) {
         const int q = te + 128 * r;
+        const int bhr = PH ? bh + r : bh, ql = PH ? te : q;
+        const int b = bhr / p.H, h = bhr % p.H;
         // queries past T: -lse2 = D = 0 (see the exp loop)
         float2 e = make_float2(0.f, 0.f);
-        if (q < p.T)
-          e = make_float2(-__ldg(p.lse + int64_t(bh) * p.T + q) * kLog2e,
-                          __ldg(p.drow + (int64_t(b) * p.T + q) * p.H + h));
+        if (ql < p.T)
+          e = make_float2(-__ldg(p.lse + int64_t(bhr) * p.T + ql) * kLog2e,
+                          __ldg(p.drow + (int64_t(b) * p.T + ql) * p.H + h));
         sLD[lb * Tr + q] = e;
       }
       mbar_arrive(&bar[LF0 + lb]);
@@ -1159,9 +1205,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       store_tile_to(&map_dq, pk, col, row0, b);
     };
     int hi = 0, kt = 0;
-    if (int(blockIdx.x) < n_units) fill_table(int(blockIdx.x) / NU, 0);
+    if (int(blockIdx.x) < n_units) fill_table(head_of(int(blockIdx.x), 0), 0);
     for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++hi) {
-      const int bh = u / NU, jb = u % NU;
+      const int bh = head_of(u, 0), jb = u % NU;
       const int b = bh / p.H, h = bh % p.H;
       if constexpr (UNIT) {
         // dQ partials of the unit's key tile, one 128-query tile at a time
@@ -1175,7 +1221,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           __syncwarp();
           if (lane == 0) mbar_arrive(&bar[(g & 1) ? DQE1 : DQE]);
           store_tile_to(&map_dqp, pq, h * kD, t * kTile, jb * (n_heads / p.H) + b);
-          if (t == 0 && u + int(gridDim.x) < n_units) fill_table((u + int(gridDim.x)) / NU, hi + 1);
+          if (t == 0 && u + int(gridDim.x) < n_units)
+            fill_table(head_of(u + int(gridDim.x), 0), hi + 1);
         }
         mbar_wait(&bar[KVF], kt & 1);
         tc_fence_after();
@@ -1203,12 +1250,16 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         __syncwarp();
         if (lane == 0) mbar_arrive(&bar[KVE]);
         EPS_TRACE(kt < 64 && warp == 2 + kBwdExpWarps && lane == 0, 512 + kt * 2 + 1);
-        store_tile(pv, 2 * HD + h * kD, j * kTile, b);
-        store_tile(pk, HD + h * kD, j * kTile, b);
+        {
+          const int hbj = head_of(u, PH ? j : 0), bj = hbj / p.H, hj = hbj % p.H;
+          store_tile(pv, 2 * HD + hj * kD, PH ? 0 : j * kTile, bj);
+          store_tile(pk, HD + hj * kD, PH ? 0 : j * kTile, bj);
+        }
         EPS_TRACE(hi < 16 && j == 0 && warp == 2 + kBwdExpWarps && lane == 0, 760 + hi * 4 + 2);
-        // the next head's table, off the key-tile hand-off path (its exp work
-        // starts only after this head's remaining iterations)
-        if (j == 0 && u + int(gridDim.x) < n_units) fill_table(u + int(gridDim.x), hi + 1);
+        // the next unit's table, off the key-tile hand-off path (its exp work
+        // starts only after this unit's remaining iterations)
+        if (j == 0 && u + int(gridDim.x) < n_units)
+          fill_table(head_of(u + int(gridDim.x), 0), hi + 1);
       }
       mbar_wait(&bar[DQF], hi & 1);
       tc_fence_after();
@@ -1222,31 +1273,36 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       EPS_TRACE(hi < 16 && warp == 2 + kBwdExpWarps && lane == 0, 640 + hi * 4 + 1);
 #pragma unroll
       for (int t = 0; t < (UNIT ? 1 : NT); ++t) {
-        if (t * kTile + row >= p.T) zero32(pq[t]);
-        store_tile(pq[t], h * kD, t * kTile, b);
+        const int hbt = head_of(u, PH ? t : 0);
+        if ((PH ? row : t * kTile + row) >= p.T) zero32(pq[t]);
+        store_tile(pq[t], (hbt % p.H) * kD, PH ? 0 : t * kTile, hbt / p.H);
       }
-      if (p.dbias != nullptr) {  // Q bias gradient: column sums of dQ
-        float u[64];
+      if (p.dbias != nullptr) {  // Q bias gradient: column sums of dQ (PH: per head)
 #pragma unroll
-        for (int d = 0; d < 32; ++d) {
-          u[2 * d] = bf16_lo(pq[0][d]);
-          u[2 * d + 1] = bf16_hi(pq[0][d]);
+        for (int grp = 0; grp < (PH ? NT : 1); ++grp) {
+          float uu[64];
 #pragma unroll
-          for (int t = 1; t < (UNIT ? 1 : NT); ++t) u[2 * d] += bf16_lo(pq[t][d]), u[2 * d + 1] += bf16_hi(pq[t][d]);
+          for (int d = 0; d < 32; ++d) {
+            uu[2 * d] = 0.f;
+            uu[2 * d + 1] = 0.f;
+#pragma unroll
+            for (int t = 0; t < (UNIT ? 1 : NT); ++t)
+              if (!PH || t == grp) uu[2 * d] += bf16_lo(pq[t][d]), uu[2 * d + 1] += bf16_hi(pq[t][d]);
+          }
+#pragma unroll
+          for (int half = 0; half < 2; ++half) {
+            float t32[32];
+#pragma unroll
+            for (int d = 0; d < 32; ++d) t32[d] = uu[half * 32 + d];
+            atomicAdd(&sRed[half * 32 + lane], warp_transpose_sum32(t32));
+          }
+          epi_sync();
+          if (te < 64) {
+            atomicAdd(p.dbias + (head_of(u, PH ? grp : 0) % p.H) * kD + te, sRed[te]);
+            sRed[te] = 0.f;
+          }
+          epi_sync();
         }
-#pragma unroll
-        for (int half = 0; half < 2; ++half) {
-          float t32[32];
-#pragma unroll
-          for (int d = 0; d < 32; ++d) t32[d] = u[half * 32 + d];
-          atomicAdd(&sRed[half * 32 + lane], warp_transpose_sum32(t32));
-        }
-        epi_sync();
-        if (te < 64) {
-          atomicAdd(p.dbias + h * kD + te, sRed[te]);
-          sRed[te] = 0.f;
-        }
-        epi_sync();
       }
       EPS_TRACE(hi < 16 && warp == 2 + kBwdExpWarps && lane == 0, 760 + hi * 4);
     }
@@ -2137,6 +2193,17 @@ static bool bwd_unit_on() {
   return on;
 }
 
+// Paired heads for T <= 128 (EPS_ATTN_BWD_PAIRS=1 enables).  Off by default:
+// measured slower at BERT-large-128 b64 (0.0478 -> 0.052 ms): 512 pair units
+// on 148 SMs balance worse (3.46 per SM) than 1024 heads (6.92).
+static bool bwd_pairs_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("EPS_ATTN_BWD_PAIRS");
+    return e != nullptr && std::atoi(e) != 0;
+  }();
+  return on;
+}
+
 bool attn_bwd_fused_supported(int T, int head_dim) {
   return head_dim == 64 && T >= 1 &&
          T <= (bwd_unit_on() ? 3 * attn_tc::kTile : 2 * attn_tc::kTile);
@@ -2203,11 +2270,16 @@ int attn_bwd_tc(const void* qkv, const void* out, const void* dout, const float*
           part, R * WO, 3, static_cast<uint16_t*>(dqkv), W, R, int(WO), dbias);
       return cudaGetLastError() == cudaSuccess ? EPS_OK : EPS_ECUDA;
     }
-    const int grid = heads < sm_count() ? heads : sm_count();
-    auto kern = T <= kTile ? attn_bwd_fused_tc_kernel<1> : attn_bwd_fused_tc_kernel<2>;
-    if (!ensure_smem(kern, sf)) return EPS_ECUDA;
+    // T <= 128 with an even head count: pairs of heads per work unit (PH)
+    const bool ph = T <= kTile && heads % 2 == 0 && bwd_pairs_on();
+    const int units = ph ? heads / 2 : heads;
+    const int grid = units < sm_count() ? units : sm_count();
+    auto kern = ph ? attn_bwd_fused_tc_kernel<2, false, true>
+                   : T <= kTile ? attn_bwd_fused_tc_kernel<1> : attn_bwd_fused_tc_kernel<2>;
+    const size_t sfk = ph ? bwd_fused_smem(2 * kTile) : sf;
+    if (!ensure_smem(kern, sfk)) return EPS_ECUDA;
     count_launch();
-    if (launch_k(kern, dim3(grid), dim3(kBwdThreads), sf, st, 1, mq, mo, mdq, mdq, p, heads) !=
+    if (launch_k(kern, dim3(grid), dim3(kBwdThreads), sfk, st, 1, mq, mo, mdq, mdq, p, heads) !=
         cudaSuccess)
       return EPS_ECUDA;
     return cudaGetLastError() == cudaSuccess ? EPS_OK : EPS_ECUDA;

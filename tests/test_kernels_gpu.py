@@ -103,7 +103,9 @@ def _attn_ref(qkv, B, T, H, dh):
                                       (40, 64, 8, 64),
                                       # 256 < T <= 384: (head, key tile) units, several per
                                       # CTA, ragged last key / query tile, dQ slice reduce
-                                      (8, 384, 12, 64), (3, 300, 4, 64), (2, 257, 3, 64)])
+                                      (8, 384, 12, 64), (3, 300, 4, 64), (2, 257, 3, 64),
+                                      # T <= 128: head pairs per unit; odd head count falls back
+                                      (3, 100, 3, 64), (37, 128, 4, 64)])
 def test_attention_fwd_bwd(cuda, B, T, H, dh):
     g = torch.Generator(device=cuda).manual_seed(T * H)
     D = H * dh
@@ -142,6 +144,40 @@ def test_attention_fwd_bwd(cuda, B, T, H, dh):
         torch.cuda.synchronize()
         assert _rel(dqkv2, dqkv) < 1e-2
         assert _rel(dbias2, dbias) < 1e-2
+
+
+def test_attention_bwd_paired_heads(cuda, monkeypatch):
+    """The paired-head backward (T <= 128, EPS_ATTN_BWD_PAIRS=1; off by default)
+    matches the per-head one, in a fresh process so the switch is read."""
+    import subprocess
+    import sys
+    code = (
+        "import torch, ctypes as C, sys; sys.path.insert(0, '.');"
+        "from paper_2102_03161_b200 import ops;"
+        "B, T, H = 6, 100, 4; D = H * 64; g = torch.Generator(device='cuda').manual_seed(3);"
+        "qkv = torch.randn(B*T, 3*D, device='cuda', generator=g).bfloat16();"
+        "out = torch.empty(B*T, D, device='cuda', dtype=torch.bfloat16);"
+        "lse = torch.empty(B, H, T, device='cuda'); s = C.c_void_p(0); sc = C.c_float(0.125);"
+        "ops.call('eps_attn_fwd', qkv, out, lse, B, T, H, 64, sc, s);"
+        "do = torch.randn(B*T, D, device='cuda', generator=g).bfloat16();"
+        "dq = torch.empty_like(qkv); db = torch.zeros(3*D, device='cuda');"
+        "ds = torch.empty(B*H*T, device='cuda');"
+        "ops.call('eps_attn_bwd_ws', qkv, out, do, lse, dq, db, ds, B, T, H, 64, sc, s);"
+        "torch.cuda.synchronize(); torch.save((dq.cpu(), db.cpu()), sys.argv[1])")
+    outs = []
+    import tempfile, os
+    with tempfile.TemporaryDirectory() as d:
+        for flag in ("0", "1"):
+            f = os.path.join(d, f"r{flag}.pt")
+            env = dict(os.environ, EPS_ATTN_BWD_PAIRS=flag)
+            r = subprocess.run([sys.executable, "-c", code, f], cwd=os.path.dirname(
+                os.path.dirname(os.path.abspath(__file__))), env=env, capture_output=True,
+                text=True, timeout=300)
+            assert r.returncode == 0, r.stderr[-2000:]
+            outs.append(torch.load(f))
+    (a, ba), (b, bb) = outs
+    assert _rel(b, a) < 1e-2
+    assert _rel(bb, ba) < 1e-2
 
 
 @pytest.mark.parametrize("T,spike", [(197, 40), (197, 196), (128, 100), (256, 255), (384, 100),
