@@ -648,7 +648,7 @@ def stage_emulation(ex, cfg, g, batch, inputs, labels, ms_whole):
             "stages": rows, "slowest_stage_ms": slow,
             "gpipe_iteration_ms": round(t_iter, 3),
             "emulated_8gpu_samples_per_s": round(batch / (t_iter / 1000.0), 1),
-            "whole_model_b400_ms": round(ms_whole, 3),
+            "whole_model_ms": round(ms_whole, 3),  # the full per-pipeline batch on one GPU
             "note": "single-GPU emulation of the 1x8 epoch-0 plan; not an 8-GPU measurement"}
 
 
