@@ -143,3 +143,16 @@ def test_native_bert_device_norm_decisions(cuda, geo_name):
         assert len(rows[e].norms) == g.layers and all(n >= 0 for n in rows[e].norms)
         if e > 0:
             assert O.next_frozen_count(st, rows[e - 1].norms, g.layers) == rows[e].l_frozen
+
+
+def test_cli_runs_bert_scenario(cuda, tmp_path):
+    subprocess.run(["make", "-C", ROOT, "train"], check=True, capture_output=True)
+    scen, _ = _bert_scenario("tiny-bert-cls", batch=16, epochs=3)
+    f = tmp_path / "s.json"
+    f.write_text(json.dumps(scen))
+    r = subprocess.run([os.path.join(ROOT, "build", "eps_train"), "--scenario", str(f),
+                        "--geometry", "tiny-bert-cls", "--iterations", "2", "--epochs", "3"],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    rows = r.stdout.strip().splitlines()
+    assert rows[0].startswith("epoch,l_frozen") and len(rows) == 4
