@@ -225,14 +225,16 @@ struct eps_vit {
     return on;
   }
   bool side_on = true;  // eps_vit_set_side_stream
+  // (off while per-class timing is on: concurrent kernels would make the
+  // class durations overlap and overstate the GEMM class time)
   cudaStream_t fork(cudaStream_t st) {
-    if (!side || !side_on) return st;
+    if (!side || !side_on || timing) return st;
     cudaEventRecord(fork_ev, st);
     cudaStreamWaitEvent(side, fork_ev, 0);
     return side;
   }
   void join(cudaStream_t st) {
-    if (!side || !side_on) return;
+    if (!side || !side_on || timing) return;
     cudaEventRecord(join_ev, side);
     cudaStreamWaitEvent(st, join_ev, 0);
   }
