@@ -203,6 +203,7 @@ __global__ void __launch_bounds__(kLnWarps * 32)
 // barrier.  (The warp-per-row kernel above holds 24 columns x 3 accumulators
 // per lane, ~200 registers, and reaches only ~8 rows in flight per SM.)
 constexpr int kLnStages = 16;
+constexpr int kLnStatRows = 384;  // d = 768 backward: rows per CTA with (mean, rstd) in smem
 
 template <int D>
 struct LnWide {
@@ -272,6 +273,22 @@ __global__ void __launch_bounds__(LnWide<D>::THREADS, 2)
   const int ct = threadIdx.x - 32;
   const int grp = ct / TPR, t = ct % TPR, wig = t >> 5;
   const int col = t * 8;
+  // (mean, rstd) of the CTA's first kLnStatRows rows, loaded by all consumer
+  // threads at once: a per-row load puts one L2 / HBM round trip in front of
+  // every row whose data is already in the ring (d = 768: ViT-B b400 90.4 ->
+  // 84.1 us, BERT-base-384 33.7 -> 30.2).  At d = 1024 (BERT-large-128, ~28
+  // rows per CTA) both this and a two-row register prefetch measured slower
+  // (19.7 -> 21.0 / 21.8 us), so the per-row load stays there.
+  constexpr bool kStage = D == 768;
+  constexpr int kStatRows = kStage ? kLnStatRows : 1;
+  __shared__ float2 stat[kStatRows];
+  if (kStage) {
+    for (int64_t k = ct; k < n_mine && k < kStatRows; k += GROUPS * TPR) {
+      const int64_t r = blockIdx.x + k * gridDim.x;
+      stat[k] = make_float2(__ldg(mean + r), __ldg(rstd + r));
+    }
+    asm volatile("bar.sync 14, %0;" ::"r"(GROUPS * TPR) : "memory");
+  }
   float gam[8], ag[8], ab[8], ac[8];
   {
     const float4 g0 = __ldg(reinterpret_cast<const float4*>(gamma + col));
@@ -285,7 +302,9 @@ __global__ void __launch_bounds__(LnWide<D>::THREADS, 2)
   for (int64_t k = grp; k < n_mine; k += GROUPS, buf ^= 1) {
     const int st = int(k % kLnStages);
     const int64_t r = blockIdx.x + k * gridDim.x;
-    const float mu = __ldg(mean + r), rs = __ldg(rstd + r);
+    const float2 ms = kStage && k < kStatRows ? stat[k]
+                                              : make_float2(__ldg(mean + r), __ldg(rstd + r));
+    const float mu = ms.x, rs = ms.y;
     mbar_wait(&full[st], uint32_t((k / kLnStages) & 1));
     const uint32_t base = smem_addr(ring + size_t(st) * 3 * ROW) + uint32_t(col * 2);
     const uint4 gy = ld_shared_v4(base), xx = ld_shared_v4(base + ROW);
@@ -331,10 +350,14 @@ __global__ void __launch_bounds__(LnWide<D>::THREADS, 2)
     atomicAdd(&acc_s[2][col + i], ac[i]);
   }
   asm volatile("bar.sync 15, %0;" ::"r"(GROUPS * TPR) : "memory");
-  for (int c = ct; c < 3 * D; c += GROUPS * TPR) {
+  // one 4-wide reduction per 4 columns (a quarter of the atomic operations;
+  // measured neutral at ViT-B and BERT shapes)
+  for (int c = ct * 4; c < 3 * D; c += GROUPS * TPR * 4) {
     const int which = c / D, cc = c % D;
     float* dst = which == 0 ? dgamma : which == 1 ? dbeta : colsum;
-    if (dst != nullptr) atomicAdd(dst + cc, acc_s[which][cc]);
+    if (dst != nullptr)
+      red_add_v4(dst + cc, acc_s[which][cc], acc_s[which][cc + 1], acc_s[which][cc + 2],
+                 acc_s[which][cc + 3]);
   }
 }
 

@@ -10,6 +10,7 @@ from paper_2102_03161_b200 import ops  # noqa: E402
 
 d = int(sys.argv[1]) if len(sys.argv) > 1 else 768
 R = int(sys.argv[2]) if len(sys.argv) > 2 else 400 * 197
+nores = len(sys.argv) > 3 and sys.argv[3] == "nores"  # post-norm BERT: no residual gradient
 dev = torch.device("cuda")
 x = torch.randn(R, d, device=dev).bfloat16()
 y = torch.empty_like(x)
@@ -31,11 +32,12 @@ def fwd():
 
 def bwd():
     s = C.c_void_p(torch.cuda.current_stream().cuda_stream)
-    ops.call("eps_layernorm_bwd", dy, x, gam, mean, rstd, dres, dx, dg, db, cs, R, d, None, s)
+    ops.call("eps_layernorm_bwd", dy, x, gam, mean, rstd, None if nores else dres, dx, dg, db,
+             None if nores else cs, R, d, None, s)
 
 
 res = {"R": R, "d": d}
-for tag, fn, nbytes in (("fwd", fwd, 4 * R * d), ("bwd", bwd, 8 * R * d)):
+for tag, fn, nbytes in (("fwd", fwd, 4 * R * d), ("bwd", bwd, (6 if nores else 8) * R * d)):
     for _ in range(3):
         fn()
     torch.cuda.synchronize()
