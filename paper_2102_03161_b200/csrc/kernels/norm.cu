@@ -239,7 +239,7 @@ __global__ void __launch_bounds__(LnWide<D>::THREADS, 2)
   uint64_t* full = reinterpret_cast<uint64_t*>(ring + size_t(kLnStages) * 3 * ROW);
   uint64_t* empty = full + kLnStages;
   __shared__ float red[GROUPS][2][WPR][2];
-  __shared__ float acc_s[3][D];
+  __shared__ __align__(16) float acc_s[3][D];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool has_res = dres != nullptr;
   const int64_t n_mine = rows > blockIdx.x ? (rows - 1 - blockIdx.x) / gridDim.x + 1 : 0;
@@ -250,7 +250,6 @@ __global__ void __launch_bounds__(LnWide<D>::THREADS, 2)
     }
     mbar_fence_init();
   }
-  for (int i = threadIdx.x; i < 3 * D; i += blockDim.x) (&acc_s[0][0])[i] = 0.f;
   pdl_launch_dependents();
   __syncthreads();
   pdl_wait();  // the predecessor grid's outputs are complete (PDL launch)
@@ -278,7 +277,8 @@ __global__ void __launch_bounds__(LnWide<D>::THREADS, 2)
   // every row whose data is already in the ring (d = 768: ViT-B b400 90.4 ->
   // 84.1 us, BERT-base-384 33.7 -> 30.2).  At d = 1024 (BERT-large-128, ~28
   // rows per CTA) both this and a two-row register prefetch measured slower
-  // (19.7 -> 21.0 / 21.8 us), so the per-row load stays there.
+  // (13.8 -> 14.6 us after the reduction change below), so the per-row load
+  // stays there.
   constexpr bool kStage = D == 768;
   constexpr int kStatRows = kStage ? kLnStatRows : 1;
   __shared__ float2 stat[kStatRows];
@@ -342,14 +342,30 @@ __global__ void __launch_bounds__(LnWide<D>::THREADS, 2)
     }
     if (dx != nullptr) store_vec<8>(dx + r * D + col, o);
   }
-  // block reduction of the three column accumulators, one atomic per column
+  // block reduction of the three column accumulators: the groups add their
+  // 8 columns into acc_s in turn (plain 16-byte shared loads / stores).  A
+  // shared-memory float atomicAdd compiles to a compare-and-swap loop; with
+  // it the kernel took 19.7 / 33.6 / 90.3 us (BERT-large / BERT-base / ViT-B
+  // shapes), now 13.8 / 25.4 / 80.5.
+  for (int gi = 0; gi < GROUPS; ++gi) {
+    if (grp == gi) {
+      float* dst[3] = {&acc_s[0][col], &acc_s[1][col], &acc_s[2][col]};
+      const float* src[3] = {ag, ab, ac};
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    atomicAdd(&acc_s[0][col + i], ag[i]);
-    atomicAdd(&acc_s[1][col + i], ab[i]);
-    atomicAdd(&acc_s[2][col + i], ac[i]);
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          float4 v = make_float4(src[a][4 * h], src[a][4 * h + 1], src[a][4 * h + 2],
+                                 src[a][4 * h + 3]);
+          if (gi > 0) {
+            const float4 o = reinterpret_cast<const float4*>(dst[a])[h];
+            v.x += o.x, v.y += o.y, v.z += o.z, v.w += o.w;
+          }
+          reinterpret_cast<float4*>(dst[a])[h] = v;
+        }
+    }
+    asm volatile("bar.sync 15, %0;" ::"r"(GROUPS * TPR) : "memory");
   }
-  asm volatile("bar.sync 15, %0;" ::"r"(GROUPS * TPR) : "memory");
   // one 4-wide reduction per 4 columns (a quarter of the atomic operations;
   // measured neutral at ViT-B and BERT shapes)
   for (int c = ct * 4; c < 3 * D; c += GROUPS * TPR * 4) {
