@@ -12,7 +12,7 @@ echo "pytest -m gpu: $(grep -E 'passed|failed' gpurun_out/pytest_gpu.log | tail 
 echo
 echo "smoke: $(head -1 gpurun_out/smoke.log)"
 echo
-echo "## bench.py (default: N=1, 5 steps, 3 warm-up)"
+echo "## bench.py (default: N=1, 10 steps, 3 warm-up)"
 echo
 python - <<'PY'
 import json
