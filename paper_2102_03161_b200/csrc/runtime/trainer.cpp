@@ -174,10 +174,19 @@ int guarded_rt(F&& body) {
   } catch (const eps::ConfigError& e) {
     eps::set_last_error(e.what());
     return EPS_ECONFIG;
+  } catch (const eps::IoError& e) {
+    eps::set_last_error(e.what());
+    return EPS_EIO;
   } catch (const std::invalid_argument& e) {
     eps::set_last_error(e.what());
     return EPS_EINVAL;
-  } catch (const std::exception& e) {
+  } catch (const std::domain_error& e) {  // planner / shard arithmetic (reference types)
+    eps::set_last_error(e.what());
+    return EPS_EDOMAIN;
+  } catch (const std::logic_error& e) {
+    eps::set_last_error(e.what());
+    return EPS_ELOGIC;
+  } catch (const std::exception& e) {  // cuda_check / eps_check failures
     eps::set_last_error(e.what());
     return EPS_ECUDA;
   }
