@@ -116,6 +116,16 @@ class ClockSampler:
         self.lines = []
         self.thread = None
 
+    def energy_mj(self):
+        # NVML total-energy counter (mJ since driver load); None when unavailable
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            return float(pynvml.nvmlDeviceGetTotalEnergyConsumption(h))
+        except Exception:  # noqa: BLE001 -- optional telemetry
+            return None
+
     def start(self):
         try:
             self.proc = subprocess.Popen(
@@ -418,14 +428,20 @@ def main_ours(args, world, rank, local):
         dist.all_reduce(t, op=op)
         return float(t.item())
 
-    def timed(fn, steps):
+    energy_mj = []  # NVML energy reads at the timed region's two barriers (value run)
+
+    def timed(fn, steps, meter=False):
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         barrier()
+        if meter:
+            energy_mj.append(clocks.energy_mj())
         s.record(stream)
         for _ in range(steps):
             fn()
         e.record(stream)
         barrier()
+        if meter:
+            energy_mj.append(clocks.energy_mj())
         return reduce(s.elapsed_time(e), dist.ReduceOp.MAX if world > 1 else None) / steps
 
     # ---- value: the epoch-0 (no-freeze) iteration, inputs resident in HBM ------
@@ -434,11 +450,23 @@ def main_ours(args, world, rank, local):
     clocks = ClockSampler(dev.index)
     clocks.start()
     n_launch0 = ops.launch_count()
-    ms = timed(lambda: step(inputs), args.steps)
+    ms = timed(lambda: step(inputs), args.steps, meter=True)
     launches = int(reduce(float(ops.launch_count() - n_launch0),
                           dist.ReduceOp.SUM if world > 1 else None))
     clock_rec = clocks.stop()
     value = plan0.R * batch / (ms / 1000.0)
+    # board energy over the timed steps (NVML counter, every rank's GPU): the
+    # B200s run at their power limit, so throughput follows energy per sample
+    energy = None
+    if len(energy_mj) == 2 and None not in energy_mj:
+        # (--gloo-one-gpu: every rank reads the same board)
+        gpus = 1 if one_gpu else world
+        ej = (energy_mj[1] - energy_mj[0]) / 1e3
+        ej = ej if gpus == 1 else reduce(ej, dist.ReduceOp.SUM)
+        energy = {"joules_per_step": round(ej / args.steps, 3),
+                  "samples_per_joule": round(plan0.R * batch * args.steps / ej, 2),
+                  "mean_w_per_gpu": round(ej / gpus / (ms * args.steps / 1000.0), 1),
+                  "source": "NVML total energy counter read at the timed region's barriers"}
 
     # ---- roofline: instrumented steps, per-class CUDA-event times --------------
     # three instrumented steps; per class the median device time (one step is
@@ -593,6 +621,7 @@ def main_ours(args, world, rank, local):
                "kernels": kernels,
                "mfu": round(mfu, 4),
                "clocks": clock_rec,
+               "energy": energy,
                "freeze_schedule": sched,
                "trainer_run": trainer,
                "trainer_run_native": trainer_native,
