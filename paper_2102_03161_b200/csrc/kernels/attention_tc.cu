@@ -682,6 +682,24 @@ constexpr int kDsChunk = kTile * kRowBytes;  // [128 keys][64 queries] bf16 = 16
 constexpr int kBwdExpWarps = 8, kBwdEpiWarps = 4;
 // dK MMAs read dS^T from the smem staging tile (SS) instead of TMEM (TS)
 constexpr bool kBwdDkSS = false;
+// T <= 128: operand regions double-buffered across heads (attn_bwd_fused_tc_kernel DB;
+// measured neutral at BERT-large-128, 0.0444 -> 0.0448 ms, off)
+#ifndef EPS_BWD_DB
+#define EPS_BWD_DB 0
+#endif
+constexpr bool kBwdDoubleBuffer = EPS_BWD_DB != 0;
+// epilogue staging tiles (16 KB each) by key-tile count: T <= 128 has room for
+// three (dV / dK / dQ of a head leave without waiting on each other: BERT-large-128
+// 0.0446 -> 0.0423 ms), unless its operands are double-buffered
+__host__ __device__ constexpr int bwd_stage_tiles(int nt) {
+  return nt == 1 && !kBwdDoubleBuffer ? 3 : 1;
+}
+// T <= 128: the epilogue fills the next head's (-lse2, D) table before it
+// waits for this head's dV / dK
+#ifndef EPS_BWD_EARLY_TABLE
+#define EPS_BWD_EARLY_TABLE 1
+#endif
+constexpr bool kBwdEarlyTable = EPS_BWD_EARLY_TABLE != 0;
 // Issue the S^T / dP^T MMAs of iteration it + 2 ahead of dQ(it) (see the post issuer)
 constexpr bool kBwdSFirst = false;  // measured 0.2937 -> 0.297 ms (ViT-B), off  // measured neutral-to-slower (0.295 -> 0.297 ms, ViT-B)
 // queries of a 64-query chunk per exp warp (4 warps per TMEM lane quarter)
@@ -750,6 +768,14 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   static_assert(NR <= 4 && NIT % 2 == 0, "regions / iterations");
   const int n_units = PH ? n_heads / 2 : n_heads * NU;
   static_assert(!PH || (NT == 2 && !UNIT), "paired heads: NT = 2 layout");
+  // DB (T <= 128): the operand regions are double-buffered across heads --
+  // head hi uses slot hi & 1 (KV region slot, QO region 2 + slot, the smem
+  // rows of tile `slot` of an NT = 2 layout), so the next head's Q / dO / K /
+  // V load while this head computes.
+  constexpr bool DB = NT == 1 && !UNIT && !PH && kBwdDoubleBuffer;
+  constexpr int TrA = DB ? 2 * kTile : Tr, KRA = DB ? 2 * kTile : KR;  // rows allocated
+  auto slot_of = [](int hi) { return DB ? (hi & 1) : 0; };
+  auto par_of = [](int hi) { return uint32_t(DB ? (hi >> 1) & 1 : hi & 1); };
   // iteration k of a unit -> (key tile j, query chunk c); PH: diagonal only
   auto jc = [](int k, int& j, int& c) {
     if (PH) {
@@ -765,14 +791,18 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   uint8_t* sQ = smem;
-  uint8_t* sO = sQ + Tr * kRowBytes;  // dO
-  uint8_t* sK = sO + Tr * kRowBytes;
-  uint8_t* sV = sK + KR * kRowBytes;
-  uint8_t* sS = sV + KR * kRowBytes;  // dS staging: 2 buffers x 2 chunks x 16 KB
-  uint8_t* sStage = sS + 4 * kDsChunk;  // epilogue: one 128x64 bf16 output tile
-  float2* sLD = reinterpret_cast<float2*>(sStage + kDsChunk);  // [2][Tr] (-lse2, D)
-  float* sRed = reinterpret_cast<float*>(sLD + 2 * Tr);  // [64] bias column sums of a head
-  uint64_t* bar = reinterpret_cast<uint64_t*>(sRed + 64);
+  uint8_t* sO = sQ + TrA * kRowBytes;  // dO
+  uint8_t* sK = sO + TrA * kRowBytes;
+  uint8_t* sV = sK + KRA * kRowBytes;
+  uint8_t* sS = sV + KRA * kRowBytes;  // dS staging: 2 buffers x 2 chunks x 16 KB
+  // epilogue: NSTG 128x64 bf16 output tiles in turn (T <= 128: three, so a
+  // head's dV / dK / dQ stores never wait for each other; the larger layouts
+  // have room for one)
+  constexpr int NSTG = bwd_stage_tiles(NT);
+  uint8_t* sStage = sS + 4 * kDsChunk;
+  float2* sLD = reinterpret_cast<float2*>(sStage + NSTG * kDsChunk);  // [2][Tr] (-lse2, D)
+  float* sRed = reinterpret_cast<float*>(sLD + 2 * Tr);  // [4][64] per-warp bias column sums
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sRed + 4 * 64);
   // Operand regions, each with its own full / empty barrier pair so a unit's
   // tiles are reloaded as soon as their last reader is done: KV_j = rows of
   // key tile j of K and V; QO_t = rows of query tile t of Q and dO.
@@ -782,8 +812,9 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   enum { FR = 0, ER = 4, SF0 = 8, SF1, PF0, PF1, AC0, AC1, KVF, KVE, DQF, DQE, LF0, LF1, LE0, LE1,
          SI0, SI1, DQF1, DQE1,
          NBAR };
-  auto kv_region = [](int j) { return j; };
-  auto qo_region = [](int t) { return UNIT ? 1 + t : 2 + t; };
+  // (DB: key tile j / query tile t are 0; `sl` is the head's slot)
+  auto kv_region = [](int j, int sl = 0) { return j + sl; };
+  auto qo_region = [](int t, int sl = 0) { return UNIT ? 1 + t : 2 + t + sl; };
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + NBAR);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int HD = p.H * kD;
@@ -791,6 +822,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
   // tile j) and by the dQ MMAs of its odd chunks; QO_t by the S and post MMAs
   // of chunks 2t, 2t+1 of the last key tile; -1: region unused
   auto last_use = [](int r) {
+    if (DB) return NC - 1;  // both slots' KV and QO: the head's last iteration
     if (PH) return r < 2 ? 2 * r + 1 : 2 * (r - 2) + 1;
     if (UNIT) return r == 0 ? NC - 1 : r <= NT ? 2 * (r - 1) + 1 : -1;
     if (r < 2) return r < NT ? r * NC + NC - 1 : -1;
@@ -809,13 +841,13 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       if (i == LF0 || i == LF1) cnt = 32 * kBwdEpiWarps;
       if (i == LE0 || i == LE1) cnt = 32 * kBwdExpWarps;
       for (int t = 0; t < NT; ++t)
-        if (i == ER + qo_region(t)) cnt = 2;  // post issuer's commit + the TMA warp's dO sums
+        for (int sl = 0; sl < (DB ? 2 : 1); ++sl)
+          if (i == ER + qo_region(t, sl)) cnt = 2;  // post issuer's commit + the TMA warp's dO sums
       mbar_init(&bar[i], cnt);
     }
     mbar_fence_init();
   }
   if (warp == 1) tmem_alloc(tmem_slot, 512);
-  if (threadIdx.x < 64) sRed[threadIdx.x] = 0.f;
   pdl_launch_dependents();
   tc_fence_before();
   __syncthreads();
@@ -831,30 +863,39 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const int b = bh / p.H, h = bh % p.H;
       // regions in the order the previous unit releases them (whole head:
       // KV0, QO0, KV1, QO1; UNIT: QO0, QO1, KV, QO2)
+      const int sl = slot_of(hi);
       int order[4] = {0, 0, 0, 0}, n_ord = 0;
-      for (int lu = 0; lu < NIT; ++lu)
-        for (int r = 0; r < 4; ++r)
-          if (last_use(r) == lu) order[n_ord++] = r;
+      if (DB) {  // this head's slot: KV, then QO
+        order[0] = kv_region(0, sl);
+        order[1] = qo_region(0, sl);
+        n_ord = 2;
+      } else {
+        for (int lu = 0; lu < NIT; ++lu)
+          for (int r = 0; r < 4; ++r)
+            if (last_use(r) == lu) order[n_ord++] = r;
+      }
       for (int oi = 0; oi < n_ord; ++oi) {
         const int r = order[oi];
         const bool kv = UNIT ? r == 0 : r < 2;
+        // smem tile (DB: the slot) and the tile's global rows (DB: tile 0)
         const int t = kv ? r : r - qo_region(0);  // key tile (KV) or query tile (QO)
-        mbar_wait(&bar[ER + r], (hi & 1) ^ 1);
+        const int tg = DB ? 0 : t;
+        mbar_wait(&bar[ER + r], par_of(hi) ^ 1);
         if (lane == 0) {
           mbar_expect_tx(&bar[FR + r], uint32_t(2 * kTile * kRowBytes));
           // PH: tile t is head 2u + t, rows 0..127 of that head
           const int bt = PH ? head_of(u, t) / p.H : b, ht = PH ? head_of(u, t) % p.H : h;
           if (kv) {
-            const int kr = PH ? 0 : (jb * NK + t) * kTile;  // global key row
+            const int kr = PH ? 0 : (jb * NK + tg) * kTile;  // global key row
             load_rows(sK + t * kTile * kRowBytes, &map_qkv, &bar[FR + r], HD + ht * kD, kr,
                       kTile, bt);
             load_rows(sV + t * kTile * kRowBytes, &map_qkv, &bar[FR + r], 2 * HD + ht * kD, kr,
                       kTile, bt);
           } else {
             load_rows(sQ + t * kTile * kRowBytes, &map_qkv, &bar[FR + r], ht * kD,
-                      PH ? 0 : t * kTile, kTile, bt);
+                      PH ? 0 : tg * kTile, kTile, bt);
             load_rows(sO + t * kTile * kRowBytes, &map_do, &bar[FR + r], ht * kD,
-                      PH ? 0 : t * kTile, kTile, bt);
+                      PH ? 0 : tg * kTile, kTile, bt);
           }
         }
       }
@@ -883,11 +924,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       // (UNIT: the head's first key-tile unit forms the sums)
       const bool vsum = p.dbias != nullptr && (!UNIT || jb == 0);
       for (int t = 0; t < NT; ++t) {
-        mbar_wait(&bar[FR + qo_region(t)], hi & 1);
+        mbar_wait(&bar[FR + qo_region(t, sl)], par_of(hi));
         if (vsum) {
           const uint32_t o_s = smem_addr(sO);
+          const int r0 = (t + sl) * kTile + rs * 32;  // (DB: the slot's rows)
 #pragma unroll 4
-          for (int r = t * kTile + rs * 32; r < t * kTile + rs * 32 + 32; ++r) {
+          for (int r = r0; r < r0 + 32; ++r) {
             const uint4 w = ld_shared_v4(o_s + swz128(r, g));
             acc[0] += bf16_lo(w.x), acc[1] += bf16_hi(w.x), acc[2] += bf16_lo(w.y);
             acc[3] += bf16_hi(w.y), acc[4] += bf16_lo(w.z), acc[5] += bf16_hi(w.z);
@@ -895,7 +937,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           }
         }
         __syncwarp();
-        if (lane == 0) mbar_arrive(&bar[ER + qo_region(t)]);
+        if (lane == 0) mbar_arrive(&bar[ER + qo_region(t, sl)]);
         if (PH && vsum) {  // each query tile is its own head
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
@@ -944,21 +986,22 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const uint64_t dV0 = umma_sdesc(smem_addr(sV), 16, 1024);
       int hi = 0;
       for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++hi) {
-        const int it0 = hi * NIT;
+        const int it0 = hi * NIT, sl = slot_of(hi);
         for (int k = 0; k < NIT; ++k) {
           const int it = it0 + k, bsel = k & 1;
           int j, c;
           jc(k, j, c);
-          mbar_wait(&bar[FR + kv_region(j)], hi & 1);       // K_j, V_j of this unit
-          mbar_wait(&bar[FR + qo_region(c >> 1)], hi & 1);  // Q, dO rows of chunk c
+          mbar_wait(&bar[FR + kv_region(j, sl)], par_of(hi));       // K_j, V_j of this unit
+          mbar_wait(&bar[FR + qo_region(c >> 1, sl)], par_of(hi));  // Q, dO rows of chunk c
           if (k == 0) EPS_TRACE(hi < 16 && lane == 0, 640 + hi * 4 + 2);
           if (it >= 2) {  // post(it - 2) finished reading this S^T / dP^T buffer
             mbar_wait(&bar[AC0 + bsel], ((it >> 1) - 1) & 1);
           }
           tc_fence_after();
           const uint32_t tS = tmem + uint32_t(bsel * 128), tdP = tS + 64;
-          const uint64_t kj = dK0 + uint64_t(j * kTile * 8), vj = dV0 + uint64_t(j * kTile * 8);
-          const uint64_t qc = dQ0 + uint64_t(c * kChunk * 8), oc = dO0 + uint64_t(c * kChunk * 8);
+          const int jr = (j + sl) * kTile, qr = sl * kTile + c * kChunk;  // smem rows (DB slot)
+          const uint64_t kj = dK0 + uint64_t(jr * 8), vj = dV0 + uint64_t(jr * 8);
+          const uint64_t qc = dQ0 + uint64_t(qr * 8), oc = dO0 + uint64_t(qr * 8);
 #pragma unroll
           for (int kk = 0; kk < kD / 16; ++kk)
             tc_mma_ss_ws(tS, kj + uint64_t(2 * kk), qc + uint64_t(2 * kk), idesc_kk, kk > 0 ? 1u : 0u);
@@ -980,6 +1023,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       const uint64_t mS0 = umma_sdesc(smem_addr(sS), kDsChunk, 1024);
       int kt = 0, hi = 0;
       for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++hi) {
+        const int sl = slot_of(hi);
         for (int k = 0; k < NIT; ++k) {
           const int it = hi * NIT + k, bsel = k & 1;
           int j, c;
@@ -992,7 +1036,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             tc_fence_after();
           }
           const uint32_t tS = tmem + uint32_t(bsel * 128), tdP = tS + 64;
-          const uint64_t qc = mQ0 + uint64_t(c * kChunk * 8), oc = mO0 + uint64_t(c * kChunk * 8);
+          const int qr = sl * kTile + c * kChunk;  // smem rows of chunk c (DB: the slot's)
+          const uint64_t qc = mQ0 + uint64_t(qr * 8), oc = mO0 + uint64_t(qr * 8);
           // dK_j += dS^T Q_c with dS^T read from its smem staging tile (K-major,
           // [128 keys][64 queries]): an SS MMA is ~15 % cheaper than the TS form
           // (tools/mma_rate.cu: M = 128, N = 64, K = 16 in 89 vs 105 cycles)
@@ -1033,7 +1078,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
               tc_fence_after();
             }
             const uint64_t stg = mS0 + uint64_t(((it >> 1) & 1) * 2 * (kDsChunk >> 4));
-            const uint64_t kj = mK0 + uint64_t(j * kTile * 8);
+            const uint64_t kj = mK0 + uint64_t((j + sl) * kTile * 8);
             const uint32_t tq = tdQ + uint32_t((UNIT ? (g & 1) : t) * kD);
 #pragma unroll
             for (int kk = 0; kk < kTile / 16; ++kk)
@@ -1044,9 +1089,16 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
           EPS_TRACE(it < 64 && lane == 0, it * 8 + 2);
           if (tile_end) ++kt;
           // operand regions whose last reader this was (tracks the dQ MMAs too)
+          if (DB) {
+            if (k == NIT - 1) {
+              tc_commit_ws(&bar[ER + kv_region(0, sl)]);
+              tc_commit_ws(&bar[ER + qo_region(0, sl)]);
+            }
+          } else {
 #pragma unroll
-          for (int r = 0; r < 4; ++r)
-            if (last_use(r) == k) tc_commit_ws(&bar[ER + r]);
+            for (int r = 0; r < 4; ++r)
+              if (last_use(r) == k) tc_commit_ws(&bar[ER + r]);
+          }
         }
         if (!UNIT) tc_commit_ws(&bar[DQF]);
       }
@@ -1184,11 +1236,14 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
     };
     // Tiles leave through a swizzled 16 KB staging buffer and TMA stores
     // (coalesced, asynchronous); `te == 0` owns the bulk groups.
-    const uint32_t stage_s = smem_addr(sStage);
     auto epi_sync = [] { asm volatile("bar.sync 1, 128;" ::: "memory"); };
+    int stg = 0;  // staging tile of the next store
     auto store_tile_to = [&](const CUtensorMap* map, const uint32_t (&pk)[32], int col, int row0,
                              int z) {
-      if (te == 0) bulk_wait_read<0>();  // previous tile read out of the staging buffer
+      uint8_t* buf = sStage + stg * kDsChunk;
+      const uint32_t stage_s = smem_addr(buf);
+      stg = stg + 1 == NSTG ? 0 : stg + 1;
+      if (te == 0) bulk_wait_read<NSTG - 1>();  // this buffer's previous tile read out
       epi_sync();
 #pragma unroll
       for (int c = 0; c < 8; ++c)
@@ -1196,8 +1251,8 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
       fence_proxy_async_smem();
       epi_sync();
       if (te == 0) {
-        tma_store_3d(map, sStage, col, row0, z);
-        tma_store_3d(map, sStage + 64 * kRowBytes, col, row0 + 64, z);
+        tma_store_3d(map, buf, col, row0, z);
+        tma_store_3d(map, buf + 64 * kRowBytes, col, row0 + 64, z);
         bulk_commit();
       }
     };
@@ -1237,6 +1292,10 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         ++kt;
         continue;
       }
+      // NT = 1: the next head's table first -- its exp work can start as soon
+      // as this head's last S^T is consumed, before dV / dK / dQ are out
+      if (kBwdEarlyTable && NT == 1 && u + int(gridDim.x) < n_units)
+        fill_table(head_of(u + int(gridDim.x), 0), hi + 1);
       // TMEM is read out and released first (the MMA warp is waiting for
       // it); stores work from the packed registers.
       for (int j = 0; j < NT; ++j, ++kt) {
@@ -1258,7 +1317,7 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
         EPS_TRACE(hi < 16 && j == 0 && warp == 2 + kBwdExpWarps && lane == 0, 760 + hi * 4 + 2);
         // the next unit's table, off the key-tile hand-off path (its exp work
         // starts only after this unit's remaining iterations)
-        if (j == 0 && u + int(gridDim.x) < n_units)
+        if (j == 0 && !(kBwdEarlyTable && NT == 1) && u + int(gridDim.x) < n_units)
           fill_table(head_of(u + int(gridDim.x), 0), hi + 1);
       }
       mbar_wait(&bar[DQF], hi & 1);
@@ -1294,13 +1353,12 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             float t32[32];
 #pragma unroll
             for (int d = 0; d < 32; ++d) t32[d] = uu[half * 32 + d];
-            atomicAdd(&sRed[half * 32 + lane], warp_transpose_sum32(t32));
+            sRed[quarter * 64 + half * 32 + lane] = warp_transpose_sum32(t32);
           }
           epi_sync();
-          if (te < 64) {
-            atomicAdd(p.dbias + (head_of(u, PH ? grp : 0) % p.H) * kD + te, sRed[te]);
-            sRed[te] = 0.f;
-          }
+          if (te < 64)
+            atomicAdd(p.dbias + (head_of(u, PH ? grp : 0) % p.H) * kD + te,
+                      sRed[te] + sRed[64 + te] + sRed[128 + te] + sRed[192 + te]);
           epi_sync();
         }
       }
@@ -1317,10 +1375,14 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
 }
 
 size_t bwd_fused_smem(int T) {
+  const int nt = (T + kTile - 1) / kTile;
   const int Tr = (T + kTile - 1) / kTile * kTile;
   const int KR = Tr > 2 * kTile ? kTile : Tr;  // UNIT (T > 256): one key tile per unit
-  return size_t(2 * Tr + 2 * KR) * kRowBytes + 5 * size_t(kDsChunk) + size_t(2 * Tr) * 8 + 256 +
-         1024 + 256;
+  // T <= 128: two operand slots (the kernel's DB layout)
+  const int ops = Tr == kTile && kBwdDoubleBuffer ? 2 : 1;
+  return size_t(ops * (2 * Tr + 2 * KR)) * kRowBytes +
+         size_t(4 + bwd_stage_tiles(nt > 3 ? 3 : nt)) * size_t(kDsChunk) + size_t(2 * Tr) * 8 +
+         1024 /* sRed */ + 1024 + 256;
 }
 
 // ---------------------------------------------------------------------------

@@ -1,6 +1,6 @@
-"""Phase timeline of CTA 0 of the fused attention backward (ViT-B/16 shape).
+"""Phase timeline of CTA 0 of the fused attention backward.
 
-    python tools/attn_trace.py      (on a B200)
+    python tools/attn_trace.py [B T H]      (on a B200; default ViT-B/16 b400: 400 197 12)
 Prints, per iteration, cycle offsets of: S issued, SF seen by the exp warp,
 PF arrive, PF seen by the MMA warp, post issued; per key tile KVF seen / KVE
 arrive; per head DQF / DQE / FULL / table-ready.
@@ -13,7 +13,7 @@ import torch
 sys.path.insert(0, ".")
 from paper_2102_03161_b200 import ops  # noqa: E402
 
-B, T, H = 400, 197, 12
+B, T, H = (int(x) for x in sys.argv[1:4]) if len(sys.argv) > 3 else (400, 197, 12)
 dev = torch.device("cuda")
 D = H * 64
 qkv = torch.randn(B * T, 3 * D, device=dev).bfloat16()
@@ -43,8 +43,8 @@ for it in range(8, 32):
     e = [r(t[it * 8 + k]) for k in range(5)]
     print(f"{it:2d} {e[0]:7d} {e[3]:7d} {e[4]:7d} {e[1]:7d} {e[2]:7d}")
 print("kt  KVF_seen KVE_arr")
-for kt in range(2, 8):
+for kt in range(2, 12):
     print(kt, r(t[512 + kt * 2]), r(t[512 + kt * 2 + 1]))
 print("hi  DQF DQE FULL_mma table_exp fill_start fill_end dq_stored dOsum_done tile0_stored")
-for hi in range(1, 4):
+for hi in range(1, 8):
     print(hi, *[r(t[640 + hi * 4 + k]) for k in range(4)], r(t[704 + hi * 2]), r(t[705 + hi * 2]), r(t[760 + hi * 4]), r(t[761 + hi * 4]), r(t[762 + hi * 4]))
