@@ -1,5 +1,5 @@
 """Phase timeline of pipeline 0 of CTA 0 of the attention forward (ViT-B/16):
-per query tile, cycle offsets of S issued, S seen by the softmax warpgroup,
+(python tools/attn_trace_fwd.py [B T H]) per query tile, cycle offsets of S issued, S seen by the softmax warpgroup,
 P written, O ready, O read out."""
 import ctypes as C
 import sys
@@ -9,7 +9,7 @@ import torch
 sys.path.insert(0, ".")
 from paper_2102_03161_b200 import ops  # noqa: E402
 
-B, T, H = 400, 197, 12
+B, T, H = (int(x) for x in sys.argv[1:4]) if len(sys.argv) > 3 else (400, 197, 12)
 dev = torch.device("cuda")
 D = H * 64
 qkv = torch.randn(B * T, 3 * D, device=dev).bfloat16()
