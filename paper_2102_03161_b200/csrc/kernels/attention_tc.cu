@@ -688,6 +688,11 @@ constexpr bool kBwdDkSS = false;
 #define EPS_BWD_DB 0
 #endif
 constexpr bool kBwdDoubleBuffer = EPS_BWD_DB != 0;
+// 256 < T <= 384 (UNIT): L2 prefetch of the next unit's operands
+#ifndef EPS_BWD_UNIT_PF
+#define EPS_BWD_UNIT_PF 1
+#endif
+constexpr bool kBwdUnitPrefetch = EPS_BWD_UNIT_PF != 0;
 // epilogue staging tiles (16 KB each) by key-tile count: T <= 128 has room for
 // three (dV / dK / dQ of a head leave without waiting on each other: BERT-large-128
 // 0.0446 -> 0.0423 ms), unless its operands are double-buffered
@@ -910,6 +915,25 @@ __global__ void __launch_bounds__(kBwdThreads, 1)
             tma_prefetch_3d(&map_do, h2 * kD, r, b2);
             tma_prefetch_3d(&map_qkv, HD + h2 * kD, r, b2);
             tma_prefetch_3d(&map_qkv, 2 * HD + h2 * kD, r, b2);
+          }
+        }
+      }
+      if (lane == 0 && UNIT && kBwdUnitPrefetch) {
+        // warm L2 with the next unit's Q / dO and K / V tile: its K / V (and
+        // last Q / dO tile) load only once this unit's last iteration is done
+        const int nu = u + int(gridDim.x);
+        if (nu < n_units) {
+          const int bh2 = head_of(nu, 0), jb2 = nu % NU;
+          const int b2 = bh2 / p.H, h2 = bh2 % p.H;
+#pragma unroll
+          for (int r = 0; r < Tr; r += kChunk) {
+            tma_prefetch_3d(&map_qkv, h2 * kD, r, b2);
+            tma_prefetch_3d(&map_do, h2 * kD, r, b2);
+          }
+#pragma unroll
+          for (int r = 0; r < kTile; r += kChunk) {
+            tma_prefetch_3d(&map_qkv, HD + h2 * kD, jb2 * kTile + r, b2);
+            tma_prefetch_3d(&map_qkv, 2 * HD + h2 * kD, jb2 * kTile + r, b2);
           }
         }
       }
