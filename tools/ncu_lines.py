@@ -34,7 +34,7 @@ def main():
     hdr = rows[1]
     idx = {h: i for i, h in enumerate(hdr)}
     reasons = [h for h in hdr if h.startswith("stall_") and "Not Issued" not in h]
-    body = [r for r in rows[2:] if len(r) == len(hdr)]
+    body = [r for r in rows[2:] if len(r) == len(hdr) and r[0] != "Address"]
     base = int(body[0][0], 16)
     tot, per, why = 0.0, Counter(), defaultdict(Counter)
     for r in body:

@@ -15,7 +15,7 @@ def main():
     hdr = rows[1]
     idx = {h: i for i, h in enumerate(hdr)}
     reasons = [h for h in hdr if h.startswith("stall_") and "Not Issued" not in h]
-    body = [r for r in rows[2:] if len(r) == len(hdr)]
+    body = [r for r in rows[2:] if len(r) == len(hdr) and r[0] != "Address"]
     tot = {h: sum(float(r[idx[h]] or 0) for r in body) for h in reasons}
     allsum = sum(tot.values())
     print("kernel:", rows[0][1][:100])
