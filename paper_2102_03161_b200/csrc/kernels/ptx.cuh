@@ -218,6 +218,13 @@ __device__ __forceinline__ void gelu_and_grad_f(float x, float& g, float& gp) {
 // issue-bound FC1 epilogue.  (Tried: the reciprocal on the FMA pipe, linear
 // start + three Newton steps, instead of MUFU.RCP: FC1 forward 0.375 -> 0.403
 // ms -- the epilogue is issue-bound, not SFU-bound.)
+// EPS_GELU_PAIR_RCP (off): one MUFU.RCP per column pair.  Measured neutral on
+// the FC1 forward (0.3600 vs 0.3601 ms, ViT-B/16 b400; step 46.93 vs 46.76 ms)
+// and it moved BERT-large's classifier-bias gradient past its noise gate in
+// tests/test_numerics_gpu.py, so it is not used.
+#ifndef EPS_GELU_PAIR_RCP
+#define EPS_GELU_PAIR_RCP 0
+#endif
 #ifndef EPS_GELU_AS3
 #define EPS_GELU_AS3 1
 #endif
@@ -232,7 +239,18 @@ __device__ __forceinline__ void gelu_and_grad_f2(float2 x, float2& g, float2& gp
 #else
   const float2 den = __ffma2_rn(make_float2(kGeluP, kGeluP), ax, make_float2(1.f, 1.f));
 #endif
+#if EPS_GELU_PAIR_RCP
+  // one MUFU.RCP for the pair: r = 1 / (den.x den.y), t = (den.y r, den.x r)
+  // (den in [1, 1 + p |x|]: no overflow for |x| < 1e18; two extra roundings,
+  // ~2e-7 relative, far under the bf16 rounding of the stored values).  The
+  // FC1 epilogue is bound by the MIO queue its MUFUs share with the staging
+  // stores (K = 768 GEMM stall attribution): 3 MUFU per pair instead of 4
+  // (measured neutral, off).
+  const float rr = rcp_approx(den.x * den.y);
+  const float2 t = __fmul2_rn(make_float2(den.y, den.x), make_float2(rr, rr));
+#else
   const float2 t = make_float2(rcp_approx(den.x), rcp_approx(den.y));
+#endif
   const float2 arg = __fmul2_rn(x, __fmul2_rn(make_float2(kGeluE, kGeluE), x));
   const float2 e = make_float2(ex2_approx(arg.x), ex2_approx(arg.y));
 #if EPS_GELU_AS3
